@@ -1,0 +1,185 @@
+/*
+ * propd.h — C ABI of libpropd.so, the B200 (sm_100a) kernels of the batched
+ * ProPD token-tree decode step.
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless its name ends in _host.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on that stream and allocates nothing persistent.
+ *   - Return value: 0 on success; nonzero on a launch/argument error, with a
+ *     message available from propd_last_error() (thread-local).  The Python
+ *     host layer raises ValueError/RuntimeError from it.
+ *   - dtype codes: PROPD_F32 = 0 (fp32 parity mode), PROPD_BF16 = 1.
+ *   - KV cache layout per layer: [slot][head][Lmax][dh], so one (sequence,
+ *     head) K or V block is a contiguous [Lmax, dh] tile.  Tree nodes of the
+ *     current pass live at slots seq_len[slot] + node (original tree index).
+ *   - Tree templates are shared by every sequence of a step (the tree SHAPE
+ *     is global per step, engine.py:246): parent[n], depth[n], rank[n] and an
+ *     ancestor bitset mask[n][W], W = ceil(n/64).
+ *
+ * Reference interfaces replaced (paths relative to
+ * /root/reference/pkg/src/treedecode/):
+ *   ModelBackend.forward_tree / commit / draft / next_argmax  backends.py:53-95
+ *   TinyTransformer._block (attention + projections)           backends.py:202-237
+ *   build_tree / make_mask / positions                         token_tree.py:125-185, engine.py:260
+ *   prune (+ early head top-K)                                 pruning.py:40-66, backends.py:320-327
+ *   verify + commit                                            verification.py:30-53, backends.py:337-348
+ *   AcceptanceStats.update + select_best_nodes                 acceptance.py:96-113, 186-206
+ */
+#ifndef PROPD_H
+#define PROPD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PROPD_F32 0
+#define PROPD_BF16 1
+
+/* Last error message of the calling thread ("" if none). */
+const char* propd_last_error(void);
+/* ABI version; bumped on any signature change. */
+int propd_abi_version(void);
+/* Number of SMs of the current device (0 if no device). */
+int propd_num_sms(void);
+
+/* ---- K1: tree materialisation (token_tree.py:125-170, engine.py:260) ----
+ * For sequence b and template node i (row m = b*n + i):
+ *   tokens[m]    = draft_tok[b][depth[i]-1][rank[i]-1]
+ *   positions[m] = seq_len[seq_slot[b]] + depth[i] - 1
+ *   x[m,:]       = emb[tokens[m]] + pos[positions[m]]        (fp32 residual)
+ *   row_seq[m] = b, row_node[m] = i, row_off[b] = b*n (row_off[B] = B*n).   */
+int propd_tree_embed(int dtype, int B, int n, int D, int kmax, int H,
+                     const int32_t* depth, const int32_t* rank, const int32_t* draft_tok,
+                     const int32_t* seq_slot, const int32_t* seq_len,
+                     const void* emb, const void* pos,
+                     int32_t* tokens, int32_t* positions, float* x,
+                     int32_t* row_seq, int32_t* row_node, int32_t* row_off, void* stream);
+
+/* Generic row embedding: x[m] = emb[tokens[m]] + pos[positions[m]]. */
+int propd_embed_rows(int dtype, int M, int H, const int32_t* tokens, const int32_t* positions,
+                     const void* emb, const void* pos, float* x, void* stream);
+
+/* Bonus rows (one per sequence): tokens[b] = bonus[b],
+ * positions[b] = seq_len[seq_slot[b]], x[b] = emb + pos; row_seq[b] = b,
+ * row_node[b] = 0, row_off[b] = b. */
+int propd_bonus_embed(int dtype, int B, int H, const int32_t* bonus, const int32_t* seq_slot,
+                      const int32_t* seq_len, const void* emb, const void* pos, float* x,
+                      int32_t* positions, int32_t* row_seq, int32_t* row_node, int32_t* row_off,
+                      void* stream);
+
+/* ---- dense helpers (backends.py:135-142, 216, 234-236) ----
+ * x += delta (if delta != NULL, dtype-typed); out = LN(x) (no affine, eps 1e-5,
+ * population variance).  in_idx/out_idx (nullable) gather/scatter rows:
+ * row m reads x[in_idx ? in_idx[m] : m], writes out[out_idx ? out_idx[m] : m].
+ * When delta is given the residual update is written back to x (in place). */
+int propd_add_ln(int dtype, int M, int H, float* x, const void* delta, void* out,
+                 const int32_t* in_idx, const int32_t* out_idx, void* stream);
+/* In-place tanh-GELU over count elements. */
+int propd_gelu(int dtype, int64_t count, void* buf, void* stream);
+/* x += delta (residual add, fp32 += dtype). */
+int propd_residual_add(int dtype, int64_t count, float* x, const void* delta, void* stream);
+/* dst[m] = (dtype) src[idx ? idx[m] : m] for fp32 rows of width H (gather + cast). */
+int propd_gather_rows(int dtype, int M, int H, const float* src, const int32_t* idx, void* dst,
+                      void* stream);
+/* First-max argmax per row of an fp32 [M, V] matrix (row stride ld). */
+int propd_argmax_rows(int M, int V, int ld, const float* logits, int32_t* out, void* stream);
+/* Stable descending top-k per row (ties -> lower index; == numpy
+ * argsort(-x, kind="stable")[:k]), k <= 1024. */
+int propd_topk_rows(int R, int V, int ld, int k, const float* logits, int32_t* out_idx,
+                    float* out_val, void* stream);
+
+/* ---- KV cache ---- */
+/* Scatter K/V of rows into the layer cache: row m of sequence b = row_seq[m]
+ * goes to slot seq_len[seq_slot[b]] + row_node[m].  k/v are columns
+ * [H,2H) and [2H,3H) of the fused qkv buffer (row stride ldqkv). */
+int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, int ldqkv,
+                    const int32_t* row_seq, const int32_t* row_node, const int32_t* seq_slot,
+                    const int32_t* seq_len, void* kcache, void* vcache, void* stream);
+
+/* ---- K2: tree-masked verification attention (backends.py:216-233) ----
+ * Rows [row_off[b], row_off[b+1]) belong to sequence b; row m sees cache keys
+ * [0, L_b) plus tree keys L_b + j for every bit j set in mask[row_node[m]]
+ * (mask == NULL: causal new rows, j visible iff j <= row_node[m]; keys
+ * beyond L_b + n_tmpl are never visible).
+ * q = columns [0,H) of qkv.  out[m, a*dh:(a+1)*dh] = softmax(q k^T / sqrt(dh)) v.
+ * `workspace` must hold propd_attn_workspace_bytes(...) bytes.
+ * impl: 0 = auto, 1 = CUDA-core split-KV kernel, 2 = tcgen05/TMA kernel
+ * (bf16, dh = 128 only). */
+int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits);
+int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax,
+                         int max_rows_per_seq, int max_keys,
+                         const void* qkv, int ldqkv, const void* kcache, const void* vcache,
+                         const int32_t* seq_slot, const int32_t* seq_len,
+                         const int32_t* row_off, const int32_t* row_node,
+                         const uint64_t* mask, int n_tmpl, int W,
+                         void* out, int ldout, void* workspace, int64_t workspace_bytes,
+                         void* stream);
+
+/* ---- K3: early prune (pruning.py:40-66, backends.py:320-327) ----
+ * early_logits: fp32 [R, V], one row per (sequence, parent-slot): row
+ * b*P + parent_slot[p] holds the early head output of node p of sequence b.
+ * member[b*n+i] = (parent[i] < 0) or rank of tokens[b*n+i] in its parent's
+ * row < topk, rank(t) = #{v: l[v] > l[t]} + #{v < t: l[v] == l[t]}. */
+int propd_early_member(int B, int n, int P, int V, int topk, const float* early_logits,
+                       const int32_t* parent, const int32_t* parent_slot, const int32_t* tokens,
+                       uint8_t* member, void* stream);
+/* Top-down closure + compaction of surviving rows (ballot/prefix sum):
+ * alive[b*n+i] = member && (parent < 0 || alive[parent]); new rows are the
+ * survivors in (b, i) order: new_row_seq/new_row_node/new_row_src (old row
+ * index b*n+i), new_row_off[B+1]; node_row[b*n+i] = new row or -1;
+ * surv_cnt[b]; *total = sum. */
+int propd_prune_compact(int B, int n, const int32_t* parent, const uint8_t* member, uint8_t* alive,
+                        int32_t* new_row_seq, int32_t* new_row_node, int32_t* new_row_src,
+                        int32_t* new_row_off, int32_t* node_row, int32_t* surv_cnt, int32_t* total,
+                        void* stream);
+
+/* ---- K5: greedy accept + in-place KV compaction (verification.py:30-53,
+ * backends.py:337-348) ----
+ * Walks each sequence's (pruned) tree from root[slot]; accepted nodes
+ * (original indices) -> acc_node[b][D], survivor-row indices -> acc_surv[b][D],
+ * acc_len[b]; bonus[b]; committed[b][0..acc_len] = accepted tokens + bonus;
+ * ranks[b][d] (int8) = 1-based rank of committed[b][d] in draft head d+1's
+ * list, -1 if absent, 0 for depths beyond acc_len+1 (the acceptance record).
+ * Then moves K/V of accepted node j from slot L+acc_node[j] to L+j in every
+ * layer/head (read-before-write per element) and sets seq_len += acc_len.
+ * alive may be NULL (no pruning); node_row may be NULL (row = b*n+i).
+ * kcache/vcache: base of layer 0; layer_stride in elements. */
+int propd_verify_commit(int dtype, int B, int n, int D, int kmax, int layers, int A, int dh, int Lmax,
+                        int64_t layer_stride, const int32_t* parent, const int32_t* tokens,
+                        const uint8_t* alive, const int32_t* node_row, const int32_t* row_argmax,
+                        const int32_t* root, const int32_t* draft_tok, const int32_t* seq_slot,
+                        int32_t* seq_len, void* kcache, void* vcache,
+                        int32_t* acc_node, int32_t* acc_surv, int32_t* acc_len, int32_t* bonus,
+                        int32_t* committed, int8_t* ranks, void* stream);
+
+/* Explicit-index compaction (per-sequence commit path): same move as in
+ * propd_verify_commit for given acc_node/acc_len, plus seq_len += acc_len. */
+int propd_kv_compact(int dtype, int B, int D, int layers, int A, int dh, int Lmax, int64_t layer_stride,
+                     const int32_t* seq_slot, int32_t* seq_len, const int32_t* acc_node,
+                     const int32_t* acc_len, void* kcache, void* vcache, void* stream);
+
+/* seq_len[seq_slot[b]] += delta (delta_dev[b] if non-NULL, else delta). */
+int propd_seq_advance(int B, const int32_t* seq_slot, int32_t* seq_len, const int32_t* delta_dev,
+                      int delta, void* stream);
+/* root[seq_slot[b]] = argmax[b] (first max of each bonus row). */
+int propd_scatter_i32(int B, const int32_t* idx, const int32_t* src, int32_t* dst, void* stream);
+
+/* ---- K4: dynamic tree generation (acceptance.py:96-206) ----
+ * Replays acceptance records in global sequence order into P[D][k] (fp64,
+ * in/out) and counts[D] (int64): for each record r = ranks[s][d] != 0,
+ * counts[d] += 1, step = alpha > 0 ? alpha : 1/counts[d],
+ * P[d][j] = (1-step)*P[d][j] + step*[j >= r-1 and r > 0]  (no FMA contraction).
+ * Then scores the grid universe (1,..,1,r): contrib = spine[d]*m[d][r] with
+ * m = diff(P, prepend 0), spine = cumprod(m[:,0]) and writes the selection
+ * order (candidate c = d*k + r, sorted by (-contrib, depth, rank)) and the
+ * expected-length curve l[s-1] = sum of the first s contributions. */
+int propd_stats_replay_select(int S, int D, int k, const int8_t* ranks, double alpha, double* P,
+                              int64_t* counts, int32_t* order, double* lcurve, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROPD_H */

@@ -1,0 +1,613 @@
+"""B200Backend: the reference's ModelBackend plugin API on sm_100a kernels.
+
+Drop-in boundary (paths relative to /root/reference/pkg/src/treedecode/):
+`ModelBackend` (backends.py:53-95) — vocab_size / num_layers /
+draft_head_count, prefill, draft, next_argmax, forward_tree (with the
+mid-stack prune callback), commit — with the reference's argument meaning and
+ValueError messages (backends.py:98-108, 239-348).  A reference
+`DecodeEngine(B200Backend(cfg), ...)` runs unchanged on it.
+
+On top of that per-sequence API the backend offers the batched step used by
+`paper_2402_13485_b200.engine.DecodeEngine`: one call runs draft (K4a),
+tree materialisation (K1), the tree pass with on-device early pruning (K3),
+greedy accept + KV compaction (K5) and the bonus pass for the whole batch.
+
+Device state per sequence slot: KV cache [layer][slot][head][Lmax][dh],
+committed length, root token (argmax of the last committed row's logits),
+final LN'd hidden of that row (the draft heads' input).
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import call, ptr
+from .config import TinyTransformerConfig
+from .planning import HeadPredictions
+from .tree import TreeTemplate, mask_to_bits
+from .weights import DeviceWeights, seeded_weights
+
+MAX_TREE = 256  # ancestor bitsets of <= 4 x 64 bits per row
+
+
+@dataclass
+class DecodeState:
+    """Per-sequence committed context + the last verified tree (backends.py:31-40)."""
+
+    committed: list = field(default_factory=list)
+    last_tree: tuple | None = None
+    slot: int = -1
+    _tree: dict | None = field(default=None, repr=False)
+    _fin: object = field(default=None, repr=False, compare=False)
+
+    @property
+    def length(self) -> int:
+        return len(self.committed)
+
+
+@dataclass(frozen=True)
+class TreeForward:
+    """Survivor indices into the drafted tree, their argmax and logits (backends.py:43-50)."""
+
+    survivors: tuple
+    argmax: np.ndarray
+    logits: np.ndarray | None
+
+
+def validate_commit_path(mask: np.ndarray, accepted) -> None:
+    """Each accepted node must see exactly the earlier accepted nodes (backends.py:98-108)."""
+    seen: set = set()
+    for idx in accepted:
+        if not 0 <= idx < mask.shape[0]:
+            raise ValueError(f"accepted index {idx} outside the verified tree")
+        if set(np.nonzero(mask[idx])[0].tolist()) != seen | {idx}:
+            raise ValueError("accepted path is not a contiguous root chain")
+        seen.add(idx)
+
+
+def subsample_mask(mask: np.ndarray, survivors) -> np.ndarray:
+    """Ancestor-closed row/column gather with the reference's checks (token_tree.py:188-207)."""
+    n = mask.shape[0]
+    s = np.asarray(survivors, dtype=np.int64)
+    if s.ndim != 1:
+        raise ValueError("survivors must be a flat index list")
+    if s.size and (s[0] < 0 or s[-1] >= n):
+        raise ValueError("survivor index out of range")
+    if np.any(np.diff(s) <= 0):
+        raise ValueError("survivors must be strictly increasing")
+    kept = np.zeros(n, dtype=bool)
+    kept[s] = True
+    for i in s:
+        if not kept[mask[i]].all():
+            raise ValueError(f"survivor {i}: an ancestor was dropped (set is not ancestor-closed)")
+    return mask[np.ix_(s, s)].copy()
+
+
+@dataclass
+class Rows:
+    """Device row tables of one pass: rows [row_off[b], row_off[b+1]) belong
+    to batch entry b (sequence slot seq_slot[b]); row_node = tree node index."""
+
+    M: int
+    B: int
+    seq_slot: object
+    row_seq: object
+    row_node: object
+    row_off: object
+    max_keys: int
+    max_rows: int
+    kv_keys: int = 0  # host count of K/V rows the pass streams (roofline accounting)
+
+
+@dataclass
+class StepOutput:
+    """Host copies of one batched tree step (engine bookkeeping)."""
+
+    committed: np.ndarray  # [B, D+1] accepted tokens + bonus, -1 padded
+    acc_len: np.ndarray  # [B]
+    acc_surv: np.ndarray  # [B, D] accepted indices into the pruned tree
+    surv_cnt: np.ndarray  # [B]
+    ranks_dev: object  # device int8 [B, D] acceptance records
+    trace: dict | None = None
+
+
+class B200Backend:
+    """ModelBackend on B200 kernels.  dtype "fp32" is the parity mode (all
+    GEMMs in true fp32, TF32 off); "bf16" is the performance mode."""
+
+    def __init__(self, config: TinyTransformerConfig = TinyTransformerConfig(), *, dtype: str = "fp32",
+                 device=None, weights: dict | None = None, random_device_init: bool = False,
+                 max_slots: int = 16, max_tree: int = MAX_TREE, kv_len: int | None = None,
+                 attn_impl: int = 0) -> None:
+        import torch
+
+        self.lib = _lib.load()
+        if not torch.cuda.is_available():
+            raise RuntimeError("B200Backend needs a CUDA device; there is no CPU fallback")
+        self.torch = torch
+        self.config = config
+        self.device = torch.device(device if device is not None else "cuda")
+        if dtype not in ("fp32", "bf16"):
+            raise ValueError("dtype must be 'fp32' or 'bf16'")
+        self.dtype_name = dtype
+        self.tdtype = torch.float32 if dtype == "fp32" else torch.bfloat16
+        self.code = _lib.F32 if dtype == "fp32" else _lib.BF16
+        if dtype == "fp32":
+            torch.backends.cuda.matmul.allow_tf32 = False  # true fp32 GEMMs for parity
+        self.attn_impl = attn_impl
+        self.max_tree = int(max_tree)
+        if self.max_tree > MAX_TREE:
+            raise ValueError(f"max_tree must be <= {MAX_TREE}")
+        cfg = config
+        if random_device_init:
+            self.w = DeviceWeights(cfg, self.tdtype, self.device)
+        else:
+            self.w = DeviceWeights(cfg, self.tdtype, self.device,
+                                   host=weights if weights is not None else seeded_weights(cfg))
+        self.A, self.dh, self.H, self.V = cfg.heads, cfg.head_dim, cfg.hidden, cfg.vocab
+        # cache slots hold committed rows (< max_positions) plus one tree
+        self.Lmax = (kv_len if kv_len is not None else cfg.max_positions) + self.max_tree
+        self.max_slots = int(max_slots)
+        dev, T = self.device, self.tdtype
+        shape = (cfg.layers, self.max_slots, self.A, self.Lmax, self.dh)
+        self.kcache = torch.empty(shape, device=dev, dtype=T)
+        self.vcache = torch.empty(shape, device=dev, dtype=T)
+        self.layer_stride = self.max_slots * self.A * self.Lmax * self.dh
+        self.seq_len = torch.zeros(self.max_slots, device=dev, dtype=torch.int32)
+        self.root = torch.zeros(self.max_slots, device=dev, dtype=torch.int32)
+        self.hidden = torch.zeros(self.max_slots, self.H, device=dev, dtype=T)
+        self.last_logits = torch.zeros(self.max_slots, self.V, device=dev, dtype=torch.float32)
+        self._len = [0] * self.max_slots  # host mirror of seq_len
+        self._free = list(range(self.max_slots - 1, -1, -1))
+        self._ws = torch.empty(0, device=dev, dtype=torch.uint8)
+        self._one_mask = torch.ones(1, device=dev, dtype=torch.int64)  # single-node template {0}
+        self.launches = 0  # libpropd kernel launches issued (bench accounting)
+        self.attn_timer = None  # list -> (start, end, rows) CUDA events of every K2 launch
+
+    # ------------------------------------------------------------------ API
+    @property
+    def vocab_size(self) -> int:
+        return self.config.vocab
+
+    @property
+    def num_layers(self) -> int:
+        return self.config.layers
+
+    @property
+    def draft_head_count(self) -> int:
+        return self.config.draft_heads
+
+    def stream(self):
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def _call(self, name, *args):
+        self.launches += 1
+        call(name, *args)
+
+    # ------------------------------------------------------------- slots
+    def _alloc_slot(self, state: DecodeState) -> int:
+        if not self._free:
+            raise RuntimeError(f"no free sequence slots (max_slots={self.max_slots})")
+        slot = self._free.pop()
+        state.slot = slot
+        self._len[slot] = 0
+        self.seq_len[slot] = 0
+        state._fin = weakref.finalize(state, self._release, slot)
+        return slot
+
+    def _release(self, slot: int) -> None:
+        self._free.append(slot)
+
+    def release(self, state: DecodeState) -> None:
+        """Return a finished sequence's cache slot to the pool."""
+        fin = getattr(state, "_fin", None)
+        if fin is not None and fin.alive:
+            fin()
+        state.slot = -1
+
+    def _i32(self, values):
+        return self.torch.tensor(np.asarray(values, dtype=np.int32), device=self.device)
+
+    def _workspace(self, M: int) -> object:
+        need = int(self.lib.propd_attn_workspace_bytes(M, self.A, self.dh, 0))
+        if self._ws.numel() < need:
+            self._ws = self.torch.empty(need, device=self.device, dtype=self.torch.uint8)
+        return self._ws
+
+    # ----------------------------------------------------------- layers
+    def _run_layers(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
+        """Blocks l0..l1-1 over the rows of `rt` (backends.py:202-237).  Returns
+        the last MLP output not yet added to the residual stream x."""
+        torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
+        M = rt.M
+        ws = self._workspace(M)
+        h = torch.empty(M, H, device=self.device, dtype=T)
+        ctx = torch.empty(M, H, device=self.device, dtype=T)
+        for l in range(l0, l1):
+            self._call("propd_add_ln", self.code, M, H, ptr(x), ptr(pending), ptr(h), None, None, st)
+            qkv = torch.mm(h, self.w.wqkv[l])
+            kc, vc = self.kcache[l], self.vcache[l]
+            self._call("propd_kv_append", self.code, M, self.A, self.dh, self.Lmax, ptr(qkv), 3 * H,
+                       ptr(rt.row_seq), ptr(rt.row_node), ptr(rt.seq_slot), ptr(self.seq_len), ptr(kc), ptr(vc), st)
+            if self.attn_timer is not None:
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record()
+            self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
+                       rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
+                       ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
+                       ptr(ws), ws.numel(), st)
+            if self.attn_timer is not None:
+                ev1 = torch.cuda.Event(enable_timing=True)
+                ev1.record()
+                self.attn_timer.append((ev0, ev1, rt))
+            o = torch.mm(ctx, self.w.wo[l])
+            self._call("propd_add_ln", self.code, M, H, ptr(x), ptr(o), ptr(h), None, None, st)
+            g = torch.mm(h, self.w.w1[l])
+            self._call("propd_gelu", self.code, g.numel(), ptr(g), st)
+            pending = torch.mm(g, self.w.w2[l])
+        return pending
+
+    def _flush(self, x, pending):
+        if pending is not None:
+            self._call("propd_residual_add", self.code, x.numel(), ptr(x), ptr(pending), self.stream())
+
+    def _lm_argmax(self, hfin):
+        logits = self.torch.mm(hfin, self.w.w_lm)
+        if logits.dtype != self.torch.float32:
+            logits = logits.float()
+        am = self.torch.empty(hfin.shape[0], device=self.device, dtype=self.torch.int32)
+        self._call("propd_argmax_rows", hfin.shape[0], self.V, self.V, ptr(logits), ptr(am), self.stream())
+        return logits, am
+
+    # ------------------------------------------------- causal append (prefill/extend)
+    def _extend(self, slots, token_lists, keep_logits: bool = True) -> None:
+        """Causal forward of new committed rows for each slot; appends K/V,
+        updates hidden/root/last_logits/seq_len (backends.py:239-259)."""
+        torch, st = self.torch, self.stream()
+        B = len(slots)
+        lens = [len(t) for t in token_lists]
+        offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        M = int(offs[-1])
+        toks = np.concatenate([np.asarray(t, dtype=np.int32) for t in token_lists])
+        pos = np.concatenate([np.arange(self._len[s], self._len[s] + n, dtype=np.int32) for s, n in zip(slots, lens)])
+        node = np.concatenate([np.arange(n, dtype=np.int32) for n in lens])
+        seq = np.repeat(np.arange(B, dtype=np.int32), lens)
+        x = torch.empty(M, self.H, device=self.device, dtype=torch.float32)
+        d_tok, d_pos = self._i32(toks), self._i32(pos)
+        self._call("propd_embed_rows", self.code, M, self.H, ptr(d_tok), ptr(d_pos), ptr(self.w.emb),
+                   ptr(self.w.pos), ptr(x), st)
+        seq_slot = self._i32(slots)
+        rt = Rows(M, B, seq_slot, self._i32(seq), self._i32(node), self._i32(offs),
+                  max_keys=max(self._len[s] + n for s, n in zip(slots, lens)), max_rows=max(lens),
+                  kv_keys=sum(self._len[s] + n for s, n in zip(slots, lens)))
+        pending = self._run_layers(x, rt, 0, self.num_layers, None, max(lens), 0)
+        last = self._i32(offs[1:] - 1)
+        hfin = torch.empty(B, self.H, device=self.device, dtype=self.tdtype)
+        self._call("propd_add_ln", self.code, B, self.H, ptr(x), ptr(pending), ptr(hfin), ptr(last), None, st)
+        logits, am = self._lm_argmax(hfin)
+        idx = seq_slot.long()
+        self.hidden.index_copy_(0, idx, hfin)
+        if keep_logits:
+            self.last_logits.index_copy_(0, idx, logits)
+        self._call("propd_scatter_i32", B, ptr(seq_slot), ptr(am), ptr(self.root), st)
+        self._call("propd_seq_advance", B, ptr(seq_slot), ptr(self.seq_len), ptr(self._i32(lens)), 0, st)
+        for s, n in zip(slots, lens):
+            self._len[s] += n
+
+    def _check_tokens(self, toks) -> None:
+        a = np.asarray(toks, dtype=np.int64)
+        if a.size == 0:
+            raise ValueError("cannot extend with zero tokens")
+        if np.any((a < 0) | (a >= self.config.vocab)):
+            raise ValueError("token id outside the vocabulary")
+
+    # ------------------------------------------------- ModelBackend methods
+    def prefill(self, prompt) -> DecodeState:
+        if len(prompt) == 0:
+            raise ValueError("prompt must be non-empty")
+        return self.prefill_batch([prompt])[0]
+
+    def prefill_batch(self, prompts) -> list:
+        """Ingest several prompts in one causal pass (engine.py:209 batched)."""
+        for p in prompts:
+            if len(p) == 0:
+                raise ValueError("prompt must be non-empty")
+            self._check_tokens(p)
+            if len(p) > self.config.max_positions:
+                raise ValueError("sequence exceeds max_positions")
+        states = [DecodeState() for _ in prompts]
+        slots = [self._alloc_slot(s) for s in states]
+        self._extend(slots, [list(map(int, p)) for p in prompts])
+        for s, p in zip(states, prompts):
+            s.committed.extend(int(t) for t in p)
+        return states
+
+    def synthetic_states(self, B: int, L: int, seed: int = 0) -> list:
+        """B sequences whose committed context is L random tokens and whose
+        device state (K/V cache rows, last hidden, root token) is random
+        synthetic data of the right shape — the bench's stand-in for a
+        prefill of L tokens (decode-step cost does not depend on the values)."""
+        torch = self.torch
+        if L + 1 > self.config.max_positions:
+            raise ValueError("sequence exceeds max_positions")
+        g = torch.Generator(device=self.device)
+        g.manual_seed(seed)
+        rng = np.random.default_rng(seed)
+        states = []
+        for _ in range(B):
+            st = DecodeState(committed=rng.integers(0, self.V, size=L).tolist())
+            slot = self._alloc_slot(st)
+            for l in range(self.num_layers):
+                for cache in (self.kcache, self.vcache):
+                    blk = cache[l, slot, :, :L]
+                    blk.copy_(torch.randn(blk.shape, device=self.device, generator=g, dtype=torch.float32))
+            self.hidden[slot].copy_(torch.randn(self.H, device=self.device, generator=g))
+            self.root[slot] = int(rng.integers(0, self.V))
+            self.seq_len[slot] = L
+            self._len[slot] = L
+            states.append(st)
+        return states
+
+    def draft(self, state: DecodeState, k: int) -> HeadPredictions:
+        """D draft heads on the last committed row, stable top-k (backends.py:274-285)."""
+        if not 1 <= k <= self.config.vocab:
+            raise ValueError("k outside 1..vocab")
+        tok, val = self._draft_dev(self._i32([state.slot]), 1, k)
+        return HeadPredictions(tok[0].cpu().numpy().astype(np.int64), val[0].cpu().numpy().astype(np.float64))
+
+    def _draft_dev(self, seq_slot, B: int, k: int):
+        if k > 1024:
+            raise ValueError("draft top-k above 1024 is not supported by the device top-k")
+        torch, D, V = self.torch, self.config.draft_heads, self.V
+        hid = self.hidden.index_select(0, seq_slot.long())
+        logits = torch.mm(hid, self.w.w_draft)
+        if logits.dtype != torch.float32:
+            logits = logits.float()
+        tok = torch.empty(B, D, k, device=self.device, dtype=torch.int32)
+        val = torch.empty(B, D, k, device=self.device, dtype=torch.float32)
+        self._call("propd_topk_rows", B * D, V, V, k, ptr(logits), ptr(tok), ptr(val), self.stream())
+        return tok, val
+
+    def next_argmax(self, state: DecodeState) -> int:
+        return int(self.root[state.slot].item())
+
+    def last_logits_of(self, state: DecodeState) -> np.ndarray:
+        """Logits of the last committed row (the reference's state.last_logits)."""
+        return self.last_logits[state.slot].double().cpu().numpy()
+
+    def forward_tree(self, state: DecodeState, tokens, positions, mask, *, prune_layer=None, early_topk=0,
+                     prune_callback=None) -> TreeForward:
+        """One masked pass over all tree nodes, optional mid-stack prune (backends.py:290-335)."""
+        torch, st, cfg = self.torch, self.stream(), self.config
+        toks = np.asarray(tokens, dtype=np.int64)
+        pos = np.asarray(positions, dtype=np.int64)
+        n = toks.size
+        mask = np.asarray(mask)
+        if mask.shape != (n, n) or pos.shape != (n,):
+            raise ValueError("tokens, positions, and mask sizes disagree")
+        if np.any((toks < 0) | (toks >= cfg.vocab)):
+            raise ValueError("token id outside the vocabulary")
+        if np.any(pos < state.length) or np.any(pos >= cfg.max_positions):
+            raise ValueError("tree positions must follow the committed context")
+        if prune_callback is not None:
+            if prune_layer is None or not 1 <= prune_layer < cfg.layers:
+                raise ValueError("prune layer must lie strictly inside the stack")
+            if early_topk < 1:
+                raise ValueError("early_topk must be positive when pruning")
+        if n > self.max_tree:
+            raise ValueError(f"tree of {n} nodes exceeds the backend's max_tree={self.max_tree}")
+        vis = mask.astype(bool)
+        slot, L = state.slot, self._len[state.slot]
+        bits = torch.from_numpy(mask_to_bits(vis).view(np.int64)).to(self.device)
+        W = bits.shape[1]
+        x = torch.empty(n, self.H, device=self.device, dtype=torch.float32)
+        self._call("propd_embed_rows", self.code, n, self.H, ptr(self._i32(toks)), ptr(self._i32(pos)),
+                   ptr(self.w.emb), ptr(self.w.pos), ptr(x), st)
+        seq_slot = self._i32([slot])
+        rt = Rows(n, 1, seq_slot, self._i32(np.zeros(n)), self._i32(np.arange(n)), self._i32([0, n]),
+                  max_keys=L + n, max_rows=n)
+        keep = np.arange(n)
+        if prune_callback is not None:
+            pending = self._run_layers(x, rt, 0, prune_layer, bits, n, W)
+            self._flush(x, pending)
+            xe = x.to(self.tdtype)
+            early = torch.mm(xe, self.w.w_early)
+            if early.dtype != torch.float32:
+                early = early.float()
+            kk = min(early_topk, cfg.vocab)
+            if kk > 1024:
+                raise ValueError("early top-K above 1024 is not supported by the device top-k")
+            idx = torch.empty(n, kk, device=self.device, dtype=torch.int32)
+            self._call("propd_topk_rows", n, self.V, self.V, kk, ptr(early), ptr(idx), None, st)
+            lists = [list(map(int, r)) for r in idx.cpu().numpy()]
+            surv = [int(s) for s in prune_callback(lists)]
+            vis = subsample_mask(vis, surv)
+            keep = np.asarray(surv, dtype=np.int64)
+            S = keep.size
+            x2 = torch.empty(S, self.H, device=self.device, dtype=torch.float32)
+            self._call("propd_gather_rows", _lib.F32, S, self.H, ptr(x), ptr(self._i32(keep)), ptr(x2), st)
+            x = x2
+            rt = Rows(S, 1, seq_slot, self._i32(np.zeros(S)), self._i32(keep), self._i32([0, S]),
+                      max_keys=L + n, max_rows=S)
+            pending = self._run_layers(x, rt, prune_layer, cfg.layers, bits, n, W)
+        else:
+            pending = self._run_layers(x, rt, 0, cfg.layers, bits, n, W)
+        S = rt.M
+        hfin = torch.empty(S, self.H, device=self.device, dtype=self.tdtype)
+        self._call("propd_add_ln", self.code, S, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
+        logits, am = self._lm_argmax(hfin)
+        state.last_tree = (toks[keep].copy(), vis.copy())
+        state._tree = {"keep": keep, "positions": pos, "L": L}
+        return TreeForward(tuple(int(i) for i in keep), am.cpu().numpy().astype(np.int64),
+                           logits.double().cpu().numpy())
+
+    def commit(self, state: DecodeState, accepted, bonus) -> None:
+        """Append the accepted root chain + bonus (backends.py:337-348).  The
+        accepted rows' K/V are moved into place from the tree pass (no
+        recompute) whenever the chain sat at its commit positions."""
+        acc = [int(a) for a in accepted]
+        if acc:
+            if state.last_tree is None:
+                raise ValueError("commit with accepted nodes needs a preceding tree forward")
+            ttoks, tmask = state.last_tree
+            validate_commit_path(tmask, acc)
+            new = [int(ttoks[i]) for i in acc] + [int(bonus)]
+        else:
+            new = [int(bonus)]
+        self._check_tokens(new)
+        slot, L = state.slot, self._len[state.slot]
+        if L + len(new) > self.config.max_positions:
+            raise ValueError("sequence exceeds max_positions")
+        info = state._tree
+        nodes = [int(info["keep"][a]) for a in acc] if (acc and info) else []
+        fast = bool(acc) and info is not None and info["L"] == L and all(
+            int(info["positions"][nd]) == L + j for j, nd in enumerate(nodes)) and all(
+            b > a for a, b in zip(nodes, nodes[1:]))
+        if fast:
+            D = len(nodes)
+            self._call("propd_kv_compact", self.code, 1, D, self.num_layers, self.A, self.dh, self.Lmax,
+                       self.layer_stride, ptr(self._i32([slot])), ptr(self.seq_len), ptr(self._i32(nodes)),
+                       ptr(self._i32([D])), ptr(self.kcache), ptr(self.vcache), self.stream())
+            self._len[slot] += D
+            self._extend([slot], [[int(bonus)]])
+        else:
+            self._extend([slot], [new])
+        state.committed.extend(new)
+        state.last_tree = None
+        state._tree = None
+
+    # ------------------------------------------------- batched steps
+    def step_autoregressive(self, states) -> np.ndarray:
+        """AR iteration for a batch: commit each sequence's root argmax (engine.py:231-241)."""
+        torch = self.torch
+        B = len(states)
+        seq_slot = self._i32([s.slot for s in states])
+        bonus = self.root.index_select(0, seq_slot.long())
+        self._bonus_pass(seq_slot, bonus, B, max(self._len[s.slot] for s in states) + 1,
+                         sum(self._len[s.slot] + 1 for s in states))
+        out = bonus.cpu().numpy()
+        for s, t in zip(states, out):
+            s.committed.append(int(t))
+            self._len[s.slot] += 1
+        del torch
+        return out
+
+    def _bonus_pass(self, seq_slot, bonus, B: int, max_keys: int, kv_keys: int = 0) -> None:
+        """One committed row per sequence at position seq_len (backends.py:239-259
+        for the bonus token): K/V append, hidden/root update, seq_len += 1."""
+        torch, st = self.torch, self.stream()
+        x = torch.empty(B, self.H, device=self.device, dtype=torch.float32)
+        positions = torch.empty(B, device=self.device, dtype=torch.int32)
+        row_seq = torch.empty(B, device=self.device, dtype=torch.int32)
+        row_node = torch.empty(B, device=self.device, dtype=torch.int32)
+        row_off = torch.empty(B + 1, device=self.device, dtype=torch.int32)
+        self._call("propd_bonus_embed", self.code, B, self.H, ptr(bonus), ptr(seq_slot), ptr(self.seq_len),
+                   ptr(self.w.emb), ptr(self.w.pos), ptr(x), ptr(positions), ptr(row_seq), ptr(row_node),
+                   ptr(row_off), st)
+        rt = Rows(B, B, seq_slot, row_seq, row_node, row_off, max_keys=max_keys, max_rows=1, kv_keys=kv_keys)
+        pending = self._run_layers(x, rt, 0, self.num_layers, self._one_mask, 1, 1)
+        hfin = torch.empty(B, self.H, device=self.device, dtype=self.tdtype)
+        self._call("propd_add_ln", self.code, B, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
+        logits, am = self._lm_argmax(hfin)
+        self.hidden.index_copy_(0, seq_slot.long(), hfin)
+        self._call("propd_scatter_i32", B, ptr(seq_slot), ptr(am), ptr(self.root), st)
+        self._call("propd_seq_advance", B, ptr(seq_slot), ptr(self.seq_len), None, 1, st)
+
+    def step_tree(self, states, tmpl: TreeTemplate, k: int, prune=None, trace: bool = False) -> StepOutput:
+        """One batched ProPD tree iteration on the device (engine.py:243-303):
+        K4a draft -> K1 tree embed -> layers 1..p -> K3 early prune + row
+        compaction -> layers p+1..Ly on survivors -> LM argmax -> K5 accept +
+        KV compaction -> bonus pass.  One mid-step sync (survivor count)."""
+        torch, st, cfg = self.torch, self.stream(), self.config
+        B, n, D, H, V = len(states), len(tmpl), cfg.draft_heads, self.H, self.V
+        if n > self.max_tree:
+            raise ValueError(f"tree of {n} nodes exceeds the backend's max_tree={self.max_tree}")
+        if tmpl.max_depth > D:
+            raise ValueError("tree deeper than the draft heads")
+        lens = [self._len[s.slot] for s in states]
+        if max(lens) + tmpl.max_depth + 1 > cfg.max_positions:
+            raise ValueError("sequence exceeds max_positions")
+        dev = self.device
+        td = tmpl.device(dev)
+        seq_slot = self._i32([s.slot for s in states])
+        draft_tok, _ = self._draft_dev(seq_slot, B, k)
+        M = B * n
+        i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
+        tokens, positions, row_seq, row_node, row_off = i32(M), i32(M), i32(M), i32(M), i32(B + 1)
+        x = torch.empty(M, H, device=dev, dtype=torch.float32)
+        self._call("propd_tree_embed", self.code, B, n, D, k, H, ptr(td["depth"]), ptr(td["rank"]), ptr(draft_tok),
+                   ptr(seq_slot), ptr(self.seq_len), ptr(self.w.emb), ptr(self.w.pos), ptr(tokens),
+                   ptr(positions), ptr(x), ptr(row_seq), ptr(row_node), ptr(row_off), st)
+        rt = Rows(M, B, seq_slot, row_seq, row_node, row_off, max_keys=max(lens) + n, max_rows=n,
+                  kv_keys=sum(lens) + B * n)
+        mask, W = td["mask"], tmpl.words
+        alive = node_row = None
+        surv_cnt = None
+        p = prune.layer if prune is not None else cfg.layers
+        pending = self._run_layers(x, rt, 0, p, mask, n, W)
+        if prune is not None:
+            self._flush(x, pending)
+            pending = None
+            Pn = len(tmpl.parent_nodes)
+            member = torch.ones(M, device=dev, dtype=torch.uint8)
+            if Pn > 0:
+                par_rows = (np.arange(B, dtype=np.int32)[:, None] * n + tmpl.parent_nodes[None, :]).reshape(-1)
+                xp = torch.empty(B * Pn, H, device=dev, dtype=self.tdtype)
+                self._call("propd_gather_rows", self.code, B * Pn, H, ptr(x), ptr(self._i32(par_rows)), ptr(xp), st)
+                early = torch.mm(xp, self.w.w_early)
+                if early.dtype != torch.float32:
+                    early = early.float()
+                self._call("propd_early_member", B, n, Pn, V, min(prune.topk, V), ptr(early), ptr(td["parent"]),
+                           ptr(td["parent_slot"]), ptr(tokens), ptr(member), st)
+            alive = torch.empty(M, device=dev, dtype=torch.uint8)
+            nrs, nrn, nsrc, node_row = i32(M), i32(M), i32(M), i32(M)
+            noff, surv_cnt, total = i32(B + 1), i32(B), i32(1)
+            self._call("propd_prune_compact", B, n, ptr(td["parent"]), ptr(member), ptr(alive), ptr(nrs), ptr(nrn),
+                       ptr(nsrc), ptr(noff), ptr(node_row), ptr(surv_cnt), ptr(total), st)
+            S = int(total.item())  # the one mid-step sync: row count of layers > p
+            x2 = torch.empty(S, H, device=dev, dtype=torch.float32)
+            self._call("propd_gather_rows", _lib.F32, S, H, ptr(x), ptr(nsrc), ptr(x2), st)
+            x = x2
+            rt = Rows(S, B, seq_slot, nrs, nrn, noff, max_keys=max(lens) + n, max_rows=n, kv_keys=sum(lens) + S)
+            pending = self._run_layers(x, rt, p, cfg.layers, mask, n, W)
+        S = rt.M
+        hfin = torch.empty(S, H, device=dev, dtype=self.tdtype)
+        self._call("propd_add_ln", self.code, S, H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
+        _, row_argmax = self._lm_argmax(hfin)
+        acc_node, acc_surv = i32(B * D), i32(B * D)
+        acc_len, bonus = i32(B), i32(B)
+        committed = i32(B * (D + 1))
+        ranks = torch.empty(B, D, device=dev, dtype=torch.int8)
+        root_before = self.root.index_select(0, seq_slot.long()) if trace else None
+        self._call("propd_verify_commit", self.code, B, n, D, k, cfg.layers, self.A, self.dh, self.Lmax,
+                   self.layer_stride, ptr(td["parent"]), ptr(tokens), ptr(alive), ptr(node_row), ptr(row_argmax),
+                   ptr(self.root), ptr(draft_tok), ptr(seq_slot), ptr(self.seq_len), ptr(self.kcache),
+                   ptr(self.vcache), ptr(acc_node), ptr(acc_surv), ptr(acc_len), ptr(bonus), ptr(committed),
+                   ptr(ranks), st)
+        self._bonus_pass(seq_slot, bonus, B, max(lens) + D + 1, sum(lens) + B)
+        out = StepOutput(committed.view(B, D + 1).cpu().numpy(), acc_len.cpu().numpy(),
+                         acc_surv.view(B, D).cpu().numpy(),
+                         surv_cnt.cpu().numpy() if surv_cnt is not None else np.full(B, n, dtype=np.int32),
+                         ranks)
+        for s, row, a in zip(states, out.committed, out.acc_len):
+            new = [int(t) for t in row[: a + 1]]
+            s.committed.extend(new)
+            self._len[s.slot] += len(new)
+        if trace:
+            out.trace = {"tokens": tokens.view(B, n).cpu().numpy(), "positions": positions.view(B, n).cpu().numpy(),
+                         "draft_tokens": draft_tok.cpu().numpy(), "root": root_before.cpu().numpy(),
+                         "alive": alive.view(B, n).cpu().numpy() if alive is not None else np.ones((B, n), np.uint8),
+                         "node_row": node_row.view(B, n).cpu().numpy() if node_row is not None else
+                         np.arange(M).reshape(B, n), "row_argmax": row_argmax.cpu().numpy()}
+        return out
+
+    def stats_replay_select(self, ranks_dev, S: int, P, counts, alpha, order, lcurve) -> None:
+        """K4 on device: ordered fp64 replay of acceptance records + grid
+        selection (acceptance.py:96-113, 186-206)."""
+        D, k = P.shape
+        self._call("propd_stats_replay_select", S, D, k, ptr(ranks_dev), float(alpha) if alpha is not None else -1.0,
+                   ptr(P), ptr(counts), ptr(order), ptr(lcurve), self.stream())

@@ -1,0 +1,426 @@
+// Row-level kernels of the tree pass: K1 tree materialisation + embedding,
+// residual/LN/GELU helpers, KV append, argmax and stable top-k.
+//
+// Reference semantics (paths relative to /root/reference/pkg/src/treedecode/):
+//   build_tree canonical order + positions  token_tree.py:125-170, engine.py:260
+//   x = emb[tok] + pos[pos]                 backends.py:315
+//   _ln / _gelu                              backends.py:135-142
+//   argmax (first max)                       backends.py:288, 333
+//   stable argsort top-k                     backends.py:282, 323
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+
+namespace propd {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string& msg) { g_error = msg; }
+
+int fail(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_error = buf;
+  return 1;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail("%s: %s", what, cudaGetErrorString(e));
+  return 0;
+}
+
+// ---------------------------------------------------------------- K1 ------
+template <typename T>
+__global__ void tree_embed_kernel(int n, int D, int kmax, int H, const int32_t* __restrict__ depth,
+                                  const int32_t* __restrict__ rank, const int32_t* __restrict__ draft_tok,
+                                  const int32_t* __restrict__ seq_slot, const int32_t* __restrict__ seq_len,
+                                  const T* __restrict__ emb, const T* __restrict__ pos,
+                                  int32_t* tokens, int32_t* positions, float* __restrict__ x,
+                                  int32_t* row_seq, int32_t* row_node, int32_t* row_off, int B) {
+  const int m = blockIdx.x;
+  const int b = m / n, i = m - b * n;
+  const int d = depth[i], r = rank[i];
+  const int tok = draft_tok[((size_t)b * D + (d - 1)) * kmax + (r - 1)];
+  const int p = seq_len[seq_slot[b]] + d - 1;
+  if (threadIdx.x == 0) {
+    tokens[m] = tok;
+    positions[m] = p;
+    row_seq[m] = b;
+    row_node[m] = i;
+    if (i == 0) row_off[b] = b * n;
+    if (m == 0) row_off[B] = B * n;
+  }
+  const T* e = emb + (size_t)tok * H;
+  const T* q = pos + (size_t)p * H;
+  float* o = x + (size_t)m * H;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) o[h] = to_f(e[h]) + to_f(q[h]);
+}
+
+template <typename T>
+__global__ void embed_rows_kernel(int H, const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
+                                  const T* __restrict__ emb, const T* __restrict__ pos, float* __restrict__ x) {
+  const int m = blockIdx.x;
+  const T* e = emb + (size_t)tokens[m] * H;
+  const T* q = pos + (size_t)positions[m] * H;
+  float* o = x + (size_t)m * H;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) o[h] = to_f(e[h]) + to_f(q[h]);
+}
+
+template <typename T>
+__global__ void bonus_embed_kernel(int B, int H, const int32_t* __restrict__ bonus,
+                                   const int32_t* __restrict__ seq_slot, const int32_t* __restrict__ seq_len,
+                                   const T* __restrict__ emb, const T* __restrict__ pos, float* __restrict__ x,
+                                   int32_t* positions, int32_t* row_seq, int32_t* row_node, int32_t* row_off) {
+  const int b = blockIdx.x;
+  const int p = seq_len[seq_slot[b]];
+  const int tok = bonus[b];
+  if (threadIdx.x == 0) {
+    positions[b] = p;
+    row_seq[b] = b;
+    row_node[b] = 0;
+    row_off[b] = b;
+    if (b == 0) row_off[B] = B;
+  }
+  const T* e = emb + (size_t)tok * H;
+  const T* q = pos + (size_t)p * H;
+  float* o = x + (size_t)b * H;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) o[h] = to_f(e[h]) + to_f(q[h]);
+}
+
+// ------------------------------------------------------------- dense ------
+// One CTA per row.  Two-pass mean/variance like numpy's x.var().
+template <typename T>
+__global__ void add_ln_kernel(int H, float* __restrict__ x, const T* __restrict__ delta, T* __restrict__ out,
+                              const int32_t* __restrict__ in_idx, const int32_t* __restrict__ out_idx) {
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  const int src = in_idx ? in_idx[m] : m;
+  const int dst = out_idx ? out_idx[m] : m;
+  float* xr = x + (size_t)src * H;
+  float s = 0.f;
+  if (delta) {
+    const T* dr = delta + (size_t)src * H;
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+      float v = xr[h] + to_f(dr[h]);
+      xr[h] = v;
+      s += v;
+    }
+  } else {
+    for (int h = threadIdx.x; h < H; h += blockDim.x) s += xr[h];
+  }
+  const float mu = block_sum(s, red) / (float)H;
+  float ss = 0.f;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    float c = xr[h] - mu;
+    ss += c * c;
+  }
+  const float var = block_sum(ss, red) / (float)H;
+  const float den = sqrtf(var + 1e-5f);
+  T* o = out + (size_t)dst * H;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) o[h] = from_f<T>((xr[h] - mu) / den);
+}
+
+template <typename T>
+__global__ void gelu_kernel(int64_t count, T* __restrict__ buf) {
+  const float c = 0.7978845608028654f;  // sqrt(2/pi)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    float v = to_f(buf[i]);
+    buf[i] = from_f<T>(0.5f * v * (1.f + tanhf(c * (v + 0.044715f * v * v * v))));
+  }
+}
+
+template <typename T>
+__global__ void residual_add_kernel(int64_t count, float* __restrict__ x, const T* __restrict__ d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] += to_f(d[i]);
+}
+
+template <typename T>
+__global__ void gather_rows_kernel(int H, const float* __restrict__ src, const int32_t* __restrict__ idx,
+                                   T* __restrict__ dst) {
+  const int m = blockIdx.x;
+  const float* s = src + (size_t)(idx ? idx[m] : m) * H;
+  T* d = dst + (size_t)m * H;
+  for (int h = threadIdx.x; h < H; h += blockDim.x) d[h] = from_f<T>(s[h]);
+}
+
+// First maximum per row (numpy argmax semantics).
+__global__ void argmax_rows_kernel(int V, int ld, const float* __restrict__ logits, int32_t* __restrict__ out) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const float* x = logits + (size_t)blockIdx.x * ld;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    float t = x[v];
+    if (t > best) { best = t; bi = v; }  // strided scan visits v in increasing order
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { sv[wid] = best; si[wid] = bi; }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    best = lane < nw ? sv[lane] : -INFINITY;
+    bi = lane < nw ? si[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) out[blockIdx.x] = bi;
+  }
+}
+
+// Stable descending top-k: radix select on the unique 64-bit key
+// (float_key(x) << 32) | ~index, then bitonic sort of the k winners.
+constexpr int TOPK_MAX = 1024;
+__global__ void __launch_bounds__(512) topk_rows_kernel(int V, int ld, int k, const float* __restrict__ logits,
+                                                          int32_t* __restrict__ out_idx, float* __restrict__ out_val) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long cand[TOPK_MAX];
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_shift, s_need, s_done, s_cnt;
+  const float* x = logits + (size_t)blockIdx.x * ld;
+  auto key_of = [&](int v) -> unsigned long long {
+    return ((unsigned long long)float_key(x[v]) << 32) | (unsigned long long)(0xffffffffu - (unsigned)v);
+  };
+  if (threadIdx.x == 0) { s_prefix = 0ull; s_need = k; s_done = 0; s_shift = 56; s_cnt = 0; }
+  __syncthreads();
+  for (int pass = 0; pass < 8; ++pass) {
+    const int shift = 56 - 8 * pass;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    const unsigned long long pre = s_prefix;
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+      unsigned long long kk = key_of(v);
+      if (pass == 0 || (kk >> (shift + 8)) == (pre >> (shift + 8))) atomicAdd(&hist[(kk >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int need = s_need;
+      unsigned cum = 0;
+      int bsel = 0;
+      for (int bkt = 255; bkt >= 0; --bkt) {
+        if (cum + hist[bkt] >= (unsigned)need) { bsel = bkt; break; }
+        cum += hist[bkt];
+      }
+      need -= (int)cum;  // still needed from bucket bsel
+      s_prefix = pre | ((unsigned long long)bsel << shift);
+      s_shift = shift;
+      s_need = need;
+      if (hist[bsel] == (unsigned)need) s_done = 1;
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+  // winners: top (64 - shift) bits >= prefix bits  (exactly k elements)
+  const int shift = s_shift;
+  const unsigned long long thr = s_prefix >> shift;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    unsigned long long kk = key_of(v);
+    if ((kk >> shift) >= thr) {
+      int p = atomicAdd(&s_cnt, 1);
+      if (p < TOPK_MAX) cand[p] = kk;
+    }
+  }
+  __syncthreads();
+  int P2 = 1;
+  while (P2 < k) P2 <<= 1;
+  for (int i = k + threadIdx.x; i < P2; i += blockDim.x) cand[i] = 0ull;
+  __syncthreads();
+  // bitonic sort, descending
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        int j = i ^ stride;
+        if (j > i) {
+          bool desc = ((i & size) == 0);
+          unsigned long long a = cand[i], c = cand[j];
+          if (desc ? (a < c) : (a > c)) { cand[i] = c; cand[j] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    int v = (int)(0xffffffffu - (unsigned)(cand[i] & 0xffffffffull));
+    out_idx[(size_t)blockIdx.x * k + i] = v;
+    if (out_val) out_val[(size_t)blockIdx.x * k + i] = x[v];
+  }
+}
+
+// ------------------------------------------------------------ KV cache ----
+template <typename T>
+__global__ void kv_append_kernel(int A, int dh, int Lmax, const T* __restrict__ qkv, int ld,
+                                 const int32_t* __restrict__ row_seq, const int32_t* __restrict__ row_node,
+                                 const int32_t* __restrict__ seq_slot, const int32_t* __restrict__ seq_len,
+                                 T* __restrict__ kc, T* __restrict__ vc) {
+  const int m = blockIdx.x;
+  const int b = row_seq[m];
+  const int slot = seq_slot[b];
+  const int t = seq_len[slot] + row_node[m];
+  const int H = A * dh;
+  const T* kr = qkv + (size_t)m * ld + H;
+  const T* vr = kr + H;
+  for (int e = threadIdx.x; e < H; e += blockDim.x) {
+    const int a = e / dh, d = e - a * dh;
+    const size_t off = (((size_t)slot * A + a) * Lmax + t) * dh + d;
+    kc[off] = kr[e];
+    vc[off] = vr[e];
+  }
+}
+
+__global__ void seq_advance_kernel(int B, const int32_t* seq_slot, int32_t* seq_len, const int32_t* delta_dev, int delta) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) seq_len[seq_slot[b]] += delta_dev ? delta_dev[b] : delta;
+}
+
+__global__ void scatter_i32_kernel(int B, const int32_t* idx, const int32_t* src, int32_t* dst) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) dst[idx[b]] = src[b];
+}
+
+static int threads_for(int H) {
+  int t = ((H + 31) / 32) * 32;
+  return t < 256 ? t : 256;
+}
+
+}  // namespace propd
+
+using namespace propd;
+
+extern "C" {
+
+const char* propd_last_error(void) { return g_error.c_str(); }
+int propd_abi_version(void) { return 1; }
+int propd_num_sms(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+  return n;
+}
+
+int propd_tree_embed(int dtype, int B, int n, int D, int kmax, int H, const int32_t* depth, const int32_t* rank,
+                     const int32_t* draft_tok, const int32_t* seq_slot, const int32_t* seq_len, const void* emb,
+                     const void* pos, int32_t* tokens, int32_t* positions, float* x, int32_t* row_seq,
+                     int32_t* row_node, int32_t* row_off, void* stream) {
+  PROPD_REQUIRE(B > 0 && n > 0 && H > 0, "tree_embed: empty batch/tree (B=%d n=%d H=%d)", B, n, H);
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    tree_embed_kernel<T><<<B * n, threads_for(H), 0, as_stream(stream)>>>(
+        n, D, kmax, H, depth, rank, draft_tok, seq_slot, seq_len, (const T*)emb, (const T*)pos, tokens, positions,
+        x, row_seq, row_node, row_off, B);
+    return check_launch("tree_embed");
+  });
+}
+
+int propd_embed_rows(int dtype, int M, int H, const int32_t* tokens, const int32_t* positions, const void* emb,
+                     const void* pos, float* x, void* stream) {
+  if (M == 0) return 0;
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    embed_rows_kernel<T><<<M, threads_for(H), 0, as_stream(stream)>>>(H, tokens, positions, (const T*)emb,
+                                                                        (const T*)pos, x);
+    return check_launch("embed_rows");
+  });
+}
+
+int propd_bonus_embed(int dtype, int B, int H, const int32_t* bonus, const int32_t* seq_slot, const int32_t* seq_len,
+                      const void* emb, const void* pos, float* x, int32_t* positions, int32_t* row_seq,
+                      int32_t* row_node, int32_t* row_off, void* stream) {
+  if (B == 0) return 0;
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    bonus_embed_kernel<T><<<B, threads_for(H), 0, as_stream(stream)>>>(B, H, bonus, seq_slot, seq_len, (const T*)emb,
+                                                                        (const T*)pos, x, positions, row_seq,
+                                                                        row_node, row_off);
+    return check_launch("bonus_embed");
+  });
+}
+
+int propd_add_ln(int dtype, int M, int H, float* x, const void* delta, void* out, const int32_t* in_idx,
+                 const int32_t* out_idx, void* stream) {
+  if (M == 0) return 0;
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    add_ln_kernel<T><<<M, threads_for(H), 0, as_stream(stream)>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx);
+    return check_launch("add_ln");
+  });
+}
+
+int propd_gelu(int dtype, int64_t count, void* buf, void* stream) {
+  if (count == 0) return 0;
+  int blocks = (int)((count + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    gelu_kernel<T><<<blocks, 256, 0, as_stream(stream)>>>(count, (T*)buf);
+    return check_launch("gelu");
+  });
+}
+
+int propd_residual_add(int dtype, int64_t count, float* x, const void* delta, void* stream) {
+  if (count == 0) return 0;
+  int blocks = (int)((count + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    residual_add_kernel<T><<<blocks, 256, 0, as_stream(stream)>>>(count, x, (const T*)delta);
+    return check_launch("residual_add");
+  });
+}
+
+int propd_gather_rows(int dtype, int M, int H, const float* src, const int32_t* idx, void* dst, void* stream) {
+  if (M == 0) return 0;
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    gather_rows_kernel<T><<<M, threads_for(H), 0, as_stream(stream)>>>(H, src, idx, (T*)dst);
+    return check_launch("gather_rows");
+  });
+}
+
+int propd_argmax_rows(int M, int V, int ld, const float* logits, int32_t* out, void* stream) {
+  if (M == 0) return 0;
+  PROPD_REQUIRE(V > 0 && ld >= V, "argmax_rows: bad V=%d ld=%d", V, ld);
+  argmax_rows_kernel<<<M, 256, 0, as_stream(stream)>>>(V, ld, logits, out);
+  return check_launch("argmax_rows");
+}
+
+int propd_topk_rows(int R, int V, int ld, int k, const float* logits, int32_t* out_idx, float* out_val, void* stream) {
+  if (R == 0) return 0;
+  PROPD_REQUIRE(k >= 1 && k <= TOPK_MAX && k <= V, "topk_rows: k=%d outside 1..min(%d, V=%d)", k, TOPK_MAX, V);
+  topk_rows_kernel<<<R, 512, 0, as_stream(stream)>>>(V, ld, k, logits, out_idx, out_val);
+  return check_launch("topk_rows");
+}
+
+int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, int ldqkv, const int32_t* row_seq,
+                    const int32_t* row_node, const int32_t* seq_slot, const int32_t* seq_len, void* kcache,
+                    void* vcache, void* stream) {
+  if (M == 0) return 0;
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    kv_append_kernel<T><<<M, threads_for(A * dh), 0, as_stream(stream)>>>(
+        A, dh, Lmax, (const T*)qkv, ldqkv, row_seq, row_node, seq_slot, seq_len, (T*)kcache, (T*)vcache);
+    return check_launch("kv_append");
+  });
+}
+
+int propd_seq_advance(int B, const int32_t* seq_slot, int32_t* seq_len, const int32_t* delta_dev, int delta,
+                      void* stream) {
+  if (B == 0) return 0;
+  seq_advance_kernel<<<(B + 127) / 128, 128, 0, as_stream(stream)>>>(B, seq_slot, seq_len, delta_dev, delta);
+  return check_launch("seq_advance");
+}
+
+int propd_scatter_i32(int B, const int32_t* idx, const int32_t* src, int32_t* dst, void* stream) {
+  if (B == 0) return 0;
+  scatter_i32_kernel<<<(B + 127) / 128, 128, 0, as_stream(stream)>>>(B, idx, src, dst);
+  return check_launch("scatter_i32");
+}
+
+}  // extern "C"

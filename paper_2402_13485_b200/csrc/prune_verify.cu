@@ -1,0 +1,355 @@
+// K3 early prune, K5 greedy accept + in-place KV compaction, K4 acceptance
+// statistics replay + grid node selection.
+//
+// Reference semantics (paths relative to /root/reference/pkg/src/treedecode/):
+//   prune: depth-1 exempt, child alive iff parent alive and token in the
+//          parent's early top-K (stable argsort)      pruning.py:40-66, backends.py:320-323
+//   verify: greedy root-chain walk, bonus = last target verification.py:30-53
+//   commit: accepted rows + bonus join the context    backends.py:337-348 (the
+//          recompute is replaced by compaction of the tree-pass K/V rows; the
+//          two are bit-identical in the reference)
+//   stats update / marginals / selection             acceptance.py:96-117, 186-206
+//   realized ranks per depth                          engine.py:283-288, acceptance.py:53-57
+#include "common.cuh"
+
+namespace propd {
+
+// ---------------------------------------------------------------- K3 ------
+// One CTA per (sequence, node).  Counting rank: number of vocabulary entries
+// that a stable descending argsort would place before the child's token.
+__global__ void early_member_kernel(int n, int P, int V, int topk, const float* __restrict__ early,
+                                    const int32_t* __restrict__ parent, const int32_t* __restrict__ parent_slot,
+                                    const int32_t* __restrict__ tokens, uint8_t* __restrict__ member) {
+  __shared__ int red[32];
+  const int m = blockIdx.x;
+  const int b = m / n, i = m - b * n;
+  const int par = parent[i];
+  if (par < 0) {
+    if (threadIdx.x == 0) member[m] = 1;
+    return;
+  }
+  const float* row = early + ((size_t)b * P + parent_slot[par]) * V;
+  const int t = tokens[m];
+  const float target = row[t];
+  int cnt = 0;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    const float x = row[v];
+    cnt += (x > target) || (x == target && v < t);
+  }
+  cnt = warp_isum(cnt);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = cnt;
+  __syncthreads();
+  if (wid == 0) {
+    int c = lane < (int)(blockDim.x >> 5) ? red[lane] : 0;
+    c = warp_isum(c);
+    if (lane == 0) member[m] = c < topk ? 1 : 0;
+  }
+}
+
+// Single CTA: closure per sequence, block-wide exclusive scan of survivor
+// counts, scatter of the compacted row tables.
+__global__ void prune_compact_kernel(int B, int n, const int32_t* __restrict__ parent,
+                                     const uint8_t* __restrict__ member, uint8_t* __restrict__ alive,
+                                     int32_t* new_row_seq, int32_t* new_row_node, int32_t* new_row_src,
+                                     int32_t* new_row_off, int32_t* node_row, int32_t* surv_cnt, int32_t* total) {
+  __shared__ int scan[1024];
+  const int b = threadIdx.x;
+  int cnt = 0;
+  if (b < B) {
+    for (int i = 0; i < n; ++i) {
+      const int par = parent[i];
+      const bool ok = member[b * n + i] && (par < 0 || alive[b * n + par]);
+      alive[b * n + i] = ok;
+      cnt += ok;
+    }
+  }
+  scan[threadIdx.x] = cnt;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // Hillis-Steele inclusive scan
+    int v = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
+    __syncthreads();
+    scan[threadIdx.x] += v;
+    __syncthreads();
+  }
+  if (b < B) {
+    int o = scan[b] - cnt;
+    new_row_off[b] = o;
+    surv_cnt[b] = cnt;
+    for (int i = 0; i < n; ++i) {
+      if (alive[b * n + i]) {
+        new_row_seq[o] = b;
+        new_row_node[o] = i;
+        new_row_src[o] = b * n + i;
+        node_row[b * n + i] = o++;
+      } else {
+        node_row[b * n + i] = -1;
+      }
+    }
+    if (b == B - 1) {
+      new_row_off[B] = o;
+      *total = o;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K5 ------
+constexpr int MAX_D = 32;
+
+// Moves accepted rows j (slot L + node[j]) to L + j for every layer/head.
+// Each thread owns a fixed 16-byte column chunk of one (layer, head) block and
+// walks j upward; since node[j] >= j and node is increasing, dst L+j never
+// aliases a source still to be read (read-before-write per element).
+template <typename T>
+__device__ void compact_rows(int len, const int* acc, int slot, int L, int layers, int A, int dh, int Lmax,
+                             int64_t layer_stride, T* kc, T* vc) {
+  if (len == 0) return;
+  constexpr int VEC = 16 / sizeof(T);
+  const int chunks = dh / VEC;
+  const int items = layers * A * chunks;
+  for (int w = threadIdx.x; w < items; w += blockDim.x) {
+    const int c = w % chunks;
+    const int la = w / chunks;
+    const int a = la % A, l = la / A;
+    const size_t base = (size_t)l * layer_stride + ((size_t)slot * A + a) * Lmax * dh + (size_t)c * VEC;
+    for (int j = 0; j < len; ++j) {
+      const int src = acc[j];
+      if (src == j) continue;
+      const size_t so = base + (size_t)(L + src) * dh, dof = base + (size_t)(L + j) * dh;
+      *reinterpret_cast<uint4*>(kc + dof) = *reinterpret_cast<const uint4*>(kc + so);
+      *reinterpret_cast<uint4*>(vc + dof) = *reinterpret_cast<const uint4*>(vc + so);
+    }
+  }
+}
+
+template <typename T>
+__global__ void verify_commit_kernel(int n, int D, int kmax, int layers, int A, int dh, int Lmax, int64_t layer_stride,
+                                     const int32_t* __restrict__ parent, const int32_t* __restrict__ tokens,
+                                     const uint8_t* __restrict__ alive, const int32_t* __restrict__ node_row,
+                                     const int32_t* __restrict__ row_argmax, const int32_t* __restrict__ root,
+                                     const int32_t* __restrict__ draft_tok, const int32_t* __restrict__ seq_slot,
+                                     int32_t* seq_len, T* kc, T* vc, int32_t* acc_node, int32_t* acc_surv,
+                                     int32_t* acc_len, int32_t* bonus, int32_t* committed, int8_t* ranks) {
+  __shared__ int s_acc[MAX_D];
+  __shared__ int s_len, s_L;
+  const int b = blockIdx.x;
+  const int slot = seq_slot[b];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    const int L = seq_len[slot];
+    int target = root[slot];
+    int cur = -1, len = 0;
+    for (int step = 0; step < D; ++step) {
+      int found = -1;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < n && parent[i] == cur && (alive == nullptr || alive[b * n + i]) &&
+                        tokens[b * n + i] == target;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (bal) { found = base + __ffs(bal) - 1; break; }
+      }
+      if (found < 0) break;
+      if (lane == 0) s_acc[len] = found;
+      const int row = node_row ? node_row[b * n + found] : b * n + found;
+      target = row_argmax[row];
+      cur = found;
+      ++len;
+    }
+    __syncwarp();
+    // survivor-row index of each accepted node = #alive nodes before it
+    for (int j = 0; j < len; ++j) {
+      const int node = s_acc[j];
+      int cnt = 0;
+      for (int base = 0; base < node; base += 32) {
+        const int i = base + lane;
+        const bool ok = i < node && (alive == nullptr || alive[b * n + i]);
+        cnt += __popc(__ballot_sync(0xffffffffu, ok));
+      }
+      if (lane == 0) {
+        acc_node[b * D + j] = node;
+        acc_surv[b * D + j] = cnt;
+      }
+    }
+    if (lane == 0) {
+      for (int j = len; j < D; ++j) { acc_node[b * D + j] = -1; acc_surv[b * D + j] = -1; }
+      s_len = len;
+      s_L = L;
+      acc_len[b] = len;
+      bonus[b] = target;
+      int32_t* cm = committed + (size_t)b * (D + 1);
+      for (int j = 0; j < len; ++j) cm[j] = tokens[b * n + s_acc[j]];
+      cm[len] = target;
+      for (int j = len + 1; j <= D; ++j) cm[j] = -1;
+      // acceptance record: realized[d] = newly[d-1], d <= min(len+1, D)
+      for (int d = 0; d < D; ++d) {
+        int8_t r = 0;
+        if (d <= len) {
+          const int tok = cm[d];
+          const int32_t* lst = draft_tok + ((size_t)b * D + d) * kmax;
+          r = -1;
+          for (int k = 0; k < kmax; ++k)
+            if (lst[k] == tok) { r = (int8_t)(k + 1); break; }
+        }
+        ranks[(size_t)b * D + d] = r;
+      }
+    }
+  }
+  __syncthreads();
+  compact_rows<T>(s_len, s_acc, slot, s_L, layers, A, dh, Lmax, layer_stride, kc, vc);
+  __syncthreads();
+  if (threadIdx.x == 0) seq_len[slot] = s_L + s_len;
+}
+
+template <typename T>
+__global__ void kv_compact_kernel(int D, int layers, int A, int dh, int Lmax, int64_t layer_stride,
+                                  const int32_t* seq_slot, int32_t* seq_len, const int32_t* acc_node,
+                                  const int32_t* acc_len, T* kc, T* vc) {
+  __shared__ int s_acc[MAX_D];
+  __shared__ int s_L;
+  const int b = blockIdx.x;
+  const int slot = seq_slot[b];
+  const int len = acc_len[b];
+  if (threadIdx.x < len) s_acc[threadIdx.x] = acc_node[b * D + threadIdx.x];
+  if (threadIdx.x == 0) s_L = seq_len[slot];
+  __syncthreads();
+  compact_rows<T>(len, s_acc, slot, s_L, layers, A, dh, Lmax, layer_stride, kc, vc);
+  __syncthreads();
+  if (threadIdx.x == 0) seq_len[slot] = s_L + len;
+}
+
+// ---------------------------------------------------------------- K4 ------
+// fp64 with explicit round-to-nearest intrinsics: no FMA contraction, so the
+// results are bit-identical to numpy's separate multiply and add.
+__global__ void stats_replay_select_kernel(int S, int D, int k, const int8_t* __restrict__ ranks, double alpha,
+                                           double* P, int64_t* counts, int32_t* order, double* lcurve) {
+  extern __shared__ double sm[];
+  double* Ps = sm;               // D*k
+  double* contrib = sm + D * k;  // D*k
+  double* spine = contrib + D * k;  // D+1
+  __shared__ long long cnt_s[MAX_D];
+  const int N = D * k;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) Ps[i] = P[i];
+  if (threadIdx.x < D) cnt_s[threadIdx.x] = counts[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int s = 0; s < S; ++s) {
+      for (int d = 0; d < D; ++d) {
+        const int r = ranks[(size_t)s * D + d];
+        if (r == 0) continue;
+        const long long c = cnt_s[d] + 1;
+        __syncwarp();
+        if (lane == 0) cnt_s[d] = c;
+        const double step = alpha > 0.0 ? alpha : __ddiv_rn(1.0, (double)c);
+        const double keep = __dsub_rn(1.0, step);
+        for (int j = lane; j < k; j += 32) {
+          const double hit = (r > 0 && j >= r - 1) ? 1.0 : 0.0;
+          Ps[d * k + j] = __dadd_rn(__dmul_rn(keep, Ps[d * k + j]), __dmul_rn(step, hit));
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < N; i += blockDim.x) P[i] = Ps[i];
+  if (threadIdx.x < D) counts[threadIdx.x] = cnt_s[threadIdx.x];
+  if (threadIdx.x == 0) {
+    spine[0] = 1.0;
+    for (int d = 0; d < D; ++d) spine[d + 1] = __dmul_rn(spine[d], __dsub_rn(Ps[d * k], 0.0));
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    const int d = c / k, r = c - d * k;
+    const double m = __dsub_rn(Ps[c], r > 0 ? Ps[c - 1] : 0.0);
+    contrib[c] = __dmul_rn(spine[d], m);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < N; c += blockDim.x) {
+    const double v = contrib[c];
+    int pos = 0;
+    for (int c2 = 0; c2 < N; ++c2) {
+      const double w = contrib[c2];
+      pos += (w > v) || (w == v && c2 < c);
+    }
+    order[pos] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int s = 0; s < N; ++s) {
+      acc = __dadd_rn(acc, contrib[order[s]]);
+      lcurve[s] = acc;
+    }
+  }
+}
+
+}  // namespace propd
+
+using namespace propd;
+
+extern "C" {
+
+int propd_early_member(int B, int n, int P, int V, int topk, const float* early_logits, const int32_t* parent,
+                       const int32_t* parent_slot, const int32_t* tokens, uint8_t* member, void* stream) {
+  if (B == 0 || n == 0) return 0;
+  PROPD_REQUIRE(topk >= 1, "early_member: topk must be positive");
+  early_member_kernel<<<B * n, 256, 0, as_stream(stream)>>>(n, P, V, topk, early_logits, parent, parent_slot, tokens,
+                                                            member);
+  return check_launch("early_member");
+}
+
+int propd_prune_compact(int B, int n, const int32_t* parent, const uint8_t* member, uint8_t* alive,
+                        int32_t* new_row_seq, int32_t* new_row_node, int32_t* new_row_src, int32_t* new_row_off,
+                        int32_t* node_row, int32_t* surv_cnt, int32_t* total, void* stream) {
+  if (B == 0) return 0;
+  PROPD_REQUIRE(B <= 1024, "prune_compact: batch %d > 1024", B);
+  int threads = ((B + 31) / 32) * 32;
+  prune_compact_kernel<<<1, threads, 0, as_stream(stream)>>>(B, n, parent, member, alive, new_row_seq, new_row_node,
+                                                             new_row_src, new_row_off, node_row, surv_cnt, total);
+  return check_launch("prune_compact");
+}
+
+int propd_verify_commit(int dtype, int B, int n, int D, int kmax, int layers, int A, int dh, int Lmax,
+                        int64_t layer_stride, const int32_t* parent, const int32_t* tokens, const uint8_t* alive,
+                        const int32_t* node_row, const int32_t* row_argmax, const int32_t* root,
+                        const int32_t* draft_tok, const int32_t* seq_slot, int32_t* seq_len, void* kcache,
+                        void* vcache, int32_t* acc_node, int32_t* acc_surv, int32_t* acc_len, int32_t* bonus,
+                        int32_t* committed, int8_t* ranks, void* stream) {
+  if (B == 0) return 0;
+  PROPD_REQUIRE(D >= 1 && D <= MAX_D, "verify_commit: D=%d outside 1..%d", D, MAX_D);
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    PROPD_REQUIRE((dh * (int)sizeof(T)) % 16 == 0, "verify_commit: dh*sizeof must be a multiple of 16");
+    verify_commit_kernel<T><<<B, 256, 0, as_stream(stream)>>>(
+        n, D, kmax, layers, A, dh, Lmax, layer_stride, parent, tokens, alive, node_row, row_argmax, root, draft_tok,
+        seq_slot, seq_len, (T*)kcache, (T*)vcache, acc_node, acc_surv, acc_len, bonus, committed, ranks);
+    return check_launch("verify_commit");
+  });
+}
+
+int propd_kv_compact(int dtype, int B, int D, int layers, int A, int dh, int Lmax, int64_t layer_stride,
+                     const int32_t* seq_slot, int32_t* seq_len, const int32_t* acc_node, const int32_t* acc_len,
+                     void* kcache, void* vcache, void* stream) {
+  if (B == 0) return 0;
+  PROPD_REQUIRE(D >= 1 && D <= MAX_D, "kv_compact: D=%d outside 1..%d", D, MAX_D);
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    PROPD_REQUIRE((dh * (int)sizeof(T)) % 16 == 0, "kv_compact: dh*sizeof must be a multiple of 16");
+    kv_compact_kernel<T><<<B, 256, 0, as_stream(stream)>>>(D, layers, A, dh, Lmax, layer_stride, seq_slot, seq_len,
+                                                           acc_node, acc_len, (T*)kcache, (T*)vcache);
+    return check_launch("kv_compact");
+  });
+}
+
+int propd_stats_replay_select(int S, int D, int k, const int8_t* ranks, double alpha, double* P, int64_t* counts,
+                              int32_t* order, double* lcurve, void* stream) {
+  PROPD_REQUIRE(D >= 1 && D <= MAX_D && k >= 1 && D * k <= 4096, "stats_replay_select: bad grid D=%d k=%d", D, k);
+  const size_t smem = (size_t)(2 * D * k + D + 1) * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(stats_replay_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return fail("stats_replay_select: %s", cudaGetErrorString(e));
+  }
+  stats_replay_select_kernel<<<1, 256, smem, as_stream(stream)>>>(S, D, k, ranks, alpha, P, counts, order, lcurve);
+  return check_launch("stats_replay_select");
+}
+
+}  // extern "C"

@@ -1,0 +1,208 @@
+"""End-to-end parity of the B200 decode path (fp32 parity mode) with the
+reference, through golden fixtures of the real reference and the CPU oracle.
+
+Bar: bit-exact transcripts, per-iteration metrics (simulated clock), plan
+events, tree tokens/positions, survivor sets, accepted indices, bonus tokens
+and the fp64 acceptance statistics; logits within
+  max |err| <= 2e-5 * max(1, |ref|_inf)   (fp32 vs the reference's fp64).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import treedecode_port as op  # noqa: E402
+from paper_2402_13485_b200 import (B200Backend, DecodeEngine, EngineConfig, PruneConfig,  # noqa: E402
+                                   SchedulerConfig, TinyTransformerConfig)
+from paper_2402_13485_b200.tree import TreeTemplate  # noqa: E402
+
+MODES = op.MODES
+RUN_TINY = op.RUN_TINY
+
+
+def load(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as fh:
+        return json.load(fh)
+
+
+def product_cfg(ecfg: op.EngineCfg, mode: str) -> EngineConfig:
+    s = ecfg.scheduler
+    return EngineConfig(mode=mode, draft_heads=ecfg.draft_heads, draft_topk=ecfg.draft_topk,
+                        prune=PruneConfig(ecfg.prune.layer, ecfg.prune.topk) if ecfg.prune else None,
+                        scheduler=SchedulerConfig(s.resize_batch_delta, s.resize_seqlen_delta, s.replan_period,
+                                                  s.size_candidates),
+                        acceptance_alpha=ecfg.acceptance_alpha)
+
+
+def tiny_backend(mc: op.TinyCfg, slots=8, **kw):
+    return B200Backend(TinyTransformerConfig(**mc.__dict__), dtype="fp32", max_slots=slots, **kw)
+
+
+@pytest.fixture(scope="module")
+def run_tiny_backend():
+    return tiny_backend(RUN_TINY["model"])
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_run_tiny_batched_engine_matches_reference(golden_dir, run_tiny_backend, mode):
+    g = load(golden_dir, f"run_tiny_{mode}.json")
+    eng = DecodeEngine(run_tiny_backend, product_cfg(RUN_TINY["engine"], mode), op.Clock(**RUN_TINY["clock"]))
+    w = RUN_TINY["workload"]
+    res = eng.run(g["prompts"], w["max_tokens"], batch_size=w["batch_size"])
+    assert res.transcripts == g["transcripts"]
+    assert [json.dumps(m.to_json()) for m in res.metrics] == [json.dumps(m) for m in g["metrics"]]
+    s = res.summary
+    assert {k: getattr(s, k) for k in g["summary"]} == g["summary"]
+    ev = [{"iteration": e.iteration, "trigger": e.trigger, "chosen_size": e.chosen_size,
+           "l_curve": {str(k): v for k, v in e.l_curve.items()},
+           "v_curve": {str(k): v for k, v in e.v_curve.items()}} for e in res.plan_events]
+    assert ev == g["plan_events"]
+    if mode != "autoregressive":
+        assert np.array_equal(eng.stats_P, np.array(g["final_P"]))
+
+
+def test_step_records_match_reference_trace(golden_dir, run_tiny_backend):
+    g = load(golden_dir, "run_tiny_trace.json")["records"]
+    mine = []
+    eng = DecodeEngine(run_tiny_backend, product_cfg(RUN_TINY["engine"], "propd_full"),
+                       op.Clock(**RUN_TINY["clock"]), trace=lambda it, rec: mine.append(rec))
+    w = RUN_TINY["workload"]
+    prompts = op.synthetic_prompts(256, w["num_prompts"], w["prompt_len"], w["seed"])
+    eng.run(prompts, w["max_tokens"], batch_size=w["batch_size"])
+    assert len(mine) == len(g)
+    for a, b in zip(mine, g):
+        for key in ("tokens", "positions", "draft_tokens", "root", "survivors", "argmax", "accepted", "bonus"):
+            assert a[key] == b[key], key
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_per_sequence_plugin_api_in_reference_loop(golden_dir, mode):
+    """The oracle's restatement of the reference DecodeEngine driving
+    B200Backend through the per-sequence ModelBackend API (drop-in path)."""
+    g = load(golden_dir, f"run_tiny_{mode}.json")
+    be = tiny_backend(RUN_TINY["model"], slots=12)
+    ecfg = op.EngineCfg(**{**RUN_TINY["engine"].__dict__, "mode": mode})
+    eng = op.Engine(be, ecfg, op.Clock(**RUN_TINY["clock"]))
+    w = RUN_TINY["workload"]
+    res = eng.run(g["prompts"], w["max_tokens"], batch_size=w["batch_size"])
+    assert res["transcripts"] == g["transcripts"]
+    assert [json.dumps(m) for m in res["metrics"]] == [json.dumps(m) for m in g["metrics"]]
+
+
+def test_c1_losslessness_all_tree_modes(golden_dir):
+    """Acceptance-gate C1 (tests/test_acceptance.py:77-121): every tree mode
+    emits the greedy AR stream, 200 prompts, batch 25."""
+    g = load(golden_dir, "c1_ar.json")
+    mc = op.TinyCfg(layers=4, hidden=64, heads=4, vocab=256, draft_heads=4, max_positions=64, seed=17)
+    be = tiny_backend(mc, slots=32)
+    sched = SchedulerConfig(replan_period=8, size_candidates=(1, 2, 4, 6, 8))
+    for mode in ("autoregressive", "static_tree", "prune_only", "dynamic_only", "propd_full"):
+        cfg = EngineConfig(mode=mode, draft_heads=4, draft_topk=3, scheduler=sched, acceptance_alpha=None,
+                           prune=PruneConfig(layer=2, topk=16) if mode in ("prune_only", "propd_full") else None)
+        res = DecodeEngine(be, cfg, op.Clock()).run(g["prompts"], g["max_tokens"], batch_size=25)
+        assert res.transcripts == g["transcripts"], mode
+
+
+def test_forward_tree_logits_and_early_lists(golden_dir):
+    meta = load(golden_dir, "forward_cases.json")
+    arr = np.load(os.path.join(golden_dir, "forward_cases.npz"))
+    backends = {}
+    for m in meta:
+        key = m["key"]
+        tag = key.split("_")[0]
+        if tag not in backends:
+            backends[tag] = tiny_backend(op.TinyCfg(**m["model"]), slots=4)
+        be = backends[tag]
+        st = be.prefill(arr[key + "_ctx"].tolist())
+        ref_last = arr[key + "_last_logits"]
+        assert np.abs(be.last_logits_of(st) - ref_last).max() <= 2e-5 * max(1.0, np.abs(ref_last).max())
+        surv = arr[key + "_survivors"].tolist()
+        kw = {}
+        box = {}
+        if m["prune_layer"] is not None:
+            def cb(lists, _s=surv, _b=box):
+                _b["lists"] = lists
+                return _s
+            kw = dict(prune_layer=m["prune_layer"], early_topk=5, prune_callback=cb)
+        fwd = be.forward_tree(st, arr[key + "_tokens"], arr[key + "_positions"], arr[key + "_mask"], **kw)
+        ref = arr[key + "_logits"]
+        assert list(fwd.survivors) == surv
+        assert np.abs(fwd.logits - ref).max() <= 2e-5 * max(1.0, np.abs(ref).max())
+        assert np.array_equal(fwd.argmax, np.argmax(ref, axis=1))
+        if kw:
+            assert np.array_equal(np.asarray(box["lists"]), arr[key + "_early"])
+
+
+def test_plugin_api_errors_match_reference():
+    be = tiny_backend(op.TinyCfg(layers=3, hidden=32, heads=2, vocab=64, draft_heads=3, max_positions=96, seed=5),
+                      slots=4)
+    with pytest.raises(ValueError, match="non-empty"):
+        be.prefill([])
+    with pytest.raises(ValueError, match="vocabulary"):
+        be.prefill([0, 64])
+    with pytest.raises(ValueError, match="max_positions"):
+        be.prefill([0] * 97)
+    st = be.prefill([3, 1, 4, 1])
+    tmpl = TreeTemplate.from_paths([(1,), (2,), (1, 1)])
+    toks = np.array([7, 9, 11])
+    pos = 4 + tmpl.depth - 1
+    mask = tmpl.mask()
+    with pytest.raises(ValueError, match="sizes disagree"):
+        be.forward_tree(st, toks, pos, mask[:-1])
+    with pytest.raises(ValueError, match="follow the committed context"):
+        be.forward_tree(st, toks, pos - 4, mask)
+    with pytest.raises(ValueError, match="vocabulary"):
+        be.forward_tree(st, toks + 64, pos, mask)
+    cb = lambda lists: list(range(len(lists)))
+    with pytest.raises(ValueError, match="strictly inside"):
+        be.forward_tree(st, toks, pos, mask, prune_layer=3, early_topk=4, prune_callback=cb)
+    with pytest.raises(ValueError, match="early_topk"):
+        be.forward_tree(st, toks, pos, mask, prune_layer=1, early_topk=0, prune_callback=cb)
+    with pytest.raises(ValueError, match="preceding tree forward"):
+        be.commit(be.prefill([1, 2]), [0], 5)
+    be.forward_tree(st, toks, pos, mask)
+    with pytest.raises(ValueError, match="contiguous root chain"):
+        be.commit(st, [0, 1], 0)
+    be.commit(st, [0, 2], 42)
+    assert st.committed == [3, 1, 4, 1, 7, 11, 42]
+    fresh = be.prefill(st.committed)
+    a, b = be.last_logits_of(st), be.last_logits_of(fresh)
+    assert np.abs(a - b).max() <= 2e-5 * max(1.0, np.abs(b).max())
+    with pytest.raises(ValueError):
+        be.draft(st, 0)
+
+
+def test_commit_equals_scratch_prefill_and_oracle():
+    """commit (KV compaction) == scratch prefill == the fp64 oracle (tests/test_backends.py:140-155)."""
+    mc = op.TinyCfg(layers=3, hidden=32, heads=2, vocab=64, draft_heads=3, max_positions=96, seed=5)
+    be = tiny_backend(mc, slots=6)
+    ref = op.TinyModel(mc)
+    ctx = [3, 1, 4, 1, 5]
+    st, rs = be.prefill(ctx), ref.prefill(ctx)
+    rng = np.random.default_rng(0)
+    for _ in range(6):
+        pred = ref.draft(rs, 2)
+        tree = op.build_tree(pred, op.complete_tree_paths(3, 2), root_token=0)
+        mask = op.make_mask(tree)
+        pos = rs.length + tree.depths - 1
+        f1 = be.forward_tree(st, tree.tokens, pos, mask)
+        f0 = ref.forward_tree(rs, tree.tokens, pos, mask)
+        assert np.array_equal(f1.argmax, f0.argmax)
+        acc, bonus = op.verify(tree, f0.argmax, ref.next_argmax(rs))
+        if not acc and rng.random() < 0.7:  # force an accepted chain to exercise compaction
+            acc = (0, 1)
+            bonus = int(f0.argmax[1])
+        be.commit(st, list(acc), bonus)
+        ref.commit(rs, list(acc), bonus)
+        assert st.committed == rs.committed
+        assert np.abs(be.last_logits_of(st) - rs.last_logits).max() <= 2e-5 * max(1.0, np.abs(rs.last_logits).max())
+        assert be.next_argmax(st) == ref.next_argmax(rs)
+        d1, d0 = be.draft(st, 2), ref.draft(rs, 2)
+        assert np.array_equal(d1.tokens, d0.tokens)

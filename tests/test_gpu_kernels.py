@@ -1,0 +1,334 @@
+"""Kernel-level parity of libpropd against numpy / torch fp32 references.
+
+Integer and selection kernels must be bit-exact; attention is compared with
+a plain torch fp32 implementation of the reference's masked softmax
+attention (backends.py:216-233) at a stated tolerance:
+  fp32 KV:  max |err| <= 2e-5 * max(1, |ref|_inf)
+  bf16 KV:  max |err| <= 2e-2 * max(1, |ref|_inf)   (inputs rounded to bf16 first)
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import treedecode_port as op  # noqa: E402
+from paper_2402_13485_b200 import _lib  # noqa: E402
+from paper_2402_13485_b200._lib import call, ptr  # noqa: E402
+from paper_2402_13485_b200.tree import TreeTemplate  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def st():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def i32(a):
+    return torch.tensor(np.asarray(a, dtype=np.int32), device=DEV)
+
+
+# --------------------------------------------------------------- top-k / argmax
+@pytest.mark.parametrize("V,k", [(256, 3), (256, 24), (32000, 64), (32000, 1), (1000, 1000), (64, 64)])
+def test_topk_matches_stable_argsort(V, k):
+    rng = np.random.default_rng(V + k)
+    x = rng.normal(size=(7, V)).astype(np.float32)
+    x[1, : V // 2] = 0.0  # massive ties
+    x[2] = np.round(x[2] * 4) / 4  # coarse ties
+    x[3, 5] = -0.0
+    x[3, 6] = 0.0
+    dx = torch.from_numpy(x).to(DEV)
+    idx = torch.empty(7, k, dtype=torch.int32, device=DEV)
+    val = torch.empty(7, k, dtype=torch.float32, device=DEV)
+    call("propd_topk_rows", 7, V, V, k, ptr(dx), ptr(idx), ptr(val), st())
+    ref = np.argsort(-x, axis=1, kind="stable")[:, :k]
+    assert np.array_equal(idx.cpu().numpy(), ref)
+    assert np.array_equal(val.cpu().numpy(), np.take_along_axis(x, ref, axis=1))
+
+
+def test_argmax_first_max():
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(9, 32000)).astype(np.float32)
+    x[0, [5, 77, 31999]] = 100.0
+    x[1] = 0.0
+    dx = torch.from_numpy(x).to(DEV)
+    out = torch.empty(9, dtype=torch.int32, device=DEV)
+    call("propd_argmax_rows", 9, 32000, 32000, ptr(dx), ptr(out), st())
+    assert np.array_equal(out.cpu().numpy(), np.argmax(x, axis=1))
+
+
+# --------------------------------------------------------------- attention
+def torch_tree_attention(q, kc, vc, slots, lens, row_off, row_node, mask_bool, A, dh):
+    """Plain fp32 reference: for each row, softmax over cache keys [0,L) and
+    visible tree keys L+j, scaled by 1/sqrt(dh) (backends.py:227-233)."""
+    M = q.shape[0]
+    out = torch.zeros(M, A * dh, dtype=torch.float32, device=q.device)
+    B = len(slots)
+    for b in range(B):
+        L = lens[b]
+        for m in range(row_off[b], row_off[b + 1]):
+            node = row_node[m]
+            if mask_bool is None:
+                tree_vis = np.arange(node + 1)
+            else:
+                tree_vis = np.flatnonzero(mask_bool[node])
+            keys = np.concatenate([np.arange(L), L + tree_vis])
+            kk = torch.from_numpy(keys).to(q.device)
+            for a in range(A):
+                K = kc[slots[b], a, kk].float()
+                Vv = vc[slots[b], a, kk].float()
+                s = (K @ q[m, a * dh:(a + 1) * dh].float()) / np.sqrt(dh)
+                p = torch.softmax(s, dim=0)
+                out[m, a * dh:(a + 1) * dh] = p @ Vv
+    return out
+
+
+@pytest.mark.parametrize("dtype,dh,A,lens,paths,impl", [
+    ("fp32", 16, 4, [6, 40, 1], "grid43", 1),
+    ("fp32", 16, 2, [300], "full33", 1),
+    ("fp32", 64, 2, [33, 129], "grid43", 1),
+    ("bf16", 128, 4, [512, 77, 1000], "grid43", 1),
+    ("bf16", 128, 2, [1500, 64], "full33", 1),
+    ("bf16", 128, 4, [512, 77, 1000], "grid43", 0),
+    ("bf16", 128, 3, [4096, 200], "full44", 0),
+    ("bf16", 128, 2, [130, 2000, 7, 900], "chain", 0),
+])
+def test_tree_attention_vs_torch(dtype, dh, A, lens, paths, impl):
+    rng = np.random.default_rng(dh * 7 + len(lens))
+    universe = {"grid43": op.grid_candidates(4, 3), "full33": op.complete_tree_paths(3, 3),
+                "full44": op.complete_tree_paths(4, 4)[:200], "chain": [(1,) * d for d in range(1, 5)]}[paths]
+    tmpl = TreeTemplate.from_paths(universe)
+    n = len(tmpl)
+    B = len(lens)
+    slots = list(range(B))[::-1]
+    H = A * dh
+    Lmax = max(lens) + n + 8
+    T = torch.float32 if dtype == "fp32" else torch.bfloat16
+    code = _lib.F32 if dtype == "fp32" else _lib.BF16
+    kc = torch.randn(B, A, Lmax, dh, device=DEV).to(T)
+    vc = torch.randn(B, A, Lmax, dh, device=DEV).to(T)
+    M = B * n
+    qkv = torch.randn(M, 3 * H, device=DEV).to(T)
+    row_off = [b * n for b in range(B + 1)]
+    row_node = [i for b in range(B) for i in range(n)]
+    seq_len = torch.zeros(B, dtype=torch.int32, device=DEV)
+    for b, s in enumerate(slots):
+        seq_len[s] = lens[b]
+    out = torch.zeros(M, H, device=DEV, dtype=T)
+    ws_bytes = _lib.load().propd_attn_workspace_bytes(M, A, dh, 0)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=DEV)
+    mask = torch.from_numpy(tmpl.mask_bits.view(np.int64)).to(DEV)
+    call("propd_tree_attention", code, impl, B, M, A, dh, Lmax, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
+         ptr(i32(slots)), ptr(seq_len), ptr(i32(row_off)), ptr(i32(row_node)), ptr(mask), n, tmpl.words, ptr(out), H,
+         ptr(ws), ws_bytes, st())
+    torch.cuda.synchronize()
+    ref = torch_tree_attention(qkv[:, :H], kc, vc, slots, lens, row_off, row_node, tmpl.mask(), A, dh)
+    err = (out.float() - ref).abs().max().item()
+    tol = (2e-5 if dtype == "fp32" else 2e-2) * max(1.0, ref.abs().max().item())
+    assert err <= tol, (err, tol)
+
+
+def test_tree_attention_causal_and_pruned_rows():
+    """Causal new rows (mask=NULL) and a compacted subset of tree rows."""
+    dh, A, B = 16, 2, 2
+    H = A * dh
+    lens = [5, 9]
+    n = 10
+    Lmax = 32
+    kc = torch.randn(B, A, Lmax, dh, device=DEV)
+    vc = torch.randn(B, A, Lmax, dh, device=DEV)
+    # causal: rows = nodes 0..n-1 of each seq
+    M = B * n
+    qkv = torch.randn(M, 3 * H, device=DEV)
+    row_off = [0, n, 2 * n]
+    row_node = list(range(n)) * 2
+    seq_len = i32(lens)
+    out = torch.zeros(M, H, device=DEV)
+    call("propd_tree_attention", _lib.F32, 1, B, M, A, dh, Lmax, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
+         ptr(i32([0, 1])), ptr(seq_len), ptr(i32(row_off)), ptr(i32(row_node)), None, n, 0, ptr(out), H, None, 0, st())
+    ref = torch_tree_attention(qkv[:, :H], kc, vc, [0, 1], lens, row_off, row_node, None, A, dh)
+    assert (out - ref).abs().max().item() <= 2e-5 * max(1.0, ref.abs().max().item())
+    # pruned: keep an ancestor-closed subset of the grid tree rows
+    tmpl = TreeTemplate.from_paths(op.grid_candidates(4, 3))
+    keep = [0, 1, 2, 3, 5, 6]
+    M = B * len(keep)
+    qkv = torch.randn(M, 3 * H, device=DEV)
+    row_off = [0, len(keep), 2 * len(keep)]
+    row_node = keep * 2
+    out = torch.zeros(M, H, device=DEV)
+    mask = torch.from_numpy(tmpl.mask_bits.view(np.int64)).to(DEV)
+    call("propd_tree_attention", _lib.F32, 1, B, M, A, dh, Lmax, 12, max(lens) + 12, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
+         ptr(i32([0, 1])), ptr(seq_len), ptr(i32(row_off)), ptr(i32(row_node)), ptr(mask), 12, 1, ptr(out), H, None, 0,
+         st())
+    ref = torch_tree_attention(qkv[:, :H], kc, vc, [0, 1], lens, row_off, row_node, tmpl.mask(), A, dh)
+    assert (out - ref).abs().max().item() <= 2e-5 * max(1.0, ref.abs().max().item())
+
+
+# --------------------------------------------------------------- K3 prune
+def test_early_member_and_compaction_match_prune():
+    rng = np.random.default_rng(5)
+    V, topk = 300, 7
+    paths = op.complete_tree_paths(3, 3)
+    sel = op.grid_candidates(3, 3) + ((1, 2), (2,), (2, 1), (2, 1, 3), (1, 2, 2))
+    sel = tuple(dict.fromkeys(p for p in sel if p in set(paths)))
+    tmpl = TreeTemplate.from_paths(sel)
+    n = len(tmpl)
+    B = 5
+    Pn = len(tmpl.parent_nodes)
+    early = np.round(rng.normal(size=(B * Pn, V)).astype(np.float32) * 3) / 3  # ties
+    tokens = rng.integers(0, V, size=(B, n)).astype(np.int32)
+    # make some children land inside their parent's top-K
+    for b in range(B):
+        for i in range(n):
+            par = tmpl.parent[i]
+            if par >= 0 and rng.random() < 0.6:
+                row = early[b * Pn + tmpl.parent_slot[par]]
+                order = np.argsort(-row, kind="stable")
+                tokens[b, i] = order[rng.integers(0, topk + 2)]
+    td = tmpl.device(DEV)
+    member = torch.empty(B * n, dtype=torch.uint8, device=DEV)
+    d_early = torch.from_numpy(early).to(DEV)
+    d_tok = torch.from_numpy(tokens.reshape(-1)).to(DEV)
+    call("propd_early_member", B, n, Pn, V, topk, ptr(d_early), ptr(td["parent"]), ptr(td["parent_slot"]),
+         ptr(d_tok), ptr(member), st())
+    alive = torch.empty(B * n, dtype=torch.uint8, device=DEV)
+    z = lambda m: torch.empty(m, dtype=torch.int32, device=DEV)
+    nrs, nrn, nsrc, node_row, noff, cnt, total = z(B * n), z(B * n), z(B * n), z(B * n), z(B + 1), z(B), z(1)
+    call("propd_prune_compact", B, n, ptr(td["parent"]), ptr(member), ptr(alive), ptr(nrs), ptr(nrn), ptr(nsrc),
+         ptr(noff), ptr(node_row), ptr(cnt), ptr(total), st())
+    alive = alive.cpu().numpy().reshape(B, n)
+    off = 0
+    for b in range(B):
+        lists = []
+        for i in range(n):
+            if i in set(tmpl.parent_nodes.tolist()):
+                row = early[b * Pn + tmpl.parent_slot[i]]
+                lists.append(np.argsort(-row, kind="stable")[:topk].tolist())
+            else:
+                lists.append([])
+        preds = op.Preds(np.arange(100, 100 + 9).reshape(3, 3), -np.tile(np.arange(3.0), (3, 1)))
+        tree = op.build_tree(preds, sel, root_token=0)
+        tree = op.Tree(tuple(op.Node(int(tokens[b, i]), nd.parent, nd.depth, nd.rank) for i, nd in
+                             enumerate(tree.nodes)), 0)
+        surv, _ = op.prune(tree, lists, op.PruneCfg(layer=1, topk=topk))
+        assert np.flatnonzero(alive[b]).tolist() == list(surv)
+        assert cnt[b].item() == len(surv)
+        assert nrn[off: off + len(surv)].cpu().tolist() == list(surv)
+        off += len(surv)
+    assert total.item() == off
+
+
+# --------------------------------------------------------------- K4 stats
+@pytest.mark.parametrize("D,k,alpha", [(4, 3, 0.05), (4, 3, None), (3, 16, 0.05), (4, 64, None)])
+def test_stats_replay_select_bit_exact(D, k, alpha):
+    rng = np.random.default_rng(D * k)
+    stats = op.Stats(D, k, alpha=alpha)
+    P = torch.tensor(stats.P, dtype=torch.float64, device=DEV)
+    counts = torch.zeros(D, dtype=torch.int64, device=DEV)
+    order = torch.empty(D * k, dtype=torch.int32, device=DEV)
+    lcurve = torch.empty(D * k, dtype=torch.float64, device=DEV)
+    for step in range(6):
+        S = int(rng.integers(1, 9))
+        ranks = np.zeros((S, D), dtype=np.int8)
+        for s in range(S):
+            known = int(rng.integers(1, D + 1))
+            toks = np.arange(D * k).reshape(D, k) + 1000
+            preds = op.Preds(toks, -np.tile(np.arange(float(k)), (D, 1)))
+            realized = {}
+            for d in range(1, known + 1):
+                r = int(rng.integers(0, k + 2))  # 0 or >k means miss
+                tok = int(toks[d - 1, r - 1]) if 1 <= r <= k else 7
+                realized[d] = tok
+                ranks[s, d - 1] = r if 1 <= r <= k else -1
+            stats.update(realized, preds)
+        call("propd_stats_replay_select", S, D, k, ptr(torch.from_numpy(ranks).to(DEV)),
+             float(alpha) if alpha is not None else -1.0, ptr(P), ptr(counts), ptr(order), ptr(lcurve), st())
+        assert np.array_equal(P.cpu().numpy(), stats.P)  # bit-exact fp64
+        sel = op.select_best_nodes(stats, list(range(1, D * k + 1)))
+        universe = op.grid_candidates(D, k)
+        got = [universe[c] for c in order.cpu().numpy()]
+        assert tuple(got) == sel[D * k][0]
+        assert lcurve.cpu().numpy().tolist() == [sel[s][1] for s in range(1, D * k + 1)]
+
+
+# --------------------------------------------------------------- K5 verify + compaction
+def test_verify_commit_walk_and_compaction():
+    rng = np.random.default_rng(11)
+    D, k = 3, 3
+    sel = op.complete_tree_paths(3, 3)[:20]
+    sel = [p for p in sel if len(p) == 1 or p[:-1] in set(sel)]
+    tmpl = TreeTemplate.from_paths(sel)
+    n, B = len(tmpl), 6
+    layers, A, dh, Lmax = 2, 2, 16, 64
+    lens = rng.integers(3, 20, size=B)
+    draft = rng.permutation(50)[: D * k].reshape(D, k)
+    draft_tok = np.stack([rng.permutation(60)[: D * k].reshape(D, k) for _ in range(B)]).astype(np.int32)
+    tokens = np.stack([[draft_tok[b, tmpl.depth[i] - 1, tmpl.rank[i] - 1] for i in range(n)] for b in range(B)])
+    alive = (rng.random((B, n)) < 0.8)
+    for b in range(B):
+        for i in range(n):
+            if tmpl.parent[i] >= 0 and not alive[b, tmpl.parent[i]]:
+                alive[b, i] = False
+    node_row = np.full((B, n), -1, dtype=np.int32)
+    r = 0
+    for b in range(B):
+        for i in range(n):
+            if alive[b, i]:
+                node_row[b, i] = r
+                r += 1
+    # argmax per surviving row: often follow a chain so that something is accepted
+    row_argmax = rng.integers(0, 60, size=r).astype(np.int32)
+    root = np.zeros(B, dtype=np.int32)
+    for b in range(B):
+        root[b] = tokens[b, 0] if rng.random() < 0.8 else 59
+        for i in range(n):
+            if alive[b, i] and rng.random() < 0.5:
+                kids = [c for c in range(n) if tmpl.parent[c] == i and alive[b, c]]
+                if kids:
+                    row_argmax[node_row[b, i]] = tokens[b, kids[-1]]
+    kc = torch.randn(layers, B, A, Lmax, dh, device=DEV)
+    vc = torch.randn(layers, B, A, Lmax, dh, device=DEV)
+    kc0, vc0 = kc.clone(), vc.clone()
+    td = tmpl.device(DEV)
+    seq_len = i32(lens)
+    z = lambda m: torch.empty(m, dtype=torch.int32, device=DEV)
+    acc_node, acc_surv, acc_len, bonus, committed = z(B * D), z(B * D), z(B), z(B), z(B * (D + 1))
+    ranks = torch.empty(B, D, dtype=torch.int8, device=DEV)
+    call("propd_verify_commit", _lib.F32, B, n, D, k, layers, A, dh, Lmax, B * A * Lmax * dh, ptr(td["parent"]),
+         ptr(i32(tokens.reshape(-1))), ptr(torch.from_numpy(alive.astype(np.uint8).reshape(-1)).to(DEV)),
+         ptr(i32(node_row.reshape(-1))), ptr(i32(row_argmax)), ptr(i32(root)), ptr(i32(draft_tok.reshape(-1))),
+         ptr(i32(np.arange(B))), ptr(seq_len), ptr(kc), ptr(vc), ptr(acc_node), ptr(acc_surv), ptr(acc_len),
+         ptr(bonus), ptr(committed), ptr(ranks), st())
+    acc_node, acc_surv = acc_node.cpu().numpy().reshape(B, D), acc_surv.cpu().numpy().reshape(B, D)
+    acc_len, bonus = acc_len.cpu().numpy(), bonus.cpu().numpy()
+    committed, ranks = committed.cpu().numpy().reshape(B, D + 1), ranks.cpu().numpy()
+    for b in range(B):
+        preds = op.Preds(draft_tok[b], -np.tile(np.arange(float(k)), (D, 1)))
+        tree = op.build_tree(preds, sel, root_token=0)
+        surv = np.flatnonzero(alive[b]).tolist()
+        vtree = op.restrict(tree, surv)
+        am = [row_argmax[node_row[b, i]] for i in surv]
+        acc, bon = op.verify(vtree, am, int(root[b]))
+        assert acc_len[b] == len(acc) and bonus[b] == bon
+        assert acc_surv[b, : len(acc)].tolist() == list(acc)
+        nodes = [surv[a] for a in acc]
+        assert acc_node[b, : len(acc)].tolist() == nodes
+        newly = [int(tokens[b, nd]) for nd in nodes] + [bon]
+        assert committed[b, : len(newly)].tolist() == newly
+        for d in range(D):
+            exp = 0
+            if d < min(len(newly), D):
+                rk = preds.rank_of(d + 1, newly[d])
+                exp = rk if rk is not None else -1
+            assert ranks[b, d] == exp
+        assert seq_len[b].item() == lens[b] + len(acc)
+        L = int(lens[b])
+        for j, nd in enumerate(nodes):
+            assert torch.equal(kc[:, b, :, L + j], kc0[:, b, :, L + nd])
+            assert torch.equal(vc[:, b, :, L + j], vc0[:, b, :, L + nd])
+        assert torch.equal(kc[:, b, :, :L], kc0[:, b, :, :L])
