@@ -107,9 +107,10 @@ int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, 
  * q = columns [0,H) of qkv.  out[m, a*dh:(a+1)*dh] = softmax(q k^T / sqrt(dh)) v.
  * `workspace` must hold propd_attn_workspace_bytes(...) bytes.
  * impl: 0 = auto, 1 = CUDA-core split-KV kernel, 2 = tcgen05/TMA kernel
- * (bf16, dh = 128 only). */
+ * (bf16, dh = 128 only).  n_slots = number of [A, Lmax, dh] slot blocks in the
+ * cache layer (bounds of the TMA tensor map). */
 int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits);
-int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax,
+int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int n_slots,
                          int max_rows_per_seq, int max_keys,
                          const void* qkv, int ldqkv, const void* kcache, const void* vcache,
                          const int32_t* seq_slot, const int32_t* seq_len,

@@ -12,7 +12,7 @@ import os
 from ctypes import c_double, c_int, c_int64, c_void_p
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpropd.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 F32 = 0
 BF16 = 1
@@ -37,7 +37,7 @@ SIGNATURES = {
     "propd_topk_rows": [I, I, I, I, P, P, P, P],
     "propd_kv_append": [I, I, I, I, I, P, I, P, P, P, P, P, P, P],
     "propd_attn_workspace_bytes": [I, I, I, I],
-    "propd_tree_attention": [I, I, I, I, I, I, I, I, I, P, I, P, P, P, P, P, P, P, I, I, P, I, P, L, P],
+    "propd_tree_attention": [I, I, I, I, I, I, I, I, I, I, P, I, P, P, P, P, P, P, P, I, I, P, I, P, L, P],
     "propd_early_member": [I, I, I, I, I, P, P, P, P, P, P],
     "propd_prune_compact": [I, I, P, P, P, P, P, P, P, P, P, P, P],
     "propd_verify_commit": [I, I, I, I, I, I, I, I, I, L, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],

@@ -237,7 +237,7 @@ class B200Backend:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
             self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
-                       rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
+                       self.max_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
                        ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
                        ptr(ws), ws.numel(), st)
             if self.attn_timer is not None:

@@ -218,7 +218,8 @@ static int choose_splits(int B, int A, int max_keys, int max_splits) {
   return want < 1 ? 1 : want;
 }
 
-int attention_tc_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv, int ldqkv,
+int attention_tc_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
+                      int ldqkv,
                       const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                       const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                       void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled);
@@ -236,8 +237,8 @@ int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits) {
   return (int64_t)M * A * max_splits * (dh + 2) * (int64_t)sizeof(float) + 256;
 }
 
-int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int max_rows_per_seq,
-                         int max_keys, const void* qkv, int ldqkv, const void* kcache, const void* vcache,
+int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int n_slots,
+                         int max_rows_per_seq, int max_keys, const void* qkv, int ldqkv, const void* kcache, const void* vcache,
                          const int32_t* seq_slot, const int32_t* seq_len, const int32_t* row_off,
                          const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W, void* out, int ldout,
                          void* workspace, int64_t workspace_bytes, void* stream) {
@@ -248,7 +249,7 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
   cudaStream_t st = as_stream(stream);
   if (impl == 2 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {
     bool handled = false;
-    int e = attention_tc_bf16(B, M, A, Lmax, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
+    int e = attention_tc_bf16(B, M, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
                               seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, workspace, workspace_bytes,
                               st, &handled);
     if (e || handled) return e;

@@ -305,7 +305,7 @@ using namespace propd;
 extern "C" {
 
 const char* propd_last_error(void) { return g_error.c_str(); }
-int propd_abi_version(void) { return 1; }
+int propd_abi_version(void) { return 2; }
 int propd_num_sms(void) {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }

@@ -275,10 +275,21 @@ __global__ void stats_replay_select_kernel(int S, int D, int k, const int8_t* __
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int s = 0; s < N; ++s) {
-      acc = __dadd_rn(acc, contrib[order[s]]);
-      lcurve[s] = acc;
+    // l(s) = Python sum() of the first s contributions.  CPython >= 3.12 sums
+    // floats with Neumaier compensation (bltinmodule.c builtin_sum_impl):
+    // the first term seeds the running sum, later terms update (f, c), and
+    // the result is f + c when c is non-zero and finite.
+    double f = contrib[order[0]], c = 0.0;
+    lcurve[0] = f;
+    for (int s = 1; s < N; ++s) {
+      const double x = contrib[order[s]];
+      const double t = __dadd_rn(f, x);
+      if (fabs(f) >= fabs(x))
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+      else
+        c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+      f = t;
+      lcurve[s] = (c != 0.0 && isfinite(c)) ? __dadd_rn(f, c) : f;
     }
   }
 }

@@ -123,7 +123,7 @@ def test_tree_attention_vs_torch(dtype, dh, A, lens, paths, impl):
     ws_bytes = _lib.load().propd_attn_workspace_bytes(M, A, dh, 0)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=DEV)
     mask = torch.from_numpy(tmpl.mask_bits.view(np.int64)).to(DEV)
-    call("propd_tree_attention", code, impl, B, M, A, dh, Lmax, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
+    call("propd_tree_attention", code, impl, B, M, A, dh, Lmax, B, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
          ptr(i32(slots)), ptr(seq_len), ptr(i32(row_off)), ptr(i32(row_node)), ptr(mask), n, tmpl.words, ptr(out), H,
          ptr(ws), ws_bytes, st())
     torch.cuda.synchronize()
@@ -149,7 +149,7 @@ def test_tree_attention_causal_and_pruned_rows():
     row_node = list(range(n)) * 2
     seq_len = i32(lens)
     out = torch.zeros(M, H, device=DEV)
-    call("propd_tree_attention", _lib.F32, 1, B, M, A, dh, Lmax, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
+    call("propd_tree_attention", _lib.F32, 1, B, M, A, dh, Lmax, B, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
          ptr(i32([0, 1])), ptr(seq_len), ptr(i32(row_off)), ptr(i32(row_node)), None, n, 0, ptr(out), H, None, 0, st())
     ref = torch_tree_attention(qkv[:, :H], kc, vc, [0, 1], lens, row_off, row_node, None, A, dh)
     assert (out - ref).abs().max().item() <= 2e-5 * max(1.0, ref.abs().max().item())
@@ -162,7 +162,7 @@ def test_tree_attention_causal_and_pruned_rows():
     row_node = keep * 2
     out = torch.zeros(M, H, device=DEV)
     mask = torch.from_numpy(tmpl.mask_bits.view(np.int64)).to(DEV)
-    call("propd_tree_attention", _lib.F32, 1, B, M, A, dh, Lmax, 12, max(lens) + 12, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
+    call("propd_tree_attention", _lib.F32, 1, B, M, A, dh, Lmax, B, 12, max(lens) + 12, ptr(qkv), 3 * H, ptr(kc), ptr(vc),
          ptr(i32([0, 1])), ptr(seq_len), ptr(i32(row_off)), ptr(i32(row_node)), ptr(mask), 12, 1, ptr(out), H, None, 0,
          st())
     ref = torch_tree_attention(qkv[:, :H], kc, vc, [0, 1], lens, row_off, row_node, tmpl.mask(), A, dh)
