@@ -165,6 +165,7 @@ class B200Backend:
         self._free = list(range(self.max_slots - 1, -1, -1))
         self._ws = torch.empty(0, device=dev, dtype=torch.uint8)
         self._one_mask = torch.ones(1, device=dev, dtype=torch.int64)  # single-node template {0}
+        self._keepalive: list = []
         self.launches = 0  # libpropd kernel launches issued (bench accounting)
         self.attn_timer = None  # list -> (start, end, rows) CUDA events of every K2 launch
 
@@ -187,6 +188,9 @@ class B200Backend:
     def _call(self, name, *args):
         self.launches += 1
         call(name, *args)
+        # temporaries created for this launch may be recycled only after it
+        # has been issued (their blocks are then reused in stream order)
+        self._keepalive.clear()
 
     # ------------------------------------------------------------- slots
     def _alloc_slot(self, state: DecodeState) -> int:
@@ -210,7 +214,12 @@ class B200Backend:
         state.slot = -1
 
     def _i32(self, values):
-        return self.torch.tensor(np.asarray(values, dtype=np.int32), device=self.device)
+        """Device int32 copy of host values, kept alive until the next launch
+        is issued (an inline `ptr(self._i32(a))` would otherwise free the
+        block before the kernel reads it and alias the next temporary)."""
+        t = self.torch.tensor(np.asarray(values, dtype=np.int32), device=self.device)
+        self._keepalive.append(t)
+        return t
 
     def _workspace(self, M: int) -> object:
         need = int(self.lib.propd_attn_workspace_bytes(M, self.A, self.dh, 0))

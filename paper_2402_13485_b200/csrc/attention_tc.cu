@@ -75,14 +75,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Bounded wait: a protocol bug traps (with a diagnostic) instead of hanging the GPU.
+__device__ __noinline__ void mbar_timeout(int tag, uint32_t parity) {
+  printf("propd attn_tc: mbarrier wait timed out (tag %d parity %u) block (%d,%d,%d) thread %d\n", tag, parity,
+         blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
+  uint32_t spins = 0;
+  while (!mbar_try(bar, parity)) {
+    if (++spins > (1u << 26)) mbar_timeout(tag, parity);
+  }
 }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 32 * min(4, (nrows + 31) / 32));  // softmax warps that own rows
     mbar_init(o_done, 1);
     fence_barrier_init();
   }
@@ -229,7 +243,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       for (int j = 0; j < nblk; ++j) {
         const int st = j % STAGES;
-        mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1);
+        mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1, 1);
         mbar_expect_tx(&kv_full[st], 2 * TILE_BYTES);
         const int row = (int)(row_base + k_begin + j * BN);
         uint8_t* kd = smem + SMEM_K + st * TILE_BYTES;
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t q_addr = smem_u32(smem + SMEM_Q), p_addr = smem_u32(smem + SMEM_P);
       auto issue_pv = [&](int jj) {
         const int st = jj % STAGES;
-        mbar_wait(p_full, jj & 1);
+        mbar_wait(p_full, jj & 1, 2);
         tc_after_sync();
         const uint32_t v_addr = smem_u32(smem + SMEM_V + st * TILE_BYTES);
 #pragma unroll
@@ -261,7 +275,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       for (int j = 0; j < nblk; ++j) {
         const int st = j % STAGES;
-        mbar_wait(&kv_full[st], (j / STAGES) & 1);
+        mbar_wait(&kv_full[st], (j / STAGES) & 1, 3);
         tc_after_sync();
         const uint32_t k_addr = smem_u32(smem + SMEM_K + st * TILE_BYTES);
         const uint32_t s_tmem = tmem + 128 + 128 * (j & 1);
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int j = 0; j < nblk; ++j) {
       float sv[128];
       if (warp_live) {
-        mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&s_full[j & 1], (j >> 1) & 1, 4);
         tc_after_sync();
         const uint32_t sa = lane_addr + 128 + 128 * (j & 1);
 #pragma unroll
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           mx = fmaxf(mx, sv[i]);
         }
         if (j > 0) {  // PV_{j-1} finished: P buffer free, O stable
-          mbar_wait(o_done, (j - 1) & 1);
+          mbar_wait(o_done, (j - 1) & 1, 5);
           tc_after_sync();
         }
         if (mx > m_ref + 8.f) {  // lazy max update; exact since O and l share m_ref
@@ -360,12 +374,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         l_sum += ls;
         fence_proxy_async();
       }
-      tc_before_sync();
-      mbar_arrive(p_full);
+      if (warp_live) {
+        tc_before_sync();
+        mbar_arrive(p_full);
+      }
     }
     // epilogue: O row from TMEM
     if (warp_live) {
-      mbar_wait(o_done, (nblk - 1) & 1);
+      mbar_wait(o_done, (nblk - 1) & 1, 6);
       tc_after_sync();
       float o[128];
 #pragma unroll
@@ -404,7 +420,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
 }
 
 // ------------------------------------------------------------------ host --

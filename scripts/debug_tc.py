@@ -1,0 +1,84 @@
+"""Run one tree-attention case through impl=2 (tcgen05) and impl=1 (CUDA
+core) and print the max error of each against a torch fp32 reference.
+  python scripts/debug_tc.py B A L n [rows]     (n: grid-tree size selector)
+  python scripts/debug_tc.py all                 (loop over cases in subprocesses)
+"""
+import os
+import subprocess
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+if sys.argv[1] == "all":
+    cases = [(1, 1, 1, 1), (1, 1, 100, 1), (1, 1, 128, 4), (1, 1, 300, 12), (1, 2, 1000, 12), (2, 4, 512, 12),
+             (3, 4, 77, 39), (1, 32, 1024, 37), (2, 2, 4096, 160), (4, 32, 2048, 64)]
+    for c in cases:
+        try:
+            r = subprocess.run([sys.executable, __file__, *map(str, c)], capture_output=True, text=True, timeout=120)
+            print(c, "rc", r.returncode, (r.stdout + r.stderr).strip().splitlines()[-3:])
+        except subprocess.TimeoutExpired:
+            print(c, "TIMEOUT")
+    sys.exit(0)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2402_13485_b200 import _lib  # noqa: E402
+from paper_2402_13485_b200._lib import call, ptr  # noqa: E402
+from paper_2402_13485_b200.tree import TreeTemplate  # noqa: E402
+from oracle import treedecode_port as op  # noqa: E402
+
+B, A, L, nsel = map(int, sys.argv[1:5])
+dev = torch.device("cuda:0")
+paths = op.complete_tree_paths(4, 4)
+paths = sorted(paths, key=lambda p: (len(p), p))[:nsel]
+tmpl = TreeTemplate.from_paths(paths)
+n = len(tmpl)
+dh = 128
+H = A * dh
+lens = [max(1, L - 37 * b) for b in range(B)]
+Lmax = max(lens) + n + 8
+torch.manual_seed(0)
+kc = torch.randn(B, A, Lmax, dh, device=dev).bfloat16()
+vc = torch.randn(B, A, Lmax, dh, device=dev).bfloat16()
+M = B * n
+qkv = torch.randn(M, 3 * H, device=dev).bfloat16()
+keep = []
+
+
+def t32(a):
+    t = torch.tensor(np.asarray(a, dtype=np.int32), device=dev)
+    keep.append(t)
+    return t
+
+
+slots = t32(list(range(B)))
+seq_len = t32(lens)
+row_off = t32([b * n for b in range(B + 1)])
+row_node = t32([i for b in range(B) for i in range(n)])
+mask = torch.from_numpy(tmpl.mask_bits.view(np.int64)).to(dev)
+ws_bytes = _lib.load().propd_attn_workspace_bytes(M, A, dh, 0)
+ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+outs = {}
+for impl in (1, 2):
+    out = torch.zeros(M, H, device=dev, dtype=torch.bfloat16)
+    call("propd_tree_attention", _lib.BF16, impl, B, M, A, dh, Lmax, B, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc),
+         ptr(vc), ptr(slots), ptr(seq_len), ptr(row_off), ptr(row_node), ptr(mask), n, tmpl.words, ptr(out), H,
+         ptr(ws), ws_bytes, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    outs[impl] = out.float()
+mb = tmpl.mask()
+ref = torch.zeros(M, H, device=dev)
+for b in range(B):
+    for i in range(n):
+        keys = np.concatenate([np.arange(lens[b]), lens[b] + np.flatnonzero(mb[i])])
+        kk = torch.from_numpy(keys).to(dev)
+        for a in range(A):
+            K = kc[b, a, kk].float()
+            V = vc[b, a, kk].float()
+            s = K @ qkv[b * n + i, a * dh:(a + 1) * dh].float() / np.sqrt(dh)
+            ref[b * n + i, a * dh:(a + 1) * dh] = torch.softmax(s, 0) @ V
+for impl in (1, 2):
+    e = (outs[impl] - ref).abs()
+    print(f"impl {impl}: max err {e.max().item():.3e}  rows with err>0.05: "
+          f"{sorted(set((e > 0.05).nonzero()[:, 0].tolist()))[:10]}")

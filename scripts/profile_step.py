@@ -33,7 +33,7 @@ be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=args.batc
 eng = DecodeEngine(be, bench.engine_cfg(args), None)
 states = be.synthetic_states(args.batch, args.kv)
 seqs = [_Seq(st, st.committed[:], i) for i, st in enumerate(states)]
-for _ in range(args.warmup):
+for _ in range(len(eng._probe_queue) + 1 + args.warmup):
     eng._step(seqs, 10 ** 9)
 torch.cuda.synchronize()
 t0 = time.perf_counter()

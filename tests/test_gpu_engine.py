@@ -197,8 +197,8 @@ def test_commit_equals_scratch_prefill_and_oracle():
         assert np.array_equal(f1.argmax, f0.argmax)
         acc, bonus = op.verify(tree, f0.argmax, ref.next_argmax(rs))
         if not acc and rng.random() < 0.7:  # force an accepted chain to exercise compaction
-            acc = (0, 1)
-            bonus = int(f0.argmax[1])
+            acc = (0, 2)  # nodes (1,) -> (1, 1)
+            bonus = int(f0.argmax[2])
         be.commit(st, list(acc), bonus)
         ref.commit(rs, list(acc), bonus)
         assert st.committed == rs.committed

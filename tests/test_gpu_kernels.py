@@ -29,8 +29,18 @@ def st():
     return torch.cuda.current_stream().cuda_stream
 
 
+_KEEP = []  # inline temporaries must outlive the launch that reads them
+
+
 def i32(a):
-    return torch.tensor(np.asarray(a, dtype=np.int32), device=DEV)
+    t = torch.tensor(np.asarray(a, dtype=np.int32), device=DEV)
+    _KEEP.append(t)
+    return t
+
+
+def keep(t):
+    _KEEP.append(t)
+    return t
 
 
 # --------------------------------------------------------------- top-k / argmax
@@ -246,7 +256,7 @@ def test_stats_replay_select_bit_exact(D, k, alpha):
                 realized[d] = tok
                 ranks[s, d - 1] = r if 1 <= r <= k else -1
             stats.update(realized, preds)
-        call("propd_stats_replay_select", S, D, k, ptr(torch.from_numpy(ranks).to(DEV)),
+        call("propd_stats_replay_select", S, D, k, ptr(keep(torch.from_numpy(ranks).to(DEV))),
              float(alpha) if alpha is not None else -1.0, ptr(P), ptr(counts), ptr(order), ptr(lcurve), st())
         assert np.array_equal(P.cpu().numpy(), stats.P)  # bit-exact fp64
         sel = op.select_best_nodes(stats, list(range(1, D * k + 1)))
@@ -300,7 +310,7 @@ def test_verify_commit_walk_and_compaction():
     acc_node, acc_surv, acc_len, bonus, committed = z(B * D), z(B * D), z(B), z(B), z(B * (D + 1))
     ranks = torch.empty(B, D, dtype=torch.int8, device=DEV)
     call("propd_verify_commit", _lib.F32, B, n, D, k, layers, A, dh, Lmax, B * A * Lmax * dh, ptr(td["parent"]),
-         ptr(i32(tokens.reshape(-1))), ptr(torch.from_numpy(alive.astype(np.uint8).reshape(-1)).to(DEV)),
+         ptr(i32(tokens.reshape(-1))), ptr(keep(torch.from_numpy(alive.astype(np.uint8).reshape(-1)).to(DEV))),
          ptr(i32(node_row.reshape(-1))), ptr(i32(row_argmax)), ptr(i32(root)), ptr(i32(draft_tok.reshape(-1))),
          ptr(i32(np.arange(B))), ptr(seq_len), ptr(kc), ptr(vc), ptr(acc_node), ptr(acc_surv), ptr(acc_len),
          ptr(bonus), ptr(committed), ptr(ranks), st())
