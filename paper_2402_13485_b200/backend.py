@@ -154,8 +154,11 @@ class B200Backend:
         self.max_slots = int(max_slots)
         dev, T = self.device, self.tdtype
         shape = (cfg.layers, self.max_slots, self.A, self.Lmax, self.dh)
-        self.kcache = torch.empty(shape, device=dev, dtype=T)
-        self.vcache = torch.empty(shape, device=dev, dtype=T)
+        # zero-filled: key blocks streamed by the tensor-core kernel may extend
+        # past the live keys; masked keys get p = 0, and 0 * garbage-NaN would
+        # poison the P.V product, so every cache row must hold a finite value
+        self.kcache = torch.zeros(shape, device=dev, dtype=T)
+        self.vcache = torch.zeros(shape, device=dev, dtype=T)
         self.layer_stride = self.max_slots * self.A * self.Lmax * self.dh
         self.seq_len = torch.zeros(self.max_slots, device=dev, dtype=torch.int32)
         self.root = torch.zeros(self.max_slots, device=dev, dtype=torch.int32)

@@ -340,22 +340,27 @@ __global__ void __launch_bounds__(THREADS, 1)
           mbar_wait(o_done, (j - 1) & 1, 5);
           tc_after_sync();
         }
-        if (mx > m_ref + 8.f) {  // lazy max update; exact since O and l share m_ref
-          const float corr = exp2f(m_ref - mx);
-          if (j > 0) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t rr[32];
-              TMEM_LD32(lane_addr + c * 32, rr);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
-              TMEM_ST32(lane_addr + c * 32, rr);
-            }
-            tmem_wait_st();
-          }
+        // lazy max update (exact: O and l always share m_ref); the decision is
+        // per row but tcgen05.ld/st are warp-collective, so the O rescale
+        // runs for the whole warp with corr = 1 on rows that keep their max
+        float corr = 1.f;
+        const bool grow = mx > m_ref + 8.f;
+        if (grow) {
+          corr = exp2f(m_ref - mx);
           l_sum *= corr;
           m_ref = mx;
+        }
+        if (j > 0 && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t rr[32];
+            TMEM_LD32(lane_addr + c * 32, rr);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
+            TMEM_ST32(lane_addr + c * 32, rr);
+          }
+          tmem_wait_st();
         }
         float ls = 0.f;
 #pragma unroll

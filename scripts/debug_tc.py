@@ -10,12 +10,16 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 if sys.argv[1] == "all":
-    cases = [(1, 1, 1, 1), (1, 1, 100, 1), (1, 1, 128, 4), (1, 1, 300, 12), (1, 2, 1000, 12), (2, 4, 512, 12),
-             (3, 4, 77, 39), (1, 32, 1024, 37), (2, 2, 4096, 160), (4, 32, 2048, 64)]
+    cases = [tuple(c.split(",")) for c in sys.argv[2:]] or [
+        (1, 1, 1, 1), (1, 1, 100, 1), (1, 1, 128, 4), (1, 1, 300, 12), (1, 2, 1000, 12), (2, 4, 512, 12),
+        (3, 4, 77, 39), (1, 32, 1024, 37), (2, 2, 4096, 160), (4, 32, 2048, 64)]
     for c in cases:
         try:
-            r = subprocess.run([sys.executable, __file__, *map(str, c)], capture_output=True, text=True, timeout=120)
-            print(c, "rc", r.returncode, (r.stdout + r.stderr).strip().splitlines()[-3:])
+            extra = [c[4] if len(c) > 4 else None]
+            r = subprocess.run([sys.executable, __file__, *map(str, c[:4]), *([str(c[4])] if len(c) > 4 else [])],
+                               capture_output=True, text=True, timeout=120)
+            lines = (r.stdout + r.stderr).strip().splitlines()
+            print(c, "rc", r.returncode, [ln for ln in lines if "propd attn_tc" in ln][:3], lines[-3:])
         except subprocess.TimeoutExpired:
             print(c, "TIMEOUT")
     sys.exit(0)
@@ -29,6 +33,7 @@ from paper_2402_13485_b200.tree import TreeTemplate  # noqa: E402
 from oracle import treedecode_port as op  # noqa: E402
 
 B, A, L, nsel = map(int, sys.argv[1:5])
+REV = os.environ.get("REV_SLOTS") == "1"
 dev = torch.device("cuda:0")
 paths = op.complete_tree_paths(4, 4)
 paths = sorted(paths, key=lambda p: (len(p), p))[:nsel]
@@ -36,7 +41,8 @@ tmpl = TreeTemplate.from_paths(paths)
 n = len(tmpl)
 dh = 128
 H = A * dh
-lens = [max(1, L - 37 * b) for b in range(B)]
+lens = [max(1, L - 37 * b) for b in range(B)] if len(sys.argv) < 6 else list(map(int, sys.argv[5].split("/")))
+B = len(lens)
 Lmax = max(lens) + n + 8
 torch.manual_seed(0)
 kc = torch.randn(B, A, Lmax, dh, device=dev).bfloat16()
@@ -52,8 +58,12 @@ def t32(a):
     return t
 
 
-slots = t32(list(range(B)))
-seq_len = t32(lens)
+slot_list = list(range(B))[::-1] if REV else list(range(B))
+slots = t32(slot_list)
+sl = [0] * B
+for b, s_ in enumerate(slot_list):
+    sl[s_] = lens[b]
+seq_len = t32(sl)
 row_off = t32([b * n for b in range(B + 1)])
 row_node = t32([i for b in range(B) for i in range(n)])
 mask = torch.from_numpy(tmpl.mask_bits.view(np.int64)).to(dev)
@@ -74,8 +84,8 @@ for b in range(B):
         keys = np.concatenate([np.arange(lens[b]), lens[b] + np.flatnonzero(mb[i])])
         kk = torch.from_numpy(keys).to(dev)
         for a in range(A):
-            K = kc[b, a, kk].float()
-            V = vc[b, a, kk].float()
+            K = kc[slot_list[b], a, kk].float()
+            V = vc[slot_list[b], a, kk].float()
             s = K @ qkv[b * n + i, a * dh:(a + 1) * dh].float() / np.sqrt(dh)
             ref[b * n + i, a * dh:(a + 1) * dh] = torch.softmax(s, 0) @ V
 for impl in (1, 2):
