@@ -40,7 +40,8 @@ constexpr int SMEM_Q = 0;
 constexpr int SMEM_K = SMEM_Q + TILE_BYTES;
 constexpr int SMEM_V = SMEM_K + STAGES * TILE_BYTES;
 constexpr int SMEM_P = SMEM_V + STAGES * TILE_BYTES;
-constexpr int SMEM_BAR = SMEM_P + TILE_BYTES;
+constexpr int SMEM_MASK = SMEM_P + TILE_BYTES;        // [128 rows][8] u32 ancestor bitsets
+constexpr int SMEM_BAR = SMEM_MASK + BM * 8 * 4;
 constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;  // + barriers + alignment slack
 constexpr uint32_t TMEM_COLS = 512;               // O: [0,128), S buffers: [128,256), [256,384)
 
@@ -59,7 +60,10 @@ struct Args {
   float* part_ml;
   __nv_bfloat16* out;
   int ldout;
+  unsigned long long* trace;  // debug: phase timestamps of CTA (0,0,0), or null
 };
+
+static unsigned long long* g_trace = nullptr;
 
 // ------------------------------------------------------------------ PTX --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -163,11 +167,40 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// Bits [t0, t0+32) of a 256-bit row mask held as 8 u32 words in smem (0 outside).
+__device__ __forceinline__ uint32_t mask_bits32(const uint32_t* m, int t0) {
+  if (t0 >= 256 || t0 <= -32) return 0u;
+  const int w = (t0 + 32) / 32 - 1;  // floor(t0 / 32) for t0 > -32
+  const int sh = t0 - 32 * w;
+  const uint32_t lo = (w >= 0) ? m[w] : 0u;
+  const uint32_t hi = (w + 1 < 8) ? m[w + 1] : 0u;
+  return sh ? __funnelshift_r(lo, hi, sh) : lo;
+}
+// Low `k` bits set, k clamped to [0, 32].
+__device__ __forceinline__ uint32_t low_bits(int k) {
+  return k >= 32 ? 0xffffffffu : (k <= 0 ? 0u : ((1u << k) - 1u));
+}
+
 // Byte offset of 16-byte chunk `c` (0..15 over 128 bf16 columns) of row r in
 // a [128 x 128] bf16 tile stored as two SW128 K-major column blocks.
 __device__ __forceinline__ uint32_t sw128_chunk(int r, int c) {
   return (uint32_t)((c >> 3) * HALF + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(k)                                                                          \
+  do {                                                                                    \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) p.trace[k] = gtime(); \
+  } while (0)
 
 // ------------------------------------------------------------------ kernel --
 __global__ void __launch_bounds__(THREADS, 1)
@@ -183,6 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TRACE(0);
   const int s = blockIdx.x / p.mtiles, mt = blockIdx.x % p.mtiles;
   const int a = blockIdx.y, b = blockIdx.z;
   const int slot = p.seq_slot[b];
@@ -222,20 +256,44 @@ __global__ void __launch_bounds__(THREADS, 1)
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  {  // Q rows -> SW128 K-major smem (manual swizzle; rows past nrows are zero)
+  {  // Q rows -> SW128 K-major smem with cp.async (manual swizzle; rows past nrows are zero)
     const __nv_bfloat16* qbase = p.qkv + a * DH;
     for (int i = threadIdx.x; i < BM * 16; i += THREADS) {
       const int r = i >> 4, c = i & 15;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < nrows) v = *reinterpret_cast<const uint4*>(qbase + (size_t)(r0 + r) * p.ldq + c * 8);
-      *reinterpret_cast<uint4*>(smem + SMEM_Q + sw128_chunk(r, c)) = v;
+      uint8_t* dst = smem + SMEM_Q + sw128_chunk(r, c);
+      if (r < nrows) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
+                     "l"(qbase + (size_t)(r0 + r) * p.ldq + c * 8)
+                     : "memory");
+      } else {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+      }
     }
+    uint32_t* msk = reinterpret_cast<uint32_t*>(smem + SMEM_MASK);
+    for (int i = threadIdx.x; i < BM * 8; i += THREADS) {
+      const int r = i >> 3, w = i & 7;
+      uint32_t v = 0u;
+      if (r < nrows) {
+        if (p.mask != nullptr) {
+          if ((w >> 1) < p.W) {
+            const uint64_t word = p.mask[(size_t)p.row_node[r0 + r] * p.W + (w >> 1)];
+            v = (w & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+          }
+        } else {  // causal: tree nodes 0..row_node visible
+          const int node = p.row_node[r0 + r];
+          v = low_bits(node + 1 - 32 * w);
+        }
+      }
+      msk[i] = v;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   fence_proxy_async();
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(1);
 
   const size_t row_base = ((size_t)slot * p.A + a) * p.Lmax;
   if (warp == 0) {
@@ -263,6 +321,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int st = jj % STAGES;
         mbar_wait(p_full, jj & 1, 2);
         tc_after_sync();
+        if (jj == 0) TRACE(6);
         const uint32_t v_addr = smem_u32(smem + SMEM_V + st * TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K = 128 keys in steps of 16
@@ -277,6 +336,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int st = j % STAGES;
         mbar_wait(&kv_full[st], (j / STAGES) & 1, 3);
         tc_after_sync();
+        if (j == 0) TRACE(2);
         const uint32_t k_addr = smem_u32(smem + SMEM_K + st * TILE_BYTES);
         const uint32_t s_tmem = tmem + 128 + 128 * (j & 1);
 #pragma unroll
@@ -286,6 +346,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma_bf16(s_tmem, ad, bd, id_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(&s_full[j & 1]);
+        if (j == 0) TRACE(3);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(nblk - 1);
@@ -297,97 +358,95 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool valid = r < nrows;
     const bool warp_live = q4 * 32 < nrows;
     const int row = r0 + r;
-    uint64_t bits[4] = {0ull, 0ull, 0ull, 0ull};
-    int node = 0;
-    if (valid) {
-      node = p.row_node[row];
-      if (p.mask != nullptr)
-        for (int w = 0; w < p.W && w < 4; ++w) bits[w] = p.mask[(size_t)node * p.W + w];
-    }
+    const uint32_t* mrow = reinterpret_cast<const uint32_t*>(smem + SMEM_MASK) + r * 8;
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
+    const float scale = p.scale_log2;
     float m_ref = -INFINITY, l_sum = 0.f;
     uint8_t* prow = smem + SMEM_P;
-    for (int j = 0; j < nblk; ++j) {
+    for (int j = 0; j < nblk && warp_live; ++j) {
       float sv[128];
-      if (warp_live) {
-        mbar_wait(&s_full[j & 1], (j >> 1) & 1, 4);
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1, 4);
+      tc_after_sync();
+      if (j == 0 && r == 0) TRACE(4);
+      const uint32_t sa = lane_addr + 128 + 128 * (j & 1);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rr[32];
+        TMEM_LD32(sa + c * 32, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]);
+      }
+      // visibility of the block's 128 keys as 4 x 32-bit words (all uniform
+      // except the row's own ancestor bits): cache keys, tree keys, range end
+      const int key0 = k_begin + j * BN;
+      const int ncache = L - key0, nvalid = k_end - key0;
+      uint32_t vis[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t cache_bits = low_bits(ncache - 32 * q);
+        const uint32_t tree_bits = mask_bits32(mrow, key0 + 32 * q - L);
+        vis[q] = valid ? ((cache_bits | tree_bits) & low_bits(nvalid - 32 * q)) : 0u;
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        sv[i] = ((vis[i >> 5] >> (i & 31)) & 1u) ? sv[i] : -INFINITY;
+        mx = fmaxf(mx, sv[i]);
+      }
+      mx *= scale;  // scale > 0: max commutes with scaling (-inf stays -inf)
+      if (j > 0) {  // PV_{j-1} finished: P buffer free, O stable
+        mbar_wait(o_done, (j - 1) & 1, 5);
         tc_after_sync();
-        const uint32_t sa = lane_addr + 128 + 128 * (j & 1);
+      }
+      // lazy max update (exact: O and l always share m_ref); the decision is
+      // per row but tcgen05.ld/st are warp-collective, so the O rescale
+      // runs for the whole warp with corr = 1 on rows that keep their max
+      float corr = 1.f;
+      const bool grow = mx > m_ref + 8.f;
+      if (grow) {
+        corr = ex2(m_ref - mx);
+        l_sum *= corr;
+        m_ref = mx;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t rr[32];
-          TMEM_LD32(sa + c * 32, rr);
+          TMEM_LD32(lane_addr + c * 32, rr);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]);
+          for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
+          TMEM_ST32(lane_addr + c * 32, rr);
         }
-        const int key0 = k_begin + j * BN;
-        float mx = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          const int key = key0 + i;
-          bool vis;
-          if (key >= k_end) vis = false;
-          else if (key < L) vis = true;
-          else {
-            const int t = key - L;
-            vis = p.mask == nullptr ? (t <= node) : (bool)((bits[t >> 6] >> (t & 63)) & 1ull);
-          }
-          sv[i] = (vis && valid) ? sv[i] * p.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, sv[i]);
-        }
-        if (j > 0) {  // PV_{j-1} finished: P buffer free, O stable
-          mbar_wait(o_done, (j - 1) & 1, 5);
-          tc_after_sync();
-        }
-        // lazy max update (exact: O and l always share m_ref); the decision is
-        // per row but tcgen05.ld/st are warp-collective, so the O rescale
-        // runs for the whole warp with corr = 1 on rows that keep their max
-        float corr = 1.f;
-        const bool grow = mx > m_ref + 8.f;
-        if (grow) {
-          corr = exp2f(m_ref - mx);
-          l_sum *= corr;
-          m_ref = mx;
-        }
-        if (j > 0 && __any_sync(0xffffffffu, grow)) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t rr[32];
-            TMEM_LD32(lane_addr + c * 32, rr);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * corr);
-            TMEM_ST32(lane_addr + c * 32, rr);
-          }
-          tmem_wait_st();
-        }
-        float ls = 0.f;
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          uint32_t pk[4];
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const float p0 = m_ref == -INFINITY ? 0.f : exp2f(sv[c * 8 + 2 * h] - m_ref);
-            const float p1 = m_ref == -INFINITY ? 0.f : exp2f(sv[c * 8 + 2 * h + 1] - m_ref);
-            ls += p0 + p1;
-            __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
-            pk[h] = *reinterpret_cast<uint32_t*>(&v2);
-          }
-          *reinterpret_cast<uint4*>(prow + sw128_chunk(r, c)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        }
-        l_sum += ls;
-        fence_proxy_async();
+        tmem_wait_st();
       }
-      if (warp_live) {
-        tc_before_sync();
-        mbar_arrive(p_full);
+      const float mneg = m_ref == -INFINITY ? 0.f : -m_ref;  // masked keys: ex2(-inf) = 0
+      float ls = 0.f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float p0 = ex2(fmaf(sv[c * 8 + 2 * h], scale, mneg));
+          const float p1 = ex2(fmaf(sv[c * 8 + 2 * h + 1], scale, mneg));
+          ls += p0 + p1;
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+          pk[h] = *reinterpret_cast<uint32_t*>(&v2);
+        }
+        *reinterpret_cast<uint4*>(prow + sw128_chunk(r, c)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
+      l_sum += ls;
+      fence_proxy_async();
+      tc_before_sync();
+      mbar_arrive(p_full);
+      if (j == 0 && r == 0) TRACE(5);
     }
     // epilogue: O row from TMEM
     if (warp_live) {
       mbar_wait(o_done, (nblk - 1) & 1, 6);
       tc_after_sync();
+      if (r == 0) TRACE(7);
       float o[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -422,9 +481,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   }
+  if (threadIdx.x == 128) TRACE(8);
   tc_before_sync();
   __syncthreads();
   tc_after_sync();
+  if (threadIdx.x == 0) TRACE(9);
   if (warp == 1) {
     __syncwarp();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
@@ -484,10 +545,10 @@ int attention_tc_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_p
   const uint64_t rows = (uint64_t)n_slots * A * Lmax;
   if (!tc::kv_map(&km, kc, rows) || !tc::kv_map(&vm, vc, rows)) return 0;
   const int mtiles = (max_rows_per_seq + tc::BM - 1) / tc::BM;
-  // split the key range so that ~2 CTAs per SM are in flight
+  // split the key range so that one wave (one CTA per SM) covers the grid
   const int ctas = B * A * mtiles;
   const int nblk_max = (max_keys + tc::BN - 1) / tc::BN;
-  int nsplit = (2 * 148 + ctas - 1) / ctas;
+  int nsplit = 148 / ctas;
   if (nsplit > nblk_max) nsplit = nblk_max;
   if (nsplit > 64) nsplit = 64;
   if (nsplit < 1) nsplit = 1;
@@ -515,6 +576,7 @@ int attention_tc_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_p
   p.part_ml = p.part_o + (size_t)M * A * nsplit * tc::DH;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
+  p.trace = tc::g_trace;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -535,3 +597,8 @@ int attention_tc_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_p
 }
 
 }  // namespace propd
+
+extern "C" int propd_debug_trace(void* buf) {  // development aid: phase timestamps of one CTA
+  propd::tc::g_trace = reinterpret_cast<unsigned long long*>(buf);
+  return 0;
+}

@@ -3,6 +3,7 @@ core) and print the max error of each against a torch fp32 reference.
   python scripts/debug_tc.py B A L n [rows]     (n: grid-tree size selector)
   python scripts/debug_tc.py all                 (loop over cases in subprocesses)
 """
+import ctypes
 import os
 import subprocess
 import sys
@@ -92,3 +93,31 @@ for impl in (1, 2):
     e = (outs[impl] - ref).abs()
     print(f"impl {impl}: max err {e.max().item():.3e}  rows with err>0.05: "
           f"{sorted(set((e > 0.05).nonzero()[:, 0].tolist()))[:10]}")
+if os.environ.get("TRACE") == "1":
+    tb = torch.zeros(16, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    lib.propd_debug_trace.argtypes = [ctypes.c_void_p]
+    lib.propd_debug_trace(tb.data_ptr())
+    out = torch.zeros(M, H, device=dev, dtype=torch.bfloat16)
+    for impl in (2, 1):
+        args = (_lib.BF16, impl, B, M, A, dh, Lmax, B, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc),
+                ptr(vc), ptr(slots), ptr(seq_len), ptr(row_off), ptr(row_node), ptr(mask), n, tmpl.words, ptr(out), H,
+                ptr(ws), ws_bytes, torch.cuda.current_stream().cuda_stream)
+        call("propd_tree_attention", *args)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(20):
+                call("propd_tree_attention", *args[:-1], torch.cuda.current_stream().cuda_stream)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / 20
+        byts = sum(2 * (lens[b] + n) * H * 2 for b in range(B)) + 2 * M * H * 2
+        t = tb.cpu().numpy()
+        print(f"impl {impl}: {us:.1f} us/launch (graph, 20 back-to-back), {byts / us / 1e3:.0f} GB/s algorithmic; "
+              f"CTA(0,0,0) phases ns: {[int(x - t[0]) if x else None for x in t[:10]]}")
