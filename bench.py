@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--attn-impl", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA graphs")
     return ap.parse_args()
 
 
@@ -175,7 +176,7 @@ def run_b200(args, rank: int, world: int, group):
     cfg = model_cfg(args)
     B = args.batch
     be = B200Backend(cfg, dtype="bf16", device=dev, random_device_init=True, max_slots=B + 1, max_tree=256,
-                     kv_len=cfg.max_positions, attn_impl=args.attn_impl)
+                     kv_len=cfg.max_positions, attn_impl=args.attn_impl, use_graphs=not args.no_graphs)
     eng = DecodeEngine(be, engine_cfg(args), None, group=group)
     states = be.synthetic_states(B, args.kv, seed=1000 + rank)
     seqs = [_Seq(st, st.committed[:], rank * B + i) for i, st in enumerate(states)]

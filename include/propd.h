@@ -44,6 +44,8 @@ const char* propd_last_error(void);
 int propd_abi_version(void);
 /* Number of SMs of the current device (0 if no device). */
 int propd_num_sms(void);
+/* One-time kernel attribute setup; call before capturing CUDA graphs. */
+int propd_prepare(void);
 
 /* ---- K1: tree materialisation (token_tree.py:125-170, engine.py:260) ----
  * For sequence b and template node i (row m = b*n + i):
@@ -161,6 +163,12 @@ int propd_verify_commit(int dtype, int B, int n, int D, int kmax, int layers, in
 int propd_kv_compact(int dtype, int B, int D, int layers, int A, int dh, int Lmax, int64_t layer_stride,
                      const int32_t* seq_slot, int32_t* seq_len, const int32_t* acc_node,
                      const int32_t* acc_len, void* kcache, void* vcache, void* stream);
+
+/* Padding for graph-captured passes: rows [*total, S_pad) of the compacted
+ * tables become batch entry B (row_seq = B, row_node = 0, row_src = 0) and
+ * row_off[B+1] = S_pad. */
+int propd_pad_rows(int B, int S_pad, const int32_t* total, int32_t* row_seq, int32_t* row_node, int32_t* row_src,
+                   int32_t* row_off, void* stream);
 
 /* seq_len[seq_slot[b]] += delta (delta_dev[b] if non-NULL, else delta). */
 int propd_seq_advance(int B, const int32_t* seq_slot, int32_t* seq_len, const int32_t* delta_dev,

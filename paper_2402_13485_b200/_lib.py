@@ -26,6 +26,8 @@ SIGNATURES = {
     "propd_last_error": [],
     "propd_abi_version": [],
     "propd_num_sms": [],
+    "propd_prepare": [],
+    "propd_pad_rows": [I, I, P, P, P, P, P, P],
     "propd_tree_embed": [I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "propd_embed_rows": [I, I, I, P, P, P, P, P, P],
     "propd_bonus_embed": [I, I, I, P, P, P, P, P, P, P, P, P, P, P],

@@ -122,7 +122,7 @@ class B200Backend:
     def __init__(self, config: TinyTransformerConfig = TinyTransformerConfig(), *, dtype: str = "fp32",
                  device=None, weights: dict | None = None, random_device_init: bool = False,
                  max_slots: int = 16, max_tree: int = MAX_TREE, kv_len: int | None = None,
-                 attn_impl: int = 0) -> None:
+                 attn_impl: int = 0, use_graphs: bool = False) -> None:
         import torch
 
         self.lib = _lib.load()
@@ -152,21 +152,28 @@ class B200Backend:
         # cache slots hold committed rows (< max_positions) plus one tree
         self.Lmax = (kv_len if kv_len is not None else cfg.max_positions) + self.max_tree
         self.max_slots = int(max_slots)
+        self.scratch_slot = self.max_slots  # extra cache slot: pad rows of graph-captured passes
         dev, T = self.device, self.tdtype
-        shape = (cfg.layers, self.max_slots, self.A, self.Lmax, self.dh)
+        shape = (cfg.layers, self.max_slots + 1, self.A, self.Lmax, self.dh)
         # zero-filled: key blocks streamed by the tensor-core kernel may extend
         # past the live keys; masked keys get p = 0, and 0 * garbage-NaN would
         # poison the P.V product, so every cache row must hold a finite value
         self.kcache = torch.zeros(shape, device=dev, dtype=T)
         self.vcache = torch.zeros(shape, device=dev, dtype=T)
-        self.layer_stride = self.max_slots * self.A * self.Lmax * self.dh
-        self.seq_len = torch.zeros(self.max_slots, device=dev, dtype=torch.int32)
-        self.root = torch.zeros(self.max_slots, device=dev, dtype=torch.int32)
-        self.hidden = torch.zeros(self.max_slots, self.H, device=dev, dtype=T)
-        self.last_logits = torch.zeros(self.max_slots, self.V, device=dev, dtype=torch.float32)
+        self.n_slots = self.max_slots + 1
+        self.layer_stride = self.n_slots * self.A * self.Lmax * self.dh
+        self.seq_len = torch.zeros(self.n_slots, device=dev, dtype=torch.int32)
+        self.root = torch.zeros(self.n_slots, device=dev, dtype=torch.int32)
+        self.hidden = torch.zeros(self.n_slots, self.H, device=dev, dtype=T)
+        self.last_logits = torch.zeros(self.n_slots, self.V, device=dev, dtype=torch.float32)
+        self.use_graphs = bool(use_graphs)
+        self._graphs: dict = {}
+        self._slot_static: dict = {}
+        self._pool = torch.cuda.graph_pool_handle() if self.use_graphs else None
         self._len = [0] * self.max_slots  # host mirror of seq_len
         self._free = list(range(self.max_slots - 1, -1, -1))
         self._ws = torch.empty(0, device=dev, dtype=torch.uint8)
+        call("propd_prepare")
         self._one_mask = torch.ones(1, device=dev, dtype=torch.int64)  # single-node template {0}
         self._keepalive: list = []
         self.launches = 0  # libpropd kernel launches issued (bench accounting)
@@ -224,8 +231,15 @@ class B200Backend:
         self._keepalive.append(t)
         return t
 
-    def _workspace(self, M: int) -> object:
-        need = int(self.lib.propd_attn_workspace_bytes(M, self.A, self.dh, 0))
+    def _workspace(self, M: int, B: int) -> object:
+        """Split-KV partials for one attention launch.  Under graph capture a
+        fresh (graph-owned) buffer per launch; eagerly a grown shared one."""
+        splits = min(64, -(-296 // max(1, B * self.A)))
+        if splits <= 1:
+            return None
+        need = int(self.lib.propd_attn_workspace_bytes(M, self.A, self.dh, splits))
+        if self.use_graphs:
+            return self.torch.empty(need, device=self.device, dtype=self.torch.uint8)
         if self._ws.numel() < need:
             self._ws = self.torch.empty(need, device=self.device, dtype=self.torch.uint8)
         return self._ws
@@ -236,7 +250,8 @@ class B200Backend:
         the last MLP output not yet added to the residual stream x."""
         torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
         M = rt.M
-        ws = self._workspace(M)
+        ws = self._workspace(M, rt.B)
+        ws_bytes = 0 if ws is None else ws.numel()
         h = torch.empty(M, H, device=self.device, dtype=T)
         ctx = torch.empty(M, H, device=self.device, dtype=T)
         for l in range(l0, l1):
@@ -249,9 +264,9 @@ class B200Backend:
                 ev0 = torch.cuda.Event(enable_timing=True)
                 ev0.record()
             self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
-                       self.max_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
+                       self.n_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
                        ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
-                       ptr(ws), ws.numel(), st)
+                       ptr(ws), ws_bytes, st)
             if self.attn_timer is not None:
                 ev1 = torch.cuda.Event(enable_timing=True)
                 ev1.record()
@@ -493,49 +508,192 @@ class B200Backend:
         state._tree = None
 
     # ------------------------------------------------- batched steps
-    def step_autoregressive(self, states) -> np.ndarray:
-        """AR iteration for a batch: commit each sequence's root argmax (engine.py:231-241)."""
-        torch = self.torch
-        B = len(states)
-        seq_slot = self._i32([s.slot for s in states])
-        bonus = self.root.index_select(0, seq_slot.long())
-        self._bonus_pass(seq_slot, bonus, B, max(self._len[s.slot] for s in states) + 1,
-                         sum(self._len[s.slot] + 1 for s in states))
-        out = bonus.cpu().numpy()
-        for s, t in zip(states, out):
-            s.committed.append(int(t))
-            self._len[s.slot] += 1
-        del torch
-        return out
+    # The batched step is organised as two device programs so that each can
+    # be captured once in a CUDA graph and replayed (the per-step host cost
+    # is then a few copies and two graph launches):
+    #   part A  (B, tree, key bucket)        draft -> K1 -> layers 1..p
+    #           [-> early head -> K3 membership + closure/compaction]
+    #   part B  (B, tree, S_pad, key bucket) layers p+1..Ly on the S
+    #           surviving rows padded to S_pad (pad rows form one extra
+    #           scratch "sequence"), LM argmax, K5 accept + KV compaction,
+    #           bonus pass.
+    # Between them the host reads the survivor count S (the one mid-step sync).
+    # Without pruning part A runs all layers and part B starts at the LM head.
 
-    def _bonus_pass(self, seq_slot, bonus, B: int, max_keys: int, kv_keys: int = 0) -> None:
+    def _key_bucket(self, need: int) -> int:
+        """Attention launch geometry (key range) is captured in the graph:
+        round the largest per-sequence key count up to a 256-key bucket."""
+        return min(self.Lmax, ((need + 255) // 256) * 256)
+
+    def _slot_buf(self, B: int, slots):
+        """Device int32 [B+1] = active slots + the scratch slot (pad rows)."""
+        torch = self.torch
+        host = np.asarray(list(slots) + [self.scratch_slot], dtype=np.int32)
+        if not self.use_graphs:
+            t = torch.from_numpy(host).to(self.device)
+            self._keepalive.append(t)
+            return t
+        buf = self._slot_static.get(B)
+        if buf is None:
+            buf = self._slot_static[B] = torch.empty(B + 1, device=self.device, dtype=torch.int32)
+        pin = torch.from_numpy(host).pin_memory()
+        buf.copy_(pin, non_blocking=True)
+        return buf
+
+    def _run(self, key, fn):
+        """Eager: run fn.  Graph mode: capture fn once per key, then replay."""
+        if not self.use_graphs:
+            return fn()
+        ent = self._graphs.get(key)
+        if ent is None:
+            torch = self.torch
+            n0 = self.launches
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=self._pool):
+                outs = fn()
+            ent = self._graphs[key] = (g, outs, self.launches - n0)
+        else:
+            self.launches += ent[2]
+        ent[0].replay()
+        return ent[1]
+
+    def _bonus_program(self, seq_slot, bonus, B: int, max_keys: int):
         """One committed row per sequence at position seq_len (backends.py:239-259
         for the bonus token): K/V append, hidden/root update, seq_len += 1."""
         torch, st = self.torch, self.stream()
-        x = torch.empty(B, self.H, device=self.device, dtype=torch.float32)
-        positions = torch.empty(B, device=self.device, dtype=torch.int32)
-        row_seq = torch.empty(B, device=self.device, dtype=torch.int32)
-        row_node = torch.empty(B, device=self.device, dtype=torch.int32)
-        row_off = torch.empty(B + 1, device=self.device, dtype=torch.int32)
+        dev = self.device
+        x = torch.empty(B, self.H, device=dev, dtype=torch.float32)
+        positions = torch.empty(B, device=dev, dtype=torch.int32)
+        row_seq = torch.empty(B, device=dev, dtype=torch.int32)
+        row_node = torch.empty(B, device=dev, dtype=torch.int32)
+        row_off = torch.empty(B + 1, device=dev, dtype=torch.int32)
         self._call("propd_bonus_embed", self.code, B, self.H, ptr(bonus), ptr(seq_slot), ptr(self.seq_len),
                    ptr(self.w.emb), ptr(self.w.pos), ptr(x), ptr(positions), ptr(row_seq), ptr(row_node),
                    ptr(row_off), st)
-        rt = Rows(B, B, seq_slot, row_seq, row_node, row_off, max_keys=max_keys, max_rows=1, kv_keys=kv_keys)
+        rt = Rows(B, B, seq_slot, row_seq, row_node, row_off, max_keys=max_keys, max_rows=1)
         pending = self._run_layers(x, rt, 0, self.num_layers, self._one_mask, 1, 1)
-        hfin = torch.empty(B, self.H, device=self.device, dtype=self.tdtype)
+        hfin = torch.empty(B, self.H, device=dev, dtype=self.tdtype)
         self._call("propd_add_ln", self.code, B, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
         logits, am = self._lm_argmax(hfin)
         self.hidden.index_copy_(0, seq_slot.long(), hfin)
         self._call("propd_scatter_i32", B, ptr(seq_slot), ptr(am), ptr(self.root), st)
         self._call("propd_seq_advance", B, ptr(seq_slot), ptr(self.seq_len), None, 1, st)
 
+    def step_autoregressive(self, states) -> np.ndarray:
+        """AR iteration for a batch: commit each sequence's root argmax (engine.py:231-241)."""
+        B = len(states)
+        lens = [self._len[s.slot] for s in states]
+        if max(lens) + 1 > self.config.max_positions:
+            raise ValueError("sequence exceeds max_positions")
+        slot_buf = self._slot_buf(B, [s.slot for s in states])
+        kb = self._key_bucket(max(lens) + 1)
+
+        def program():
+            seq_slot = slot_buf[:B]
+            bonus = self.root.index_select(0, seq_slot.long())
+            self._bonus_program(seq_slot, bonus, B, kb)
+            return bonus
+
+        bonus = self._run(("ar", B, kb), program)
+        out = bonus.cpu().numpy()
+        for s, t in zip(states, out):
+            s.committed.append(int(t))
+            self._len[s.slot] += 1
+        return out
+
+    def _part_a(self, B, tmpl, k, prune, slot_buf, kb):
+        torch, st, cfg = self.torch, self.stream(), self.config
+        n, D, H, V = len(tmpl), cfg.draft_heads, self.H, self.V
+        dev = self.device
+        td = tmpl.device(dev)
+        seq_slot = slot_buf[:B]
+        o = {}
+        o["draft_tok"], _ = self._draft_dev(seq_slot, B, k)
+        M = B * n
+        i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
+        o["tokens"], o["positions"] = i32(M), i32(M)
+        row_seq, row_node, row_off = i32(M), i32(M), i32(B + 1)
+        x = torch.empty(M, H, device=dev, dtype=torch.float32)
+        self._call("propd_tree_embed", self.code, B, n, D, k, H, ptr(td["depth"]), ptr(td["rank"]),
+                   ptr(o["draft_tok"]), ptr(seq_slot), ptr(self.seq_len), ptr(self.w.emb), ptr(self.w.pos),
+                   ptr(o["tokens"]), ptr(o["positions"]), ptr(x), ptr(row_seq), ptr(row_node), ptr(row_off), st)
+        rt = Rows(M, B, seq_slot, row_seq, row_node, row_off, max_keys=kb, max_rows=n)
+        p = prune.layer if prune is not None else cfg.layers
+        pending = self._run_layers(x, rt, 0, p, td["mask"], n, tmpl.words)
+        o["x"], o["rt"] = x, rt
+        if prune is None:
+            o["pending"] = pending
+            return o
+        self._flush(x, pending)
+        Pn = len(tmpl.parent_nodes)
+        member = torch.ones(M, device=dev, dtype=torch.uint8)
+        if Pn > 0:
+            par = td[("par_rows", B)]
+            xp = torch.empty(B * Pn, H, device=dev, dtype=self.tdtype)
+            self._call("propd_gather_rows", self.code, B * Pn, H, ptr(x), ptr(par), ptr(xp), st)
+            early = torch.mm(xp, self.w.w_early)
+            if early.dtype != torch.float32:
+                early = early.float()
+            self._call("propd_early_member", B, n, Pn, V, min(prune.topk, V), ptr(early), ptr(td["parent"]),
+                       ptr(td["parent_slot"]), ptr(o["tokens"]), ptr(member), st)
+        o["alive"] = torch.empty(M, device=dev, dtype=torch.uint8)
+        # compacted row tables sized for the worst case + pad entry
+        cap = max(M, self._s_bucket(M))
+        o["nrs"], o["nrn"], o["nsrc"], o["node_row"] = i32(cap), i32(cap), i32(cap), i32(M)
+        o["noff"], o["surv_cnt"], o["total"] = i32(B + 2), i32(B), i32(1)
+        self._call("propd_prune_compact", B, n, ptr(td["parent"]), ptr(member), ptr(o["alive"]), ptr(o["nrs"]),
+                   ptr(o["nrn"]), ptr(o["nsrc"]), ptr(o["noff"]), ptr(o["node_row"]), ptr(o["surv_cnt"]),
+                   ptr(o["total"]), st)
+        return o
+
+    def _part_b(self, B, tmpl, k, prune, slot_buf, kb, a, S_pad):
+        torch, st, cfg = self.torch, self.stream(), self.config
+        n, D, H = len(tmpl), cfg.draft_heads, self.H
+        dev = self.device
+        td = tmpl.device(dev)
+        seq_slot = slot_buf[:B]
+        if prune is not None:
+            # rows [S, S_pad) become the scratch sequence (batch entry B)
+            self._call("propd_pad_rows", B, S_pad, ptr(a["total"]), ptr(a["nrs"]), ptr(a["nrn"]), ptr(a["nsrc"]),
+                       ptr(a["noff"]), st)
+            x = torch.empty(S_pad, H, device=dev, dtype=torch.float32)
+            self._call("propd_gather_rows", 0, S_pad, H, ptr(a["x"]), ptr(a["nsrc"]), ptr(x), st)
+            rt = Rows(S_pad, B + 1, slot_buf, a["nrs"], a["nrn"], a["noff"], max_keys=kb, max_rows=n)
+            pending = self._run_layers(x, rt, prune.layer, cfg.layers, td["mask"], n, tmpl.words)
+            alive, node_row = a["alive"], a["node_row"]
+        else:
+            x, pending, alive, node_row = a["x"], a["pending"], None, None
+        S = x.shape[0]
+        hfin = torch.empty(S, H, device=dev, dtype=self.tdtype)
+        self._call("propd_add_ln", self.code, S, H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
+        _, row_argmax = self._lm_argmax(hfin)
+        i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
+        o = {"acc_node": i32(B * D), "acc_surv": i32(B * D), "acc_len": i32(B), "bonus": i32(B),
+             "committed": i32(B * (D + 1)), "ranks": torch.empty(B, D, device=dev, dtype=torch.int8),
+             "row_argmax": row_argmax, "root_before": self.root.index_select(0, seq_slot.long())}
+        self._call("propd_verify_commit", self.code, B, n, D, k, cfg.layers, self.A, self.dh, self.Lmax,
+                   self.layer_stride, ptr(td["parent"]), ptr(a["tokens"]), ptr(alive), ptr(node_row),
+                   ptr(row_argmax), ptr(self.root), ptr(a["draft_tok"]), ptr(seq_slot), ptr(self.seq_len),
+                   ptr(self.kcache), ptr(self.vcache), ptr(o["acc_node"]), ptr(o["acc_surv"]), ptr(o["acc_len"]),
+                   ptr(o["bonus"]), ptr(o["committed"]), ptr(o["ranks"]), st)
+        self._bonus_program(seq_slot, o["bonus"], B, kb)
+        return o
+
+    @staticmethod
+    def _s_bucket(S: int) -> int:
+        """Post-prune row counts padded to few distinct values (graph reuse):
+        multiples of 8 up to 64, of 32 up to 512, then of 128."""
+        step = 8 if S <= 64 else (32 if S <= 512 else 128)
+        return ((S + step - 1) // step) * step
+
     def step_tree(self, states, tmpl: TreeTemplate, k: int, prune=None, trace: bool = False) -> StepOutput:
         """One batched ProPD tree iteration on the device (engine.py:243-303):
         K4a draft -> K1 tree embed -> layers 1..p -> K3 early prune + row
         compaction -> layers p+1..Ly on survivors -> LM argmax -> K5 accept +
         KV compaction -> bonus pass.  One mid-step sync (survivor count)."""
-        torch, st, cfg = self.torch, self.stream(), self.config
-        B, n, D, H, V = len(states), len(tmpl), cfg.draft_heads, self.H, self.V
+        cfg = self.config
+        B, n, D = len(states), len(tmpl), cfg.draft_heads
         if n > self.max_tree:
             raise ValueError(f"tree of {n} nodes exceeds the backend's max_tree={self.max_tree}")
         if tmpl.max_depth > D:
@@ -543,78 +701,36 @@ class B200Backend:
         lens = [self._len[s.slot] for s in states]
         if max(lens) + tmpl.max_depth + 1 > cfg.max_positions:
             raise ValueError("sequence exceeds max_positions")
-        dev = self.device
-        td = tmpl.device(dev)
-        seq_slot = self._i32([s.slot for s in states])
-        draft_tok, _ = self._draft_dev(seq_slot, B, k)
-        M = B * n
-        i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
-        tokens, positions, row_seq, row_node, row_off = i32(M), i32(M), i32(M), i32(M), i32(B + 1)
-        x = torch.empty(M, H, device=dev, dtype=torch.float32)
-        self._call("propd_tree_embed", self.code, B, n, D, k, H, ptr(td["depth"]), ptr(td["rank"]), ptr(draft_tok),
-                   ptr(seq_slot), ptr(self.seq_len), ptr(self.w.emb), ptr(self.w.pos), ptr(tokens),
-                   ptr(positions), ptr(x), ptr(row_seq), ptr(row_node), ptr(row_off), st)
-        rt = Rows(M, B, seq_slot, row_seq, row_node, row_off, max_keys=max(lens) + n, max_rows=n,
-                  kv_keys=sum(lens) + B * n)
-        mask, W = td["mask"], tmpl.words
-        alive = node_row = None
-        surv_cnt = None
-        p = prune.layer if prune is not None else cfg.layers
-        pending = self._run_layers(x, rt, 0, p, mask, n, W)
+        slot_buf = self._slot_buf(B, [s.slot for s in states])
+        kb = self._key_bucket(max(lens) + n + D + 1)
+        td = tmpl.device(self.device)  # host->device uploads happen outside any capture
+        if ("par_rows", B) not in td:
+            rows = (np.arange(B, dtype=np.int32)[:, None] * n + tmpl.parent_nodes[None, :]).reshape(-1)
+            td[("par_rows", B)] = self.torch.from_numpy(np.ascontiguousarray(rows)).to(self.device)
+        pkey = (prune.layer, prune.topk) if prune is not None else None
+        a = self._run(("A", B, tmpl.paths, k, pkey, kb), lambda: self._part_a(B, tmpl, k, prune, slot_buf, kb))
         if prune is not None:
-            self._flush(x, pending)
-            pending = None
-            Pn = len(tmpl.parent_nodes)
-            member = torch.ones(M, device=dev, dtype=torch.uint8)
-            if Pn > 0:
-                par_rows = (np.arange(B, dtype=np.int32)[:, None] * n + tmpl.parent_nodes[None, :]).reshape(-1)
-                xp = torch.empty(B * Pn, H, device=dev, dtype=self.tdtype)
-                self._call("propd_gather_rows", self.code, B * Pn, H, ptr(x), ptr(self._i32(par_rows)), ptr(xp), st)
-                early = torch.mm(xp, self.w.w_early)
-                if early.dtype != torch.float32:
-                    early = early.float()
-                self._call("propd_early_member", B, n, Pn, V, min(prune.topk, V), ptr(early), ptr(td["parent"]),
-                           ptr(td["parent_slot"]), ptr(tokens), ptr(member), st)
-            alive = torch.empty(M, device=dev, dtype=torch.uint8)
-            nrs, nrn, nsrc, node_row = i32(M), i32(M), i32(M), i32(M)
-            noff, surv_cnt, total = i32(B + 1), i32(B), i32(1)
-            self._call("propd_prune_compact", B, n, ptr(td["parent"]), ptr(member), ptr(alive), ptr(nrs), ptr(nrn),
-                       ptr(nsrc), ptr(noff), ptr(node_row), ptr(surv_cnt), ptr(total), st)
-            S = int(total.item())  # the one mid-step sync: row count of layers > p
-            x2 = torch.empty(S, H, device=dev, dtype=torch.float32)
-            self._call("propd_gather_rows", _lib.F32, S, H, ptr(x), ptr(nsrc), ptr(x2), st)
-            x = x2
-            rt = Rows(S, B, seq_slot, nrs, nrn, noff, max_keys=max(lens) + n, max_rows=n, kv_keys=sum(lens) + S)
-            pending = self._run_layers(x, rt, p, cfg.layers, mask, n, W)
-        S = rt.M
-        hfin = torch.empty(S, H, device=dev, dtype=self.tdtype)
-        self._call("propd_add_ln", self.code, S, H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
-        _, row_argmax = self._lm_argmax(hfin)
-        acc_node, acc_surv = i32(B * D), i32(B * D)
-        acc_len, bonus = i32(B), i32(B)
-        committed = i32(B * (D + 1))
-        ranks = torch.empty(B, D, device=dev, dtype=torch.int8)
-        root_before = self.root.index_select(0, seq_slot.long()) if trace else None
-        self._call("propd_verify_commit", self.code, B, n, D, k, cfg.layers, self.A, self.dh, self.Lmax,
-                   self.layer_stride, ptr(td["parent"]), ptr(tokens), ptr(alive), ptr(node_row), ptr(row_argmax),
-                   ptr(self.root), ptr(draft_tok), ptr(seq_slot), ptr(self.seq_len), ptr(self.kcache),
-                   ptr(self.vcache), ptr(acc_node), ptr(acc_surv), ptr(acc_len), ptr(bonus), ptr(committed),
-                   ptr(ranks), st)
-        self._bonus_pass(seq_slot, bonus, B, max(lens) + D + 1, sum(lens) + B)
-        out = StepOutput(committed.view(B, D + 1).cpu().numpy(), acc_len.cpu().numpy(),
-                         acc_surv.view(B, D).cpu().numpy(),
-                         surv_cnt.cpu().numpy() if surv_cnt is not None else np.full(B, n, dtype=np.int32),
-                         ranks)
-        for s, row, a in zip(states, out.committed, out.acc_len):
-            new = [int(t) for t in row[: a + 1]]
+            S = int(a["total"].item())  # the one mid-step sync: row count of layers > p
+            S_pad = self._s_bucket(S) if self.use_graphs else S
+        else:
+            S = S_pad = B * n
+        b = self._run(("B", B, tmpl.paths, k, pkey, kb, S_pad),
+                      lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad))
+        out = StepOutput(b["committed"].view(B, D + 1).cpu().numpy(), b["acc_len"].cpu().numpy(),
+                         b["acc_surv"].view(B, D).cpu().numpy(),
+                         a["surv_cnt"].cpu().numpy() if prune is not None else np.full(B, n, dtype=np.int32),
+                         b["ranks"])
+        for s, row, acc in zip(states, out.committed, out.acc_len):
+            new = [int(t) for t in row[: acc + 1]]
             s.committed.extend(new)
             self._len[s.slot] += len(new)
         if trace:
-            out.trace = {"tokens": tokens.view(B, n).cpu().numpy(), "positions": positions.view(B, n).cpu().numpy(),
-                         "draft_tokens": draft_tok.cpu().numpy(), "root": root_before.cpu().numpy(),
-                         "alive": alive.view(B, n).cpu().numpy() if alive is not None else np.ones((B, n), np.uint8),
-                         "node_row": node_row.view(B, n).cpu().numpy() if node_row is not None else
-                         np.arange(M).reshape(B, n), "row_argmax": row_argmax.cpu().numpy()}
+            alive = a["alive"].view(B, n).cpu().numpy() if prune is not None else np.ones((B, n), np.uint8)
+            node_row = a["node_row"].view(B, n).cpu().numpy() if prune is not None else np.arange(B * n).reshape(B, n)
+            out.trace = {"tokens": a["tokens"].view(B, n).cpu().numpy(),
+                         "positions": a["positions"].view(B, n).cpu().numpy(),
+                         "draft_tokens": a["draft_tok"].cpu().numpy(), "root": b["root_before"].cpu().numpy(),
+                         "alive": alive, "node_row": node_row, "row_argmax": b["row_argmax"].cpu().numpy()}
         return out
 
     def stats_replay_select(self, ranks_dev, S: int, P, counts, alpha, order, lcurve) -> None:

@@ -598,6 +598,13 @@ int attention_tc_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_p
 
 }  // namespace propd
 
+extern "C" int propd_prepare(void) {  // one-time function attributes (before any graph capture)
+  cudaError_t e = cudaFuncSetAttribute(propd::tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       propd::tc::SMEM_TOTAL);
+  if (e != cudaSuccess) return propd::fail("prepare: %s", cudaGetErrorString(e));
+  return 0;
+}
+
 extern "C" int propd_debug_trace(void* buf) {  // development aid: phase timestamps of one CTA
   propd::tc::g_trace = reinterpret_cast<unsigned long long*>(buf);
   return 0;

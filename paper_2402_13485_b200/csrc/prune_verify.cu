@@ -93,6 +93,19 @@ __global__ void prune_compact_kernel(int B, int n, const int32_t* __restrict__ p
   }
 }
 
+// Graph-captured passes run layers > p on a padded row count: rows
+// [total, S_pad) become batch entry B (the scratch slot, node 0).
+__global__ void pad_rows_kernel(int B, int S_pad, const int32_t* __restrict__ total, int32_t* row_seq,
+                                int32_t* row_node, int32_t* row_src, int32_t* row_off) {
+  const int S = *total;
+  for (int i = S + blockIdx.x * blockDim.x + threadIdx.x; i < S_pad; i += gridDim.x * blockDim.x) {
+    row_seq[i] = B;
+    row_node[i] = 0;
+    row_src[i] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) row_off[B + 1] = S_pad;
+}
+
 // ---------------------------------------------------------------- K5 ------
 constexpr int MAX_D = 32;
 
@@ -318,6 +331,12 @@ int propd_prune_compact(int B, int n, const int32_t* parent, const uint8_t* memb
   prune_compact_kernel<<<1, threads, 0, as_stream(stream)>>>(B, n, parent, member, alive, new_row_seq, new_row_node,
                                                              new_row_src, new_row_off, node_row, surv_cnt, total);
   return check_launch("prune_compact");
+}
+
+int propd_pad_rows(int B, int S_pad, const int32_t* total, int32_t* row_seq, int32_t* row_node, int32_t* row_src,
+                   int32_t* row_off, void* stream) {
+  pad_rows_kernel<<<1, 256, 0, as_stream(stream)>>>(B, S_pad, total, row_seq, row_node, row_src, row_off);
+  return check_launch("pad_rows");
 }
 
 int propd_verify_commit(int dtype, int B, int n, int D, int kmax, int layers, int A, int dh, int Lmax,

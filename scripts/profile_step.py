@@ -25,11 +25,13 @@ ap.add_argument("--mode", default="propd_full")
 ap.add_argument("--topk", type=int, default=16)
 ap.add_argument("--attn-impl", type=int, default=0)
 ap.add_argument("--out", default="gpurun_out/profile")
+ap.add_argument("--graphs", action="store_true")
+ap.add_argument("--no-cpu-baseline", action="store_true")
 args = ap.parse_args()
 
 cfg = bench.model_cfg(args)
 be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=args.batch + 1, kv_len=cfg.max_positions,
-                 attn_impl=args.attn_impl)
+                 attn_impl=args.attn_impl, use_graphs=args.graphs)
 eng = DecodeEngine(be, bench.engine_cfg(args), None)
 states = be.synthetic_states(args.batch, args.kv)
 seqs = [_Seq(st, st.committed[:], i) for i, st in enumerate(states)]

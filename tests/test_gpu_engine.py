@@ -50,10 +50,18 @@ def run_tiny_backend():
     return tiny_backend(RUN_TINY["model"])
 
 
+@pytest.fixture(scope="module")
+def run_tiny_graph_backend():
+    return tiny_backend(RUN_TINY["model"], use_graphs=True)
+
+
+@pytest.mark.parametrize("graphs", [False, True])
 @pytest.mark.parametrize("mode", MODES)
-def test_run_tiny_batched_engine_matches_reference(golden_dir, run_tiny_backend, mode):
+def test_run_tiny_batched_engine_matches_reference(golden_dir, run_tiny_backend, run_tiny_graph_backend, mode,
+                                                   graphs):
     g = load(golden_dir, f"run_tiny_{mode}.json")
-    eng = DecodeEngine(run_tiny_backend, product_cfg(RUN_TINY["engine"], mode), op.Clock(**RUN_TINY["clock"]))
+    be = run_tiny_graph_backend if graphs else run_tiny_backend
+    eng = DecodeEngine(be, product_cfg(RUN_TINY["engine"], mode), op.Clock(**RUN_TINY["clock"]))
     w = RUN_TINY["workload"]
     res = eng.run(g["prompts"], w["max_tokens"], batch_size=w["batch_size"])
     assert res.transcripts == g["transcripts"]
