@@ -113,6 +113,8 @@ class StepOutput:
     surv_cnt: np.ndarray  # [B]
     ranks_dev: object  # device int8 [B, D] acceptance records
     trace: dict | None = None
+    order: np.ndarray | None = None  # selection order after this step's stats replay (single process)
+    lcurve: np.ndarray | None = None
 
 
 class B200Backend:
@@ -168,8 +170,11 @@ class B200Backend:
         self.last_logits = torch.zeros(self.n_slots, self.V, device=dev, dtype=torch.float32)
         self.use_graphs = bool(use_graphs)
         self._graphs: dict = {}
+        self._templates: dict = {}
+        self._host: dict = {}
         self._slot_static: dict = {}
         self._pool = torch.cuda.graph_pool_handle() if self.use_graphs else None
+        self._cap_stream = None
         self._len = [0] * self.max_slots  # host mirror of seq_len
         self._free = list(range(self.max_slots - 1, -1, -1))
         self._ws = torch.empty(0, device=dev, dtype=torch.uint8)
@@ -177,7 +182,11 @@ class B200Backend:
         self._one_mask = torch.ones(1, device=dev, dtype=torch.int64)  # single-node template {0}
         self._keepalive: list = []
         self.launches = 0  # libpropd kernel launches issued (bench accounting)
-        self.attn_timer = None  # list -> (start, end, rows) CUDA events of every K2 launch
+        self.attn_timer = None  # list -> per-launch {ms, bytes, role} of every K2 launch (bench)
+        self._capturing = False
+        self._capture_events: list = []
+        self._pending_events: list = []
+        self._role = "eager"
 
     # ------------------------------------------------------------------ API
     @property
@@ -261,22 +270,45 @@ class B200Backend:
             self._call("propd_kv_append", self.code, M, self.A, self.dh, self.Lmax, ptr(qkv), 3 * H,
                        ptr(rt.row_seq), ptr(rt.row_node), ptr(rt.seq_slot), ptr(self.seq_len), ptr(kc), ptr(vc), st)
             if self.attn_timer is not None:
-                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0 = self._timing_event()
                 ev0.record()
             self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
                        self.n_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
                        ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
                        ptr(ws), ws_bytes, st)
             if self.attn_timer is not None:
-                ev1 = torch.cuda.Event(enable_timing=True)
+                ev1 = self._timing_event()
                 ev1.record()
-                self.attn_timer.append((ev0, ev1, rt))
+                self._events_sink().append((ev0, ev1, self._role, M))
             o = torch.mm(ctx, self.w.wo[l])
             self._call("propd_add_ln", self.code, M, H, ptr(x), ptr(o), ptr(h), None, None, st)
             g = torch.mm(h, self.w.w1[l])
             self._call("propd_gelu", self.code, g.numel(), ptr(g), st)
             pending = torch.mm(g, self.w.w2[l])
         return pending
+
+    # ------------------------------------------------- K2 timing (bench)
+    def _timing_event(self):
+        torch = self.torch
+        if self._capturing:  # event-record nodes inside the graph
+            return torch.cuda.Event(enable_timing=True, external=True)
+        return torch.cuda.Event(enable_timing=True)
+
+    def _events_sink(self) -> list:
+        return self._capture_events if self._capturing else self._pending_events
+
+    def _harvest(self, keys: dict) -> None:
+        """After a step's synchronisation: per-launch K2 time + algorithmic bytes
+        (K/V rows streamed + Q read + O written, bf16/fp32 elements)."""
+        if self.attn_timer is None:
+            self._pending_events.clear()
+            return
+        elt = 2 if self.tdtype != self.torch.float32 else 4
+        for e0, e1, role, M in self._pending_events:
+            kv, rows = keys.get(role, (0, M))
+            self.attn_timer.append({"ms": e0.elapsed_time(e1), "role": role,
+                                    "bytes": kv * 2 * self.H * elt + 2 * rows * self.H * elt})
+        self._pending_events.clear()
 
     def _flush(self, x, pending):
         if pending is not None:
@@ -548,14 +580,27 @@ class B200Backend:
         if ent is None:
             torch = self.torch
             n0 = self.launches
+            if self._cap_stream is None:
+                # cuBLAS handles/workspaces must exist for the capture stream
+                # before capture begins (they cannot be created while capturing)
+                self._cap_stream = torch.cuda.Stream(self.device)
+                with torch.cuda.stream(self._cap_stream):
+                    for dt in {self.tdtype, torch.float32}:
+                        z = torch.zeros(16, 16, device=self.device, dtype=dt)
+                        torch.mm(z, z)
             torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, pool=self._pool):
-                outs = fn()
-            ent = self._graphs[key] = (g, outs, self.launches - n0)
+            self._capturing, self._capture_events = True, []
+            try:
+                with torch.cuda.graph(g, pool=self._pool, stream=self._cap_stream):
+                    outs = fn()
+            finally:
+                self._capturing = False
+            ent = self._graphs[key] = (g, outs, self.launches - n0, self._capture_events)
         else:
             self.launches += ent[2]
         ent[0].replay()
+        self._pending_events.extend(ent[3])
         return ent[1]
 
     def _bonus_program(self, seq_slot, bonus, B: int, max_keys: int):
@@ -572,7 +617,9 @@ class B200Backend:
                    ptr(self.w.emb), ptr(self.w.pos), ptr(x), ptr(positions), ptr(row_seq), ptr(row_node),
                    ptr(row_off), st)
         rt = Rows(B, B, seq_slot, row_seq, row_node, row_off, max_keys=max_keys, max_rows=1)
+        role, self._role = self._role, "bonus"
         pending = self._run_layers(x, rt, 0, self.num_layers, self._one_mask, 1, 1)
+        self._role = role
         hfin = torch.empty(B, self.H, device=dev, dtype=self.tdtype)
         self._call("propd_add_ln", self.code, B, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
         logits, am = self._lm_argmax(hfin)
@@ -595,8 +642,10 @@ class B200Backend:
             self._bonus_program(seq_slot, bonus, B, kb)
             return bonus
 
+        self._role = "bonus"
         bonus = self._run(("ar", B, kb), program)
         out = bonus.cpu().numpy()
+        self._harvest({"bonus": (sum(lens) + B, B)})
         for s, t in zip(states, out):
             s.committed.append(int(t))
             self._len[s.slot] += 1
@@ -687,7 +736,20 @@ class B200Backend:
         step = 8 if S <= 64 else (32 if S <= 512 else 128)
         return ((S + step - 1) // step) * step
 
-    def step_tree(self, states, tmpl: TreeTemplate, k: int, prune=None, trace: bool = False) -> StepOutput:
+    def _host_bufs(self, B: int, D: int, G: int) -> dict:
+        """Pinned host staging buffers for the per-step readback (per shape)."""
+        key = (B, D, G)
+        hb = self._host.get(key)
+        if hb is None:
+            torch = self.torch
+            pin = lambda n, dt: torch.empty(n, dtype=dt).pin_memory()
+            hb = self._host[key] = {"committed": pin(B * (D + 1), torch.int32), "acc_len": pin(B, torch.int32),
+                                    "acc_surv": pin(B * D, torch.int32), "surv_cnt": pin(B, torch.int32),
+                                    "order": pin(G, torch.int32), "lcurve": pin(G, torch.float64)}
+        return hb
+
+    def step_tree(self, states, tmpl: TreeTemplate, k: int, prune=None, trace: bool = False,
+                  stats=None) -> StepOutput:
         """One batched ProPD tree iteration on the device (engine.py:243-303):
         K4a draft -> K1 tree embed -> layers 1..p -> K3 early prune + row
         compaction -> layers p+1..Ly on survivors -> LM argmax -> K5 accept +
@@ -701,6 +763,9 @@ class B200Backend:
         lens = [self._len[s.slot] for s in states]
         if max(lens) + tmpl.max_depth + 1 > cfg.max_positions:
             raise ValueError("sequence exceeds max_positions")
+        # captured graphs hold the template's device pointers: the backend owns
+        # one canonical template per tree shape for its whole lifetime
+        tmpl = self._templates.setdefault(tmpl.paths, tmpl)
         slot_buf = self._slot_buf(B, [s.slot for s in states])
         kb = self._key_bucket(max(lens) + n + D + 1)
         td = tmpl.device(self.device)  # host->device uploads happen outside any capture
@@ -708,18 +773,41 @@ class B200Backend:
             rows = (np.arange(B, dtype=np.int32)[:, None] * n + tmpl.parent_nodes[None, :]).reshape(-1)
             td[("par_rows", B)] = self.torch.from_numpy(np.ascontiguousarray(rows)).to(self.device)
         pkey = (prune.layer, prune.topk) if prune is not None else None
+        self._role = "tree"
         a = self._run(("A", B, tmpl.paths, k, pkey, kb), lambda: self._part_a(B, tmpl, k, prune, slot_buf, kb))
         if prune is not None:
             S = int(a["total"].item())  # the one mid-step sync: row count of layers > p
             S_pad = self._s_bucket(S) if self.use_graphs else S
         else:
             S = S_pad = B * n
+        self._role = "tree_pruned"
         b = self._run(("B", B, tmpl.paths, k, pkey, kb, S_pad),
                       lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad))
-        out = StepOutput(b["committed"].view(B, D + 1).cpu().numpy(), b["acc_len"].cpu().numpy(),
-                         b["acc_surv"].view(B, D).cpu().numpy(),
-                         a["surv_cnt"].cpu().numpy() if prune is not None else np.full(B, n, dtype=np.int32),
+        if stats is not None:  # single process: replay this batch's records right away (K4)
+            P, counts, alpha, order_dev, lcurve_dev = stats
+            self.stats_replay_select(b["ranks"], B, P, counts, alpha, order_dev, lcurve_dev)
+        # one synchronisation for every host-visible result of the step
+        hb = self._host_bufs(B, D, order_dev.numel() if stats is not None else 0)
+        hb["committed"].copy_(b["committed"], non_blocking=True)
+        hb["acc_len"].copy_(b["acc_len"], non_blocking=True)
+        hb["acc_surv"].copy_(b["acc_surv"], non_blocking=True)
+        if prune is not None:
+            hb["surv_cnt"].copy_(a["surv_cnt"], non_blocking=True)
+        if stats is not None:
+            hb["order"].copy_(order_dev, non_blocking=True)
+            hb["lcurve"].copy_(lcurve_dev, non_blocking=True)
+        self.torch.cuda.current_stream(self.device).synchronize()
+        out = StepOutput(hb["committed"].numpy().reshape(B, D + 1).copy(), hb["acc_len"].numpy().copy(),
+                         hb["acc_surv"].numpy().reshape(B, D).copy(),
+                         hb["surv_cnt"].numpy().copy() if prune is not None else np.full(B, n, dtype=np.int32),
                          b["ranks"])
+        if stats is not None:
+            out.order = hb["order"].numpy().copy()
+            out.lcurve = hb["lcurve"].numpy().copy()
+        L0 = sum(lens)
+        S_real = int(out.surv_cnt.sum())
+        self._harvest({"tree": (L0 + B * n, B * n), "tree_pruned": (L0 + B * n, S_real),
+                       "bonus": (L0 + int(out.acc_len.sum()) + B, B)})
         for s, row, acc in zip(states, out.committed, out.acc_len):
             new = [int(t) for t in row[: acc + 1]]
             s.committed.extend(new)

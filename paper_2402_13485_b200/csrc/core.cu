@@ -94,7 +94,69 @@ __global__ void bonus_embed_kernel(int B, int H, const int32_t* __restrict__ bon
 }
 
 // ------------------------------------------------------------- dense ------
-// One CTA per row.  Two-pass mean/variance like numpy's x.var().
+// One CTA per row, the row held in registers (8 floats per thread per
+// chunk): x (+ delta) is read once, the residual written back once, the
+// normalised row written once.  Two-pass mean / variance like numpy's
+// x.var() (the second pass runs over registers).
+template <typename T, int CHUNKS>
+__global__ void __launch_bounds__(512) add_ln_vec_kernel(int H, float* __restrict__ x, const T* __restrict__ delta,
+                                                          T* __restrict__ out, const int32_t* __restrict__ in_idx,
+                                                          const int32_t* __restrict__ out_idx) {
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  const int src = in_idx ? in_idx[m] : m;
+  const int dst = out_idx ? out_idx[m] : m;
+  float* xr = x + (size_t)src * H;
+  float v[CHUNKS][8];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+    const int h = (c * blockDim.x + threadIdx.x) * 8;
+    if (h < H) {
+      const float4 a = *reinterpret_cast<const float4*>(xr + h);
+      const float4 b = *reinterpret_cast<const float4*>(xr + h + 4);
+      v[c][0] = a.x; v[c][1] = a.y; v[c][2] = a.z; v[c][3] = a.w;
+      v[c][4] = b.x; v[c][5] = b.y; v[c][6] = b.z; v[c][7] = b.w;
+      if (delta) {
+        const T* dr = delta + (size_t)src * H + h;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[c][i] += to_f(dr[i]);
+        *reinterpret_cast<float4*>(xr + h) = make_float4(v[c][0], v[c][1], v[c][2], v[c][3]);
+        *reinterpret_cast<float4*>(xr + h + 4) = make_float4(v[c][4], v[c][5], v[c][6], v[c][7]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += v[c][i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[c][i] = 0.f;
+    }
+  }
+  const float mu = block_sum(s, red) / (float)H;
+  float ss = 0.f;
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+    const int h = (c * blockDim.x + threadIdx.x) * 8;
+    if (h < H) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = v[c][i] - mu;
+        ss += d * d;
+      }
+    }
+  }
+  const float den = sqrtf(block_sum(ss, red) / (float)H + 1e-5f);
+  T* o = out + (size_t)dst * H;
+#pragma unroll
+  for (int c = 0; c < CHUNKS; ++c) {
+    const int h = (c * blockDim.x + threadIdx.x) * 8;
+    if (h < H) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[h + i] = from_f<T>((v[c][i] - mu) / den);
+    }
+  }
+}
+
+// Scalar fallback for widths that are not a multiple of 8.
 template <typename T>
 __global__ void add_ln_kernel(int H, float* __restrict__ x, const T* __restrict__ delta, T* __restrict__ out,
                               const int32_t* __restrict__ in_idx, const int32_t* __restrict__ out_idx) {
@@ -268,18 +330,19 @@ __global__ void kv_append_kernel(int A, int dh, int Lmax, const T* __restrict__ 
                                  const int32_t* __restrict__ row_seq, const int32_t* __restrict__ row_node,
                                  const int32_t* __restrict__ seq_slot, const int32_t* __restrict__ seq_len,
                                  T* __restrict__ kc, T* __restrict__ vc) {
+  // blockIdx.x = row, blockIdx.y = 0 (K) / 1 (V); 16-byte vectors
+  constexpr int VEC = 16 / sizeof(T);
   const int m = blockIdx.x;
   const int b = row_seq[m];
   const int slot = seq_slot[b];
   const int t = seq_len[slot] + row_node[m];
   const int H = A * dh;
-  const T* kr = qkv + (size_t)m * ld + H;
-  const T* vr = kr + H;
-  for (int e = threadIdx.x; e < H; e += blockDim.x) {
+  const T* src = qkv + (size_t)m * ld + (1 + blockIdx.y) * H;
+  T* dst = blockIdx.y == 0 ? kc : vc;
+  for (int e = threadIdx.x * VEC; e < H; e += blockDim.x * VEC) {
     const int a = e / dh, d = e - a * dh;
-    const size_t off = (((size_t)slot * A + a) * Lmax + t) * dh + d;
-    kc[off] = kr[e];
-    vc[off] = vr[e];
+    *reinterpret_cast<uint4*>(dst + (((size_t)slot * A + a) * Lmax + t) * dh + d) =
+        *reinterpret_cast<const uint4*>(src + e);
   }
 }
 
@@ -352,7 +415,22 @@ int propd_add_ln(int dtype, int M, int H, float* x, const void* delta, void* out
                  const int32_t* out_idx, void* stream) {
   if (M == 0) return 0;
   return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
-    add_ln_kernel<T><<<M, threads_for(H), 0, as_stream(stream)>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx);
+    cudaStream_t st = as_stream(stream);
+    if (H % 8 == 0 && H <= 8 * 512 * 4) {
+      // 8 elements per thread per chunk; pick threads so that <= 4 chunks
+      int threads = 32;
+      while (threads * 8 * 4 < H) threads *= 2;
+      if (threads > 512) threads = 512;
+      const int chunks = (H + threads * 8 - 1) / (threads * 8);
+      switch (chunks) {
+        case 1: add_ln_vec_kernel<T, 1><<<M, threads, 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx); break;
+        case 2: add_ln_vec_kernel<T, 2><<<M, threads, 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx); break;
+        case 3: add_ln_vec_kernel<T, 3><<<M, threads, 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx); break;
+        default: add_ln_vec_kernel<T, 4><<<M, threads, 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx); break;
+      }
+    } else {
+      add_ln_kernel<T><<<M, threads_for(H), 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx);
+    }
     return check_launch("add_ln");
   });
 }
@@ -404,7 +482,9 @@ int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, 
                     void* vcache, void* stream) {
   if (M == 0) return 0;
   return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
-    kv_append_kernel<T><<<M, threads_for(A * dh), 0, as_stream(stream)>>>(
+    PROPD_REQUIRE((dh * (int)sizeof(T)) % 16 == 0 && (ldqkv * (int)sizeof(T)) % 16 == 0,
+                  "kv_append: rows must be 16-byte aligned");
+    kv_append_kernel<T><<<dim3(M, 2), 128, 0, as_stream(stream)>>>(
         A, dh, Lmax, (const T*)qkv, ldqkv, row_seq, row_node, seq_slot, seq_len, (T*)kcache, (T*)vcache);
     return check_launch("kv_append");
   });

@@ -196,11 +196,18 @@ class DecodeEngine:
         n = len(tmpl)
         prune = cfg.prune if cfg.uses_prune else None
         states = [s.state for s in active]
-        out = self.backend.step_tree(states, tmpl, cfg.draft_topk, prune, trace=self.trace is not None) if active else None
-        ranks, S = self._gather_records(out, len(active))
-        self.backend.stats_replay_select(ranks, S, self._P, self._counts, cfg.acceptance_alpha,
-                                         self._order_dev, self._lcurve_dev)
-        self._pull_selection()
+        stats = None
+        if self.group is None:  # single process: the backend replays the records in the step's batch
+            stats = (self._P, self._counts, cfg.acceptance_alpha, self._order_dev, self._lcurve_dev)
+        out = self.backend.step_tree(states, tmpl, cfg.draft_topk, prune, trace=self.trace is not None,
+                                     stats=stats) if active else None
+        if stats is not None:
+            self._order, self._lcurve = out.order, out.lcurve
+        else:
+            ranks, S = self._gather_records(out, len(active))
+            self.backend.stats_replay_select(ranks, S, self._P, self._counts, cfg.acceptance_alpha,
+                                             self._order_dev, self._lcurve_dev)
+            self._pull_selection()
         acc_total = surv_total = committed = 0
         rates = []
         if out is not None:
