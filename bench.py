@@ -54,7 +54,7 @@ def model_cfg(args):
     from paper_2402_13485_b200 import TinyTransformerConfig
 
     return TinyTransformerConfig(layers=args.layers, hidden=4096, heads=32, vocab=32000, draft_heads=4,
-                                 max_positions=args.kv + 256 + 8 * (args.steps + args.warmup + 8), seed=0)
+                                 max_positions=args.kv + 5 * (2 * args.steps + args.warmup + 52), seed=0)
 
 
 def engine_cfg(args):
@@ -175,18 +175,24 @@ def run_b200(args, rank: int, world: int, group):
     torch.cuda.set_device(dev)
     cfg = model_cfg(args)
     B = args.batch
-    be = B200Backend(cfg, dtype="bf16", device=dev, random_device_init=True, max_slots=B + 1, max_tree=256,
+    be = B200Backend(cfg, dtype="bf16", device=dev, random_device_init=True, max_slots=B + 1, max_tree=4 * args.topk,
                      kv_len=cfg.max_positions, attn_impl=args.attn_impl, use_graphs=not args.no_graphs)
     eng = DecodeEngine(be, engine_cfg(args), None, group=group)
     states = be.synthetic_states(B, args.kv, seed=1000 + rank)
     seqs = [_Seq(st, st.committed[:], rank * B + i) for i, st in enumerate(states)]
     be.attn_timer = []  # graphs captured from here on carry K2 timing event nodes
-    # untimed priming: one pass through the probe queue visits every tree size
-    # once (first-use cuBLAS heuristics / lazy module loading), then W warm-ups
-    for _ in range(len(eng._probe_queue) + 1):
+    # untimed priming: run until no new CUDA graph has been captured for 6
+    # consecutive steps (every tree size / survivor-row bucket seen so far has
+    # its graphs), then W warm-up steps
+    stable, primed = 0, 0
+    while stable < 6 and primed < 48:
+        n_graphs = len(be._graphs)
         eng._step(seqs, 10 ** 9)
+        primed += 1
+        stable = stable + 1 if len(be._graphs) == n_graphs else 0
     for _ in range(args.warmup):
         eng._step(seqs, 10 ** 9)
+    graphs_before = len(be._graphs)
     torch.cuda.synchronize()
     if group is not None:
         torch.distributed.barrier(group)
@@ -204,6 +210,7 @@ def run_b200(args, rank: int, world: int, group):
             torch.distributed.barrier(group)
     ms = t_start.elapsed_time(t_end)
     launches = be.launches - launches0
+    captures_in_timed = len(be._graphs) - graphs_before
     # second timed region of K steps: per-launch CUDA events around every K2
     # launch (event nodes inside the graphs), harvested after each step
     be.attn_timer = []
@@ -227,8 +234,10 @@ def run_b200(args, rank: int, world: int, group):
         "attn": {"launches": len(attn), "ms_total": attn_ms, "bytes": attn_bytes, "achieved_gbs": achieved,
                  "avg_launch_us": attn_ms / max(1, len(attn)) * 1e3, "verify_ms_total": verify_attn_ms,
                  "peak": hbm, "peak_kind": peak_kind},
-        "weights_bytes": be.w.nbytes(),
+        "weights_bytes": be.w.nbytes(), "priming_steps": primed, "captures_in_timed": captures_in_timed,
     }
+    for st in states:  # free the synthetic sequences' cache slots for the e2e run
+        be.release(st)
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, be, eng, rank, world, group)
@@ -344,6 +353,7 @@ def main():
                      "launches": a["launches"], "avg_launch_us": a["avg_launch_us"]},
         "step_weight_gbs": res["weights_bytes"] * 2 / (ms / K * 1e-3) / 1e9,
         "gpu_launches": res["launches"],
+        "cuda_graphs": {"priming_steps": res["priming_steps"], "captures_in_timed_region": res["captures_in_timed"]},
         "clocks": res["clock"],
         "cpu_baseline": cpu,
         "e2e": res["e2e"],
