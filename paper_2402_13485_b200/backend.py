@@ -243,7 +243,7 @@ class B200Backend:
     def _workspace(self, M: int, B: int) -> object:
         """Split-KV partials for one attention launch.  Under graph capture a
         fresh (graph-owned) buffer per launch; eagerly a grown shared one."""
-        splits = min(64, -(-296 // max(1, B * self.A)))
+        splits = min(64, -(-(4 * 148) // max(1, B * self.A)))
         if splits <= 1:
             return None
         need = int(self.lib.propd_attn_workspace_bytes(M, self.A, self.dh, splits))

@@ -224,6 +224,11 @@ int attention_tc_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_p
                       const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                       void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled);
 
+int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
+                          int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
+                          const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
+                          void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled);
+
 }  // namespace propd
 
 using namespace propd;
@@ -247,6 +252,14 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
                 "tree_attention: template of %d nodes needs W=%d <= %d", n_tmpl, W, ATT_MAXW);
   PROPD_REQUIRE(max_keys >= 1, "tree_attention: max_keys must be positive");
   cudaStream_t st = as_stream(stream);
+  if (impl == 3 || (impl == 0 && dtype == PROPD_BF16 && dh == 128 && max_rows_per_seq <= 4)) {
+    bool handled = false;
+    int e = attention_decode_bf16(B, M, A, Lmax, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
+                                  seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, workspace,
+                                  workspace_bytes, st, &handled);
+    if (e || handled) return e;
+    PROPD_REQUIRE(impl != 3, "tree_attention: decode kernel cannot serve this shape");
+  }
   if (impl == 2 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {
     bool handled = false;
     int e = attention_tc_bf16(B, M, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,

@@ -35,6 +35,7 @@ from oracle import treedecode_port as op  # noqa: E402
 
 B, A, L, nsel = map(int, sys.argv[1:5])
 REV = os.environ.get("REV_SLOTS") == "1"
+IMPLS = tuple(int(x) for x in os.environ.get("IMPLS", "1,2").split(","))
 dev = torch.device("cuda:0")
 paths = op.complete_tree_paths(4, 4)
 paths = sorted(paths, key=lambda p: (len(p), p))[:nsel]
@@ -71,7 +72,7 @@ mask = torch.from_numpy(tmpl.mask_bits.view(np.int64)).to(dev)
 ws_bytes = _lib.load().propd_attn_workspace_bytes(M, A, dh, 0)
 ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
 outs = {}
-for impl in (1, 2):
+for impl in IMPLS:
     out = torch.zeros(M, H, device=dev, dtype=torch.bfloat16)
     call("propd_tree_attention", _lib.BF16, impl, B, M, A, dh, Lmax, B, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc),
          ptr(vc), ptr(slots), ptr(seq_len), ptr(row_off), ptr(row_node), ptr(mask), n, tmpl.words, ptr(out), H,
@@ -89,7 +90,7 @@ for b in range(B):
             V = vc[slot_list[b], a, kk].float()
             s = K @ qkv[b * n + i, a * dh:(a + 1) * dh].float() / np.sqrt(dh)
             ref[b * n + i, a * dh:(a + 1) * dh] = torch.softmax(s, 0) @ V
-for impl in (1, 2):
+for impl in IMPLS:
     e = (outs[impl] - ref).abs()
     print(f"impl {impl}: max err {e.max().item():.3e}  rows with err>0.05: "
           f"{sorted(set((e > 0.05).nonzero()[:, 0].tolist()))[:10]}")
@@ -99,7 +100,7 @@ if os.environ.get("TRACE") == "1":
     lib.propd_debug_trace.argtypes = [ctypes.c_void_p]
     lib.propd_debug_trace(tb.data_ptr())
     out = torch.zeros(M, H, device=dev, dtype=torch.bfloat16)
-    for impl in (2, 1):
+    for impl in IMPLS[::-1]:
         args = (_lib.BF16, impl, B, M, A, dh, Lmax, B, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc),
                 ptr(vc), ptr(slots), ptr(seq_len), ptr(row_off), ptr(row_node), ptr(mask), n, tmpl.words, ptr(out), H,
                 ptr(ws), ws_bytes, torch.cuda.current_stream().cuda_stream)
