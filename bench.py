@@ -21,7 +21,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -67,24 +66,34 @@ def engine_cfg(args):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled through NVML (in-process, no fork)
+    every 100 ms during the timed region."""
 
     def __init__(self, index: int) -> None:
         self.index, self.samples, self._stop = index, [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
-        while not self._stop.is_set():
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception as exc:  # pragma: no cover
+            self.samples.append(("error", str(exc)))
+            return
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        while True:
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                self.samples.append([v.strip() for v in out.stdout.strip().split(",")])
+                mhz = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((mhz, max_mhz, [k for k, b in bits.items() if r & b]))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            if self._stop.wait(0.1):
+                break
 
     def __enter__(self):
         self._t.start()
@@ -95,13 +104,11 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
-        good = [s for s in self.samples if len(s) == 6 and s[0].replace(".", "").isdigit()]
+        good = [s for s in self.samples if s and s[0] != "error"]
         if not good:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for s in good for n, v in zip(names, s[2:]) if v.lower() == "active"})
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": statistics.median(float(s[0]) for s in good), "sm_max_mhz": float(good[0][1]),
-                "reasons": reasons, "samples": len(good)}
+                "reasons": sorted({r for s in good for r in s[2]}), "samples": len(good)}
 
 
 def peaks():
