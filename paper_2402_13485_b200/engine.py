@@ -110,6 +110,7 @@ class DecodeEngine:
             self.static_paths = ()
         sizes = set(self.size_candidates) | ({len(self.static_paths)} if self.static_paths else set())
         self.cost = CostModel(sizes, alpha=config.cost_alpha, staleness_decay=config.cost_staleness)
+        _warm_host_math()
         self._templates: dict = {}
         self._iteration = 0
         self._selection = None
@@ -402,6 +403,15 @@ class DecodeEngine:
         pieces = all_gather_objects([(s.gid, s.generated) for s in seqs], self.group)
         merged = sorted((g for part in pieces for g in part), key=lambda t: t[0])
         return [g for _, g in merged]
+
+
+def _warm_host_math() -> None:
+    """The first weighted least-squares fit initialises numpy's BLAS (tens of
+    ms); do it once up front instead of inside the first replanned step."""
+    cm = CostModel([1, 2], alpha=1.0, staleness_decay=0.0)
+    cm.observe(1, 1.0, now=0)
+    cm.observe(2, 2.0, now=0)
+    cm.fit(now=1)
 
 
 def _shard(n: int, rank: int, world: int) -> list:
