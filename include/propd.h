@@ -108,9 +108,11 @@ int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, 
  * beyond L_b + n_tmpl are never visible).
  * q = columns [0,H) of qkv.  out[m, a*dh:(a+1)*dh] = softmax(q k^T / sqrt(dh)) v.
  * `workspace` must hold propd_attn_workspace_bytes(...) bytes.
- * impl: 0 = auto, 1 = CUDA-core split-KV kernel, 2 = tcgen05/TMA kernel
- * (bf16, dh = 128 only), 3 = streaming decode kernel (bf16, dh = 128, <= 4
- * rows per sequence; auto picks it for the 1-row bonus pass).  n_slots = number of [A, Lmax, dh] slot blocks in the
+ * impl: 0 = auto, 1 = CUDA-core split-KV kernel, 2 = tcgen05/TMA kernel v1
+ * (128-key blocks, one softmax warpgroup), 4 = tcgen05/TMA kernel v2 (64-key
+ * blocks, 4-stage ring, two softmax warpgroups; auto for > 4 rows), 3 =
+ * streaming decode kernel (<= 4 rows per sequence; auto for the bonus pass).
+ * impls 2-4 need bf16 and dh = 128.  n_slots = number of [A, Lmax, dh] slot blocks in the
  * cache layer (bounds of the TMA tensor map). */
 int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits);
 int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int n_slots,

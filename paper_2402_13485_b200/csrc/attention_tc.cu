@@ -20,10 +20,9 @@
 //              when the row max grows by more than 2^8), bf16 P written to
 //              smem in the UMMA SW128 K-major layout.
 // Splits of the key range are merged by attn_combine_kernel (attention.cu).
-#include <cuda.h>
 #include <unordered_map>
 
-#include "common.cuh"
+#include "tc_common.cuh"
 
 namespace propd {
 
@@ -35,7 +34,6 @@ namespace tc {
 
 constexpr int BM = 128, BN = 128, DH = 128, STAGES = 2, THREADS = 192;
 constexpr int TILE_BYTES = 128 * 128 * 2;  // one [128 x 128] bf16 operand = 2 SW128 column blocks
-constexpr int HALF = TILE_BYTES / 2;      // one 64-column SW128 block (128 rows x 128 B)
 constexpr int SMEM_Q = 0;
 constexpr int SMEM_K = SMEM_Q + TILE_BYTES;
 constexpr int SMEM_V = SMEM_K + STAGES * TILE_BYTES;
@@ -64,133 +62,6 @@ struct Args {
 };
 
 static unsigned long long* g_trace = nullptr;
-
-// ------------------------------------------------------------------ PTX --
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// Bounded wait: a protocol bug traps (with a diagnostic) instead of hanging the GPU.
-__device__ __noinline__ void mbar_timeout(int tag, uint32_t parity) {
-  printf("propd attn_tc: mbarrier wait timed out (tag %d parity %u) block (%d,%d,%d) thread %d\n", tag, parity,
-         blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x);
-  __trap();
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int tag = 0) {
-  uint32_t spins = 0;
-  while (!mbar_try(bar, parity)) {
-    if (++spins > (1u << 26)) mbar_timeout(tag, parity);
-  }
-}
-__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-// SW128 UMMA shared-memory descriptor (version 1, base offset 0).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version for sm_100
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
-  return d;
-}
-
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M=128, N=128.
-__host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((128u >> 3) << 17) |
-         ((128u >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-#define TMEM_LD32(addr, r)                                                                                      \
-  asm volatile(                                                                                                 \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                           \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),          \
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),     \
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),   \
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])    \
-      : "r"(addr))
-
-#define TMEM_ST32(addr, r)                                                                                       \
-  asm volatile(                                                                                                  \
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
-      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),                               \
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),         \
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),  \
-      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), \
-      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// Bits [t0, t0+32) of a 256-bit row mask held as 8 u32 words in smem (0 outside).
-__device__ __forceinline__ uint32_t mask_bits32(const uint32_t* m, int t0) {
-  if (t0 >= 256 || t0 <= -32) return 0u;
-  const int w = (t0 + 32) / 32 - 1;  // floor(t0 / 32) for t0 > -32
-  const int sh = t0 - 32 * w;
-  const uint32_t lo = (w >= 0) ? m[w] : 0u;
-  const uint32_t hi = (w + 1 < 8) ? m[w + 1] : 0u;
-  return sh ? __funnelshift_r(lo, hi, sh) : lo;
-}
-// Low `k` bits set, k clamped to [0, 32].
-__device__ __forceinline__ uint32_t low_bits(int k) {
-  return k >= 32 ? 0xffffffffu : (k <= 0 ? 0u : ((1u << k) - 1u));
-}
-
-// Byte offset of 16-byte chunk `c` (0..15 over 128 bf16 columns) of row r in
-// a [128 x 128] bf16 tile stored as two SW128 K-major column blocks.
-__device__ __forceinline__ uint32_t sw128_chunk(int r, int c) {
-  return (uint32_t)((c >> 3) * HALF + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4));
-}
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -369,13 +240,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_after_sync();
       if (j == 0 && r == 0) TRACE(4);
       const uint32_t sa = lane_addr + 128 + 128 * (j & 1);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t rr[32];
-        TMEM_LD32(sa + c * 32, rr);
+      {  // four 32-column loads in flight, one wait
+        uint32_t* rv = reinterpret_cast<uint32_t*>(sv);
+        TMEM_LD32(sa, rv);
+        TMEM_LD32(sa + 32, (rv + 32));
+        TMEM_LD32(sa + 64, (rv + 64));
+        TMEM_LD32(sa + 96, (rv + 96));
         tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(rr[i]);
       }
       // visibility of the block's 128 keys as 4 x 32-bit words (all uniform
       // except the row's own ancestor bits): cache keys, tree keys, range end
@@ -388,12 +259,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t tree_bits = mask_bits32(mrow, key0 + 32 * q - L);
         vis[q] = valid ? ((cache_bits | tree_bits) & low_bits(nvalid - 32 * q)) : 0u;
       }
-      float mx = -INFINITY;
+      // masked max with 8 independent accumulators (no 128-long dependency chain)
+      float mx8[8];
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        sv[i] = ((vis[i >> 5] >> (i & 31)) & 1u) ? sv[i] : -INFINITY;
-        mx = fmaxf(mx, sv[i]);
+      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+      const bool all_vis = __all_sync(0xffffffffu, (vis[0] & vis[1] & vis[2] & vis[3]) == 0xffffffffu);
+      if (all_vis) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], sv[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          sv[i] = ((vis[i >> 5] >> (i & 31)) & 1u) ? sv[i] : -INFINITY;
+          mx8[i & 7] = fmaxf(mx8[i & 7], sv[i]);
+        }
       }
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mx *= scale;  // scale > 0: max commutes with scaling (-inf stays -inf)
       if (j > 0) {  // PV_{j-1} finished: P buffer free, O stable
         mbar_wait(o_done, (j - 1) & 1, 5);
@@ -422,21 +304,23 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_wait_st();
       }
       const float mneg = m_ref == -INFINITY ? 0.f : -m_ref;  // masked keys: ex2(-inf) = 0
-      float ls = 0.f;
+      float ls8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ls8[u] = 0.f;
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         uint32_t pk[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          const float p0 = ex2(fmaf(sv[c * 8 + 2 * h], scale, mneg));
-          const float p1 = ex2(fmaf(sv[c * 8 + 2 * h + 1], scale, mneg));
-          ls += p0 + p1;
-          __nv_bfloat162 v2 = __floats2bfloat162_rn(p0, p1);
+          const float2 pp = ex2x2(fmaf(sv[c * 8 + 2 * h], scale, mneg), fmaf(sv[c * 8 + 2 * h + 1], scale, mneg));
+          ls8[(2 * h) & 7] += pp.x;
+          ls8[(2 * h + 1) & 7] += pp.y;
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(pp.x, pp.y);
           pk[h] = *reinterpret_cast<uint32_t*>(&v2);
         }
         *reinterpret_cast<uint4*>(prow + sw128_chunk(r, c)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-      l_sum += ls;
+      l_sum += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
       fence_proxy_async();
       tc_before_sync();
       mbar_arrive(p_full);
@@ -598,11 +482,15 @@ int attention_tc_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_p
 
 }  // namespace propd
 
+namespace propd {
+int attention_tc2_prepare();
+}
+
 extern "C" int propd_prepare(void) {  // one-time function attributes (before any graph capture)
   cudaError_t e = cudaFuncSetAttribute(propd::tc::attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        propd::tc::SMEM_TOTAL);
   if (e != cudaSuccess) return propd::fail("prepare: %s", cudaGetErrorString(e));
-  return 0;
+  return propd::attention_tc2_prepare();
 }
 
 extern "C" int propd_debug_trace(void* buf) {  // development aid: phase timestamps of one CTA

@@ -1,0 +1,477 @@
+// K2 v2 on tcgen05: tree-masked verification attention (bf16, dh = 128)
+// built to keep HBM busy.  Reference semantics as in attention_tc.cu
+// (backends.py:216-233).
+//
+// v1 (attention_tc.cu) serialises every 128-key block through one softmax
+// warpgroup and a 2-stage ring, so a block costs ~2 us of chain latency
+// against ~1.5 us of HBM time.  v2:
+//   - 64-key blocks, 4-stage K/V TMA ring (32 KB per stage, 128 KB in flight);
+//   - two softmax warpgroups (A: even blocks, B: odd blocks), each with its
+//     own TMEM accumulator O_g, running max/sum and P buffer, so two blocks
+//     are in softmax at once; the MMA thread interleaves S_j = Q K_j^T
+//     (M=128, N=64) and O_g += P_g V_j (M=128, N=128, K=64);
+//   - the two partial softmax states are merged in-kernel at the end
+//     (same algebra as the split-KV combine).
+// Warp roles (320 threads): warp 0 TMA, warp 1 TMEM alloc + MMA issue,
+// warps 2-5 group A, warps 6-9 group B.
+#include <unordered_map>
+
+#include "tc_common.cuh"
+
+namespace propd {
+
+template <typename T>
+__global__ void attn_combine_kernel(int A, int dh, int nsplit, const float* __restrict__ part_o,
+                                    const float* __restrict__ part_ml, T* __restrict__ out, int ldout);
+
+namespace tc2 {
+using namespace propd::tc;
+
+constexpr int BM = 128, BN = 64, DH = 128, STAGES = 4, THREADS = 320;
+constexpr int QBYTES = 128 * 128 * 2;      // Q: two SW128 blocks of [128 rows x 128 B]
+constexpr int KV_HALF = BN * 128;          // one [64 rows x 128 B] SW128 block = 8 KB
+constexpr int KV_TILE = 2 * KV_HALF;       // K (or V) of one 64-key block = 16 KB
+constexpr int STAGE_BYTES = 2 * KV_TILE;   // K + V = 32 KB
+constexpr int P_BYTES = 128 * BN * 2;      // [128 rows x 64 keys] bf16 = one SW128 block
+constexpr int SMEM_Q = 0;
+constexpr int SMEM_KV = SMEM_Q + QBYTES;
+constexpr int SMEM_P = SMEM_KV + STAGES * STAGE_BYTES;
+constexpr int SMEM_ML = SMEM_P + 2 * P_BYTES;  // [2 groups][2][128] floats (m, l)
+constexpr int SMEM_BAR = SMEM_ML + 2 * 2 * 128 * 4;
+constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
+constexpr uint32_t TMEM_COLS = 512;  // O_A [0,128), O_B [128,256), S: 256 + 64 * {A0, A1, B0, B1}
+
+struct Args {
+  const __nv_bfloat16* qkv;
+  int ldq;
+  const int32_t* seq_slot;
+  const int32_t* seq_len;
+  const int32_t* row_off;
+  const int32_t* row_node;
+  const uint64_t* mask;
+  int n_tmpl, W, A, Lmax;
+  float scale_log2;
+  int split_len, nsplit, mtiles;
+  float* part_o;
+  float* part_ml;
+  __nv_bfloat16* out;
+  int ldout;
+};
+
+// Bits [t0, t0+32) of a row's visibility over tree nodes (0 outside [0, 64W)).
+__device__ __forceinline__ uint32_t tree_bits32(const uint64_t* mrow, int W, int node, int t0) {
+  if (mrow == nullptr) return low_bits(node + 1 - t0);  // causal: nodes 0..node
+  if (t0 >= 64 * W || t0 <= -32) return 0u;
+  const uint32_t* m = reinterpret_cast<const uint32_t*>(mrow);
+  const int w = (t0 + 32) / 32 - 1;
+  const int sh = t0 - 32 * w;
+  const uint32_t lo = (w >= 0) ? m[w] : 0u;
+  const uint32_t hi = (w + 1 < 2 * W) ? m[w + 1] : 0u;
+  return sh ? __funnelshift_r(lo, hi, sh) : lo;
+}
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_tc2_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, Args p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
+  uint64_t* kv_full = bars;        // [4]
+  uint64_t* kv_empty = bars + 4;   // [4]
+  uint64_t* s_full = bars + 8;     // [4] A0 A1 B0 B1
+  uint64_t* p_full = bars + 12;    // [2] per group
+  uint64_t* o_done = bars + 14;    // [2] per group
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  float* ml = reinterpret_cast<float*>(smem + SMEM_ML);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x / p.mtiles, mt = blockIdx.x % p.mtiles;
+  const int a = blockIdx.y, b = blockIdx.z;
+  const int slot = p.seq_slot[b];
+  const int L = p.seq_len[slot];
+  const int r0 = p.row_off[b] + mt * BM;
+  const int nrows = min(BM, p.row_off[b + 1] - r0);
+  if (nrows <= 0) return;
+  const int nkeys = L + p.n_tmpl;
+  const int k_begin = s * p.split_len;
+  const int k_end = min(nkeys, k_begin + p.split_len);
+  const int nblk = k_end > k_begin ? (k_end - k_begin + BN - 1) / BN : 0;
+  if (nblk == 0) {
+    if (p.nsplit > 1) {
+      for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+        const size_t base = ((size_t)(r0 + r) * p.A + a) * p.nsplit + s;
+        p.part_ml[base * 2] = -INFINITY;
+        p.part_ml[base * 2 + 1] = 0.f;
+      }
+    }
+    return;
+  }
+  const int nlive = min(4, (nrows + 31) / 32);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+    }
+    mbar_init(&p_full[0], 32 * nlive);
+    mbar_init(&p_full[1], 32 * nlive);
+    mbar_init(&o_done[0], 1);
+    mbar_init(&o_done[1], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  {  // Q rows -> SW128 K-major smem (cp.async; rows past nrows zero)
+    const __nv_bfloat16* qbase = p.qkv + a * DH;
+    for (int i = threadIdx.x; i < BM * 16; i += THREADS) {
+      const int r = i >> 4, c = i & 15;
+      uint8_t* dst = smem + SMEM_Q + sw128_chunk(r, c);
+      if (r < nrows) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
+                     "l"(qbase + (size_t)(r0 + r) * p.ldq + c * 8)
+                     : "memory");
+      } else {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  fence_proxy_async();
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const size_t row_base = ((size_t)slot * p.A + a) * p.Lmax;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1, 11);
+        mbar_expect_tx(&kv_full[st], STAGE_BYTES);
+        const int row = (int)(row_base + k_begin + j * BN);
+        uint8_t* kd = smem + SMEM_KV + st * STAGE_BYTES;
+        uint8_t* vd = kd + KV_TILE;
+        tma_load_2d(kd, &kmap, &kv_full[st], 0, row);
+        tma_load_2d(kd + KV_HALF, &kmap, &kv_full[st], 64, row);
+        tma_load_2d(vd, &vmap, &kv_full[st], 0, row);
+        tma_load_2d(vd + KV_HALF, &vmap, &kv_full[st], 64, row);
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      const uint32_t id_s = idesc_bf16(false, BN, 128), id_o = idesc_bf16(true, 128, 128);
+      const uint32_t q_addr = smem_u32(smem + SMEM_Q);
+      auto issue_pv = [&](int jj) {
+        const int g = jj & 1, i = jj >> 1, st = jj % STAGES;
+        mbar_wait(&p_full[g], i & 1, 12);
+        tc_after_sync();
+        const uint32_t p_addr = smem_u32(smem + SMEM_P + g * P_BYTES);
+        const uint32_t v_addr = smem_u32(smem + SMEM_KV + st * STAGE_BYTES + KV_TILE);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          const uint64_t ad = sw128_desc(p_addr + kk * 32, 16, 1024);
+          const uint64_t bd = sw128_desc(v_addr + kk * 2048, KV_HALF, 1024);
+          mma_bf16(tmem + g * 128, ad, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&kv_empty[st]);
+        mma_commit(&o_done[g]);
+      };
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&kv_full[st], (j / STAGES) & 1, 13);
+        tc_after_sync();
+        const int sb = (j & 1) * 2 + ((j >> 1) & 1);
+        const uint32_t k_addr = smem_u32(smem + SMEM_KV + st * STAGE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K = dh 128 in steps of 16
+          const uint64_t ad = sw128_desc(q_addr + (kk >> 2) * HALF + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = sw128_desc(k_addr + (kk >> 2) * KV_HALF + (kk & 3) * 32, 16, 1024);
+          mma_bf16(tmem + 256 + 64 * sb, ad, bd, id_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[sb]);
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(nblk - 1);
+    }
+  } else {
+    // ================= softmax warpgroups =================
+    const int g = (warp - 2) >> 2;  // 0: even blocks, 1: odd blocks
+    const int q4 = warp & 3;        // TMEM lane quadrant
+    const int r = q4 * 32 + lane;
+    const bool valid = r < nrows;
+    const bool warp_live = q4 * 32 < nrows;
+    const int row = r0 + r;
+    const int node = valid ? p.row_node[row] : 0;
+    const uint64_t* mrow = (valid && p.mask != nullptr) ? p.mask + (size_t)node * p.W : nullptr;
+    const bool causal = p.mask == nullptr;
+    const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
+    const uint32_t o_addr = lane_addr + g * 128;
+    const float scale = p.scale_log2;
+    float m_ref = -INFINITY, l_sum = 0.f;
+    uint8_t* pbuf = smem + SMEM_P + g * P_BYTES;
+    const int nb = (nblk - g + 1) >> 1;  // blocks j = g, g+2, ...
+    for (int i = 0; i < nb && warp_live; ++i) {
+      const int j = 2 * i + g;
+      const int sb = g * 2 + (i & 1);
+      float sv[64];
+      mbar_wait(&s_full[sb], (i >> 1) & 1, 14);
+      tc_after_sync();
+      {
+        uint32_t* rv = reinterpret_cast<uint32_t*>(sv);
+        TMEM_LD32(lane_addr + 256 + 64 * sb, rv);
+        TMEM_LD32(lane_addr + 256 + 64 * sb + 32, (rv + 32));
+        tmem_wait_ld();
+      }
+      const int key0 = k_begin + j * BN;
+      const int ncache = L - key0, nvalid = k_end - key0;
+      uint32_t vis[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int t0 = key0 + 32 * q - L;
+        uint32_t tb = 0u;
+        if (valid && t0 > -32) tb = causal ? low_bits(node + 1 - t0) : tree_bits32(mrow, p.W, node, t0);
+        vis[q] = valid ? ((low_bits(ncache - 32 * q) | tb) & low_bits(nvalid - 32 * q)) : 0u;
+      }
+      float mx8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mx8[u] = -INFINITY;
+      if (__all_sync(0xffffffffu, (vis[0] & vis[1]) == 0xffffffffu)) {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) mx8[k & 7] = fmaxf(mx8[k & 7], sv[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          sv[k] = ((vis[k >> 5] >> (k & 31)) & 1u) ? sv[k] : -INFINITY;
+          mx8[k & 7] = fmaxf(mx8[k & 7], sv[k]);
+        }
+      }
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      mx *= scale;
+      if (i > 0) {  // this group's previous PV finished: P_g free, O_g stable
+        mbar_wait(&o_done[g], (i - 1) & 1, 15);
+        tc_after_sync();
+      }
+      float corr = 1.f;
+      const bool grow = mx > m_ref + 8.f;
+      if (grow) {
+        corr = ex2(m_ref - mx);
+        l_sum *= corr;
+        m_ref = mx;
+      }
+      if (i > 0 && __any_sync(0xffffffffu, grow)) {  // warp-collective O_g rescale
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t rr[32];
+          TMEM_LD32(o_addr + c * 32, rr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) rr[k] = __float_as_uint(__uint_as_float(rr[k]) * corr);
+          TMEM_ST32(o_addr + c * 32, rr);
+        }
+        tmem_wait_st();
+      }
+      const float mneg = m_ref == -INFINITY ? 0.f : -m_ref;
+      float ls8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ls8[u] = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float2 pp = ex2x2(fmaf(sv[c * 8 + 2 * h], scale, mneg), fmaf(sv[c * 8 + 2 * h + 1], scale, mneg));
+          ls8[2 * h] += pp.x;
+          ls8[2 * h + 1] += pp.y;
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(pp.x, pp.y);
+          pk[h] = *reinterpret_cast<uint32_t*>(&v2);
+        }
+        *reinterpret_cast<uint4*>(pbuf + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+      l_sum += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+      fence_proxy_async();
+      tc_before_sync();
+      mbar_arrive(&p_full[g]);
+    }
+    // ---- epilogue: merge the two groups' (m, l, O) and write ----
+    if (warp_live && nb > 0) {
+      mbar_wait(&o_done[g], (nb - 1) & 1, 16);
+      tc_after_sync();
+    }
+    ml[(g * 2 + 0) * 128 + r] = m_ref;
+    ml[(g * 2 + 1) * 128 + r] = l_sum;
+    tc_before_sync();
+    named_sync(1, 256);  // both groups' last PV observed complete
+    tc_after_sync();
+    if (warp_live) {
+      const float mA = ml[r], lA = ml[128 + r];
+      const bool hasB = nblk > 1;
+      const float mB = hasB ? ml[256 + r] : -INFINITY, lB = hasB ? ml[384 + r] : 0.f;
+      const float m = fmaxf(mA, mB);
+      const float fA = mA == -INFINITY ? 0.f : ex2(mA - m);
+      const float fB = mB == -INFINITY ? 0.f : ex2(mB - m);
+      const float l = lA * fA + lB * fB;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {  // this group writes columns [64g, 64g + 64)
+        const int col = 64 * g + 32 * c;
+        uint32_t ra[32], rb[32];
+        TMEM_LD32(lane_addr + col, ra);
+        if (hasB) TMEM_LD32(lane_addr + 128 + col, rb);
+        tmem_wait_ld();
+        float o[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          o[k] = __uint_as_float(ra[k]) * fA + (hasB ? __uint_as_float(rb[k]) * fB : 0.f);
+        if (valid) {
+          if (p.nsplit == 1) {
+            __nv_bfloat16* dst = p.out + (size_t)row * p.ldout + a * DH + col;
+#pragma unroll
+            for (int k8 = 0; k8 < 4; ++k8) {
+              uint32_t pk[4];
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                __nv_bfloat162 v2 = __floats2bfloat162_rn(o[k8 * 8 + 2 * h] * inv, o[k8 * 8 + 2 * h + 1] * inv);
+                pk[h] = *reinterpret_cast<uint32_t*>(&v2);
+              }
+              *reinterpret_cast<uint4*>(dst + k8 * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+          } else {
+            const size_t base = ((size_t)row * p.A + a) * p.nsplit + s;
+            float4* po = reinterpret_cast<float4*>(p.part_o + base * DH + col);
+#pragma unroll
+            for (int k4 = 0; k4 < 8; ++k4) po[k4] = make_float4(o[4 * k4], o[4 * k4 + 1], o[4 * k4 + 2], o[4 * k4 + 3]);
+            if (g == 0 && c == 0) {
+              p.part_ml[base * 2] = m == -INFINITY ? -INFINITY : m * 0.69314718055994531f;
+              p.part_ml[base * 2 + 1] = l;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host --
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(f);
+  }
+  return fn;
+}
+
+// [rows, 128] bf16 view of a K or V cache layer; box 64 x BN rows, SWIZZLE_128B.
+static bool kv_map64(CUtensorMap* m, const void* base, uint64_t rows) {
+  static std::unordered_map<uint64_t, std::pair<uint64_t, CUtensorMap>> cache;
+  const uint64_t key = (uint64_t)(uintptr_t)base;
+  auto it = cache.find(key);
+  if (it != cache.end() && it->second.first == rows) {
+    *m = it->second.second;
+    return true;
+  }
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {128, rows};
+  cuuint64_t strides[1] = {128 * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)BN};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  cache[key] = {rows, *m};
+  return true;
+}
+
+}  // namespace tc2
+
+int attention_tc2_prepare() {
+  cudaError_t e = cudaFuncSetAttribute(tc2::attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       tc2::SMEM_TOTAL);
+  return e == cudaSuccess ? 0 : fail("prepare(tc2): %s", cudaGetErrorString(e));
+}
+
+int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys,
+                       const void* qkv, int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot,
+                       const int32_t* seq_len, const int32_t* row_off, const int32_t* row_node, const uint64_t* mask,
+                       int n_tmpl, int W, void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st,
+                       bool* handled) {
+  *handled = false;
+  if (n_slots <= 0 || W > 4 || (ldqkv % 8) != 0 || (ldout % 8) != 0) return 0;
+  CUtensorMap km, vm;
+  const uint64_t rows = (uint64_t)n_slots * A * Lmax;
+  if (!tc2::kv_map64(&km, kc, rows) || !tc2::kv_map64(&vm, vc, rows)) return 0;
+  const int mtiles = (max_rows_per_seq + tc2::BM - 1) / tc2::BM;
+  const int ctas = B * A * mtiles;
+  const int nblk_max = (max_keys + tc2::BN - 1) / tc2::BN;
+  int nsplit = 148 / ctas;  // one wave of one CTA per SM
+  if (nsplit > nblk_max) nsplit = nblk_max;
+  if (nsplit > 64) nsplit = 64;
+  if (nsplit < 1) nsplit = 1;
+  const int64_t need = (int64_t)M * A * nsplit * (tc2::DH + 2) * (int64_t)sizeof(float);
+  if (nsplit > 1 && (ws == nullptr || ws_bytes < need)) nsplit = 1;
+  const int blocks_per_split = (nblk_max + nsplit - 1) / nsplit;
+  nsplit = (nblk_max + blocks_per_split - 1) / blocks_per_split;
+  tc2::Args p{};
+  p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  p.ldq = ldqkv;
+  p.seq_slot = seq_slot;
+  p.seq_len = seq_len;
+  p.row_off = row_off;
+  p.row_node = row_node;
+  p.mask = mask;
+  p.n_tmpl = n_tmpl;
+  p.W = W;
+  p.A = A;
+  p.Lmax = Lmax;
+  p.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
+  p.split_len = blocks_per_split * tc2::BN;
+  p.nsplit = nsplit;
+  p.mtiles = mtiles;
+  p.part_o = reinterpret_cast<float*>(ws);
+  p.part_ml = p.part_o + (size_t)M * A * nsplit * tc2::DH;
+  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.ldout = ldout;
+  static bool attr = false;
+  if (!attr) {
+    if (int e = attention_tc2_prepare()) return e;
+    attr = true;
+  }
+  *handled = true;
+  dim3 grid(nsplit * mtiles, A, B);
+  tc2::attn_tc2_kernel<<<grid, tc2::THREADS, tc2::SMEM_TOTAL, st>>>(km, vm, p);
+  if (int e = check_launch("tree_attention(tc2)")) return e;
+  if (nsplit > 1) {
+    attn_combine_kernel<__nv_bfloat16><<<dim3(M, A), 128, 0, st>>>(A, tc2::DH, nsplit, p.part_o, p.part_ml, p.out,
+                                                                  ldout);
+    if (int e = check_launch("tree_attention(tc2 combine)")) return e;
+  }
+  return 0;
+}
+
+}  // namespace propd
