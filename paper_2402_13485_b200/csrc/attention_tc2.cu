@@ -5,15 +5,19 @@
 // v1 (attention_tc.cu) serialises every 128-key block through one softmax
 // warpgroup and a 2-stage ring, so a block costs ~2 us of chain latency
 // against ~1.5 us of HBM time.  v2:
-//   - 64-key blocks, 4-stage K/V TMA ring (32 KB per stage, 128 KB in flight);
+//   - 64-key blocks streamed by two TMA producers into separate 6-stage rings:
+//     K (released as soon as S = QK^T completes) and V (released after PV),
+//     192 KB of shared memory for K/V (P never touches smem: the bf16
+//     probabilities are written with tcgen05.st over the consumed S buffer
+//     and P V reads its A operand straight from TMEM);
 //   - two softmax warpgroups (A: even blocks, B: odd blocks), each with its
 //     own TMEM accumulator O_g, running max/sum and P buffer, so two blocks
 //     are in softmax at once; the MMA thread interleaves S_j = Q K_j^T
 //     (M=128, N=64) and O_g += P_g V_j (M=128, N=128, K=64);
 //   - the two partial softmax states are merged in-kernel at the end
 //     (same algebra as the split-KV combine).
-// Warp roles (320 threads): warp 0 TMA, warp 1 TMEM alloc + MMA issue,
-// warps 2-5 group A, warps 6-9 group B.
+// Warp roles (352 threads): warp 0 TMA (K), warp 10 TMA (V), warp 1 TMEM
+// alloc + MMA issue, warps 2-5 group A, warps 6-9 group B.
 #include <unordered_map>
 
 #include "tc_common.cuh"
@@ -27,19 +31,20 @@ __global__ void attn_combine_kernel(int A, int dh, int nsplit, const float* __re
 namespace tc2 {
 using namespace propd::tc;
 
-constexpr int BM = 128, BN = 64, DH = 128, STAGES = 4, THREADS = 320;
+constexpr int BM = 128, BN = 64, DH = 128, KS = 6, VS = 6, THREADS = 352;
 constexpr int QBYTES = 128 * 128 * 2;      // Q: two SW128 blocks of [128 rows x 128 B]
 constexpr int KV_HALF = BN * 128;          // one [64 rows x 128 B] SW128 block = 8 KB
 constexpr int KV_TILE = 2 * KV_HALF;       // K (or V) of one 64-key block = 16 KB
-constexpr int STAGE_BYTES = 2 * KV_TILE;   // K + V = 32 KB
-constexpr int P_BYTES = 128 * BN * 2;      // [128 rows x 64 keys] bf16 = one SW128 block
+
 constexpr int SMEM_Q = 0;
-constexpr int SMEM_KV = SMEM_Q + QBYTES;
-constexpr int SMEM_P = SMEM_KV + STAGES * STAGE_BYTES;
-constexpr int SMEM_ML = SMEM_P + 2 * P_BYTES;  // [2 groups][2][128] floats (m, l)
+constexpr int SMEM_K = SMEM_Q + QBYTES;         // K ring: KS x 16 KB (released after S)
+constexpr int SMEM_V = SMEM_K + KS * KV_TILE;     // V ring: VS x 16 KB (released after PV)
+constexpr int SMEM_ML = SMEM_V + VS * KV_TILE;    // [2 groups][2][128] floats (m, l)
 constexpr int SMEM_BAR = SMEM_ML + 2 * 2 * 128 * 4;
-constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
-constexpr uint32_t TMEM_COLS = 512;  // O_A [0,128), O_B [128,256), S: 256 + 64 * {A0, A1, B0, B1}
+constexpr int SMEM_TOTAL = SMEM_BAR + 512;  // 32 mbarriers + TMEM slot; smem is declared 1024-aligned
+// O_A [0,128), O_B [128,256), S buffers 256 + 64*{A0,A1,B0,B1}; the bf16 P of a
+// block overwrites the first 32 columns of its own S buffer (A operand of PV)
+constexpr uint32_t TMEM_COLS = 512;
 
 struct Args {
   const __nv_bfloat16* qkv;
@@ -56,7 +61,20 @@ struct Args {
   float* part_ml;
   __nv_bfloat16* out;
   int ldout;
+  unsigned long long* trace;  // debug: per-block event timestamps of CTA (0,0,0)
 };
+
+__device__ __forceinline__ unsigned long long gtime2() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// trace slots: [0] start, [1] setup done; per block j < 24: 2+j: TMA issued,
+// 26+j: S issued, 50+j: softmax start (S seen), 74+j: P arrive, 98+j: PV issued
+#define TR2(k)                                                                                 \
+  do {                                                                                         \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) p.trace[k] = gtime2(); \
+  } while (0)
 
 // Bits [t0, t0+32) of a row's visibility over tree nodes (0 outside [0, 64W)).
 __device__ __forceinline__ uint32_t tree_bits32(const uint64_t* mrow, int W, int node, int t0) {
@@ -74,18 +92,21 @@ __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sy
 
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, Args p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;  // SW128 operands need 1024-byte alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
-  uint64_t* kv_full = bars;        // [4]
-  uint64_t* kv_empty = bars + 4;   // [4]
-  uint64_t* s_full = bars + 8;     // [4] A0 A1 B0 B1
-  uint64_t* p_full = bars + 12;    // [2] per group
-  uint64_t* o_done = bars + 14;    // [2] per group
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* k_full = bars;                 // [KS]
+  uint64_t* k_empty = k_full + KS;         // [KS]
+  uint64_t* v_full = k_empty + KS;         // [VS]
+  uint64_t* v_empty = v_full + VS;         // [VS]
+  uint64_t* s_full = v_empty + VS;         // [4] A0 A1 B0 B1
+  uint64_t* p_full = s_full + 4;           // [2] per group
+  uint64_t* o_done = p_full + 2;           // [2] per group
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
   float* ml = reinterpret_cast<float*>(smem + SMEM_ML);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TR2(0);
   const int s = blockIdx.x / p.mtiles, mt = blockIdx.x % p.mtiles;
   const int a = blockIdx.y, b = blockIdx.z;
   const int slot = p.seq_slot[b];
@@ -110,11 +131,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int nlive = min(4, (nrows + 31) / 32);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
     }
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
     mbar_init(&p_full[0], 32 * nlive);
     mbar_init(&p_full[1], 32 * nlive);
     mbar_init(&o_done[0], 1);
@@ -146,22 +171,27 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TR2(1);
   const size_t row_base = ((size_t)slot * p.A + a) * p.Lmax;
 
-  if (warp == 0) {
-    // ================= TMA producer =================
+  if (warp == 0 || warp == 10) {
+    // ================= TMA producers: warp 0 streams K, warp 10 streams V =================
     if (lane == 0) {
+      const bool isk = warp == 0;
+      const int NS = isk ? KS : VS;
+      uint64_t* full = isk ? k_full : v_full;
+      uint64_t* empty = isk ? k_empty : v_empty;
+      const CUtensorMap* map = isk ? &kmap : &vmap;
+      uint8_t* ring = smem + (isk ? SMEM_K : SMEM_V);
       for (int j = 0; j < nblk; ++j) {
-        const int st = j % STAGES;
-        mbar_wait(&kv_empty[st], ((j / STAGES) & 1) ^ 1, 11);
-        mbar_expect_tx(&kv_full[st], STAGE_BYTES);
+        const int st = j % NS;
+        mbar_wait(&empty[st], ((j / NS) & 1) ^ 1, isk ? 11 : 17);
+        mbar_expect_tx(&full[st], KV_TILE);
         const int row = (int)(row_base + k_begin + j * BN);
-        uint8_t* kd = smem + SMEM_KV + st * STAGE_BYTES;
-        uint8_t* vd = kd + KV_TILE;
-        tma_load_2d(kd, &kmap, &kv_full[st], 0, row);
-        tma_load_2d(kd + KV_HALF, &kmap, &kv_full[st], 64, row);
-        tma_load_2d(vd, &vmap, &kv_full[st], 0, row);
-        tma_load_2d(vd + KV_HALF, &vmap, &kv_full[st], 64, row);
+        uint8_t* d = ring + st * KV_TILE;
+        tma_load_2d(d, map, &full[st], 0, row);
+        tma_load_2d(d + KV_HALF, map, &full[st], 64, row);
+        if (isk && j < 24) TR2(2 + j);
       }
     }
   } else if (warp == 1) {
@@ -170,26 +200,28 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t id_s = idesc_bf16(false, BN, 128), id_o = idesc_bf16(true, 128, 128);
       const uint32_t q_addr = smem_u32(smem + SMEM_Q);
       auto issue_pv = [&](int jj) {
-        const int g = jj & 1, i = jj >> 1, st = jj % STAGES;
+        const int g = jj & 1, i = jj >> 1, st = jj % VS;
+        const int sb = g * 2 + (i & 1);
         mbar_wait(&p_full[g], i & 1, 12);
+        mbar_wait(&v_full[st], (jj / VS) & 1, 18);
         tc_after_sync();
-        const uint32_t p_addr = smem_u32(smem + SMEM_P + g * P_BYTES);
-        const uint32_t v_addr = smem_u32(smem + SMEM_KV + st * STAGE_BYTES + KV_TILE);
+        const uint32_t p_tmem = tmem + 256 + 64 * sb;  // P (bf16 pairs) over its S buffer
+        const uint32_t v_addr = smem_u32(smem + SMEM_V + st * KV_TILE);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t ad = sw128_desc(p_addr + kk * 32, 16, 1024);
           const uint64_t bd = sw128_desc(v_addr + kk * 2048, KV_HALF, 1024);
-          mma_bf16(tmem + g * 128, ad, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16_ts(tmem + g * 128, p_tmem + 8 * kk, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
         }
-        mma_commit(&kv_empty[st]);
+        if (jj < 24) TR2(98 + jj);
+        mma_commit(&v_empty[st]);
         mma_commit(&o_done[g]);
       };
       for (int j = 0; j < nblk; ++j) {
-        const int st = j % STAGES;
-        mbar_wait(&kv_full[st], (j / STAGES) & 1, 13);
+        const int st = j % KS;
+        mbar_wait(&k_full[st], (j / KS) & 1, 13);
         tc_after_sync();
         const int sb = (j & 1) * 2 + ((j >> 1) & 1);
-        const uint32_t k_addr = smem_u32(smem + SMEM_KV + st * STAGE_BYTES);
+        const uint32_t k_addr = smem_u32(smem + SMEM_K + st * KV_TILE);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K = dh 128 in steps of 16
           const uint64_t ad = sw128_desc(q_addr + (kk >> 2) * HALF + (kk & 3) * 32, 16, 1024);
@@ -197,6 +229,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           mma_bf16(tmem + 256 + 64 * sb, ad, bd, id_s, kk > 0 ? 1u : 0u);
         }
         mma_commit(&s_full[sb]);
+        mma_commit(&k_empty[st]);  // K is only needed by S: release its stage now
+        if (j < 24) TR2(26 + j);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(nblk - 1);
@@ -216,7 +250,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t o_addr = lane_addr + g * 128;
     const float scale = p.scale_log2;
     float m_ref = -INFINITY, l_sum = 0.f;
-    uint8_t* pbuf = smem + SMEM_P + g * P_BYTES;
     const int nb = (nblk - g + 1) >> 1;  // blocks j = g, g+2, ...
     for (int i = 0; i < nb && warp_live; ++i) {
       const int j = 2 * i + g;
@@ -224,6 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       float sv[64];
       mbar_wait(&s_full[sb], (i >> 1) & 1, 14);
       tc_after_sync();
+      if (j < 24 && lane == 0 && q4 == 0) TR2(50 + j);
       {
         uint32_t* rv = reinterpret_cast<uint32_t*>(sv);
         TMEM_LD32(lane_addr + 256 + 64 * sb, rv);
@@ -283,24 +317,21 @@ __global__ void __launch_bounds__(THREADS, 1)
       float ls8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) ls8[u] = 0.f;
+      uint32_t pk[32];  // P row as 32 bf16 pairs -> TMEM (A operand of O_g += P V)
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t pk[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const float2 pp = ex2x2(fmaf(sv[c * 8 + 2 * h], scale, mneg), fmaf(sv[c * 8 + 2 * h + 1], scale, mneg));
-          ls8[2 * h] += pp.x;
-          ls8[2 * h + 1] += pp.y;
-          __nv_bfloat162 v2 = __floats2bfloat162_rn(pp.x, pp.y);
-          pk[h] = *reinterpret_cast<uint32_t*>(&v2);
-        }
-        *reinterpret_cast<uint4*>(pbuf + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4)) =
-            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      for (int k2 = 0; k2 < 32; ++k2) {
+        const float2 pp = ex2x2(fmaf(sv[2 * k2], scale, mneg), fmaf(sv[2 * k2 + 1], scale, mneg));
+        ls8[(2 * k2) & 7] += pp.x;
+        ls8[(2 * k2 + 1) & 7] += pp.y;
+        __nv_bfloat162 v2 = __floats2bfloat162_rn(pp.x, pp.y);
+        pk[k2] = *reinterpret_cast<uint32_t*>(&v2);
       }
+      TMEM_ST32(lane_addr + 256 + 64 * sb, pk);
+      tmem_wait_st();
       l_sum += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
-      fence_proxy_async();
       tc_before_sync();
       mbar_arrive(&p_full[g]);
+      if (j < 24 && lane == 0 && q4 == 0) TR2(74 + j);
     }
     // ---- epilogue: merge the two groups' (m, l, O) and write ----
     if (warp_live && nb > 0) {
@@ -410,6 +441,8 @@ static bool kv_map64(CUtensorMap* m, const void* base, uint64_t rows) {
 
 }  // namespace tc2
 
+unsigned long long* g_trace2 = nullptr;
+
 int attention_tc2_prepare() {
   cudaError_t e = cudaFuncSetAttribute(tc2::attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        tc2::SMEM_TOTAL);
@@ -457,6 +490,7 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   p.part_ml = p.part_o + (size_t)M * A * nsplit * tc2::DH;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
+  p.trace = g_trace2;
   static bool attr = false;
   if (!attr) {
     if (int e = attention_tc2_prepare()) return e;
@@ -475,3 +509,69 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
 }
 
 }  // namespace propd
+
+extern "C" int propd_debug_trace2(void* buf) {  // development aid: per-block timeline of one v2 CTA
+  propd::g_trace2 = reinterpret_cast<unsigned long long*>(buf);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Development probe: stream K and V blocks of 64 keys through the same TMA
+// rings with no compute (consumer releases stages on arrival), to measure the
+// TMA streaming ceiling of this access pattern.
+namespace propd {
+namespace tc2 {
+__global__ void __launch_bounds__(128, 1) tma_stream_kernel(const __grid_constant__ CUtensorMap kmap,
+                                                            const __grid_constant__ CUtensorMap vmap, int units,
+                                                            int nblk, int Lmax, int box_split) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int NS = 6;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * 2 * KV_TILE);
+  uint64_t* empty = full + 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const size_t row_base = (size_t)u * Lmax;
+    const int jbase = ((u - blockIdx.x) / gridDim.x) * nblk;
+    if (warp == 0 && lane == 0) {
+      for (int j = 0; j < nblk; ++j) {
+        const int jj = jbase + j, st = jj % NS;
+        mbar_wait(&empty[st], ((jj / NS) & 1) ^ 1, 21);
+        mbar_expect_tx(&full[st], 2 * KV_TILE);
+        const int row = (int)(row_base + j * BN);
+        uint8_t* d = smem + st * 2 * KV_TILE;
+        tma_load_2d(d, &kmap, &full[st], 0, row);
+        tma_load_2d(d + KV_HALF, &kmap, &full[st], 64, row);
+        tma_load_2d(d + KV_TILE, &vmap, &full[st], 0, row);
+        tma_load_2d(d + KV_TILE + KV_HALF, &vmap, &full[st], 64, row);
+      }
+    } else if (warp == 1 && lane == 0) {
+      for (int j = 0; j < nblk; ++j) {
+        const int jj = jbase + j, st = jj % NS;
+        mbar_wait(&full[st], (jj / NS) & 1, 22);
+        mbar_arrive(&empty[st]);
+      }
+    }
+  }
+  (void)box_split;
+}
+}  // namespace tc2
+}  // namespace propd
+
+extern "C" int propd_debug_tma_stream(const void* kc, const void* vc, int n_slots, int A, int Lmax, int nblk,
+                                      int grid, void* stream) {
+  CUtensorMap km, vm;
+  const uint64_t rows = (uint64_t)n_slots * A * Lmax;
+  if (!propd::tc2::kv_map64(&km, kc, rows) || !propd::tc2::kv_map64(&vm, vc, rows)) return propd::fail("map");
+  const int smem = 6 * 2 * propd::tc2::KV_TILE + 256;
+  cudaFuncSetAttribute(propd::tc2::tma_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  propd::tc2::tma_stream_kernel<<<grid, 128, smem, (cudaStream_t)stream>>>(km, vm, n_slots * A, nblk, Lmax, 0);
+  return propd::check_launch("tma_stream");
+}

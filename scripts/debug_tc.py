@@ -122,3 +122,21 @@ if os.environ.get("TRACE") == "1":
         t = tb.cpu().numpy()
         print(f"impl {impl}: {us:.1f} us/launch (graph, 20 back-to-back), {byts / us / 1e3:.0f} GB/s algorithmic; "
               f"CTA(0,0,0) phases ns: {[int(x - t[0]) if x else None for x in t[:10]]}")
+
+if os.environ.get("TRACE2") == "1":
+    tb = torch.zeros(128, dtype=torch.int64, device=dev)
+    lib = _lib.load()
+    lib.propd_debug_trace2.argtypes = [ctypes.c_void_p]
+    lib.propd_debug_trace2(tb.data_ptr())
+    out = torch.zeros(M, H, device=dev, dtype=torch.bfloat16)
+    for rep in range(3):
+        call("propd_tree_attention", _lib.BF16, 4, B, M, A, dh, Lmax, B, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc),
+             ptr(vc), ptr(slots), ptr(seq_len), ptr(row_off), ptr(row_node), ptr(mask), n, tmpl.words, ptr(out), H,
+             ptr(ws), ws_bytes, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    t = tb.cpu().numpy().astype(np.int64)
+    t0 = t[0]
+    rel = lambda x: int(x - t0) if x else -1
+    print("setup done", rel(t[1]))
+    for j in range(20):
+        print(f"blk {j:2d}: tma {rel(t[2+j]):7d}  S {rel(t[26+j]):7d}  sm_start {rel(t[50+j]):7d}  P {rel(t[74+j]):7d}  PV {rel(t[98+j]):7d}")
