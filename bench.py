@@ -133,7 +133,7 @@ def cpu_reference(args, steps: int, warmup: int):
 
     cores = os.cpu_count()
     Ly = 2
-    kv = min(args.kv, 512)
+    kv = args.kv
     cfg = op.TinyCfg(layers=Ly, hidden=4096, heads=32, vocab=32000, draft_heads=4, max_positions=kv + 64, seed=0)
     rng = np.random.default_rng(0)
     H, V = cfg.hidden, cfg.vocab
@@ -296,7 +296,7 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "impl": "reference",
                 "config": {"workload": "configs[1]: Vicuna-7B-shape, batch 1, ProPD pruned+dynamic tree (CPU sample)",
-                           "batch": 1, "kv": min(args.kv, 512), "mode": args.mode},
+                           "batch": 1, "kv": args.kv, "mode": args.mode, "draft_topk": args.topk},
                 "accepted_len_per_step": ref["accepted_len_per_step"],
                 "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
