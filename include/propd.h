@@ -124,6 +124,22 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
                          void* out, int ldout, void* workspace, int64_t workspace_bytes,
                          void* stream);
 
+/* ---- weight-streaming projections for few tokens (bf16, M <= 128) ----
+ * Y[M,N] (+)= X[M,K] . W[K,N] on tcgen05 (W row-major [K,N], X row-major
+ * [M,K], Y fp32 row stride ldy).  accumulate = 1: split-K partial sums are
+ * added with fp32 reductions into Y (Y must hold the addend, e.g. the
+ * residual stream or a zeroed accumulator); 0: Y is overwritten.  N % 128 ==
+ * 0, K % 64 == 0.  max_split <= 0: automatic. */
+int propd_gemm_ws(int M, int N, int K, const void* X, int ldx, const void* W, int ldw, float* Y, int ldy,
+                  int accumulate, int max_split, void* stream);
+/* acc[M, 3H] fp32 -> qkv bf16 [M, 3H] and K/V rows into the layer cache
+ * (slot seq_len[seq_slot[row_seq[m]]] + row_node[m]); acc re-zeroed. */
+int propd_qkv_finish(int M, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,
+                     const int32_t* row_seq, const int32_t* row_node, const int32_t* seq_slot, const int32_t* seq_len,
+                     void* kcache, void* vcache, void* stream);
+/* out = bf16(tanh-GELU(acc)) for acc[M, N] fp32; acc re-zeroed. */
+int propd_gelu_finish(int M, int N, float* acc, int ldacc, void* out, int ldout, void* stream);
+
 /* ---- K3: early prune (pruning.py:40-66, backends.py:320-327) ----
  * early_logits: fp32 [R, V], one row per (sequence, parent-slot): row
  * b*P + parent_slot[p] holds the early head output of node p of sequence b.

@@ -40,6 +40,9 @@ SIGNATURES = {
     "propd_kv_append": [I, I, I, I, I, P, I, P, P, P, P, P, P, P],
     "propd_attn_workspace_bytes": [I, I, I, I],
     "propd_tree_attention": [I, I, I, I, I, I, I, I, I, I, P, I, P, P, P, P, P, P, P, I, I, P, I, P, L, P],
+    "propd_gemm_ws": [I, I, I, P, I, P, I, P, I, I, I, P],
+    "propd_qkv_finish": [I, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
+    "propd_gelu_finish": [I, I, P, I, P, I, P],
     "propd_early_member": [I, I, I, I, I, P, P, P, P, P, P],
     "propd_prune_compact": [I, I, P, P, P, P, P, P, P, P, P, P, P],
     "propd_verify_commit": [I, I, I, I, I, I, I, I, I, L, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],

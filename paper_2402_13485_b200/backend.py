@@ -124,7 +124,7 @@ class B200Backend:
     def __init__(self, config: TinyTransformerConfig = TinyTransformerConfig(), *, dtype: str = "fp32",
                  device=None, weights: dict | None = None, random_device_init: bool = False,
                  max_slots: int = 16, max_tree: int = MAX_TREE, kv_len: int | None = None,
-                 attn_impl: int = 0, use_graphs: bool = False) -> None:
+                 attn_impl: int = 0, use_graphs: bool = False, use_gws: bool = True) -> None:
         import torch
 
         self.lib = _lib.load()
@@ -169,6 +169,10 @@ class B200Backend:
         self.hidden = torch.zeros(self.n_slots, self.H, device=dev, dtype=T)
         self.last_logits = torch.zeros(self.n_slots, self.V, device=dev, dtype=torch.float32)
         self.use_graphs = bool(use_graphs)
+        # weight-streaming tcgen05 projections for <= 128 rows (bf16 mode);
+        # fp32 accumulator for QKV / W1 partial sums (kept zero between uses)
+        self.use_gws = (dtype == "bf16") and use_gws and cfg.hidden % 128 == 0
+        self._acc = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32) if self.use_gws else None
         self._graphs: dict = {}
         self._templates: dict = {}
         self._host: dict = {}
@@ -257,6 +261,8 @@ class B200Backend:
     def _run_layers(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
         """Blocks l0..l1-1 over the rows of `rt` (backends.py:202-237).  Returns
         the last MLP output not yet added to the residual stream x."""
+        if self.use_gws and rt.M <= 128:
+            return self._run_layers_ws(x, rt, l0, l1, mask, n_tmpl, W, pending)
         torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
         M = rt.M
         ws = self._workspace(M, rt.B)
@@ -310,14 +316,62 @@ class B200Backend:
                                     "bytes": kv * 2 * self.H * elt + 2 * rows * self.H * elt})
         self._pending_events.clear()
 
+    def _run_layers_ws(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
+        """Same blocks with the weight-streaming tcgen05 projections (bf16,
+        <= 128 rows): QKV / W1 accumulate into an fp32 scratch that the finish
+        kernels turn into bf16 operands (K/V go straight into the cache, GELU is
+        applied on the way); W_o and W_2 accumulate into the residual stream x."""
+        torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
+        M = rt.M
+        ws = self._workspace(M, rt.B)
+        ws_bytes = 0 if ws is None else ws.numel()
+        acc = self._acc
+        h = torch.empty(M, H, device=self.device, dtype=T)
+        ctx = torch.empty(M, H, device=self.device, dtype=T)
+        qkv = torch.empty(M, 3 * H, device=self.device, dtype=T)
+        g = torch.empty(M, 4 * H, device=self.device, dtype=T)
+        for l in range(l0, l1):
+            self._call("propd_add_ln", self.code, M, H, ptr(x), ptr(pending), ptr(h), None, None, st)
+            pending = None
+            kc, vc = self.kcache[l], self.vcache[l]
+            self._call("propd_gemm_ws", M, 3 * H, H, ptr(h), H, ptr(self.w.wqkv[l]), 3 * H, ptr(acc), 3 * H, 1, 0, st)
+            self._call("propd_qkv_finish", M, self.A, self.dh, self.Lmax, ptr(acc), 3 * H, ptr(qkv), 3 * H,
+                       ptr(rt.row_seq), ptr(rt.row_node), ptr(rt.seq_slot), ptr(self.seq_len), ptr(kc), ptr(vc), st)
+            if self.attn_timer is not None:
+                ev0 = self._timing_event()
+                ev0.record()
+            self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
+                       self.n_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
+                       ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
+                       ptr(ws), ws_bytes, st)
+            if self.attn_timer is not None:
+                ev1 = self._timing_event()
+                ev1.record()
+                self._events_sink().append((ev0, ev1, self._role, M))
+            self._call("propd_gemm_ws", M, H, H, ptr(ctx), H, ptr(self.w.wo[l]), H, ptr(x), H, 1, 0, st)
+            self._call("propd_add_ln", self.code, M, H, ptr(x), None, ptr(h), None, None, st)
+            self._call("propd_gemm_ws", M, 4 * H, H, ptr(h), H, ptr(self.w.w1[l]), 4 * H, ptr(acc), 4 * H, 1, 0, st)
+            self._call("propd_gelu_finish", M, 4 * H, ptr(acc), 4 * H, ptr(g), 4 * H, st)
+            self._call("propd_gemm_ws", M, H, 4 * H, ptr(g), 4 * H, ptr(self.w.w2[l]), H, ptr(x), H, 1, 0, st)
+        return None
+
+    def _proj_f32(self, X, Wt, N):
+        """fp32 logits X @ Wt ([M,H] x [H,N]) for the LM / early / draft heads."""
+        torch = self.torch
+        M = X.shape[0]
+        if self.use_gws and M <= 128 and N % 128 == 0 and X.dtype == torch.bfloat16:
+            out = torch.empty(M, N, device=self.device, dtype=torch.float32)
+            self._call("propd_gemm_ws", M, N, self.H, ptr(X), self.H, ptr(Wt), N, ptr(out), N, 0, 0, self.stream())
+            return out
+        out = torch.mm(X, Wt)
+        return out if out.dtype == torch.float32 else out.float()
+
     def _flush(self, x, pending):
         if pending is not None:
             self._call("propd_residual_add", self.code, x.numel(), ptr(x), ptr(pending), self.stream())
 
     def _lm_argmax(self, hfin):
-        logits = self.torch.mm(hfin, self.w.w_lm)
-        if logits.dtype != self.torch.float32:
-            logits = logits.float()
+        logits = self._proj_f32(hfin, self.w.w_lm, self.V)
         am = self.torch.empty(hfin.shape[0], device=self.device, dtype=self.torch.int32)
         self._call("propd_argmax_rows", hfin.shape[0], self.V, self.V, ptr(logits), ptr(am), self.stream())
         return logits, am
@@ -423,9 +477,7 @@ class B200Backend:
             raise ValueError("draft top-k above 1024 is not supported by the device top-k")
         torch, D, V = self.torch, self.config.draft_heads, self.V
         hid = self.hidden.index_select(0, seq_slot.long())
-        logits = torch.mm(hid, self.w.w_draft)
-        if logits.dtype != torch.float32:
-            logits = logits.float()
+        logits = self._proj_f32(hid, self.w.w_draft, D * V)
         tok = torch.empty(B, D, k, device=self.device, dtype=torch.int32)
         val = torch.empty(B, D, k, device=self.device, dtype=torch.float32)
         self._call("propd_topk_rows", B * D, V, V, k, ptr(logits), ptr(tok), ptr(val), self.stream())
@@ -681,9 +733,7 @@ class B200Backend:
             par = td[("par_rows", B)]
             xp = torch.empty(B * Pn, H, device=dev, dtype=self.tdtype)
             self._call("propd_gather_rows", self.code, B * Pn, H, ptr(x), ptr(par), ptr(xp), st)
-            early = torch.mm(xp, self.w.w_early)
-            if early.dtype != torch.float32:
-                early = early.float()
+            early = self._proj_f32(xp, self.w.w_early, V)
             self._call("propd_early_member", B, n, Pn, V, min(prune.topk, V), ptr(early), ptr(td["parent"]),
                        ptr(td["parent_slot"]), ptr(o["tokens"]), ptr(member), st)
         o["alive"] = torch.empty(M, device=dev, dtype=torch.uint8)

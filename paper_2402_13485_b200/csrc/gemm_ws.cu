@@ -1,0 +1,297 @@
+// Weight-streaming GEMM for few tokens (M <= 128): Y[M,N] (+)= X[M,K] W[K,N]
+// on tcgen05, for the projections of the tree / bonus passes at small batch
+// (backends.py:217-219, 234-236, 256, 281, 321, 329 at 7B width: every step
+// streams 27.6 GB of bf16 weights for a few dozen token rows).
+//
+// The output features are the MMA M dimension (128 per CTA) and the tokens
+// the MMA N dimension: D[f, t] = sum_k W[k, n0+f] X[t, k].  A = W^T is read
+// MN-major straight from the row-major [K, N] weight by TMA (SW128, 64
+// features x 64 k per box), B = X is K-major.  K is split across CTAs so that
+// ~2 CTAs per SM stream weights; partial sums are reduced with fp32
+// red.global.add into Y (for W_o / W_2 that is the fp32 residual stream
+// itself, which fuses the residual add).  With one split the tile is stored.
+// Finish kernels turn fp32 accumulators into the bf16 operands of the next
+// op: QKV (+ K/V scattered into the cache, replacing kv_append) and
+// W1 (+ tanh-GELU), re-zeroing the accumulator for the next use.
+#include <unordered_map>
+
+#include "tc_common.cuh"
+
+namespace propd {
+namespace gws {
+using namespace propd::tc;
+
+constexpr int BF = 128, BK = 64, STAGES = 4, THREADS = 192;
+constexpr int A_BYTES = BK * BF * 2;  // W^T tile: 2 boxes of [64 k x 128 B] = 16 KB
+
+struct Args {
+  int M, N, K, kblk_per_split, ldy, mp;
+  float* Y;
+  int accumulate;
+};
+
+template <int MP>
+__global__ void __launch_bounds__(THREADS, 2)
+    gemm_ws_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap xmap, Args p) {
+  constexpr int B_BYTES = MP * 128;  // X tile [MP rows x 64 k x 2 B]
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BF;
+  const int kb0 = blockIdx.y * p.kblk_per_split;
+  const int nkb = min(p.kblk_per_split, p.K / BK - kb0);
+  if (nkb <= 0) return;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 31);
+        mbar_expect_tx(&full[st], STAGE);
+        uint8_t* a = smem + st * STAGE;
+        const int k = (kb0 + j) * BK;
+        tma_load_2d(a, &wmap, &full[st], n0, k);
+        tma_load_2d(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k);
+        tma_load_2d(a + A_BYTES, &xmap, &full[st], k, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // A = W^T MN-major (features contiguous), B = X K-major; M = 128, N = MP
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(MP >> 3) << 17) |
+                             ((128u >> 4) << 24);
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&full[st], (j / STAGES) & 1, 32);
+        tc_after_sync();
+        const uint32_t a = smem_u32(smem + st * STAGE);
+        const uint32_t b = a + A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t ad = sw128_desc(a + kk * 2048, A_BYTES / 2, 1024);
+          const uint64_t bd = sw128_desc(b + kk * 32, 16, 1024);
+          mma_bf16(tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[st]);
+      }
+      mma_commit(acc_full);
+    }
+  } else {
+    // epilogue: lane = output feature, columns = tokens
+    const int q4 = warp & 3;
+    const int f = n0 + q4 * 32 + lane;
+    mbar_wait(acc_full, 0, 33);
+    tc_after_sync();
+    const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
+#pragma unroll
+    for (int c = 0; c < MP / 32 + (MP % 32 ? 1 : 0); ++c) {
+      uint32_t rr[32];
+      TMEM_LD32(lane_addr + c * 32, rr);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int t = c * 32 + i;
+        if (t < p.M) {
+          float* dst = p.Y + (size_t)t * p.ldy + f;
+          const float v = __uint_as_float(rr[i]);
+          if (p.accumulate)
+            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst), "f"(v) : "memory");
+          else
+            *dst = v;
+        }
+      }
+    }
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* fp = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(fp);
+  }
+  return fn;
+}
+
+// 2D bf16 map of a row-major [rows, cols] matrix (row stride ld elements), box
+// [64 cols (128 B, SW128) x box_rows].  Cached by (pointer, shape, box).
+static bool map2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+  struct Key {
+    uint64_t p, r, c, l, b;
+    bool operator==(const Key& o) const { return p == o.p && r == o.r && c == o.c && l == o.l && b == o.b; }
+  };
+  struct H {
+    size_t operator()(const Key& k) const { return k.p ^ (k.r * 1315423911u) ^ (k.c << 7) ^ (k.b << 17); }
+  };
+  static std::unordered_map<Key, CUtensorMap, H> cache;
+  const Key key{(uint64_t)(uintptr_t)base, rows, cols, ld, box_rows};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *m = it->second;
+    return true;
+  }
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  if (enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache[key] = *m;
+  return true;
+}
+
+template <int MP>
+static int launch(const CUtensorMap& wm, const CUtensorMap& xm, Args p, dim3 grid, cudaStream_t st) {
+  constexpr int smem = STAGES * (A_BYTES + MP * 128) + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_ws_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return fail("gemm_ws: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  gemm_ws_kernel<MP><<<grid, THREADS, smem, st>>>(wm, xm, p);
+  return check_launch("gemm_ws");
+}
+
+// ------------------------------------------------------------------ finish
+__global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ acc, int ldacc,
+                                  __nv_bfloat16* __restrict__ qkv, int ldqkv, const int32_t* __restrict__ row_seq,
+                                  const int32_t* __restrict__ row_node, const int32_t* __restrict__ seq_slot,
+                                  const int32_t* __restrict__ seq_len, __nv_bfloat16* __restrict__ kc,
+                                  __nv_bfloat16* __restrict__ vc) {
+  const int m = blockIdx.x;
+  const int H = A * dh;
+  const int slot = seq_slot[row_seq[m]];
+  const int t = seq_len[slot] + row_node[m];
+  float* a = acc + (size_t)m * ldacc;
+  __nv_bfloat16* q = qkv + (size_t)m * ldqkv;
+  for (int e = threadIdx.x * 4; e < 3 * H; e += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<float4*>(a + e);
+    *reinterpret_cast<float4*>(a + e) = make_float4(0.f, 0.f, 0.f, 0.f);
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+    *reinterpret_cast<uint2*>(q + e) = pk;
+    if (e >= H) {  // K or V element -> cache slot
+      const int kv = e >= 2 * H;
+      const int ee = e - (kv ? 2 * H : H);
+      const int ah = ee / dh, d = ee - ah * dh;
+      __nv_bfloat16* dst = (kv ? vc : kc) + (((size_t)slot * A + ah) * Lmax + t) * dh + d;
+      *reinterpret_cast<uint2*>(dst) = pk;
+    }
+  }
+}
+
+__global__ void gelu_finish_kernel(int N, float* __restrict__ acc, int ldacc, __nv_bfloat16* __restrict__ out,
+                                   int ldout) {
+  const int m = blockIdx.x;
+  const float c = 0.7978845608028654f;
+  float* a = acc + (size_t)m * ldacc;
+  __nv_bfloat16* o = out + (size_t)m * ldout;
+  for (int e = threadIdx.x * 4; e < N; e += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<float4*>(a + e);
+    *reinterpret_cast<float4*>(a + e) = make_float4(0.f, 0.f, 0.f, 0.f);
+    float r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) r[i] = 0.5f * r[i] * (1.f + tanhf(c * (r[i] + 0.044715f * r[i] * r[i] * r[i])));
+    __nv_bfloat162 lo = __floats2bfloat162_rn(r[0], r[1]), hi = __floats2bfloat162_rn(r[2], r[3]);
+    *reinterpret_cast<uint2*>(o + e) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+}
+
+}  // namespace gws
+}  // namespace propd
+
+using namespace propd;
+
+extern "C" {
+
+int propd_gemm_ws(int M, int N, int K, const void* X, int ldx, const void* W, int ldw, float* Y, int ldy,
+                  int accumulate, int max_split, void* stream) {
+  PROPD_REQUIRE(M >= 1 && M <= 128, "gemm_ws: M=%d outside 1..128", M);
+  PROPD_REQUIRE(N % gws::BF == 0 && K % gws::BK == 0, "gemm_ws: N=%d must be a multiple of 128, K=%d of 64", N, K);
+  const int mp = ((M + 15) / 16) * 16;
+  CUtensorMap wm, xm;
+  PROPD_REQUIRE(gws::map2d(&wm, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw, 64) &&
+                    gws::map2d(&xm, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, mp),
+                "gemm_ws: tensor map encode failed");
+  const int tiles = N / gws::BF, kb = K / gws::BK;
+  int split = 1;
+  if (accumulate) {
+    split = 296 / tiles;  // ~2 CTAs per SM stream weights
+    if (split > max_split && max_split > 0) split = max_split;
+    if (split > kb) split = kb;
+    if (split < 1) split = 1;
+  }
+  const int per = (kb + split - 1) / split;
+  split = (kb + per - 1) / per;
+  gws::Args p{M, N, K, per, ldy, mp, Y, accumulate};
+  dim3 grid(tiles, split);
+  cudaStream_t st = as_stream(stream);
+  switch (mp) {
+    case 16: return gws::launch<16>(wm, xm, p, grid, st);
+    case 32: return gws::launch<32>(wm, xm, p, grid, st);
+    case 48: return gws::launch<48>(wm, xm, p, grid, st);
+    case 64: return gws::launch<64>(wm, xm, p, grid, st);
+    case 80: return gws::launch<80>(wm, xm, p, grid, st);
+    case 96: return gws::launch<96>(wm, xm, p, grid, st);
+    case 112: return gws::launch<112>(wm, xm, p, grid, st);
+    default: return gws::launch<128>(wm, xm, p, grid, st);
+  }
+}
+
+int propd_qkv_finish(int M, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,
+                     const int32_t* row_seq, const int32_t* row_node, const int32_t* seq_slot, const int32_t* seq_len,
+                     void* kcache, void* vcache, void* stream) {
+  if (M == 0) return 0;
+  gws::qkv_finish_kernel<<<M, 256, 0, as_stream(stream)>>>(A, dh, Lmax, acc, ldacc, (__nv_bfloat16*)qkv, ldqkv,
+                                                           row_seq, row_node, seq_slot, seq_len,
+                                                           (__nv_bfloat16*)kcache, (__nv_bfloat16*)vcache);
+  return check_launch("qkv_finish");
+}
+
+int propd_gelu_finish(int M, int N, float* acc, int ldacc, void* out, int ldout, void* stream) {
+  if (M == 0) return 0;
+  gws::gelu_finish_kernel<<<M, 512, 0, as_stream(stream)>>>(N, acc, ldacc, (__nv_bfloat16*)out, ldout);
+  return check_launch("gelu_finish");
+}
+
+}  // extern "C"

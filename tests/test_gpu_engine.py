@@ -214,3 +214,23 @@ def test_commit_equals_scratch_prefill_and_oracle():
         assert be.next_argmax(st) == ref.next_argmax(rs)
         d1, d0 = be.draft(st, 2), ref.draft(rs, 2)
         assert np.array_equal(d1.tokens, d0.tokens)
+
+
+def test_bf16_streaming_projections_match_cublas_path():
+    """bf16 backend at 7B width (2 layers): the tcgen05 weight-streaming path
+    (fused KV append / GELU / residual) vs the cuBLAS path.  Tolerance: final
+    logits within 3e-2 * max(1, |ref|_inf) (bf16 rounding of different
+    reduction orders)."""
+    cfg = TinyTransformerConfig(layers=2, hidden=4096, heads=32, vocab=32000, draft_heads=4, max_positions=256, seed=1)
+    a = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=2, max_tree=16, use_gws=True)
+    b = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=2, max_tree=16, use_gws=False)
+    prompt = list(range(100, 140))
+    sa, sb = a.prefill(prompt), b.prefill(prompt)
+    la, lb = a.last_logits_of(sa), b.last_logits_of(sb)
+    assert np.abs(la - lb).max() <= 3e-2 * max(1.0, np.abs(lb).max())
+    tmpl = TreeTemplate.from_paths(op.grid_candidates(4, 3))
+    toks = np.arange(200, 200 + len(tmpl))
+    pos = len(prompt) + tmpl.depth - 1
+    fa = a.forward_tree(sa, toks, pos, tmpl.mask())
+    fb = b.forward_tree(sb, toks, pos, tmpl.mask())
+    assert np.abs(fa.logits - fb.logits).max() <= 3e-2 * max(1.0, np.abs(fb.logits).max())

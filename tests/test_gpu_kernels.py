@@ -342,3 +342,53 @@ def test_verify_commit_walk_and_compaction():
             assert torch.equal(kc[:, b, :, L + j], kc0[:, b, :, L + nd])
             assert torch.equal(vc[:, b, :, L + j], vc0[:, b, :, L + nd])
         assert torch.equal(kc[:, b, :, :L], kc0[:, b, :, :L])
+
+
+# --------------------------------------------------------------- weight-streaming GEMM
+@pytest.mark.parametrize("M,N,K,acc", [(1, 128, 64, 0), (16, 12288, 4096, 1), (37, 4096, 4096, 1),
+                                       (64, 4096, 16384, 1), (100, 32000, 4096, 0), (128, 16384, 4096, 1),
+                                       (5, 256, 1024, 1)])
+def test_gemm_ws_matches_fp32_reference(M, N, K, acc):
+    """bf16 inputs, fp32 accumulation: |err| <= 2e-3 * sqrt(K) * max|x| * max|w| scale (fp32 rounding of
+    the split-K reduction order); checked as relative to the reference's magnitude."""
+    torch.manual_seed(M + N)
+    X = torch.randn(M, K, device=DEV).bfloat16()
+    Wt = (torch.randn(K, N, device=DEV) / K ** 0.5).bfloat16()
+    ref = X.float() @ Wt.float()
+    base = torch.randn(M, N, device=DEV) if acc else torch.full((M, N), float("nan"), device=DEV)
+    Y = base.clone()
+    call("propd_gemm_ws", M, N, K, ptr(X), K, ptr(Wt), N, ptr(Y), N, acc, 0, st())
+    torch.cuda.synchronize()
+    want = ref + (base if acc else 0)
+    err = (Y - want).abs().max().item()
+    assert err <= 1e-3 * max(1.0, want.abs().max().item()), err
+
+
+def test_qkv_and_gelu_finish():
+    A, dh, M, Lmax = 4, 128, 7, 64
+    H = A * dh
+    acc = torch.randn(M, 3 * H, device=DEV)
+    acc0 = acc.clone()
+    qkv = torch.empty(M, 3 * H, device=DEV, dtype=torch.bfloat16)
+    kc = torch.zeros(2, A, Lmax, dh, device=DEV, dtype=torch.bfloat16)
+    vc = torch.zeros_like(kc)
+    row_seq, row_node = i32([0] * 3 + [1] * 4), i32([0, 1, 2, 0, 1, 2, 3])
+    seq_slot, seq_len = i32([1, 0]), i32([5, 9])
+    call("propd_qkv_finish", M, A, dh, Lmax, ptr(acc), 3 * H, ptr(qkv), 3 * H, ptr(row_seq), ptr(row_node),
+         ptr(seq_slot), ptr(seq_len), ptr(kc), ptr(vc), st())
+    torch.cuda.synchronize()
+    assert torch.equal(qkv, acc0.bfloat16()) and acc.abs().max().item() == 0.0
+    lens = {1: 5, 0: 9}
+    for m, (b, nd) in enumerate(zip([0] * 3 + [1] * 4, [0, 1, 2, 0, 1, 2, 3])):
+        slot = [1, 0][b]
+        t = lens[slot] + nd
+        assert torch.equal(kc[slot, :, t].reshape(-1), acc0[m, H:2 * H].bfloat16())
+        assert torch.equal(vc[slot, :, t].reshape(-1), acc0[m, 2 * H:].bfloat16())
+    g_acc = torch.randn(M, 4 * H, device=DEV)
+    g0 = g_acc.clone()
+    out = torch.empty(M, 4 * H, device=DEV, dtype=torch.bfloat16)
+    call("propd_gelu_finish", M, 4 * H, ptr(g_acc), 4 * H, ptr(out), 4 * H, st())
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.gelu(g0, approximate="tanh")
+    assert (out.float() - ref).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
+    assert g_acc.abs().max().item() == 0.0
