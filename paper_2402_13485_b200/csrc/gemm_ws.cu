@@ -203,7 +203,9 @@ __global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ a
   const int t = seq_len[slot] + row_node[m];
   float* a = acc + (size_t)m * ldacc;
   __nv_bfloat16* q = qkv + (size_t)m * ldqkv;
-  for (int e = threadIdx.x * 4; e < 3 * H; e += blockDim.x * 4) {
+  // blockIdx.y selects a 1024-element chunk of the row
+  for (int e = blockIdx.y * 1024 + threadIdx.x * 4; e < min(3 * H, (int)(blockIdx.y + 1) * 1024);
+       e += blockDim.x * 4) {
     float4 v = *reinterpret_cast<float4*>(a + e);
     *reinterpret_cast<float4*>(a + e) = make_float4(0.f, 0.f, 0.f, 0.f);
     __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
@@ -225,7 +227,7 @@ __global__ void gelu_finish_kernel(int N, float* __restrict__ acc, int ldacc, __
   const float c = 0.7978845608028654f;
   float* a = acc + (size_t)m * ldacc;
   __nv_bfloat16* o = out + (size_t)m * ldout;
-  for (int e = threadIdx.x * 4; e < N; e += blockDim.x * 4) {
+  for (int e = blockIdx.y * 1024 + threadIdx.x * 4; e < min(N, (int)(blockIdx.y + 1) * 1024); e += blockDim.x * 4) {
     float4 v = *reinterpret_cast<float4*>(a + e);
     *reinterpret_cast<float4*>(a + e) = make_float4(0.f, 0.f, 0.f, 0.f);
     float r[4] = {v.x, v.y, v.z, v.w};
@@ -282,7 +284,8 @@ int propd_qkv_finish(int M, int A, int dh, int Lmax, float* acc, int ldacc, void
                      const int32_t* row_seq, const int32_t* row_node, const int32_t* seq_slot, const int32_t* seq_len,
                      void* kcache, void* vcache, void* stream) {
   if (M == 0) return 0;
-  gws::qkv_finish_kernel<<<M, 256, 0, as_stream(stream)>>>(A, dh, Lmax, acc, ldacc, (__nv_bfloat16*)qkv, ldqkv,
+  PROPD_REQUIRE((A * dh) % 4 == 0, "qkv_finish: H must be a multiple of 4");
+  gws::qkv_finish_kernel<<<dim3(M, (3 * A * dh + 1023) / 1024), 256, 0, as_stream(stream)>>>(A, dh, Lmax, acc, ldacc, (__nv_bfloat16*)qkv, ldqkv,
                                                            row_seq, row_node, seq_slot, seq_len,
                                                            (__nv_bfloat16*)kcache, (__nv_bfloat16*)vcache);
   return check_launch("qkv_finish");
@@ -290,7 +293,8 @@ int propd_qkv_finish(int M, int A, int dh, int Lmax, float* acc, int ldacc, void
 
 int propd_gelu_finish(int M, int N, float* acc, int ldacc, void* out, int ldout, void* stream) {
   if (M == 0) return 0;
-  gws::gelu_finish_kernel<<<M, 512, 0, as_stream(stream)>>>(N, acc, ldacc, (__nv_bfloat16*)out, ldout);
+  PROPD_REQUIRE(N % 4 == 0, "gelu_finish: N must be a multiple of 4");
+  gws::gelu_finish_kernel<<<dim3(M, (N + 1023) / 1024), 256, 0, as_stream(stream)>>>(N, acc, ldacc, (__nv_bfloat16*)out, ldout);
   return check_launch("gelu_finish");
 }
 

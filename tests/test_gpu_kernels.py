@@ -378,7 +378,7 @@ def test_qkv_and_gelu_finish():
          ptr(seq_slot), ptr(seq_len), ptr(kc), ptr(vc), st())
     torch.cuda.synchronize()
     assert torch.equal(qkv, acc0.bfloat16()) and acc.abs().max().item() == 0.0
-    lens = {1: 5, 0: 9}
+    lens = {0: 5, 1: 9}  # seq_len is indexed by slot
     for m, (b, nd) in enumerate(zip([0] * 3 + [1] * 4, [0, 1, 2, 0, 1, 2, 3])):
         slot = [1, 0][b]
         t = lens[slot] + nd
