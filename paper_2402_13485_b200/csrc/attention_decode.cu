@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
   const int s = blockIdx.x, a = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, hl = lane & 15;  // half-warp, lane within it (dims 8*hl .. 8*hl+7)
+  pdl_wait();
+  pdl_trigger();
   const int slot = p.seq_slot[b];
   const int L = p.seq_len[slot];
   const int r0 = p.row_off[b];
@@ -247,16 +249,18 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   p.ldout = ldout;
   *handled = true;
   dim3 grid(nsplit, A, B);
+  int e = 0;
   switch (max_rows_per_seq) {
-    case 1: dec::decode_kernel<1><<<grid, dec::THREADS, 0, st>>>(p); break;
-    case 2: dec::decode_kernel<2><<<grid, dec::THREADS, 0, st>>>(p); break;
-    default: dec::decode_kernel<4><<<grid, dec::THREADS, 0, st>>>(p); break;
+    case 1: e = launch_pdl("tree_attention(decode)", dec::decode_kernel<1>, grid, dim3(dec::THREADS), 0, st, p); break;
+    case 2: e = launch_pdl("tree_attention(decode)", dec::decode_kernel<2>, grid, dim3(dec::THREADS), 0, st, p); break;
+    default: e = launch_pdl("tree_attention(decode)", dec::decode_kernel<4>, grid, dim3(dec::THREADS), 0, st, p); break;
   }
-  if (int e = check_launch("tree_attention(decode)")) return e;
+  if (e) return e;
   if (nsplit > 1) {
-    attn_combine_kernel<__nv_bfloat16><<<dim3(M, A), 128, 0, st>>>(A, dec::DH, nsplit, p.part_o, p.part_ml, p.out,
-                                                                  ldout);
-    if (int e = check_launch("tree_attention(decode combine)")) return e;
+    if (int e2 = launch_pdl("tree_attention(decode combine)", attn_combine_kernel<__nv_bfloat16>, dim3(M, A),
+                            dim3(128), 0, st, A, dec::DH, nsplit, (const float*)p.part_o, (const float*)p.part_ml,
+                            p.out, ldout))
+      return e2;
   }
   return 0;
 }

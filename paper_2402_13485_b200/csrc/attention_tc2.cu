@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TR2(0);
+  pdl_wait();
   const int s = blockIdx.x / p.mtiles, mt = blockIdx.x % p.mtiles;
   const int a = blockIdx.y, b = blockIdx.z;
   const int slot = p.seq_slot[b];
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation (see common.cuh)
   if (threadIdx.x == 0) TR2(1);
   const size_t row_base = ((size_t)slot * p.A + a) * p.Lmax;
 
@@ -498,12 +500,13 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   }
   *handled = true;
   dim3 grid(nsplit * mtiles, A, B);
-  tc2::attn_tc2_kernel<<<grid, tc2::THREADS, tc2::SMEM_TOTAL, st>>>(km, vm, p);
-  if (int e = check_launch("tree_attention(tc2)")) return e;
+  if (int e = launch_pdl("tree_attention(tc2)", tc2::attn_tc2_kernel, grid, dim3(tc2::THREADS), tc2::SMEM_TOTAL,
+                         st, km, vm, p))
+    return e;
   if (nsplit > 1) {
-    attn_combine_kernel<__nv_bfloat16><<<dim3(M, A), 128, 0, st>>>(A, tc2::DH, nsplit, p.part_o, p.part_ml, p.out,
-                                                                  ldout);
-    if (int e = check_launch("tree_attention(tc2 combine)")) return e;
+    if (int e = launch_pdl("tree_attention(tc2 combine)", attn_combine_kernel<__nv_bfloat16>, dim3(M, A), dim3(128),
+                           0, st, A, tc2::DH, nsplit, (const float*)p.part_o, (const float*)p.part_ml, p.out, ldout))
+      return e;
   }
   return 0;
 }

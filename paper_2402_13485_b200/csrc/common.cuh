@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
 
 #include "../../include/propd.h"
 
@@ -20,6 +21,41 @@ int check_launch(const char* what);
   } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- programmatic dependent launch (PDL) ----
+// The per-layer kernels are launched with programmatic stream serialisation:
+// a kernel may be scheduled while its predecessor drains, runs its
+// independent prologue (barrier init, TMEM alloc, weight prefetch), then
+// blocks in pdl_wait() until the predecessor grid has completed and its
+// writes are visible.  Every kernel launched through launch_pdl MUST call
+// pdl_wait() before it touches memory written by earlier kernels, and must
+// call pdl_trigger() only after its own TMEM allocation (a dependent CTA that
+// grabbed the SM's TMEM first would otherwise deadlock it).  Both are no-ops
+// for a normal launch.  PROPD_PDL=0 in the environment disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+
+template <typename... Exp, typename... Act>
+inline int launch_pdl(const char* what, void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail("%s: %s", what, cudaGetErrorString(e));
+  }
+  return check_launch(what);
+}
 
 // ---- element conversion ----
 __device__ __forceinline__ float to_f(float v) { return v; }

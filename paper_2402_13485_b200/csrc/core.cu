@@ -9,6 +9,7 @@
 //   stable argsort top-k                     backends.py:282, 323
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -27,6 +28,14 @@ int fail(const char* fmt, ...) {
   va_end(ap);
   g_error = buf;
   return 1;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("PROPD_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 int check_launch(const char* what) {
@@ -103,6 +112,8 @@ __global__ void __launch_bounds__(512) add_ln_vec_kernel(int H, float* __restric
                                                           T* __restrict__ out, const int32_t* __restrict__ in_idx,
                                                           const int32_t* __restrict__ out_idx) {
   __shared__ float red[32];
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const int src = in_idx ? in_idx[m] : m;
   const int dst = out_idx ? out_idx[m] : m;
@@ -423,10 +434,10 @@ int propd_add_ln(int dtype, int M, int H, float* x, const void* delta, void* out
       if (threads > 512) threads = 512;
       const int chunks = (H + threads * 8 - 1) / (threads * 8);
       switch (chunks) {
-        case 1: add_ln_vec_kernel<T, 1><<<M, threads, 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx); break;
-        case 2: add_ln_vec_kernel<T, 2><<<M, threads, 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx); break;
-        case 3: add_ln_vec_kernel<T, 3><<<M, threads, 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx); break;
-        default: add_ln_vec_kernel<T, 4><<<M, threads, 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx); break;
+        case 1: return launch_pdl("add_ln", add_ln_vec_kernel<T, 1>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx);
+        case 2: return launch_pdl("add_ln", add_ln_vec_kernel<T, 2>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx);
+        case 3: return launch_pdl("add_ln", add_ln_vec_kernel<T, 3>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx);
+        default: return launch_pdl("add_ln", add_ln_vec_kernel<T, 4>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx);
       }
     } else {
       add_ln_kernel<T><<<M, threads_for(H), 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx);

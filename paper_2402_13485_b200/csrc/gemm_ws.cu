@@ -62,9 +62,22 @@ __global__ void __launch_bounds__(THREADS, 2)
   __syncthreads();
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation (see common.cuh)
   if (warp == 0) {
     if (lane == 0) {
-      for (int j = 0; j < nkb; ++j) {
+      // The weights do not depend on the preceding kernels: fill the first
+      // stages with W while the predecessor drains, then wait for X.
+      const int pre = min(nkb, STAGES);
+      for (int j = 0; j < pre; ++j) {
+        mbar_expect_tx(&full[j], STAGE);
+        uint8_t* a = smem + j * STAGE;
+        const int k = (kb0 + j) * BK;
+        tma_load_2d(a, &wmap, &full[j], n0, k);
+        tma_load_2d(a + A_BYTES / 2, &wmap, &full[j], n0 + 64, k);
+      }
+      pdl_wait();
+      for (int j = 0; j < pre; ++j) tma_load_2d(smem + j * STAGE + A_BYTES, &xmap, &full[j], (kb0 + j) * BK, 0);
+      for (int j = pre; j < nkb; ++j) {
         const int st = j % STAGES;
         mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 31);
         mbar_expect_tx(&full[st], STAGE);
@@ -74,8 +87,11 @@ __global__ void __launch_bounds__(THREADS, 2)
         tma_load_2d(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k);
         tma_load_2d(a + A_BYTES, &xmap, &full[st], k, 0);
       }
+    } else {
+      pdl_wait();
     }
   } else if (warp == 1) {
+    pdl_wait();
     if (lane == 0) {
       // A = W^T MN-major (features contiguous), B = X K-major; M = 128, N = MP
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(MP >> 3) << 17) |
@@ -98,6 +114,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
   } else {
     // epilogue: lane = output feature, columns = tokens
+    pdl_wait();
     const int q4 = warp & 3;
     const int f = n0 + q4 * 32 + lane;
     mbar_wait(acc_full, 0, 33);
@@ -187,8 +204,7 @@ static int launch(const CUtensorMap& wm, const CUtensorMap& xm, Args p, dim3 gri
     if (e != cudaSuccess) return fail("gemm_ws: %s", cudaGetErrorString(e));
     attr = true;
   }
-  gemm_ws_kernel<MP><<<grid, THREADS, smem, st>>>(wm, xm, p);
-  return check_launch("gemm_ws");
+  return launch_pdl("gemm_ws", gemm_ws_kernel<MP>, grid, dim3(THREADS), smem, st, wm, xm, p);
 }
 
 // ------------------------------------------------------------------ finish
@@ -197,6 +213,8 @@ __global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ a
                                   const int32_t* __restrict__ row_node, const int32_t* __restrict__ seq_slot,
                                   const int32_t* __restrict__ seq_len, __nv_bfloat16* __restrict__ kc,
                                   __nv_bfloat16* __restrict__ vc) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const int H = A * dh;
   const int slot = seq_slot[row_seq[m]];
@@ -223,6 +241,8 @@ __global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ a
 
 __global__ void gelu_finish_kernel(int N, float* __restrict__ acc, int ldacc, __nv_bfloat16* __restrict__ out,
                                    int ldout) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const float c = 0.7978845608028654f;
   float* a = acc + (size_t)m * ldacc;
@@ -285,17 +305,16 @@ int propd_qkv_finish(int M, int A, int dh, int Lmax, float* acc, int ldacc, void
                      void* kcache, void* vcache, void* stream) {
   if (M == 0) return 0;
   PROPD_REQUIRE((A * dh) % 4 == 0, "qkv_finish: H must be a multiple of 4");
-  gws::qkv_finish_kernel<<<dim3(M, (3 * A * dh + 1023) / 1024), 256, 0, as_stream(stream)>>>(A, dh, Lmax, acc, ldacc, (__nv_bfloat16*)qkv, ldqkv,
-                                                           row_seq, row_node, seq_slot, seq_len,
-                                                           (__nv_bfloat16*)kcache, (__nv_bfloat16*)vcache);
-  return check_launch("qkv_finish");
+  return launch_pdl("qkv_finish", gws::qkv_finish_kernel, dim3(M, (3 * A * dh + 1023) / 1024), dim3(256), 0,
+                    as_stream(stream), A, dh, Lmax, acc, ldacc, (__nv_bfloat16*)qkv, ldqkv, row_seq, row_node,
+                    seq_slot, seq_len, (__nv_bfloat16*)kcache, (__nv_bfloat16*)vcache);
 }
 
 int propd_gelu_finish(int M, int N, float* acc, int ldacc, void* out, int ldout, void* stream) {
   if (M == 0) return 0;
   PROPD_REQUIRE(N % 4 == 0, "gelu_finish: N must be a multiple of 4");
-  gws::gelu_finish_kernel<<<dim3(M, (N + 1023) / 1024), 256, 0, as_stream(stream)>>>(N, acc, ldacc, (__nv_bfloat16*)out, ldout);
-  return check_launch("gelu_finish");
+  return launch_pdl("gelu_finish", gws::gelu_finish_kernel, dim3(M, (N + 1023) / 1024), dim3(256), 0,
+                    as_stream(stream), N, acc, ldacc, (__nv_bfloat16*)out, ldout);
 }
 
 }  // extern "C"

@@ -57,3 +57,22 @@ with open(args.out + "_cpu.txt", "w") as fh:
     fh.write(ka.table(sort_by="self_cpu_time_total", row_limit=40))
 print(ka.table(sort_by="cuda_time_total", row_limit=25))
 print(ka.table(sort_by="self_cpu_time_total", row_limit=25))
+
+# GPU idle gaps between consecutive device activities (kernels + memcpys)
+import json  # noqa: E402
+
+prof.export_chrome_trace(args.out + "_trace.json")
+ev = [e for e in json.load(open(args.out + "_trace.json"))["traceEvents"]
+      if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
+ev.sort(key=lambda e: e["ts"])
+gaps = []
+for a_, b_ in zip(ev, ev[1:]):
+    g = b_["ts"] - (a_["ts"] + a_["dur"])
+    gaps.append((g, a_["name"][:50], b_["name"][:50]))
+span = ev[-1]["ts"] + ev[-1]["dur"] - ev[0]["ts"]
+busy = sum(e["dur"] for e in ev)
+print(f"device span {span / args.steps:.1f} us/step, busy {busy / args.steps:.1f} us/step, "
+      f"{len(ev) / args.steps:.0f} activities/step, gaps<=3us sum {sum(g for g, _, _ in gaps if g <= 3) / args.steps:.1f}"
+      f" us/step, gaps>3us sum {sum(g for g, _, _ in gaps if g > 3) / args.steps:.1f} us/step")
+for g, a_, b_ in sorted(gaps, reverse=True)[:12]:
+    print(f"  gap {g:8.1f} us  after {a_}  before {b_}")
