@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA graphs")
+    ap.add_argument("--sync-rows", action="store_true",
+                    help="size the post-prune layers on the host (one mid-step sync) instead of on the device")
     return ap.parse_args()
 
 
@@ -53,7 +55,7 @@ def model_cfg(args):
     from paper_2402_13485_b200 import TinyTransformerConfig
 
     return TinyTransformerConfig(layers=args.layers, hidden=4096, heads=32, vocab=32000, draft_heads=4,
-                                 max_positions=args.kv + 5 * (2 * args.steps + args.warmup + 52), seed=0)
+                                 max_positions=args.kv + 5 * (2 * args.steps + args.warmup + 100), seed=0)
 
 
 def engine_cfg(args):
@@ -187,16 +189,22 @@ def run_b200(args, rank: int, world: int, group):
     eng = DecodeEngine(be, engine_cfg(args), None, group=group)
     states = be.synthetic_states(B, args.kv, seed=1000 + rank)
     seqs = [_Seq(st, st.committed[:], rank * B + i) for i, st in enumerate(states)]
-    be.attn_timer = []  # graphs captured from here on carry K2 timing event nodes
-    # untimed priming: run until no new CUDA graph has been captured for 6
-    # consecutive steps (every tree size / survivor-row bucket seen so far has
-    # its graphs), then W warm-up steps
-    stable, primed = 0, 0
-    while stable < 6 and primed < 48:
-        n_graphs = len(be._graphs)
-        eng._step(seqs, 10 ** 9)
-        primed += 1
-        stable = stable + 1 if len(be._graphs) == n_graphs else 0
+    if args.sync_rows:
+        be.device_rows = False
+
+    def prime():
+        # untimed priming: run until no new CUDA graph has been captured for 6
+        # consecutive steps (every tree size / survivor-row bucket seen so far
+        # has its graphs)
+        stable, n = 0, 0
+        while stable < 6 and n < 48:
+            n_graphs = len(be._graphs)
+            eng._step(seqs, 10 ** 9)
+            n += 1
+            stable = stable + 1 if len(be._graphs) == n_graphs else 0
+        return n
+
+    primed = prime()
     for _ in range(args.warmup):
         eng._step(seqs, 10 ** 9)
     graphs_before = len(be._graphs)
@@ -219,7 +227,10 @@ def run_b200(args, rank: int, world: int, group):
     launches = be.launches - launches0
     captures_in_timed = len(be._graphs) - graphs_before
     # second timed region of K steps: per-launch CUDA events around every K2
-    # launch (event nodes inside the graphs), harvested after each step
+    # launch (event nodes inside separately captured graphs), harvested after
+    # each step
+    be.attn_timer = []
+    prime()
     be.attn_timer = []
     for _ in range(args.steps):
         eng._step(seqs, 10 ** 9)

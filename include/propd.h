@@ -76,8 +76,11 @@ int propd_bonus_embed(int dtype, int B, int H, const int32_t* bonus, const int32
  * x += delta (if delta != NULL, dtype-typed); out = LN(x) (no affine, eps 1e-5,
  * population variance).  in_idx/out_idx (nullable) gather/scatter rows:
  * row m reads x[in_idx ? in_idx[m] : m], writes out[out_idx ? out_idx[m] : m].
- * When delta is given the residual update is written back to x (in place). */
-int propd_add_ln(int dtype, int M, int H, float* x, const void* delta, void* out,
+ * When delta is given the residual update is written back to x (in place).
+ * rows_dev (nullable, device int32; also on argmax_rows / qkv_finish /
+ * gelu_finish): only rows m < *rows_dev are processed — the live row count of
+ * a pass launched for a padded capacity M. */
+int propd_add_ln(int dtype, int M, const int32_t* rows_dev, int H, float* x, const void* delta, void* out,
                  const int32_t* in_idx, const int32_t* out_idx, void* stream);
 /* In-place tanh-GELU over count elements. */
 int propd_gelu(int dtype, int64_t count, void* buf, void* stream);
@@ -87,7 +90,7 @@ int propd_residual_add(int dtype, int64_t count, float* x, const void* delta, vo
 int propd_gather_rows(int dtype, int M, int H, const float* src, const int32_t* idx, void* dst,
                       void* stream);
 /* First-max argmax per row of an fp32 [M, V] matrix (row stride ld). */
-int propd_argmax_rows(int M, int V, int ld, const float* logits, int32_t* out, void* stream);
+int propd_argmax_rows(int M, const int32_t* rows_dev, int V, int ld, const float* logits, int32_t* out, void* stream);
 /* Stable descending top-k per row (ties -> lower index; == numpy
  * argsort(-x, kind="stable")[:k]), k <= 1024. */
 int propd_topk_rows(int R, int V, int ld, int k, const float* logits, int32_t* out_idx,
@@ -129,16 +132,19 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
  * [M,K], Y fp32 row stride ldy).  accumulate = 1: split-K partial sums are
  * added with fp32 reductions into Y (Y must hold the addend, e.g. the
  * residual stream or a zeroed accumulator); 0: Y is overwritten.  N % 128 ==
- * 0, K % 64 == 0.  max_split <= 0: automatic. */
-int propd_gemm_ws(int M, int N, int K, const void* X, int ldx, const void* W, int ldw, float* Y, int ldy,
-                  int accumulate, int max_split, void* stream);
+ * 0, K % 64 == 0.  max_split <= 0: automatic.  rows_dev (nullable, device
+ * int32): only rows < min(M, *rows_dev) of Y are written — the live row count
+ * of a pass whose size is known only on the device (post-prune survivors),
+ * so the launch can be captured once for the padded size M. */
+int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
+                  float* Y, int ldy, int accumulate, int max_split, void* stream);
 /* acc[M, 3H] fp32 -> qkv bf16 [M, 3H] and K/V rows into the layer cache
  * (slot seq_len[seq_slot[row_seq[m]]] + row_node[m]); acc re-zeroed. */
-int propd_qkv_finish(int M, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,
+int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,
                      const int32_t* row_seq, const int32_t* row_node, const int32_t* seq_slot, const int32_t* seq_len,
                      void* kcache, void* vcache, void* stream);
 /* out = bf16(tanh-GELU(acc)) for acc[M, N] fp32; acc re-zeroed. */
-int propd_gelu_finish(int M, int N, float* acc, int ldacc, void* out, int ldout, void* stream);
+int propd_gelu_finish(int M, const int32_t* rows_dev, int N, float* acc, int ldacc, void* out, int ldout, void* stream);
 
 /* ---- K3: early prune (pruning.py:40-66, backends.py:320-327) ----
  * early_logits: fp32 [R, V], one row per (sequence, parent-slot): row
@@ -184,9 +190,11 @@ int propd_kv_compact(int dtype, int B, int D, int layers, int A, int dh, int Lma
                      const int32_t* acc_len, void* kcache, void* vcache, void* stream);
 
 /* Padding for graph-captured passes: rows [*total, S_pad) of the compacted
- * tables become batch entry B (row_seq = B, row_node = 0, row_src = 0) and
- * row_off[B+1] = S_pad. */
-int propd_pad_rows(int B, int S_pad, const int32_t* total, int32_t* row_seq, int32_t* row_node, int32_t* row_src,
+ * tables get row_seq = B, row_node = 0, row_src = 0.  pad_seq = 1: they form
+ * batch entry B (the scratch sequence, row_off[B+1] = S_pad) and are computed
+ * like real rows; pad_seq = 0: they belong to no sequence (row_off[B+1] =
+ * *total) and the pass's kernels skip them via rows_dev. */
+int propd_pad_rows(int B, int S_pad, int pad_seq, const int32_t* total, int32_t* row_seq, int32_t* row_node, int32_t* row_src,
                    int32_t* row_off, void* stream);
 
 /* seq_len[seq_slot[b]] += delta (delta_dev[b] if non-NULL, else delta). */

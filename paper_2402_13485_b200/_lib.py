@@ -12,7 +12,7 @@ import os
 from ctypes import c_double, c_int, c_int64, c_void_p
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpropd.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 F32 = 0
 BF16 = 1
@@ -27,22 +27,22 @@ SIGNATURES = {
     "propd_abi_version": [],
     "propd_num_sms": [],
     "propd_prepare": [],
-    "propd_pad_rows": [I, I, P, P, P, P, P, P],
+    "propd_pad_rows": [I, I, I, P, P, P, P, P, P],
     "propd_tree_embed": [I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "propd_embed_rows": [I, I, I, P, P, P, P, P, P],
     "propd_bonus_embed": [I, I, I, P, P, P, P, P, P, P, P, P, P, P],
-    "propd_add_ln": [I, I, I, P, P, P, P, P, P],
+    "propd_add_ln": [I, I, P, I, P, P, P, P, P, P],
     "propd_gelu": [I, L, P, P],
     "propd_residual_add": [I, L, P, P, P],
     "propd_gather_rows": [I, I, I, P, P, P, P],
-    "propd_argmax_rows": [I, I, I, P, P, P],
+    "propd_argmax_rows": [I, P, I, I, P, P, P],
     "propd_topk_rows": [I, I, I, I, P, P, P, P],
     "propd_kv_append": [I, I, I, I, I, P, I, P, P, P, P, P, P, P],
     "propd_attn_workspace_bytes": [I, I, I, I],
     "propd_tree_attention": [I, I, I, I, I, I, I, I, I, I, P, I, P, P, P, P, P, P, P, I, I, P, I, P, L, P],
-    "propd_gemm_ws": [I, I, I, P, I, P, I, P, I, I, I, P],
-    "propd_qkv_finish": [I, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
-    "propd_gelu_finish": [I, I, P, I, P, I, P],
+    "propd_gemm_ws": [I, P, I, I, P, I, P, I, P, I, I, I, P],
+    "propd_qkv_finish": [I, P, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
+    "propd_gelu_finish": [I, P, I, P, I, P, I, P],
     "propd_early_member": [I, I, I, I, I, P, P, P, P, P, P],
     "propd_prune_compact": [I, I, P, P, P, P, P, P, P, P, P, P, P],
     "propd_verify_commit": [I, I, I, I, I, I, I, I, I, L, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],

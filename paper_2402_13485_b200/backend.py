@@ -101,6 +101,7 @@ class Rows:
     max_keys: int
     max_rows: int
     kv_keys: int = 0  # host count of K/V rows the pass streams (roofline accounting)
+    live: object = None  # device int32 [1]: live row count when M is a padded capacity
 
 
 @dataclass
@@ -173,6 +174,7 @@ class B200Backend:
         # fp32 accumulator for QKV / W1 partial sums (kept zero between uses)
         self.use_gws = (dtype == "bf16") and use_gws and cfg.hidden % 128 == 0
         self._acc = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32) if self.use_gws else None
+        self.device_rows = True  # sync-free post-prune pass when it fits the weight-streaming GEMMs
         self._graphs: dict = {}
         self._templates: dict = {}
         self._host: dict = {}
@@ -270,7 +272,7 @@ class B200Backend:
         h = torch.empty(M, H, device=self.device, dtype=T)
         ctx = torch.empty(M, H, device=self.device, dtype=T)
         for l in range(l0, l1):
-            self._call("propd_add_ln", self.code, M, H, ptr(x), ptr(pending), ptr(h), None, None, st)
+            self._call("propd_add_ln", self.code, M, None, H, ptr(x), ptr(pending), ptr(h), None, None, st)
             qkv = torch.mm(h, self.w.wqkv[l])
             kc, vc = self.kcache[l], self.vcache[l]
             self._call("propd_kv_append", self.code, M, self.A, self.dh, self.Lmax, ptr(qkv), 3 * H,
@@ -287,7 +289,7 @@ class B200Backend:
                 ev1.record()
                 self._events_sink().append((ev0, ev1, self._role, M))
             o = torch.mm(ctx, self.w.wo[l])
-            self._call("propd_add_ln", self.code, M, H, ptr(x), ptr(o), ptr(h), None, None, st)
+            self._call("propd_add_ln", self.code, M, None, H, ptr(x), ptr(o), ptr(h), None, None, st)
             g = torch.mm(h, self.w.w1[l])
             self._call("propd_gelu", self.code, g.numel(), ptr(g), st)
             pending = torch.mm(g, self.w.w2[l])
@@ -326,16 +328,17 @@ class B200Backend:
         ws = self._workspace(M, rt.B)
         ws_bytes = 0 if ws is None else ws.numel()
         acc = self._acc
+        live = ptr(rt.live)
         h = torch.empty(M, H, device=self.device, dtype=T)
         ctx = torch.empty(M, H, device=self.device, dtype=T)
         qkv = torch.empty(M, 3 * H, device=self.device, dtype=T)
         g = torch.empty(M, 4 * H, device=self.device, dtype=T)
         for l in range(l0, l1):
-            self._call("propd_add_ln", self.code, M, H, ptr(x), ptr(pending), ptr(h), None, None, st)
+            self._call("propd_add_ln", self.code, M, live, H, ptr(x), ptr(pending), ptr(h), None, None, st)
             pending = None
             kc, vc = self.kcache[l], self.vcache[l]
-            self._call("propd_gemm_ws", M, 3 * H, H, ptr(h), H, ptr(self.w.wqkv[l]), 3 * H, ptr(acc), 3 * H, 1, 0, st)
-            self._call("propd_qkv_finish", M, self.A, self.dh, self.Lmax, ptr(acc), 3 * H, ptr(qkv), 3 * H,
+            self._call("propd_gemm_ws", M, live, 3 * H, H, ptr(h), H, ptr(self.w.wqkv[l]), 3 * H, ptr(acc), 3 * H, 1, 0, st)
+            self._call("propd_qkv_finish", M, live, self.A, self.dh, self.Lmax, ptr(acc), 3 * H, ptr(qkv), 3 * H,
                        ptr(rt.row_seq), ptr(rt.row_node), ptr(rt.seq_slot), ptr(self.seq_len), ptr(kc), ptr(vc), st)
             if self.attn_timer is not None:
                 ev0 = self._timing_event()
@@ -348,20 +351,22 @@ class B200Backend:
                 ev1 = self._timing_event()
                 ev1.record()
                 self._events_sink().append((ev0, ev1, self._role, M))
-            self._call("propd_gemm_ws", M, H, H, ptr(ctx), H, ptr(self.w.wo[l]), H, ptr(x), H, 1, 0, st)
-            self._call("propd_add_ln", self.code, M, H, ptr(x), None, ptr(h), None, None, st)
-            self._call("propd_gemm_ws", M, 4 * H, H, ptr(h), H, ptr(self.w.w1[l]), 4 * H, ptr(acc), 4 * H, 1, 0, st)
-            self._call("propd_gelu_finish", M, 4 * H, ptr(acc), 4 * H, ptr(g), 4 * H, st)
-            self._call("propd_gemm_ws", M, H, 4 * H, ptr(g), 4 * H, ptr(self.w.w2[l]), H, ptr(x), H, 1, 0, st)
+            self._call("propd_gemm_ws", M, live, H, H, ptr(ctx), H, ptr(self.w.wo[l]), H, ptr(x), H, 1, 0, st)
+            self._call("propd_add_ln", self.code, M, live, H, ptr(x), None, ptr(h), None, None, st)
+            self._call("propd_gemm_ws", M, live, 4 * H, H, ptr(h), H, ptr(self.w.w1[l]), 4 * H, ptr(acc), 4 * H, 1, 0, st)
+            self._call("propd_gelu_finish", M, live, 4 * H, ptr(acc), 4 * H, ptr(g), 4 * H, st)
+            self._call("propd_gemm_ws", M, live, H, 4 * H, ptr(g), 4 * H, ptr(self.w.w2[l]), H, ptr(x), H, 1, 0, st)
         return None
 
-    def _proj_f32(self, X, Wt, N):
-        """fp32 logits X @ Wt ([M,H] x [H,N]) for the LM / early / draft heads."""
+    def _proj_f32(self, X, Wt, N, live=None):
+        """fp32 logits X @ Wt ([M,H] x [H,N]) for the LM / early / draft heads
+        (rows >= *live, when given, are left unwritten)."""
         torch = self.torch
         M = X.shape[0]
+        live = ptr(live)
         if self.use_gws and M <= 128 and N % 128 == 0 and X.dtype == torch.bfloat16:
             out = torch.empty(M, N, device=self.device, dtype=torch.float32)
-            self._call("propd_gemm_ws", M, N, self.H, ptr(X), self.H, ptr(Wt), N, ptr(out), N, 0, 0, self.stream())
+            self._call("propd_gemm_ws", M, live, N, self.H, ptr(X), self.H, ptr(Wt), N, ptr(out), N, 0, 0, self.stream())
             return out
         out = torch.mm(X, Wt)
         return out if out.dtype == torch.float32 else out.float()
@@ -370,10 +375,10 @@ class B200Backend:
         if pending is not None:
             self._call("propd_residual_add", self.code, x.numel(), ptr(x), ptr(pending), self.stream())
 
-    def _lm_argmax(self, hfin):
-        logits = self._proj_f32(hfin, self.w.w_lm, self.V)
+    def _lm_argmax(self, hfin, live=None):
+        logits = self._proj_f32(hfin, self.w.w_lm, self.V, live)
         am = self.torch.empty(hfin.shape[0], device=self.device, dtype=self.torch.int32)
-        self._call("propd_argmax_rows", hfin.shape[0], self.V, self.V, ptr(logits), ptr(am), self.stream())
+        self._call("propd_argmax_rows", hfin.shape[0], ptr(live), self.V, self.V, ptr(logits), ptr(am), self.stream())
         return logits, am
 
     # ------------------------------------------------- causal append (prefill/extend)
@@ -400,7 +405,7 @@ class B200Backend:
         pending = self._run_layers(x, rt, 0, self.num_layers, None, max(lens), 0)
         last = self._i32(offs[1:] - 1)
         hfin = torch.empty(B, self.H, device=self.device, dtype=self.tdtype)
-        self._call("propd_add_ln", self.code, B, self.H, ptr(x), ptr(pending), ptr(hfin), ptr(last), None, st)
+        self._call("propd_add_ln", self.code, B, None, self.H, ptr(x), ptr(pending), ptr(hfin), ptr(last), None, st)
         logits, am = self._lm_argmax(hfin)
         idx = seq_slot.long()
         self.hidden.index_copy_(0, idx, hfin)
@@ -549,7 +554,7 @@ class B200Backend:
             pending = self._run_layers(x, rt, 0, cfg.layers, bits, n, W)
         S = rt.M
         hfin = torch.empty(S, self.H, device=self.device, dtype=self.tdtype)
-        self._call("propd_add_ln", self.code, S, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
+        self._call("propd_add_ln", self.code, S, None, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
         logits, am = self._lm_argmax(hfin)
         state.last_tree = (toks[keep].copy(), vis.copy())
         state._tree = {"keep": keep, "positions": pos, "L": L}
@@ -628,6 +633,9 @@ class B200Backend:
         """Eager: run fn.  Graph mode: capture fn once per key, then replay."""
         if not self.use_graphs:
             return fn()
+        # graphs with K2 timing event nodes are kept apart from clean ones
+        # (an event node between two kernels also breaks their PDL overlap)
+        key = key + (self.attn_timer is not None,)
         ent = self._graphs.get(key)
         if ent is None:
             torch = self.torch
@@ -673,7 +681,7 @@ class B200Backend:
         pending = self._run_layers(x, rt, 0, self.num_layers, self._one_mask, 1, 1)
         self._role = role
         hfin = torch.empty(B, self.H, device=dev, dtype=self.tdtype)
-        self._call("propd_add_ln", self.code, B, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
+        self._call("propd_add_ln", self.code, B, None, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
         logits, am = self._lm_argmax(hfin)
         self.hidden.index_copy_(0, seq_slot.long(), hfin)
         self._call("propd_scatter_i32", B, ptr(seq_slot), ptr(am), ptr(self.root), st)
@@ -746,7 +754,7 @@ class B200Backend:
                    ptr(o["total"]), st)
         return o
 
-    def _part_b(self, B, tmpl, k, prune, slot_buf, kb, a, S_pad):
+    def _part_b(self, B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows=False):
         torch, st, cfg = self.torch, self.stream(), self.config
         n, D, H = len(tmpl), cfg.draft_heads, self.H
         dev = self.device
@@ -754,19 +762,21 @@ class B200Backend:
         seq_slot = slot_buf[:B]
         if prune is not None:
             # rows [S, S_pad) become the scratch sequence (batch entry B)
-            self._call("propd_pad_rows", B, S_pad, ptr(a["total"]), ptr(a["nrs"]), ptr(a["nrn"]), ptr(a["nsrc"]),
+            self._call("propd_pad_rows", B, S_pad, 0 if device_rows else 1, ptr(a["total"]), ptr(a["nrs"]), ptr(a["nrn"]), ptr(a["nsrc"]),
                        ptr(a["noff"]), st)
             x = torch.empty(S_pad, H, device=dev, dtype=torch.float32)
             self._call("propd_gather_rows", 0, S_pad, H, ptr(a["x"]), ptr(a["nsrc"]), ptr(x), st)
-            rt = Rows(S_pad, B + 1, slot_buf, a["nrs"], a["nrn"], a["noff"], max_keys=kb, max_rows=n)
+            rt = Rows(S_pad, B + 1, slot_buf, a["nrs"], a["nrn"], a["noff"], max_keys=kb, max_rows=n,
+                      live=a["total"] if device_rows else None)
             pending = self._run_layers(x, rt, prune.layer, cfg.layers, td["mask"], n, tmpl.words)
             alive, node_row = a["alive"], a["node_row"]
         else:
             x, pending, alive, node_row = a["x"], a["pending"], None, None
         S = x.shape[0]
+        live = a["total"] if (prune is not None and device_rows) else None
         hfin = torch.empty(S, H, device=dev, dtype=self.tdtype)
-        self._call("propd_add_ln", self.code, S, H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
-        _, row_argmax = self._lm_argmax(hfin)
+        self._call("propd_add_ln", self.code, S, ptr(live), H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
+        _, row_argmax = self._lm_argmax(hfin, live)
         i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
         o = {"acc_node": i32(B * D), "acc_surv": i32(B * D), "acc_len": i32(B), "bonus": i32(B),
              "committed": i32(B * (D + 1)), "ranks": torch.empty(B, D, device=dev, dtype=torch.int8),
@@ -825,14 +835,22 @@ class B200Backend:
         pkey = (prune.layer, prune.topk) if prune is not None else None
         self._role = "tree"
         a = self._run(("A", B, tmpl.paths, k, pkey, kb), lambda: self._part_a(B, tmpl, k, prune, slot_buf, kb))
-        if prune is not None:
-            S = int(a["total"].item())  # the one mid-step sync: row count of layers > p
-            S_pad = self._s_bucket(S) if self.use_graphs else S
+        # Layers > p run on the survivors.  When every projection of that pass
+        # is a weight-streaming GEMM (<= 128 rows), part B is launched for the
+        # padded capacity and the GEMMs read the live row count on the device
+        # (rows past it are never written back), so there is no mid-step sync.
+        cap = self._s_bucket(B * n)
+        device_rows = prune is not None and self.use_gws and self.device_rows and cap <= 128
+        if prune is None:
+            S_pad = B * n
+        elif device_rows:
+            S_pad = cap
         else:
-            S = S_pad = B * n
+            S = int(a["total"].item())  # mid-step sync: row count of layers > p
+            S_pad = self._s_bucket(S) if self.use_graphs else S
         self._role = "tree_pruned"
-        b = self._run(("B", B, tmpl.paths, k, pkey, kb, S_pad),
-                      lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad))
+        b = self._run(("B", B, tmpl.paths, k, pkey, kb, S_pad, device_rows),
+                      lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows))
         if stats is not None:  # single process: replay this batch's records right away (K4)
             P, counts, alpha, order_dev, lcurve_dev = stats
             self.stats_replay_select(b["ranks"], B, P, counts, alpha, order_dev, lcurve_dev)

@@ -110,11 +110,13 @@ __global__ void bonus_embed_kernel(int B, int H, const int32_t* __restrict__ bon
 template <typename T, int CHUNKS>
 __global__ void __launch_bounds__(512) add_ln_vec_kernel(int H, float* __restrict__ x, const T* __restrict__ delta,
                                                           T* __restrict__ out, const int32_t* __restrict__ in_idx,
-                                                          const int32_t* __restrict__ out_idx) {
+                                                          const int32_t* __restrict__ out_idx,
+                                                          const int32_t* __restrict__ rows_dev) {
   __shared__ float red[32];
   pdl_wait();
   pdl_trigger();
   const int m = blockIdx.x;
+  if (rows_dev && m >= *rows_dev) return;
   const int src = in_idx ? in_idx[m] : m;
   const int dst = out_idx ? out_idx[m] : m;
   float* xr = x + (size_t)src * H;
@@ -224,9 +226,11 @@ __global__ void gather_rows_kernel(int H, const float* __restrict__ src, const i
 }
 
 // First maximum per row (numpy argmax semantics).
-__global__ void argmax_rows_kernel(int V, int ld, const float* __restrict__ logits, int32_t* __restrict__ out) {
+__global__ void argmax_rows_kernel(int V, int ld, const float* __restrict__ logits, int32_t* __restrict__ out,
+                                   const int32_t* __restrict__ rows_dev) {
   __shared__ float sv[32];
   __shared__ int si[32];
+  if (rows_dev && (int)blockIdx.x >= *rows_dev) return;
   const float* x = logits + (size_t)blockIdx.x * ld;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -379,7 +383,7 @@ using namespace propd;
 extern "C" {
 
 const char* propd_last_error(void) { return g_error.c_str(); }
-int propd_abi_version(void) { return 2; }
+int propd_abi_version(void) { return 3; }
 int propd_num_sms(void) {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
@@ -422,8 +426,8 @@ int propd_bonus_embed(int dtype, int B, int H, const int32_t* bonus, const int32
   });
 }
 
-int propd_add_ln(int dtype, int M, int H, float* x, const void* delta, void* out, const int32_t* in_idx,
-                 const int32_t* out_idx, void* stream) {
+int propd_add_ln(int dtype, int M, const int32_t* rows_dev, int H, float* x, const void* delta, void* out,
+                 const int32_t* in_idx, const int32_t* out_idx, void* stream) {
   if (M == 0) return 0;
   return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
     cudaStream_t st = as_stream(stream);
@@ -434,12 +438,13 @@ int propd_add_ln(int dtype, int M, int H, float* x, const void* delta, void* out
       if (threads > 512) threads = 512;
       const int chunks = (H + threads * 8 - 1) / (threads * 8);
       switch (chunks) {
-        case 1: return launch_pdl("add_ln", add_ln_vec_kernel<T, 1>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx);
-        case 2: return launch_pdl("add_ln", add_ln_vec_kernel<T, 2>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx);
-        case 3: return launch_pdl("add_ln", add_ln_vec_kernel<T, 3>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx);
-        default: return launch_pdl("add_ln", add_ln_vec_kernel<T, 4>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx);
+        case 1: return launch_pdl("add_ln", add_ln_vec_kernel<T, 1>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx, rows_dev);
+        case 2: return launch_pdl("add_ln", add_ln_vec_kernel<T, 2>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx, rows_dev);
+        case 3: return launch_pdl("add_ln", add_ln_vec_kernel<T, 3>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx, rows_dev);
+        default: return launch_pdl("add_ln", add_ln_vec_kernel<T, 4>, dim3(M), dim3(threads), 0, st, H, x, (const T*)delta, (T*)out, in_idx, out_idx, rows_dev);
       }
     } else {
+      PROPD_REQUIRE(rows_dev == nullptr, "add_ln: rows_dev needs H %% 8 == 0");
       add_ln_kernel<T><<<M, threads_for(H), 0, st>>>(H, x, (const T*)delta, (T*)out, in_idx, out_idx);
     }
     return check_launch("add_ln");
@@ -474,10 +479,10 @@ int propd_gather_rows(int dtype, int M, int H, const float* src, const int32_t* 
   });
 }
 
-int propd_argmax_rows(int M, int V, int ld, const float* logits, int32_t* out, void* stream) {
+int propd_argmax_rows(int M, const int32_t* rows_dev, int V, int ld, const float* logits, int32_t* out, void* stream) {
   if (M == 0) return 0;
   PROPD_REQUIRE(V > 0 && ld >= V, "argmax_rows: bad V=%d ld=%d", V, ld);
-  argmax_rows_kernel<<<M, 256, 0, as_stream(stream)>>>(V, ld, logits, out);
+  argmax_rows_kernel<<<M, 256, 0, as_stream(stream)>>>(V, ld, logits, out, rows_dev);
   return check_launch("argmax_rows");
 }
 

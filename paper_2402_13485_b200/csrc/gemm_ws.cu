@@ -26,6 +26,7 @@ constexpr int A_BYTES = BK * BF * 2;  // W^T tile: 2 boxes of [64 k x 128 B] = 1
 
 struct Args {
   int M, N, K, kblk_per_split, ldy, mp;
+  const int32_t* m_dev;  // nullable: live row count on the device
   float* Y;
   int accumulate;
 };
@@ -33,7 +34,7 @@ struct Args {
 template <int MP>
 __global__ void __launch_bounds__(THREADS, 2)
     gemm_ws_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap xmap, Args p) {
-  constexpr int B_BYTES = MP * 128;  // X tile [MP rows x 64 k x 2 B]
+  constexpr int B_BYTES = MP * 128;  // X tile capacity [MP rows x 64 k x 2 B]
   constexpr int STAGE = A_BYTES + B_BYTES;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
@@ -63,38 +64,47 @@ __global__ void __launch_bounds__(THREADS, 2)
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();  // after the TMEM allocation (see common.cuh)
+  if (warp == 0 && lane == 0) {
+    // The weights do not depend on the preceding kernels: fill the first
+    // stages with W while the predecessor drains (tx bytes announced without
+    // the arrival), then wait for it and add X.
+    const int pre = min(nkb, STAGES);
+    for (int j = 0; j < pre; ++j) {
+      mbar_add_tx(&full[j], A_BYTES);
+      uint8_t* a = smem + j * STAGE;
+      const int k = (kb0 + j) * BK;
+      tma_load_2d(a, &wmap, &full[j], n0, k);
+      tma_load_2d(a + A_BYTES / 2, &wmap, &full[j], n0 + 64, k);
+    }
+  }
+  pdl_wait();
+  // live token rows (device count for passes captured at a padded size): X is
+  // loaded and multiplied in 16-row boxes, only as many as are live
+  const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
+  const int nbox = max(1, (M + 15) >> 4);
   if (warp == 0) {
     if (lane == 0) {
-      // The weights do not depend on the preceding kernels: fill the first
-      // stages with W while the predecessor drains, then wait for X.
       const int pre = min(nkb, STAGES);
       for (int j = 0; j < pre; ++j) {
-        mbar_expect_tx(&full[j], STAGE);
-        uint8_t* a = smem + j * STAGE;
-        const int k = (kb0 + j) * BK;
-        tma_load_2d(a, &wmap, &full[j], n0, k);
-        tma_load_2d(a + A_BYTES / 2, &wmap, &full[j], n0 + 64, k);
+        mbar_expect_tx(&full[j], nbox * 2048);
+        for (int i = 0; i < nbox; ++i)
+          tma_load_2d(smem + j * STAGE + A_BYTES + i * 2048, &xmap, &full[j], (kb0 + j) * BK, i * 16);
       }
-      pdl_wait();
-      for (int j = 0; j < pre; ++j) tma_load_2d(smem + j * STAGE + A_BYTES, &xmap, &full[j], (kb0 + j) * BK, 0);
       for (int j = pre; j < nkb; ++j) {
         const int st = j % STAGES;
         mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 31);
-        mbar_expect_tx(&full[st], STAGE);
+        mbar_expect_tx(&full[st], A_BYTES + nbox * 2048);
         uint8_t* a = smem + st * STAGE;
         const int k = (kb0 + j) * BK;
         tma_load_2d(a, &wmap, &full[st], n0, k);
         tma_load_2d(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k);
-        tma_load_2d(a + A_BYTES, &xmap, &full[st], k, 0);
+        for (int i = 0; i < nbox; ++i) tma_load_2d(a + A_BYTES + i * 2048, &xmap, &full[st], k, i * 16);
       }
-    } else {
-      pdl_wait();
     }
   } else if (warp == 1) {
-    pdl_wait();
     if (lane == 0) {
-      // A = W^T MN-major (features contiguous), B = X K-major; M = 128, N = MP
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(MP >> 3) << 17) |
+      // A = W^T MN-major (features contiguous), B = X K-major; M = 128, N = 16 * nbox
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(nbox * 2) << 17) |
                              ((128u >> 4) << 24);
       for (int j = 0; j < nkb; ++j) {
         const int st = j % STAGES;
@@ -114,21 +124,21 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
   } else {
     // epilogue: lane = output feature, columns = tokens
-    pdl_wait();
     const int q4 = warp & 3;
     const int f = n0 + q4 * 32 + lane;
     mbar_wait(acc_full, 0, 33);
     tc_after_sync();
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
-#pragma unroll
-    for (int c = 0; c < MP / 32 + (MP % 32 ? 1 : 0); ++c) {
+    const int nchunk = (M + 31) >> 5;
+#pragma unroll 1
+    for (int c = 0; c < nchunk; ++c) {
       uint32_t rr[32];
       TMEM_LD32(lane_addr + c * 32, rr);
       tmem_wait_ld();
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const int t = c * 32 + i;
-        if (t < p.M) {
+        if (t < M) {
           float* dst = p.Y + (size_t)t * p.ldy + f;
           const float v = __uint_as_float(rr[i]);
           if (p.accumulate)
@@ -212,10 +222,11 @@ __global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ a
                                   __nv_bfloat16* __restrict__ qkv, int ldqkv, const int32_t* __restrict__ row_seq,
                                   const int32_t* __restrict__ row_node, const int32_t* __restrict__ seq_slot,
                                   const int32_t* __restrict__ seq_len, __nv_bfloat16* __restrict__ kc,
-                                  __nv_bfloat16* __restrict__ vc) {
+                                  __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ rows_dev) {
   pdl_wait();
   pdl_trigger();
   const int m = blockIdx.x;
+  if (rows_dev && m >= *rows_dev) return;
   const int H = A * dh;
   const int slot = seq_slot[row_seq[m]];
   const int t = seq_len[slot] + row_node[m];
@@ -240,10 +251,11 @@ __global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ a
 }
 
 __global__ void gelu_finish_kernel(int N, float* __restrict__ acc, int ldacc, __nv_bfloat16* __restrict__ out,
-                                   int ldout) {
+                                   int ldout, const int32_t* __restrict__ rows_dev) {
   pdl_wait();
   pdl_trigger();
   const int m = blockIdx.x;
+  if (rows_dev && m >= *rows_dev) return;
   const float c = 0.7978845608028654f;
   float* a = acc + (size_t)m * ldacc;
   __nv_bfloat16* o = out + (size_t)m * ldout;
@@ -266,14 +278,14 @@ using namespace propd;
 
 extern "C" {
 
-int propd_gemm_ws(int M, int N, int K, const void* X, int ldx, const void* W, int ldw, float* Y, int ldy,
-                  int accumulate, int max_split, void* stream) {
+int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
+                  float* Y, int ldy, int accumulate, int max_split, void* stream) {
   PROPD_REQUIRE(M >= 1 && M <= 128, "gemm_ws: M=%d outside 1..128", M);
   PROPD_REQUIRE(N % gws::BF == 0 && K % gws::BK == 0, "gemm_ws: N=%d must be a multiple of 128, K=%d of 64", N, K);
   const int mp = ((M + 15) / 16) * 16;
   CUtensorMap wm, xm;
   PROPD_REQUIRE(gws::map2d(&wm, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw, 64) &&
-                    gws::map2d(&xm, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, mp),
+                    gws::map2d(&xm, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, 16),
                 "gemm_ws: tensor map encode failed");
   const int tiles = N / gws::BF, kb = K / gws::BK;
   int split = 1;
@@ -285,7 +297,7 @@ int propd_gemm_ws(int M, int N, int K, const void* X, int ldx, const void* W, in
   }
   const int per = (kb + split - 1) / split;
   split = (kb + per - 1) / per;
-  gws::Args p{M, N, K, per, ldy, mp, Y, accumulate};
+  gws::Args p{M, N, K, per, ldy, mp, rows_dev, Y, accumulate};
   dim3 grid(tiles, split);
   cudaStream_t st = as_stream(stream);
   switch (mp) {
@@ -300,21 +312,21 @@ int propd_gemm_ws(int M, int N, int K, const void* X, int ldx, const void* W, in
   }
 }
 
-int propd_qkv_finish(int M, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,
+int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,
                      const int32_t* row_seq, const int32_t* row_node, const int32_t* seq_slot, const int32_t* seq_len,
                      void* kcache, void* vcache, void* stream) {
   if (M == 0) return 0;
   PROPD_REQUIRE((A * dh) % 4 == 0, "qkv_finish: H must be a multiple of 4");
   return launch_pdl("qkv_finish", gws::qkv_finish_kernel, dim3(M, (3 * A * dh + 1023) / 1024), dim3(256), 0,
                     as_stream(stream), A, dh, Lmax, acc, ldacc, (__nv_bfloat16*)qkv, ldqkv, row_seq, row_node,
-                    seq_slot, seq_len, (__nv_bfloat16*)kcache, (__nv_bfloat16*)vcache);
+                    seq_slot, seq_len, (__nv_bfloat16*)kcache, (__nv_bfloat16*)vcache, rows_dev);
 }
 
-int propd_gelu_finish(int M, int N, float* acc, int ldacc, void* out, int ldout, void* stream) {
+int propd_gelu_finish(int M, const int32_t* rows_dev, int N, float* acc, int ldacc, void* out, int ldout, void* stream) {
   if (M == 0) return 0;
   PROPD_REQUIRE(N % 4 == 0, "gelu_finish: N must be a multiple of 4");
   return launch_pdl("gelu_finish", gws::gelu_finish_kernel, dim3(M, (N + 1023) / 1024), dim3(256), 0,
-                    as_stream(stream), N, acc, ldacc, (__nv_bfloat16*)out, ldout);
+                    as_stream(stream), N, acc, ldacc, (__nv_bfloat16*)out, ldout, rows_dev);
 }
 
 }  // extern "C"

@@ -95,7 +95,7 @@ __global__ void prune_compact_kernel(int B, int n, const int32_t* __restrict__ p
 
 // Graph-captured passes run layers > p on a padded row count: rows
 // [total, S_pad) become batch entry B (the scratch slot, node 0).
-__global__ void pad_rows_kernel(int B, int S_pad, const int32_t* __restrict__ total, int32_t* row_seq,
+__global__ void pad_rows_kernel(int B, int S_pad, int pad_seq, const int32_t* __restrict__ total, int32_t* row_seq,
                                 int32_t* row_node, int32_t* row_src, int32_t* row_off) {
   const int S = *total;
   for (int i = S + blockIdx.x * blockDim.x + threadIdx.x; i < S_pad; i += gridDim.x * blockDim.x) {
@@ -103,7 +103,7 @@ __global__ void pad_rows_kernel(int B, int S_pad, const int32_t* __restrict__ to
     row_node[i] = 0;
     row_src[i] = 0;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) row_off[B + 1] = S_pad;
+  if (blockIdx.x == 0 && threadIdx.x == 0) row_off[B + 1] = pad_seq ? S_pad : S;
 }
 
 // ---------------------------------------------------------------- K5 ------
@@ -333,9 +333,9 @@ int propd_prune_compact(int B, int n, const int32_t* parent, const uint8_t* memb
   return check_launch("prune_compact");
 }
 
-int propd_pad_rows(int B, int S_pad, const int32_t* total, int32_t* row_seq, int32_t* row_node, int32_t* row_src,
+int propd_pad_rows(int B, int S_pad, int pad_seq, const int32_t* total, int32_t* row_seq, int32_t* row_node, int32_t* row_src,
                    int32_t* row_off, void* stream) {
-  pad_rows_kernel<<<1, 256, 0, as_stream(stream)>>>(B, S_pad, total, row_seq, row_node, row_src, row_off);
+  pad_rows_kernel<<<1, 256, 0, as_stream(stream)>>>(B, S_pad, pad_seq, total, row_seq, row_node, row_src, row_off);
   return check_launch("pad_rows");
 }
 

@@ -36,7 +36,7 @@ for M in (1, 16, 48):
         W = torch.randn(K, N, device="cuda").bfloat16()
         Y = torch.zeros(M, N, device="cuda")
         max_split = int(os.environ.get("MAX_SPLIT", "0"))
-        t_ws = bench(lambda: call("propd_gemm_ws", M, N, K, X.data_ptr(), K, W.data_ptr(), N, Y.data_ptr(), N, acc,
+        t_ws = bench(lambda: call("propd_gemm_ws", M, None, N, K, X.data_ptr(), K, W.data_ptr(), N, Y.data_ptr(), N, acc,
                                   max_split, torch.cuda.current_stream().cuda_stream))
         t_mm = bench(lambda: torch.mm(X, W))
         gb = K * N * 2 / 1e9

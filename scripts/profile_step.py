@@ -27,11 +27,13 @@ ap.add_argument("--attn-impl", type=int, default=0)
 ap.add_argument("--out", default="gpurun_out/profile")
 ap.add_argument("--graphs", action="store_true")
 ap.add_argument("--no-cpu-baseline", action="store_true")
+ap.add_argument("--sync-rows", action="store_true", help="size the post-prune pass on the host (mid-step sync)")
 args = ap.parse_args()
 
 cfg = bench.model_cfg(args)
 be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=args.batch + 1, kv_len=cfg.max_positions,
                  attn_impl=args.attn_impl, use_graphs=args.graphs)
+be.device_rows = not args.sync_rows
 eng = DecodeEngine(be, bench.engine_cfg(args), None)
 states = be.synthetic_states(args.batch, args.kv)
 seqs = [_Seq(st, st.committed[:], i) for i, st in enumerate(states)]

@@ -68,8 +68,27 @@ def test_argmax_first_max():
     x[1] = 0.0
     dx = torch.from_numpy(x).to(DEV)
     out = torch.empty(9, dtype=torch.int32, device=DEV)
-    call("propd_argmax_rows", 9, 32000, 32000, ptr(dx), ptr(out), st())
+    call("propd_argmax_rows", 9, None, 32000, 32000, ptr(dx), ptr(out), st())
     assert np.array_equal(out.cpu().numpy(), np.argmax(x, axis=1))
+
+
+def test_rows_dev_skips_padded_rows():
+    """add_ln / argmax_rows with a device row count: rows < *rows_dev equal the
+    unpadded result bit for bit, rows past it are not touched."""
+    M, H, live = 8, 4096, 3
+    torch.manual_seed(0)
+    x0 = torch.randn(M, H, device=DEV)
+    d = torch.randn(M, H, device=DEV).bfloat16()
+    xa, xb = x0.clone(), x0.clone()
+    oa = torch.full((M, H), 7.0, device=DEV).bfloat16()
+    ob = oa.clone()
+    call("propd_add_ln", 1, M, None, H, ptr(xa), ptr(d), ptr(oa), None, None, st())
+    call("propd_add_ln", 1, M, ptr(i32([live])), H, ptr(xb), ptr(d), ptr(ob), None, None, st())
+    assert torch.equal(xb[:live], xa[:live]) and torch.equal(ob[:live], oa[:live])
+    assert torch.equal(xb[live:], x0[live:]) and bool((ob[live:] == 7.0).all())
+    am = torch.full((M,), -5, dtype=torch.int32, device=DEV)
+    call("propd_argmax_rows", M, ptr(i32([live])), H, H, ptr(xa), ptr(am), st())
+    assert am[:live].tolist() == xa[:live].argmax(1).tolist() and am[live:].eq(-5).all()
 
 
 # --------------------------------------------------------------- attention
@@ -357,11 +376,30 @@ def test_gemm_ws_matches_fp32_reference(M, N, K, acc):
     ref = X.float() @ Wt.float()
     base = torch.randn(M, N, device=DEV) if acc else torch.full((M, N), float("nan"), device=DEV)
     Y = base.clone()
-    call("propd_gemm_ws", M, N, K, ptr(X), K, ptr(Wt), N, ptr(Y), N, acc, 0, st())
+    call("propd_gemm_ws", M, None, N, K, ptr(X), K, ptr(Wt), N, ptr(Y), N, acc, 0, st())
     torch.cuda.synchronize()
     want = ref + (base if acc else 0)
     err = (Y - want).abs().max().item()
     assert err <= 1e-3 * max(1.0, want.abs().max().item()), err
+
+
+@pytest.mark.parametrize("live", [0, 1, 13, 37, 64])
+def test_gemm_ws_device_row_count(live):
+    """rows_dev: rows < min(M, *rows_dev) are computed, the rest of Y is left untouched (bit-exact)."""
+    M, N, K = 37, 4096, 1024
+    torch.manual_seed(live)
+    X = torch.randn(M, K, device=DEV).bfloat16()
+    Wt = (torch.randn(K, N, device=DEV) / K ** 0.5).bfloat16()
+    ref = X.float() @ Wt.float()
+    for acc in (0, 1):
+        base = torch.randn(M, N, device=DEV)
+        Y = base.clone()
+        call("propd_gemm_ws", M, ptr(i32([live])), N, K, ptr(X), K, ptr(Wt), N, ptr(Y), N, acc, 0, st())
+        torch.cuda.synchronize()
+        r = min(M, live)
+        want = ref[:r] + (base[:r] if acc else 0)
+        assert (Y[:r] - want).abs().max().item() <= 1e-3 * max(1.0, want.abs().max().item()) if r else True
+        assert torch.equal(Y[r:], base[r:])
 
 
 def test_qkv_and_gelu_finish():
@@ -374,7 +412,7 @@ def test_qkv_and_gelu_finish():
     vc = torch.zeros_like(kc)
     row_seq, row_node = i32([0] * 3 + [1] * 4), i32([0, 1, 2, 0, 1, 2, 3])
     seq_slot, seq_len = i32([1, 0]), i32([5, 9])
-    call("propd_qkv_finish", M, A, dh, Lmax, ptr(acc), 3 * H, ptr(qkv), 3 * H, ptr(row_seq), ptr(row_node),
+    call("propd_qkv_finish", M, None, A, dh, Lmax, ptr(acc), 3 * H, ptr(qkv), 3 * H, ptr(row_seq), ptr(row_node),
          ptr(seq_slot), ptr(seq_len), ptr(kc), ptr(vc), st())
     torch.cuda.synchronize()
     assert torch.equal(qkv, acc0.bfloat16()) and acc.abs().max().item() == 0.0
@@ -387,7 +425,7 @@ def test_qkv_and_gelu_finish():
     g_acc = torch.randn(M, 4 * H, device=DEV)
     g0 = g_acc.clone()
     out = torch.empty(M, 4 * H, device=DEV, dtype=torch.bfloat16)
-    call("propd_gelu_finish", M, 4 * H, ptr(g_acc), 4 * H, ptr(out), 4 * H, st())
+    call("propd_gelu_finish", M, None, 4 * H, ptr(g_acc), 4 * H, ptr(out), 4 * H, st())
     torch.cuda.synchronize()
     ref = torch.nn.functional.gelu(g0, approximate="tanh")
     assert (out.float() - ref).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
