@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(ATT_THREADS) attn_core_kernel(AttnArgs p) {
 template <typename T>
 __global__ void attn_combine_kernel(int A, int dh, int nsplit, const float* __restrict__ part_o,
                                     const float* __restrict__ part_ml, T* __restrict__ out, int ldout) {
+  pdl_trigger();  // early: the dependent only prefetches weights before its own wait
   pdl_wait();
-  pdl_trigger();
   const int row = blockIdx.x, a = blockIdx.y;
   const size_t base = ((size_t)row * A + a) * nsplit;
   float mx = -INFINITY;

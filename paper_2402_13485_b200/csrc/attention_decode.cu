@@ -36,6 +36,8 @@ struct Args {
   float* part_ml;
   __nv_bfloat16* out;
   int ldout;
+  unsigned long long* tl;  // development timeline (common.cuh)
+  unsigned int tag;
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -60,7 +62,9 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
   const int s = blockIdx.x, a = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, hl = lane & 15;  // half-warp, lane within it (dims 8*hl .. 8*hl+7)
+  const unsigned long long t_entry = p.tl ? gtimer() : 0ull;
   pdl_wait();
+  const unsigned long long t_wait = p.tl ? gtimer() : 0ull;
   pdl_trigger();
   const int slot = p.seq_slot[b];
   const int L = p.seq_len[slot];
@@ -203,6 +207,7 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
       }
     }
   }
+  if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait);
 }
 
 }  // namespace dec
@@ -247,6 +252,8 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   p.part_ml = p.part_o + (size_t)M * A * nsplit * dec::DH;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
+  p.tl = g_dbg_trace;
+  p.tag = g_dbg_tag++;
   *handled = true;
   dim3 grid(nsplit, A, B);
   int e = 0;

@@ -62,6 +62,8 @@ struct Args {
   __nv_bfloat16* out;
   int ldout;
   unsigned long long* trace;  // debug: per-block event timestamps of CTA (0,0,0)
+  unsigned long long* tl;     // development timeline (common.cuh)
+  unsigned int tag;
 };
 
 __device__ __forceinline__ unsigned long long gtime2() {
@@ -107,7 +109,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TR2(0);
+  const unsigned long long t_entry = p.tl ? gtimer() : 0ull;
   pdl_wait();
+  const unsigned long long t_wait = p.tl ? gtimer() : 0ull;
   const int s = blockIdx.x / p.mtiles, mt = blockIdx.x % p.mtiles;
   const int a = blockIdx.y, b = blockIdx.z;
   const int slot = p.seq_slot[b];
@@ -399,6 +403,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncwarp();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
+  if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait);
 }
 
 // ------------------------------------------------------------------ host --
@@ -493,6 +498,8 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
   p.trace = g_trace2;
+  p.tl = g_dbg_trace;
+  p.tag = g_dbg_tag++;
   static bool attr = false;
   if (!attr) {
     if (int e = attention_tc2_prepare()) return e;

@@ -30,8 +30,11 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // writes are visible.  Every kernel launched through launch_pdl MUST call
 // pdl_wait() before it touches memory written by earlier kernels, and must
 // call pdl_trigger() only after its own TMEM allocation (a dependent CTA that
-// grabbed the SM's TMEM first would otherwise deadlock it).  Both are no-ops
-// for a normal launch.  PROPD_PDL=0 in the environment disables it.
+// grabbed the SM's TMEM first would otherwise deadlock it).  Kernels without
+// TMEM trigger before their own wait, so the next weight-streaming GEMM is
+// launched early and prefetches its weights while they run (its pre-wait
+// section touches nothing but the weights).  Both are no-ops for a normal
+// launch.  PROPD_PDL=0 in the environment disables it.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();
@@ -55,6 +58,38 @@ inline int launch_pdl(const char* what, void (*kern)(Exp...), dim3 grid, dim3 bl
     return fail("%s: %s", what, cudaGetErrorString(e));
   }
   return check_launch(what);
+}
+
+// ---- development trace (scripts/kernel_timeline.py) ----
+// When a trace buffer is installed (propd_debug_timeline), instrumented kernels
+// append one record per CTA: [tag, cta, smid, t_entry, t_after_pdl_wait,
+// t_main_done, t_exit] (globaltimer ns); buf[0] is the record counter, records
+// start at buf[8].  tag = host launch sequence number.  Off (NULL) normally.
+extern unsigned long long* g_dbg_trace;
+extern unsigned int g_dbg_tag;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned int smid() {
+  unsigned int s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
+__device__ __forceinline__ void trace_record(unsigned long long* buf, unsigned int tag, unsigned long long t0,
+                                             unsigned long long t1, unsigned long long t2) {
+  if (buf == nullptr) return;
+  const unsigned long long t3 = gtimer();
+  const unsigned long long i = atomicAdd(buf, 1ull);
+  unsigned long long* r = buf + 8 + i * 8;
+  r[0] = tag;
+  r[1] = blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
+  r[2] = smid();
+  r[3] = t0;
+  r[4] = t1;
+  r[5] = t2;
+  r[6] = t3;
 }
 
 // ---- element conversion ----

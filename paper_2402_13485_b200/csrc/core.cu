@@ -113,8 +113,8 @@ __global__ void __launch_bounds__(512) add_ln_vec_kernel(int H, float* __restric
                                                           const int32_t* __restrict__ out_idx,
                                                           const int32_t* __restrict__ rows_dev) {
   __shared__ float red[32];
+  pdl_trigger();  // early: the dependent only prefetches weights before its own wait
   pdl_wait();
-  pdl_trigger();
   const int m = blockIdx.x;
   if (rows_dev && m >= *rows_dev) return;
   const int src = in_idx ? in_idx[m] : m;
@@ -380,7 +380,18 @@ static int threads_for(int H) {
 
 using namespace propd;
 
+namespace propd {
+unsigned long long* g_dbg_trace = nullptr;
+unsigned int g_dbg_tag = 0;
+}  // namespace propd
+
 extern "C" {
+
+int propd_debug_timeline(void* buf) {  // development aid: per-CTA timeline records (common.cuh)
+  propd::g_dbg_trace = reinterpret_cast<unsigned long long*>(buf);
+  propd::g_dbg_tag = 0;
+  return 0;
+}
 
 const char* propd_last_error(void) { return g_error.c_str(); }
 int propd_abi_version(void) { return 3; }

@@ -21,7 +21,7 @@ namespace propd {
 namespace gws {
 using namespace propd::tc;
 
-constexpr int BF = 128, BK = 64, STAGES = 4, THREADS = 192;
+constexpr int BF = 128, BK = 64, THREADS = 192;
 constexpr int A_BYTES = BK * BF * 2;  // W^T tile: 2 boxes of [64 k x 128 B] = 16 KB
 
 struct Args {
@@ -29,18 +29,31 @@ struct Args {
   const int32_t* m_dev;  // nullable: live row count on the device
   float* Y;
   int accumulate;
+  unsigned long long* trace;  // development timeline (common.cuh)
+  unsigned int tag;
 };
+
+// Ring depth per X-tile size: as deep as two CTAs per SM allow (deeper rings
+// keep more weight bytes in flight and prefetch more of them while the
+// predecessor kernel drains).
+__host__ __device__ constexpr int stages_for(int mp) { return mp <= 16 ? 6 : (mp <= 32 ? 5 : (mp <= 64 ? 4 : 3)); }
 
 template <int MP>
 __global__ void __launch_bounds__(THREADS, 2)
     gemm_ws_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap xmap, Args p) {
+  constexpr int STAGES = stages_for(MP);
   constexpr int B_BYTES = MP * 128;  // X tile capacity [MP rows x 64 k x 2 B]
   constexpr int STAGE = A_BYTES + B_BYTES;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // SW128 operands need 1024-byte alignment; static shared (timeline scratch)
+  // may precede the dynamic window, so align explicitly (+1 KB requested)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const unsigned long long t_entry = p.trace ? gtimer() : 0ull;
+  __shared__ unsigned long long s_t[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BF;
   const int kb0 = blockIdx.y * p.kblk_per_split;
@@ -78,6 +91,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
   }
   pdl_wait();
+  if (p.trace && threadIdx.x == 0) s_t[0] = gtimer();
   // live token rows (device count for passes captured at a padded size): X is
   // loaded and multiplied in 16-row boxes, only as many as are live
   const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
@@ -128,6 +142,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int f = n0 + q4 * 32 + lane;
     mbar_wait(acc_full, 0, 33);
     tc_after_sync();
+    if (p.trace && threadIdx.x == 64) s_t[1] = gtimer();
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
     const int nchunk = (M + 31) >> 5;
 #pragma unroll 1
@@ -156,6 +171,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     __syncwarp();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
   }
+  if (p.trace && threadIdx.x == 0) trace_record(p.trace, p.tag, t_entry, s_t[0], s_t[1]);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -207,10 +223,14 @@ static bool map2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
 
 template <int MP>
 static int launch(const CUtensorMap& wm, const CUtensorMap& xm, Args p, dim3 grid, cudaStream_t st) {
-  constexpr int smem = STAGES * (A_BYTES + MP * 128) + 256;
+  constexpr int smem = stages_for(MP) * (A_BYTES + MP * 128) + 256 + 1024;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm_ws_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // two CTAs per SM need the maximum shared-memory carveout
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_ws_kernel<MP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return fail("gemm_ws: %s", cudaGetErrorString(e));
     attr = true;
   }
@@ -223,8 +243,8 @@ __global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ a
                                   const int32_t* __restrict__ row_node, const int32_t* __restrict__ seq_slot,
                                   const int32_t* __restrict__ seq_len, __nv_bfloat16* __restrict__ kc,
                                   __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ rows_dev) {
+  pdl_trigger();  // early: the dependent only prefetches weights before its own wait
   pdl_wait();
-  pdl_trigger();
   const int m = blockIdx.x;
   if (rows_dev && m >= *rows_dev) return;
   const int H = A * dh;
@@ -252,8 +272,8 @@ __global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ a
 
 __global__ void gelu_finish_kernel(int N, float* __restrict__ acc, int ldacc, __nv_bfloat16* __restrict__ out,
                                    int ldout, const int32_t* __restrict__ rows_dev) {
+  pdl_trigger();  // early: the dependent only prefetches weights before its own wait
   pdl_wait();
-  pdl_trigger();
   const int m = blockIdx.x;
   if (rows_dev && m >= *rows_dev) return;
   const float c = 0.7978845608028654f;
@@ -297,7 +317,7 @@ int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, i
   }
   const int per = (kb + split - 1) / split;
   split = (kb + per - 1) / per;
-  gws::Args p{M, N, K, per, ldy, mp, rows_dev, Y, accumulate};
+  gws::Args p{M, N, K, per, ldy, mp, rows_dev, Y, accumulate, g_dbg_trace, g_dbg_tag++};
   dim3 grid(tiles, split);
   cudaStream_t st = as_stream(stream);
   switch (mp) {

@@ -21,6 +21,7 @@ ap.add_argument("--rows", type=int, default=16)
 ap.add_argument("--kv", type=int, default=1024)
 ap.add_argument("--layers", type=int, default=8)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--unfused", action="store_true")
 args = ap.parse_args()
 
 cfg = TinyTransformerConfig(layers=args.layers, hidden=4096, heads=32, vocab=32000, draft_heads=4,
@@ -52,10 +53,10 @@ def run(skip):
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
-        be._run_layers_ws(x, rt, 0, args.layers, td["mask"], n, tmpl.words)
+        be._run_layers(x, rt, 0, args.layers, td["mask"], n, tmpl.words)
     torch.cuda.synchronize()
     with torch.cuda.graph(g, stream=s):
-        be._run_layers_ws(x, rt, 0, args.layers, td["mask"], n, tmpl.words)
+        be._run_layers(x, rt, 0, args.layers, td["mask"], n, tmpl.words)
     be._call = orig_call
     g.replay()
     torch.cuda.synchronize()
@@ -70,6 +71,8 @@ def run(skip):
 
 floor = 402653184 / 6543.1e9 * 1e6
 print(f"rows {n}, kv {args.kv}: weight floor {floor:.1f} us/layer")
+if "--unfused" in sys.argv:
+    be.fused_epi = False
 for label, skip in [("full layer", set()), ("no attention", {"propd_tree_attention"}),
                     ("no add_ln", {"propd_add_ln"}), ("no finish", {"propd_qkv_finish", "propd_gelu_finish"}),
                     ("GEMMs only", {"propd_tree_attention", "propd_add_ln", "propd_qkv_finish", "propd_gelu_finish"})]:
