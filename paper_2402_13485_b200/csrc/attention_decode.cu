@@ -1,23 +1,30 @@
 // K2 for few query rows per sequence (the bonus pass: 1 row; tiny trees):
-// a streaming split-KV decode kernel on the CUDA cores.
+// a streaming split-KV decode kernel on the CUDA cores with the split-KV
+// combine done inside a thread-block cluster.
 //
 // With one row per sequence there is no GEMM to feed a tensor core; the work
 // is a pure stream of the sequence's K/V cache (backends.py:216-233 with
-// n = 1).  A half-warp covers one key (16 lanes x 8 bf16 = the 256-byte
-// row), so one warp-wide 16-byte load fetches two keys; scores are reduced
-// with 4 shuffles, softmax is online per 8-key batch, and each lane
-// accumulates 8 output dims.  Up to ROWS query rows share every K/V load.
-#include "common.cuh"
+// n = 1).  Design for B200:
+//   - every (sequence, head) is cut into <= 8 key splits that form ONE
+//     cluster (grid.x = splits), so that even batch 1 puts ~2 CTAs on every
+//     SM and the whole cache of a launch is in flight at once;
+//   - each CTA streams its split in 64-key chunks (K and V of a chunk are two
+//     contiguous 16 KB rows of the [Lmax, 128] cache tile) with bulk async
+//     copies into a 3-deep shared-memory ring, one mbarrier per stage;
+//   - a half-warp covers one key (16 lanes x 8 bf16 = the 256-byte row) for
+//     up to ROWS query rows; scores are reduced with 4 shuffles and softmax is
+//     online per 8-key batch;
+//   - the per-split (m, l, o) states are merged through distributed shared
+//     memory by the cluster (each rank finishes a slice of the output), so
+//     there is no workspace and no second combine launch.
+#include "tc_common.cuh"
 
 namespace propd {
-
-template <typename T>
-__global__ void attn_combine_kernel(int A, int dh, int nsplit, const float* __restrict__ part_o,
-                                    const float* __restrict__ part_ml, T* __restrict__ out, int ldout);
-
 namespace dec {
+using namespace propd::tc;
 
 constexpr int DH = 128, THREADS = 128, KB = 8;  // keys per half-warp batch
+constexpr int CHUNK = 64, RING = 3, MAX_SPLIT = 8;
 
 struct Args {
   const __nv_bfloat16* qkv;
@@ -31,20 +38,12 @@ struct Args {
   const uint64_t* mask;
   int n_tmpl, W, A, Lmax;
   float scale_log2;
-  int split_len, nsplit;
-  float* part_o;
-  float* part_ml;
+  int split_len;
   __nv_bfloat16* out;
   int ldout;
   unsigned long long* tl;  // development timeline (common.cuh)
   unsigned int tag;
 };
-
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -55,25 +54,84 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
   }
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_nrank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
+  float v;
+  asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+// contiguous global -> shared bulk copy completing on an mbarrier
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int ROWS>
+struct Smem {
+  __nv_bfloat16 k[RING][CHUNK * DH];
+  __nv_bfloat16 v[RING][CHUNK * DH];
+  float red_m[4][ROWS], red_l[4][ROWS];
+  float red_o[4][ROWS][DH];
+  float part_m[ROWS], part_l[ROWS];  // this split's merged state (read by the cluster)
+  float part_o[ROWS][DH];
+  uint64_t full[RING];
+};
+
 template <int ROWS>
 __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
-  __shared__ float red_m[4][ROWS], red_l[4][ROWS];
-  __shared__ float red_o[4][ROWS][DH];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Smem<ROWS>& sm = *reinterpret_cast<Smem<ROWS>*>(smem_raw);
   const int s = blockIdx.x, a = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int half = lane >> 4, hl = lane & 15;  // half-warp, lane within it (dims 8*hl .. 8*hl+7)
   const unsigned long long t_entry = p.tl ? gtimer() : 0ull;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < RING; ++i) mbar_init(&sm.full[i], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
   pdl_wait();
-  const unsigned long long t_wait = p.tl ? gtimer() : 0ull;
   pdl_trigger();
+  const unsigned long long t_wait = p.tl ? gtimer() : 0ull;
   const int slot = p.seq_slot[b];
   const int L = p.seq_len[slot];
   const int r0 = p.row_off[b];
-  const int nrows = p.row_off[b + 1] - r0;
-  if (nrows <= 0) return;
+  const int nrows = min(ROWS, p.row_off[b + 1] - r0);
   const int nkeys = L + p.n_tmpl;
   const int k_begin = s * p.split_len;
-  const int k_end = min(nkeys, k_begin + p.split_len);
+  const int k_end = nrows > 0 ? min(nkeys, k_begin + p.split_len) : k_begin;
+  const int nchunk = k_end > k_begin ? (k_end - k_begin + CHUNK - 1) / CHUNK : 0;
+  const size_t tile = ((size_t)slot * p.A + a) * p.Lmax;  // first cache row of this (sequence, head)
+  auto issue = [&](int c) {
+    const int st = c % RING;
+    const int key0 = k_begin + c * CHUNK;
+    const int nk = min(CHUNK, p.Lmax - key0);  // whole chunk unless the tile ends
+    const uint32_t bytes = (uint32_t)nk * DH * 2;
+    mbar_expect_tx(&sm.full[st], 2 * bytes);
+    bulk_load(sm.k[st], p.kc + (tile + key0) * DH, bytes, &sm.full[st]);
+    bulk_load(sm.v[st], p.vc + (tile + key0) * DH, bytes, &sm.full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int c = 0; c < min(RING, nchunk); ++c) issue(c);
 
   // query rows (8 dims per lane) and their tree-visibility bitsets
   float q[ROWS][8];
@@ -105,17 +163,18 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) o[r][i] = 0.f;
   }
-  const size_t base = ((size_t)slot * p.A + a) * p.Lmax * DH + hl * 8;
-  // each warp handles 2*KB consecutive keys per iteration (KB per half-warp)
-  for (int k0 = k_begin + warp * 2 * KB; k0 < k_end; k0 += 4 * 2 * KB) {
+  for (int c = 0; c < nchunk; ++c) {
+    const int st = c % RING;
+    mbar_wait(&sm.full[st], (c / RING) & 1, 41);
+    // warp w: keys [16w, 16w + 16) of the chunk, half-warp h: 8 of them
+    const int kc0 = warp * 2 * KB + half * KB;
     uint4 kr[KB], vr[KB];
 #pragma unroll
     for (int t = 0; t < KB; ++t) {
-      const int key = k0 + half * KB + t;
-      const int kk = key < k_end ? key : k_end - 1;  // clamp: masked below
-      kr[t] = *reinterpret_cast<const uint4*>(p.kc + base + (size_t)kk * DH);
-      vr[t] = *reinterpret_cast<const uint4*>(p.vc + base + (size_t)kk * DH);
+      kr[t] = *reinterpret_cast<const uint4*>(&sm.k[st][(kc0 + t) * DH + hl * 8]);
+      vr[t] = *reinterpret_cast<const uint4*>(&sm.v[st][(kc0 + t) * DH + hl * 8]);
     }
+    const int kbase = k_begin + c * CHUNK + kc0;
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
       if (r >= nrows) break;
@@ -129,7 +188,7 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
         for (int i = 0; i < 8; ++i) d = fmaf(q[r][i], kf[i], d);
 #pragma unroll
         for (int off = 8; off > 0; off >>= 1) d += __shfl_xor_sync(0xffffffffu, d, off);
-        const int key = k0 + half * KB + t;
+        const int key = kbase + t;
         bool vis;
         if (key >= k_end) vis = false;
         else if (key < L) vis = true;
@@ -152,6 +211,9 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
       for (int i = 0; i < 8; ++i) o[r][i] *= corr;
 #pragma unroll
       for (int t = 0; t < KB; ++t) {
+        // masked keys are skipped, not multiplied by 0: the ring tail past
+        // the cache tile holds stale shared memory (possibly NaN patterns)
+        if (sc[t] == -INFINITY) continue;
         const float pt = ex2(sc[t] - mn);
         ps += pt;
         float vf[8];
@@ -162,6 +224,8 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
       ps += __shfl_xor_sync(0xffffffffu, ps, 16);
       l[r] = l[r] * corr + ps;
     }
+    __syncthreads();  // every warp is done with stage st
+    if (threadIdx.x == 0 && c + RING < nchunk) issue(c + RING);
   }
   // merge the two half-warps (same dims, different keys), then the 4 warps
 #pragma unroll
@@ -172,42 +236,120 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) red_o[warp][r][hl * 8 + i] = o[r][i];
+      for (int i = 0; i < 8; ++i) sm.red_o[warp][r][hl * 8 + i] = o[r][i];
       if (hl == 0) {
-        red_m[warp][r] = m[r];
-        red_l[warp][r] = l[r];
+        sm.red_m[warp][r] = m[r];
+        sm.red_l[warp][r] = l[r];
       }
     }
   }
   __syncthreads();
+  const int nsplit = (int)cluster_nrank();
   for (int idx = threadIdx.x; idx < ROWS * DH; idx += THREADS) {
     const int r = idx / DH, d = idx - r * DH;
     if (r >= nrows) continue;
     float mx = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) mx = fmaxf(mx, red_m[w][r]);
+    for (int w = 0; w < 4; ++w) mx = fmaxf(mx, sm.red_m[w][r]);
     float lsum = 0.f, acc = 0.f;
     if (mx != -INFINITY) {
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        const float f = red_m[w][r] == -INFINITY ? 0.f : ex2(red_m[w][r] - mx);
-        lsum += red_l[w][r] * f;
-        acc += red_o[w][r][d] * f;
+        const float f = sm.red_m[w][r] == -INFINITY ? 0.f : ex2(sm.red_m[w][r] - mx);
+        lsum += sm.red_l[w][r] * f;
+        acc += sm.red_o[w][r][d] * f;
       }
     }
-    const int row = r0 + r;
-    if (p.nsplit == 1) {
-      p.out[(size_t)row * p.ldout + a * DH + d] = __float2bfloat16_rn(lsum > 0.f ? acc / lsum : 0.f);
+    if (nsplit == 1) {
+      p.out[(size_t)(r0 + r) * p.ldout + a * DH + d] = __float2bfloat16_rn(lsum > 0.f ? acc / lsum : 0.f);
     } else {
-      const size_t pb = ((size_t)row * p.A + a) * p.nsplit + s;
-      p.part_o[pb * DH + d] = acc;
+      sm.part_o[r][d] = acc;
       if (d == 0) {
-        p.part_ml[pb * 2] = mx == -INFINITY ? -INFINITY : mx * 0.69314718055994531f;
-        p.part_ml[pb * 2 + 1] = lsum;
+        sm.part_m[r] = mx;
+        sm.part_l[r] = lsum;
       }
     }
   }
+  if (nsplit > 1) {
+    // cluster combine: rank q finishes elements [q * per, (q + 1) * per) of the
+    // nrows x 128 output through distributed shared memory
+    cluster_sync_all();
+    const int rank = (int)cluster_rank();
+    const int total = nrows * DH;
+    const int per = (total + nsplit - 1) / nsplit;
+    uint32_t base_m[MAX_SPLIT], base_l[MAX_SPLIT], base_o[MAX_SPLIT];
+#pragma unroll
+    for (int qq = 0; qq < MAX_SPLIT; ++qq) {
+      const uint32_t rk = qq < nsplit ? qq : 0;
+      base_m[qq] = map_rank(smem_u32(sm.part_m), rk);
+      base_l[qq] = map_rank(smem_u32(sm.part_l), rk);
+      base_o[qq] = map_rank(smem_u32(&sm.part_o[0][0]), rk);
+    }
+    for (int e = rank * per + threadIdx.x; e < min(total, (rank + 1) * per); e += THREADS) {
+      const int r = e / DH, d = e - r * DH;
+      float ms[MAX_SPLIT], mx = -INFINITY;
+#pragma unroll
+      for (int qq = 0; qq < MAX_SPLIT; ++qq) {
+        ms[qq] = qq < nsplit ? ld_dsmem(base_m[qq] + r * 4) : -INFINITY;
+        mx = fmaxf(mx, ms[qq]);
+      }
+      float lsum = 0.f, acc = 0.f;
+      if (mx != -INFINITY) {
+#pragma unroll
+        for (int qq = 0; qq < MAX_SPLIT; ++qq) {
+          if (qq < nsplit && ms[qq] != -INFINITY) {
+            const float f = ex2(ms[qq] - mx);
+            lsum += ld_dsmem(base_l[qq] + r * 4) * f;
+            acc += ld_dsmem(base_o[qq] + (r * DH + d) * 4) * f;
+          }
+        }
+      }
+      p.out[(size_t)(r0 + r) * p.ldout + a * DH + d] = __float2bfloat16_rn(lsum > 0.f ? acc / lsum : 0.f);
+    }
+    cluster_sync_all();  // peers may still read this CTA's state
+  }
   if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait);
+}
+
+template <int ROWS>
+static int launch(const Args& p, dim3 grid, cudaStream_t st) {
+  static bool attr = false;
+  constexpr int smem = (int)sizeof(Smem<ROWS>);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(decode_kernel<ROWS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return fail("tree_attention(decode): %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (grid.x > 1) {  // the key splits of one (sequence, head) form a cluster
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = grid.x;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, decode_kernel<ROWS>, p);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail("tree_attention(decode): %s", cudaGetErrorString(e));
+  }
+  return check_launch("tree_attention(decode)");
 }
 
 }  // namespace dec
@@ -218,18 +360,19 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
                           const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                           void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled) {
   *handled = false;
+  (void)M;
+  (void)ws;
+  (void)ws_bytes;
   if (max_rows_per_seq > 4 || W > 4 || (ldqkv % 8) != 0) return 0;
-  // enough CTAs for ~4 per SM; >= 256 keys per split
-  const int ctas = B * A;
-  int nsplit = (4 * 148 + ctas - 1) / ctas;
-  const int cap = (max_keys + 255) / 256;
+  // splits per (sequence, head): enough CTAs for ~2 per SM, one cluster each
+  const int pairs = B * A;
+  int nsplit = (2 * 148 + pairs - 1) / pairs;
+  const int cap = (max_keys + dec::CHUNK - 1) / dec::CHUNK;
   if (nsplit > cap) nsplit = cap;
-  if (nsplit > 64) nsplit = 64;
+  if (nsplit > dec::MAX_SPLIT) nsplit = dec::MAX_SPLIT;
   if (nsplit < 1) nsplit = 1;
-  const int64_t need = (int64_t)M * A * nsplit * (dec::DH + 2) * (int64_t)sizeof(float);
-  if (nsplit > 1 && (ws == nullptr || ws_bytes < need)) nsplit = 1;
   int split_len = (max_keys + nsplit - 1) / nsplit;
-  split_len = ((split_len + 63) / 64) * 64;
+  split_len = ((split_len + dec::CHUNK - 1) / dec::CHUNK) * dec::CHUNK;
   nsplit = (max_keys + split_len - 1) / split_len;
   dec::Args p{};
   p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
@@ -247,29 +390,17 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   p.Lmax = Lmax;
   p.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
   p.split_len = split_len;
-  p.nsplit = nsplit;
-  p.part_o = reinterpret_cast<float*>(ws);
-  p.part_ml = p.part_o + (size_t)M * A * nsplit * dec::DH;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
   p.tl = g_dbg_trace;
   p.tag = g_dbg_tag++;
   *handled = true;
   dim3 grid(nsplit, A, B);
-  int e = 0;
   switch (max_rows_per_seq) {
-    case 1: e = launch_pdl("tree_attention(decode)", dec::decode_kernel<1>, grid, dim3(dec::THREADS), 0, st, p); break;
-    case 2: e = launch_pdl("tree_attention(decode)", dec::decode_kernel<2>, grid, dim3(dec::THREADS), 0, st, p); break;
-    default: e = launch_pdl("tree_attention(decode)", dec::decode_kernel<4>, grid, dim3(dec::THREADS), 0, st, p); break;
+    case 1: return dec::launch<1>(p, grid, st);
+    case 2: return dec::launch<2>(p, grid, st);
+    default: return dec::launch<4>(p, grid, st);
   }
-  if (e) return e;
-  if (nsplit > 1) {
-    if (int e2 = launch_pdl("tree_attention(decode combine)", attn_combine_kernel<__nv_bfloat16>, dim3(M, A),
-                            dim3(128), 0, st, A, dec::DH, nsplit, (const float*)p.part_o, (const float*)p.part_ml,
-                            p.out, ldout))
-      return e2;
-  }
-  return 0;
 }
 
 }  // namespace propd

@@ -162,6 +162,34 @@ def test_tree_attention_vs_torch(dtype, dh, A, lens, paths, impl):
     assert err <= tol, (err, tol)
 
 
+@pytest.mark.parametrize("A,lens,rows", [(32, [1030], 1), (32, [5, 700, 64, 4096], 1), (8, [63, 65, 2000], 2),
+                                          (32, [1], 1), (4, [300, 129], 3)])
+def test_decode_attention_cluster_combine(A, lens, rows):
+    """Streaming decode kernel (impl 3: <= 4 rows per sequence, key splits of one (sequence, head) reduced in a
+    thread-block cluster) vs the torch fp32 reference; causal rows = the last `rows` tree nodes."""
+    dh, B = 128, len(lens)
+    H = A * dh
+    n = rows
+    Lmax = max(lens) + n + 8
+    rng = np.random.default_rng(A + B)
+    kc = torch.randn(B, A, Lmax, dh, device=DEV).bfloat16()
+    vc = torch.randn(B, A, Lmax, dh, device=DEV).bfloat16()
+    M = B * n
+    qkv = (torch.randn(M, 3 * H, device=DEV) * 2).bfloat16()
+    slots = list(range(B))
+    row_off = [b * n for b in range(B + 1)]
+    row_node = [i for b in range(B) for i in range(n)]
+    out = torch.zeros(M, H, device=DEV, dtype=torch.bfloat16)
+    call("propd_tree_attention", _lib.BF16, 3, B, M, A, dh, Lmax, B, n, max(lens) + n, ptr(qkv), 3 * H, ptr(kc),
+         ptr(vc), ptr(i32(slots)), ptr(i32(lens)), ptr(i32(row_off)), ptr(i32(row_node)), None, n, 0, ptr(out), H,
+         None, 0, st())
+    torch.cuda.synchronize()
+    ref = torch_tree_attention(qkv[:, :H], kc, vc, slots, lens, row_off, row_node, None, A, dh)
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+    del rng
+
+
 def test_tree_attention_causal_and_pruned_rows():
     """Causal new rows (mask=NULL) and a compacted subset of tree rows."""
     dh, A, B = 16, 2, 2
