@@ -138,6 +138,45 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
  * so the launch can be captured once for the padded size M. */
 int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
                   float* Y, int ldy, int accumulate, int max_split, void* stream);
+/* In-kernel phases of a weight-streaming GEMM launch (all CTAs co-resident:
+ * tiles x splits <= 2 x SMs; phases meet at grid barriers on `bar`, 4 zeroed
+ * uint32 that every launch leaves zeroed).  They replace the small kernels
+ * between projections, so a layer is five launches and the weight stream of
+ * a launch keeps flowing while its prologue runs:
+ *   prologue PROPD_PRO_LN:   X[t] = bf16(LN(pro_src[t])) (no affine, eps 1e-5,
+ *            population variance; backends.py:135-142), pro_cols = K <= 4096
+ *   prologue PROPD_PRO_GELU: X = bf16(tanh-GELU(pro_src)), pro_src re-zeroed
+ *            (the previous launch's split-K accumulator)
+ *   (X = pro_dst must be this launch's X operand, row stride pro_ldd = ldx)
+ *   tail PROPD_TAIL_QKV:     after the split-K reduction into Y (= the zeroed
+ *            fp32 QKV accumulator, N = 3H): Q rows -> tail_q (bf16, stride
+ *            tail_ldq), K/V rows -> the layer cache exactly as
+ *            propd_qkv_finish; Y re-zeroed. */
+#define PROPD_PRO_NONE 0
+#define PROPD_PRO_LN 1
+#define PROPD_PRO_GELU 2
+#define PROPD_TAIL_NONE 0
+#define PROPD_TAIL_QKV 1
+typedef struct propd_ws_phases {
+  int pro_mode;
+  float* pro_src;
+  int pro_ld;
+  void* pro_dst;
+  int pro_ldd, pro_cols;
+  int tail_mode;
+  void* tail_q;
+  int tail_ldq;
+  int A, dh, Lmax;
+  const int32_t* row_seq;
+  const int32_t* row_node;
+  const int32_t* seq_slot;
+  const int32_t* seq_len;
+  void* kcache;
+  void* vcache;
+  uint32_t* bar;
+} propd_ws_phases;
+int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
+                     float* Y, int ldy, int accumulate, int max_split, const propd_ws_phases* phases, void* stream);
 /* acc[M, 3H] fp32 -> qkv bf16 [M, 3H] and K/V rows into the layer cache
  * (slot seq_len[seq_slot[row_seq[m]]] + row_node[m]); acc re-zeroed. */
 int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,

@@ -41,6 +41,7 @@ SIGNATURES = {
     "propd_attn_workspace_bytes": [I, I, I, I],
     "propd_tree_attention": [I, I, I, I, I, I, I, I, I, I, P, I, P, P, P, P, P, P, P, I, I, P, I, P, L, P],
     "propd_gemm_ws": [I, P, I, I, P, I, P, I, P, I, I, I, P],
+    "propd_gemm_ws_ph": [I, P, I, I, P, I, P, I, P, I, I, I, "phases", P],
     "propd_qkv_finish": [I, P, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
     "propd_gelu_finish": [I, P, I, P, I, P, I, P],
     "propd_early_member": [I, I, I, I, I, P, P, P, P, P, P],
@@ -52,6 +53,19 @@ SIGNATURES = {
     "propd_stats_replay_select": [I, I, I, P, c_double, P, P, P, P, P],
 }
 _RESTYPES = {"propd_last_error": ctypes.c_char_p, "propd_attn_workspace_bytes": c_int64}
+
+
+PRO_NONE, PRO_LN, PRO_GELU = 0, 1, 2
+TAIL_NONE, TAIL_QKV = 0, 1
+
+
+class WsPhases(ctypes.Structure):
+    """propd_ws_phases (include/propd.h): in-kernel prologue / tail phases of a weight-streaming GEMM."""
+
+    _fields_ = [("pro_mode", c_int), ("pro_src", P), ("pro_ld", c_int), ("pro_dst", P), ("pro_ldd", c_int),
+                ("pro_cols", c_int), ("tail_mode", c_int), ("tail_q", P), ("tail_ldq", c_int), ("A", c_int),
+                ("dh", c_int), ("Lmax", c_int), ("row_seq", P), ("row_node", P), ("seq_slot", P), ("seq_len", P),
+                ("kcache", P), ("vcache", P), ("bar", P)]
 
 
 class PropdError(RuntimeError):
@@ -73,7 +87,7 @@ def load():
     lib = ctypes.CDLL(LIB_PATH)
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
-        fn.argtypes = argtypes
+        fn.argtypes = [ctypes.POINTER(WsPhases) if a == "phases" else a for a in argtypes]
         fn.restype = _RESTYPES.get(name, c_int)
     if lib.propd_abi_version() != ABI_VERSION:
         raise ImportError(f"libpropd ABI {lib.propd_abi_version()} != expected {ABI_VERSION}; rebuild")

@@ -174,6 +174,12 @@ class B200Backend:
         # fp32 accumulator for QKV / W1 partial sums (kept zero between uses)
         self.use_gws = (dtype == "bf16") and use_gws and cfg.hidden % 128 == 0
         self._acc = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32) if self.use_gws else None
+        # in-kernel prologue/tail phases (LN, GELU, QKV finish) between the
+        # weight-streaming projections: five launches per layer
+        self.ws_phases = self.use_gws and cfg.hidden <= 4096
+        if self.ws_phases:
+            self._acc2 = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32)
+            self._bar = torch.zeros(4, device=dev, dtype=torch.int32)
         self.device_rows = True  # sync-free post-prune pass when it fits the weight-streaming GEMMs
         self._graphs: dict = {}
         self._templates: dict = {}
@@ -264,6 +270,8 @@ class B200Backend:
         """Blocks l0..l1-1 over the rows of `rt` (backends.py:202-237).  Returns
         the last MLP output not yet added to the residual stream x."""
         if self.use_gws and rt.M <= 128:
+            if self.ws_phases:
+                return self._run_layers_phased(x, rt, l0, l1, mask, n_tmpl, W, pending)
             return self._run_layers_ws(x, rt, l0, l1, mask, n_tmpl, W, pending)
         torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
         M = rt.M
@@ -317,6 +325,51 @@ class B200Backend:
             self.attn_timer.append({"ms": e0.elapsed_time(e1), "role": role,
                                     "bytes": kv * 2 * self.H * elt + 2 * rows * self.H * elt})
         self._pending_events.clear()
+
+    def _run_layers_phased(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
+        """Blocks l0..l1-1 as five launches per layer (bf16, <= 128 rows):
+        QKV GEMM [prologue LN(x), tail Q -> qkv, K/V -> cache] -> K2 -> W_o
+        GEMM (adds into x) -> W_1 GEMM [prologue LN(x)] -> W_2 GEMM [prologue
+        GELU(acc), adds into x].  The prologues/tails meet at in-kernel grid
+        barriers while the weight ring keeps streaming (propd_ws_phases)."""
+        torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
+        self._flush(x, pending)
+        M = rt.M
+        ws = self._workspace(M, rt.B)
+        ws_bytes = 0 if ws is None else ws.numel()
+        acc1, acc2, live, bar = self._acc, self._acc2, ptr(rt.live), ptr(self._bar)
+        h = torch.empty(M, H, device=self.device, dtype=T)
+        ctx = torch.empty(M, H, device=self.device, dtype=T)
+        qkv = torch.empty(M, 3 * H, device=self.device, dtype=T)
+        g = torch.empty(M, 4 * H, device=self.device, dtype=T)
+        ln = dict(pro_mode=_lib.PRO_LN, pro_src=ptr(x), pro_ld=H, pro_dst=ptr(h), pro_ldd=H, pro_cols=H, bar=bar)
+        for l in range(l0, l1):
+            kc, vc = self.kcache[l], self.vcache[l]
+            ph = _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A, dh=self.dh,
+                               Lmax=self.Lmax, row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node),
+                               seq_slot=ptr(rt.seq_slot), seq_len=ptr(self.seq_len), kcache=ptr(kc), vcache=ptr(vc),
+                               **ln)
+            self._call("propd_gemm_ws_ph", M, live, 3 * H, H, ptr(h), H, ptr(self.w.wqkv[l]), 3 * H, ptr(acc1), 3 * H,
+                       1, 0, ph, st)
+            if self.attn_timer is not None:
+                ev0 = self._timing_event()
+                ev0.record()
+            self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
+                       self.n_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
+                       ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
+                       ptr(ws), ws_bytes, st)
+            if self.attn_timer is not None:
+                ev1 = self._timing_event()
+                ev1.record()
+                self._events_sink().append((ev0, ev1, self._role, M))
+            self._call("propd_gemm_ws", M, live, H, H, ptr(ctx), H, ptr(self.w.wo[l]), H, ptr(x), H, 1, 0, st)
+            self._call("propd_gemm_ws_ph", M, live, 4 * H, H, ptr(h), H, ptr(self.w.w1[l]), 4 * H, ptr(acc2), 4 * H,
+                       1, 0, _lib.WsPhases(**ln), st)
+            ph = _lib.WsPhases(pro_mode=_lib.PRO_GELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g), pro_ldd=4 * H,
+                               pro_cols=4 * H, bar=bar)
+            self._call("propd_gemm_ws_ph", M, live, H, 4 * H, ptr(g), 4 * H, ptr(self.w.w2[l]), H, ptr(x), H, 1, 0,
+                       ph, st)
+        return None
 
     def _run_layers_ws(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
         """Same blocks with the weight-streaming tcgen05 projections (bf16,

@@ -92,6 +92,85 @@ __device__ __forceinline__ uint32_t tree_bits32(const uint64_t* mrow, int W, int
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
+// ---- split-KV combine inside a thread-block cluster (the key splits of one
+// (sequence, head, row tile) are the cluster's CTAs): every CTA parks its
+// unnormalised O and (m, l) in its now idle K ring; rank q finishes rows
+// [q * ceil(nrows / splits), ...) reading all ranks through DSMEM.
+constexpr int SMEM_PO = SMEM_K;                  // [128 rows][128] fp32 partial O (64 KB)
+constexpr int SMEM_PM = SMEM_K + BM * DH * 4;    // [128] m (log2 domain)
+constexpr int SMEM_PL = SMEM_PM + BM * 4;        // [128] l
+static_assert(SMEM_PL + BM * 4 <= SMEM_V, "partial state must fit in the K ring");
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float cl_ld(uint32_t a) {
+  float v;
+  asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 cl_ld4(uint32_t a) {
+  float4 v;
+  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+constexpr int MAX_SPLIT = 8;
+
+__device__ __forceinline__ void cluster_combine(const uint8_t* smem, int nsplit, int nrows, int r0, int a,
+                                                __nv_bfloat16* out, int ldout) {
+  cl_sync();  // every split's partial state is visible cluster-wide
+  const int rank = (int)cl_rank();
+  const int per = (nrows + nsplit - 1) / nsplit;
+  const int rb = rank * per, re = min(nrows, rb + per);
+  uint32_t po[MAX_SPLIT], pm[MAX_SPLIT], pl[MAX_SPLIT];
+#pragma unroll
+  for (int q = 0; q < MAX_SPLIT; ++q) {
+    const uint32_t rk = q < nsplit ? q : 0;
+    po[q] = cl_map(smem_u32(smem + SMEM_PO), rk);
+    pm[q] = cl_map(smem_u32(smem + SMEM_PM), rk);
+    pl[q] = cl_map(smem_u32(smem + SMEM_PL), rk);
+  }
+  for (int e = threadIdx.x; e < (re - rb) * (DH / 4); e += blockDim.x) {
+    const int r = rb + e / (DH / 4), d4 = (e % (DH / 4)) * 4;
+    float ms[MAX_SPLIT], mx = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < MAX_SPLIT; ++q) {
+      ms[q] = q < nsplit ? cl_ld(pm[q] + r * 4) : -INFINITY;
+      mx = fmaxf(mx, ms[q]);
+    }
+    float l = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (mx != -INFINITY) {
+#pragma unroll
+      for (int q = 0; q < MAX_SPLIT; ++q) {
+        if (q < nsplit && ms[q] != -INFINITY) {
+          const float f = ex2(ms[q] - mx);
+          l += cl_ld(pl[q] + r * 4) * f;
+          const float4 o = cl_ld4(po[q] + (r * DH + d4) * 4);
+          acc.x += o.x * f;
+          acc.y += o.y * f;
+          acc.z += o.z * f;
+          acc.w += o.w * f;
+        }
+      }
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    *reinterpret_cast<uint2*>(out + (size_t)(r0 + r) * ldout + a * DH + d4) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+  cl_sync();  // peers may still be reading this CTA's state
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, Args p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -112,7 +191,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const unsigned long long t_entry = p.tl ? gtimer() : 0ull;
   pdl_wait();
   const unsigned long long t_wait = p.tl ? gtimer() : 0ull;
-  const int s = blockIdx.x / p.mtiles, mt = blockIdx.x % p.mtiles;
+  const int s = blockIdx.x % p.nsplit, mt = blockIdx.x / p.nsplit;  // the splits of a row tile are one cluster
   const int a = blockIdx.y, b = blockIdx.z;
   const int slot = p.seq_slot[b];
   const int L = p.seq_len[slot];
@@ -123,13 +202,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int k_begin = s * p.split_len;
   const int k_end = min(nkeys, k_begin + p.split_len);
   const int nblk = k_end > k_begin ? (k_end - k_begin + BN - 1) / BN : 0;
-  if (nblk == 0) {
+  if (nblk == 0) {  // no keys in this split: contribute an empty state to the cluster combine
     if (p.nsplit > 1) {
-      for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
-        const size_t base = ((size_t)(r0 + r) * p.A + a) * p.nsplit + s;
-        p.part_ml[base * 2] = -INFINITY;
-        p.part_ml[base * 2 + 1] = 0.f;
+      float* pmv = reinterpret_cast<float*>(smem + SMEM_PM);
+      float* plv = reinterpret_cast<float*>(smem + SMEM_PL);
+      for (int r = threadIdx.x; r < BM; r += blockDim.x) {
+        pmv[r] = -INFINITY;
+        plv[r] = 0.f;
       }
+      __syncthreads();
+      cluster_combine(smem, p.nsplit, nrows, r0, a, p.out, p.ldout);
     }
     return;
   }
@@ -382,14 +464,13 @@ __global__ void __launch_bounds__(THREADS, 1)
               }
               *reinterpret_cast<uint4*>(dst + k8 * 8) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
-          } else {
-            const size_t base = ((size_t)row * p.A + a) * p.nsplit + s;
-            float4* po = reinterpret_cast<float4*>(p.part_o + base * DH + col);
+          } else {  // unnormalised partial state of this split -> own shared memory
+            float4* po = reinterpret_cast<float4*>(smem + SMEM_PO + ((size_t)r * DH + col) * 4);
 #pragma unroll
             for (int k4 = 0; k4 < 8; ++k4) po[k4] = make_float4(o[4 * k4], o[4 * k4 + 1], o[4 * k4 + 2], o[4 * k4 + 3]);
             if (g == 0 && c == 0) {
-              p.part_ml[base * 2] = m == -INFINITY ? -INFINITY : m * 0.69314718055994531f;
-              p.part_ml[base * 2 + 1] = l;
+              reinterpret_cast<float*>(smem + SMEM_PM)[r] = m;
+              reinterpret_cast<float*>(smem + SMEM_PL)[r] = l;
             }
           }
         }
@@ -402,6 +483,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1) {
     __syncwarp();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+  if (p.nsplit > 1) {
+    __syncwarp();
+    cluster_combine(smem, p.nsplit, nrows, r0, a, p.out, p.ldout);
   }
   if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait);
 }
@@ -471,10 +556,10 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   const int nblk_max = (max_keys + tc2::BN - 1) / tc2::BN;
   int nsplit = 148 / ctas;  // one wave of one CTA per SM
   if (nsplit > nblk_max) nsplit = nblk_max;
-  if (nsplit > 64) nsplit = 64;
+  if (nsplit > tc2::MAX_SPLIT) nsplit = tc2::MAX_SPLIT;  // the splits of a row tile form one cluster
   if (nsplit < 1) nsplit = 1;
-  const int64_t need = (int64_t)M * A * nsplit * (tc2::DH + 2) * (int64_t)sizeof(float);
-  if (nsplit > 1 && (ws == nullptr || ws_bytes < need)) nsplit = 1;
+  (void)ws;
+  (void)ws_bytes;
   const int blocks_per_split = (nblk_max + nsplit - 1) / nsplit;
   nsplit = (nblk_max + blocks_per_split - 1) / blocks_per_split;
   tc2::Args p{};
@@ -493,8 +578,8 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   p.split_len = blocks_per_split * tc2::BN;
   p.nsplit = nsplit;
   p.mtiles = mtiles;
-  p.part_o = reinterpret_cast<float*>(ws);
-  p.part_ml = p.part_o + (size_t)M * A * nsplit * tc2::DH;
+  p.part_o = nullptr;
+  p.part_ml = nullptr;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
   p.trace = g_trace2;
@@ -506,16 +591,35 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
     attr = true;
   }
   *handled = true;
+  (void)M;
   dim3 grid(nsplit * mtiles, A, B);
-  if (int e = launch_pdl("tree_attention(tc2)", tc2::attn_tc2_kernel, grid, dim3(tc2::THREADS), tc2::SMEM_TOTAL,
-                         st, km, vm, p))
-    return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(tc2::THREADS);
+  cfg.dynamicSmemBytes = tc2::SMEM_TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
   if (nsplit > 1) {
-    if (int e = launch_pdl("tree_attention(tc2 combine)", attn_combine_kernel<__nv_bfloat16>, dim3(M, A), dim3(128),
-                           0, st, A, tc2::DH, nsplit, (const float*)p.part_o, (const float*)p.part_ml, p.out, ldout))
-      return e;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = nsplit;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
   }
-  return 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc2::attn_tc2_kernel, km, vm, p);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail("tree_attention(tc2): %s", cudaGetErrorString(e));
+  }
+  return check_launch("tree_attention(tc2)");
 }
 
 }  // namespace propd

@@ -31,7 +31,127 @@ struct Args {
   int accumulate;
   unsigned long long* trace;  // development timeline (common.cuh)
   unsigned int tag;
+  propd_ws_phases ph;  // in-kernel prologue / tail phases (grid barriers)
 };
+
+// ---- grid barrier (all CTAs of a barrier-using launch are co-resident:
+// grid <= 2 CTAs x SMs; see the host check).  ctr[0] counts arrivals,
+// ctr[1] departures; the last CTA to depart re-arms both for the next launch.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned n) {  // one thread per CTA
+  __threadfence();
+  atomicAdd(ctr, 1u);
+  while (ld_acquire(ctr) < n) __nanosleep(64);
+  if (atomicAdd(ctr + 1, 1u) == n - 1) {
+    ctr[0] = 0u;
+    ctr[1] = 0u;
+  }
+}
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ float gelu_tanh(float v) {
+  return 0.5f * v * (1.f + tanhf(0.7978845608028654f * (v + 0.044715f * v * v * v)));
+}
+__device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  return make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+
+// Prologue, run by the 128 epilogue threads (tid) of every CTA while the
+// weight ring fills: the bf16 X operand of this launch is produced from the
+// previous launch's fp32 output, spread over all CTAs.
+//   LN:   X[t] = LN(src[t]) (no affine, eps 1e-5, population variance); CTA c
+//         normalises rows c, c + nCTA, ... (backends.py:135-142)
+//   GELU: X = bf16(tanh-GELU(src)), src re-zeroed (the split-K accumulator of
+//         the previous launch)
+__device__ __forceinline__ void prologue_phase(const propd_ws_phases& ph, int M, int tid, int cta, int ncta) {
+  __shared__ float red[2][4];
+  __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ph.pro_dst);
+  const int C = ph.pro_cols;
+  if (ph.pro_mode == PROPD_PRO_LN) {
+    const int w = tid >> 5, lane = tid & 31;
+    for (int t = cta; t < M; t += ncta) {
+      const float* xr = ph.pro_src + (size_t)t * ph.pro_ld;
+      float v[32];
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = (i * 128 + tid) * 4;
+        float4 f = c < C ? __ldcg(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[4 * i] = f.x; v[4 * i + 1] = f.y; v[4 * i + 2] = f.z; v[4 * i + 3] = f.w;
+        s += (f.x + f.y) + (f.z + f.w);
+      }
+      s = warp_sum(s);
+      if (lane == 0) red[0][w] = s;
+      epi_sync();
+      const float mu = ((red[0][0] + red[0][1]) + (red[0][2] + red[0][3])) / (float)C;
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = (i * 128 + tid) * 4;
+        if (c < C)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float d = v[4 * i + j] - mu;
+            ss += d * d;
+          }
+      }
+      ss = warp_sum(ss);
+      if (lane == 0) red[1][w] = ss;
+      epi_sync();
+      const float inv = 1.f / sqrtf(((red[1][0] + red[1][1]) + (red[1][2] + red[1][3])) / (float)C + 1e-5f);
+      __nv_bfloat16* o = dst + (size_t)t * ph.pro_ldd;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int c = (i * 128 + tid) * 4;
+        if (c < C)
+          *reinterpret_cast<uint2*>(o + c) = pack_bf16x4((v[4 * i] - mu) * inv, (v[4 * i + 1] - mu) * inv,
+                                                         (v[4 * i + 2] - mu) * inv, (v[4 * i + 3] - mu) * inv);
+      }
+      epi_sync();  // red[] is reused by the next row
+    }
+  } else if (ph.pro_mode == PROPD_PRO_GELU) {
+    const int per_row = C / 4;
+    for (int e = cta * 128 + tid; e < M * per_row; e += ncta * 128) {
+      const int t = e / per_row, c = (e - t * per_row) * 4;
+      float4* a = reinterpret_cast<float4*>(ph.pro_src + (size_t)t * ph.pro_ld + c);
+      const float4 f = __ldcg(a);
+      *a = make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<uint2*>(dst + (size_t)t * ph.pro_ldd + c) =
+          pack_bf16x4(gelu_tanh(f.x), gelu_tanh(f.y), gelu_tanh(f.z), gelu_tanh(f.w));
+    }
+  }
+}
+
+// Tail (QKV): after every CTA's split-K reduction into Y, the fp32 Q/K/V rows
+// become bf16 Q rows (tail_q) and K/V rows of the layer cache, Y re-zeroed
+// (same contract as propd_qkv_finish), spread over all CTAs.
+__device__ __forceinline__ void tail_phase(const Args& p, int M, int tid, int cta, int ncta) {
+  const propd_ws_phases& ph = p.ph;
+  const int H = ph.A * ph.dh, per_row = 3 * H / 4;
+  __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(ph.tail_q);
+  for (int e = cta * 128 + tid; e < M * per_row; e += ncta * 128) {
+    const int t = e / per_row, c = (e - t * per_row) * 4;
+    float4* a = reinterpret_cast<float4*>(p.Y + (size_t)t * p.ldy + c);
+    const float4 f = __ldcg(a);
+    *a = make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint2 pk = pack_bf16x4(f.x, f.y, f.z, f.w);
+    if (c < H) {
+      *reinterpret_cast<uint2*>(q + (size_t)t * ph.tail_ldq + c) = pk;
+    } else {
+      const int kv = c >= 2 * H;
+      const int ee = c - (kv ? 2 * H : H);
+      const int ah = ee / ph.dh, d = ee - ah * ph.dh;
+      const int slot = ph.seq_slot[ph.row_seq[t]];
+      const int pos = ph.seq_len[slot] + ph.row_node[t];
+      __nv_bfloat16* cache = reinterpret_cast<__nv_bfloat16*>(kv ? ph.vcache : ph.kcache);
+      *reinterpret_cast<uint2*>(cache + (((size_t)slot * ph.A + ah) * ph.Lmax + pos) * ph.dh + d) = pk;
+    }
+  }
+}
 
 // Ring depth per X-tile size: as deep as two CTAs per SM allow (deeper rings
 // keep more weight bytes in flight and prefetch more of them while the
@@ -54,6 +174,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const unsigned long long t_entry = p.trace ? gtimer() : 0ull;
   __shared__ unsigned long long s_t[2];
+  __shared__ int s_pro_done;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BF;
   const int kb0 = blockIdx.y * p.kblk_per_split;
@@ -66,6 +187,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
     mbar_init(acc_full, 1);
     fence_barrier_init();
+    s_pro_done = 0;
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -96,8 +218,16 @@ __global__ void __launch_bounds__(THREADS, 2)
   // loaded and multiplied in 16-row boxes, only as many as are live
   const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
   const int nbox = max(1, (M + 15) >> 4);
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x, ncta = gridDim.x * gridDim.y;
   if (warp == 0) {
     if (lane == 0) {
+      if (p.ph.pro_mode != PROPD_PRO_NONE) {
+        // X is produced in this launch's prologue by every CTA: wait for the
+        // grid barrier (the weight stages above keep streaming meanwhile),
+        // then order those generic writes before the TMA reads of X
+        while (*reinterpret_cast<volatile int*>(&s_pro_done) == 0) __nanosleep(32);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       const int pre = min(nkb, STAGES);
       for (int j = 0; j < pre; ++j) {
         mbar_expect_tx(&full[j], nbox * 2048);
@@ -137,6 +267,15 @@ __global__ void __launch_bounds__(THREADS, 2)
       mma_commit(acc_full);
     }
   } else {
+    const int tid = threadIdx.x - 64;
+    if (p.ph.pro_mode != PROPD_PRO_NONE) {
+      prologue_phase(p.ph, M, tid, cta, ncta);
+      epi_sync();
+      if (tid == 0) {
+        grid_barrier(p.ph.bar, (unsigned)ncta);
+        *reinterpret_cast<volatile int*>(&s_pro_done) = 1;
+      }
+    }
     // epilogue: lane = output feature, columns = tokens
     const int q4 = warp & 3;
     const int f = n0 + q4 * 32 + lane;
@@ -162,6 +301,12 @@ __global__ void __launch_bounds__(THREADS, 2)
             *dst = v;
         }
       }
+    }
+    if (p.ph.tail_mode != PROPD_TAIL_NONE) {  // every CTA's reduction lands, then the tile rows are finished
+      epi_sync();
+      if (tid == 0) grid_barrier(p.ph.bar + 2, (unsigned)ncta);
+      epi_sync();
+      tail_phase(p, M, tid, cta, ncta);
     }
   }
   tc_before_sync();
@@ -300,6 +445,11 @@ extern "C" {
 
 int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
                   float* Y, int ldy, int accumulate, int max_split, void* stream) {
+  return propd_gemm_ws_ph(M, rows_dev, N, K, X, ldx, W, ldw, Y, ldy, accumulate, max_split, nullptr, stream);
+}
+
+int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
+                     float* Y, int ldy, int accumulate, int max_split, const propd_ws_phases* ph, void* stream) {
   PROPD_REQUIRE(M >= 1 && M <= 128, "gemm_ws: M=%d outside 1..128", M);
   PROPD_REQUIRE(N % gws::BF == 0 && K % gws::BK == 0, "gemm_ws: N=%d must be a multiple of 128, K=%d of 64", N, K);
   const int mp = ((M + 15) / 16) * 16;
@@ -317,7 +467,23 @@ int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, i
   }
   const int per = (kb + split - 1) / split;
   split = (kb + per - 1) / per;
-  gws::Args p{M, N, K, per, ldy, mp, rows_dev, Y, accumulate, g_dbg_trace, g_dbg_tag++};
+  gws::Args p{M, N, K, per, ldy, mp, rows_dev, Y, accumulate, g_dbg_trace, g_dbg_tag++, {}};
+  if (ph != nullptr && (ph->pro_mode != PROPD_PRO_NONE || ph->tail_mode != PROPD_TAIL_NONE)) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    PROPD_REQUIRE(tiles * split <= 2 * sms, "gemm_ws: %d CTAs cannot all be co-resident for the grid barrier",
+                  tiles * split);
+    PROPD_REQUIRE(ph->bar != nullptr, "gemm_ws: phases need the barrier counters");
+    PROPD_REQUIRE(ph->pro_mode == PROPD_PRO_NONE ||
+                      (ph->pro_src && ph->pro_dst == X && ph->pro_ldd == ldx && ph->pro_cols == K && K <= 4096 * 4),
+                  "gemm_ws: the prologue must produce this launch's X operand");
+    PROPD_REQUIRE(ph->pro_mode != PROPD_PRO_LN || K <= 4096, "gemm_ws: LN prologue supports rows <= 4096");
+    PROPD_REQUIRE(ph->tail_mode == PROPD_TAIL_NONE ||
+                      (accumulate && N == 3 * ph->A * ph->dh && (ph->dh % 4) == 0 && ph->tail_q && ph->kcache &&
+                       ph->vcache && ph->row_seq && ph->row_node && ph->seq_slot && ph->seq_len),
+                  "gemm_ws: QKV tail needs N = 3H, an accumulating launch and the cache tables");
+    p.ph = *ph;
+  }
   dim3 grid(tiles, split);
   cudaStream_t st = as_stream(stream);
   switch (mp) {

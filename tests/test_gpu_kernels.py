@@ -458,3 +458,43 @@ def test_qkv_and_gelu_finish():
     ref = torch.nn.functional.gelu(g0, approximate="tanh")
     assert (out.float() - ref).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
     assert g_acc.abs().max().item() == 0.0
+
+
+# --------------------------------------------------------------- in-kernel GEMM phases
+@pytest.mark.parametrize("rows,live", [(1, None), (16, None), (40, 23), (128, None)])
+def test_phased_layers_match_separate_kernels(rows, live):
+    """Layer stack with the LN / GELU prologues and the QKV tail inside the weight-streaming GEMMs
+    (propd_gemm_ws_ph, grid barriers) == the same stack with separate add_ln / finish kernels: residual
+    stream and the K/V rows written to the cache within bf16 rounding (the paths differ only in where the
+    bf16 conversions happen)."""
+    from paper_2402_13485_b200 import B200Backend, TinyTransformerConfig
+    from paper_2402_13485_b200.backend import Rows
+
+    cfg = TinyTransformerConfig(layers=3, hidden=1024, heads=8, vocab=1024, draft_heads=2, max_positions=600, seed=1)
+    be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=3, max_tree=rows)
+    states = be.synthetic_states(2, 300, seed=3)
+    n = rows
+    tmpl_mask = None
+    half = (n + 1) // 2
+    rt = Rows(n, 2, i32([states[0].slot, states[1].slot]), i32([0] * half + [1] * (n - half)),
+              i32(list(range(half)) + list(range(n - half))), i32([0, half, n]), max_keys=300 + n, max_rows=half,
+              live=i32([live]) if live is not None else None)
+    torch.manual_seed(rows)
+    x0 = torch.randn(n, 1024, device=DEV)
+    outs = []
+    for phased in (False, True):
+        be.ws_phases = phased
+        be.kcache.zero_()
+        be.vcache.zero_()
+        x = x0.clone()
+        be._run_layers(x, rt, 0, 3, tmpl_mask, n, 0)
+        torch.cuda.synchronize()
+        outs.append((x.clone(), be.kcache[:, :2, :, 300:300 + half].float().clone(),
+                     be.vcache[:, :2, :, 300:300 + half].float().clone()))
+    r = n if live is None else live
+    (xa, ka, va), (xb, kb, vb) = outs
+    scale = max(1.0, xa[:r].abs().max().item())
+    assert (xa[:r] - xb[:r]).abs().max().item() <= 3e-2 * scale
+    assert (ka - kb).abs().max().item() <= 3e-2 * max(1.0, ka.abs().max().item())
+    assert (va - vb).abs().max().item() <= 3e-2 * max(1.0, va.abs().max().item())
+    assert be._bar.abs().max().item() == 0 and be._acc.abs().max().item() == 0 and be._acc2.abs().max().item() == 0
