@@ -122,6 +122,56 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def roofline_line(dom: str, name: str, d: dict, ts: dict, traffic: dict, K: int, ms: float) -> dict:
+    """Roofline of the dominant kernel family.  achieved = its algorithmic
+    bytes per step / its busy device time per step inside the PDL-chained
+    step (per-CTA globaltimer records, one traced step).  CUDA events around
+    each launch (the event-bracketed region) serialise the chained launches
+    and add each launch's ramp, so they are reported beside it."""
+    ev = {"events_achieved": d["achieved_gbs"], "events_frac": d["achieved_gbs"] / d["peak"],
+          "events_avg_launch_us": d["avg_launch_us"]}
+    busy = ts.get(dom, {}).get("busy_ms")
+    if busy:
+        ach = (d["bytes"] / K) / (busy * 1e-3) / 1e9
+        base = {"achieved": ach, "frac": ach / d["peak"], "avg_launch_us": busy * 1e3 / max(1, ts[dom]["launches"]),
+                "share_of_step": busy / (ms / K),
+                "timer": "device globaltimer per CTA: union of [dependency release, last CTA exit] per launch"}
+    else:
+        base = {"achieved": d["achieved_gbs"], "frac": d["achieved_gbs"] / d["peak"],
+                "avg_launch_us": d["avg_launch_us"], "share_of_step": d["ms_total"] / ms, "timer": "CUDA events"}
+    return {"kernel": name, "bound": "hbm", "achieved": base["achieved"], "peak": d["peak"], "unit": "GB/s",
+            "frac": base["frac"], "traffic": traffic.get("bytes_per_launch"), "traffic_note": traffic.get("note"),
+            "peak_kind": d["peak_kind"], "launches_per_step": d["launches"] / K,
+            "avg_launch_us": base["avg_launch_us"], "share_of_step": base["share_of_step"], "timer": base["timer"],
+            **ev}
+
+
+def in_step_view(ts: dict, kern: dict, K: int) -> dict:
+    """Kernel families inside the PDL-chained step (globaltimer records):
+    busy ms per step and the algorithmic bytes of one step over that time."""
+    out = {"step_ms": ts.get("step_ms"), "note": "one traced step; busy = union of [release, last exit] per launch"}
+    for k in ("gemm", "attn"):
+        if k in ts and ts[k]["busy_ms"] > 0:
+            bytes_step = kern[k]["bytes"] / K
+            gbs = bytes_step / (ts[k]["busy_ms"] * 1e-3) / 1e9
+            out[k] = {"busy_ms": ts[k]["busy_ms"], "launches": ts[k]["launches"], "achieved": gbs,
+                      "frac": gbs / kern[k]["peak"]}
+    return out
+
+
+def ncu_traffic(kind: str, args) -> dict:
+    """DRAM bytes of one launch of the dominant kernel from a committed
+    `ncu --set full` capture of this bench configuration (profiles/), if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            table = json.load(fh)
+    except Exception:
+        return {}
+    key = f"{kind}:b{args.batch}:kv{args.kv}:{args.mode}"
+    return table.get(key, {})
+
+
 # ---------------------------------------------------------------- CPU reference arm
 def cpu_reference(args, steps: int, warmup: int):
     """The reference algorithm on host cores: oracle/treedecode_port (the
@@ -237,21 +287,25 @@ def run_b200(args, rank: int, world: int, group):
     torch.cuda.synchronize()
     attn = be.attn_timer
     be.attn_timer = None
+    in_step = timeline_region(be, eng, seqs, prime, dev)
     if group is not None:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=group)
         ms = float(t.item())
     tokens = sum(m.tokens_committed for m in metrics)  # engine metrics are already global
-    attn_ms = sum(r["ms"] for r in attn)
-    attn_bytes = sum(r["bytes"] for r in attn)
-    verify_attn_ms = sum(r["ms"] for r in attn if r["role"].startswith("tree"))
     hbm, peak_kind = peaks()
-    achieved = attn_bytes / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else 0.0
+    kernels = {}
+    for kind in ("gemm", "attn"):
+        rs = [r for r in attn if r.get("kind", "attn") == kind]
+        k_ms, k_bytes = sum(r["ms"] for r in rs), sum(r["bytes"] for r in rs)
+        kernels[kind] = {"launches": len(rs), "ms_total": k_ms, "bytes": k_bytes,
+                         "achieved_gbs": k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0,
+                         "avg_launch_us": k_ms / max(1, len(rs)) * 1e3, "peak": hbm, "peak_kind": peak_kind}
+    kernels["attn"]["verify_ms_total"] = sum(r["ms"] for r in attn
+                                             if r.get("kind", "attn") == "attn" and r["role"].startswith("tree"))
     out = {
         "ms": ms, "tokens": tokens, "metrics": metrics, "launches": launches, "clock": clk.summary(),
-        "attn": {"launches": len(attn), "ms_total": attn_ms, "bytes": attn_bytes, "achieved_gbs": achieved,
-                 "avg_launch_us": attn_ms / max(1, len(attn)) * 1e3, "verify_ms_total": verify_attn_ms,
-                 "peak": hbm, "peak_kind": peak_kind},
+        "kernels": kernels, "in_step": in_step,
         "weights_bytes": be.w.nbytes(), "priming_steps": primed, "captures_in_timed": captures_in_timed,
     }
     for st in states:  # free the synthetic sequences' cache slots for the e2e run
@@ -260,6 +314,60 @@ def run_b200(args, rank: int, world: int, group):
     if not args.no_e2e:
         e2e = run_e2e(args, be, eng, rank, world, group)
     out["e2e"] = e2e
+    return out
+
+
+def timeline_region(be, eng, seqs, prime, dev):
+    """One more step with per-CTA globaltimer records (graphs captured with
+    the trace on): busy time of each kernel family inside the PDL-chained
+    step = union over its launches of [first dependency release, last CTA
+    exit].  Unlike the event-bracketed region this keeps the programmatic
+    overlap between launches, so it is the in-step view of the same kernels."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    cap = 1 << 20
+    buf = torch.zeros(8 + 8 * cap, device=dev, dtype=torch.int64)
+    buf[1] = cap
+    lib = be.lib
+    lib.propd_debug_timeline(ctypes.c_void_p(buf.data_ptr()))
+    be.timeline = buf
+    try:
+        prime()
+        torch.cuda.synchronize()
+        buf[0] = 0
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        eng._step(seqs, 10 ** 9)
+        t1.record()
+        torch.cuda.synchronize()
+    finally:
+        lib.propd_debug_timeline(ctypes.c_void_p(0))
+        be.timeline = None
+    n = min(int(buf[0].item()), cap)
+    rec = buf[8: 8 + 8 * n].view(n, 8).cpu().numpy()
+    out = {"step_ms": t0.elapsed_time(t1), "records": n}
+    for kind, name in ((1, "gemm"), (2, "attn")):
+        r = rec[rec[:, 7] == kind]
+        if len(r) == 0:
+            continue
+        spans = []
+        for tag in np.unique(r[:, 0]):
+            g = r[r[:, 0] == tag]
+            spans.append((int(g[:, 4].min()), int(g[:, 6].max())))
+        spans.sort()
+        busy, cur0, cur1 = 0, None, None
+        for a, b in spans:
+            if cur1 is None or a > cur1:
+                if cur1 is not None:
+                    busy += cur1 - cur0
+                cur0, cur1 = a, b
+            else:
+                cur1 = max(cur1, b)
+        busy += cur1 - cur0
+        out[name] = {"launches": len(spans), "busy_ms": busy / 1e6}
     return out
 
 
@@ -339,7 +447,13 @@ def main():
     m = res["metrics"]
     ms = res["ms"]
     K = args.steps
-    a = res["attn"]
+    kern = res["kernels"]
+    a = kern["attn"]
+    dom = max(kern, key=lambda k: kern[k]["ms_total"])  # the kernel family with the largest share of the step
+    d = kern[dom]
+    names = {"gemm": "weight-streaming tcgen05 projections (propd_gemm_ws) + cuBLAS above 128 rows",
+             "attn": "K2 tree-masked verification attention (tc2 tcgen05 / streaming decode kernel)"}
+    traffic = ncu_traffic(dom, args)
     line = {
         "metric": METRIC,
         "value": res["tokens"] / (ms * 1e-3),
@@ -364,11 +478,12 @@ def main():
         "prune_rate_mean": sum(x.prune_rate for x in m) / K,
         "verify_attention_ms_per_step": a["verify_ms_total"] / K,
         "attention_ms_per_step": a["ms_total"] / K,
-        "roofline": {"kernel": "K2 tree_attention (every launch of a second K-step timed region, CUDA events)",
-                     "bound": "hbm",
-                     "achieved": a["achieved_gbs"], "peak": a["peak"], "unit": "GB/s",
-                     "frac": a["achieved_gbs"] / a["peak"], "traffic": None, "peak_kind": a["peak_kind"],
-                     "launches": a["launches"], "avg_launch_us": a["avg_launch_us"]},
+        "projection_ms_per_step": kern["gemm"]["ms_total"] / K,
+        "roofline": roofline_line(dom, names[dom], d, res["in_step"], traffic, K, ms),
+        "roofline_by_kernel": {k: {"achieved": v["achieved_gbs"], "frac": v["achieved_gbs"] / v["peak"],
+                                   "ms_per_step": v["ms_total"] / K, "launches_per_step": v["launches"] / K,
+                                   "avg_launch_us": v["avg_launch_us"]} for k, v in kern.items()},
+        "in_step": in_step_view(res["in_step"], kern, K),
         "step_weight_gbs": res["weights_bytes"] * 2 / (ms / K * 1e-3) / 1e9,
         "gpu_launches": res["launches"],
         "cuda_graphs": {"priming_steps": res["priming_steps"], "captures_in_timed_region": res["captures_in_timed"]},

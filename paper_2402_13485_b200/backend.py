@@ -194,7 +194,8 @@ class B200Backend:
         self._one_mask = torch.ones(1, device=dev, dtype=torch.int64)  # single-node template {0}
         self._keepalive: list = []
         self.launches = 0  # libpropd kernel launches issued (bench accounting)
-        self.attn_timer = None  # list -> per-launch {ms, bytes, role} of every K2 launch (bench)
+        self.attn_timer = None  # list -> per-launch {ms, bytes, role, kind} of K2 / GEMM launches (bench)
+        self.timeline = None  # device trace buffer while kernels record per-CTA timelines (bench)
         self._capturing = False
         self._capture_events: list = []
         self._pending_events: list = []
@@ -276,34 +277,36 @@ class B200Backend:
         torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
         M = rt.M
         ws = self._workspace(M, rt.B)
-        ws_bytes = 0 if ws is None else ws.numel()
         h = torch.empty(M, H, device=self.device, dtype=T)
         ctx = torch.empty(M, H, device=self.device, dtype=T)
         for l in range(l0, l1):
             self._call("propd_add_ln", self.code, M, None, H, ptr(x), ptr(pending), ptr(h), None, None, st)
-            qkv = torch.mm(h, self.w.wqkv[l])
+            qkv = self._timed("gemm", lambda: torch.mm(h, self.w.wqkv[l]), M, H, 3 * H)
             kc, vc = self.kcache[l], self.vcache[l]
             self._call("propd_kv_append", self.code, M, self.A, self.dh, self.Lmax, ptr(qkv), 3 * H,
                        ptr(rt.row_seq), ptr(rt.row_node), ptr(rt.seq_slot), ptr(self.seq_len), ptr(kc), ptr(vc), st)
-            if self.attn_timer is not None:
-                ev0 = self._timing_event()
-                ev0.record()
-            self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
-                       self.n_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
-                       ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
-                       ptr(ws), ws_bytes, st)
-            if self.attn_timer is not None:
-                ev1 = self._timing_event()
-                ev1.record()
-                self._events_sink().append((ev0, ev1, self._role, M))
-            o = torch.mm(ctx, self.w.wo[l])
+            self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
+            o = self._timed("gemm", lambda: torch.mm(ctx, self.w.wo[l]), M, H, H)
             self._call("propd_add_ln", self.code, M, None, H, ptr(x), ptr(o), ptr(h), None, None, st)
-            g = torch.mm(h, self.w.w1[l])
+            g = self._timed("gemm", lambda: torch.mm(h, self.w.w1[l]), M, H, 4 * H)
             self._call("propd_gelu", self.code, g.numel(), ptr(g), st)
-            pending = torch.mm(g, self.w.w2[l])
+            pending = self._timed("gemm", lambda: torch.mm(g, self.w.w2[l]), M, 4 * H, H)
         return pending
 
-    # ------------------------------------------------- K2 timing (bench)
+    # ------------------------------------------------- per-launch timing (bench)
+    def _timed(self, kind: str, launch, M: int = 0, K: int = 0, N: int = 0, acc: bool = False):
+        """Run `launch` bracketed by CUDA events when the bench's kernel timer
+        is on (kind "attn": K2; "gemm": a projection [M,K] x [K,N])."""
+        if self.attn_timer is None:
+            return launch()
+        ev0 = self._timing_event()
+        ev0.record()
+        out = launch()
+        ev1 = self._timing_event()
+        ev1.record()
+        self._events_sink().append((ev0, ev1, self._role, M, kind, K, N, acc))
+        return out
+
     def _timing_event(self):
         torch = self.torch
         if self._capturing:  # event-record nodes inside the graph
@@ -314,17 +317,43 @@ class B200Backend:
         return self._capture_events if self._capturing else self._pending_events
 
     def _harvest(self, keys: dict) -> None:
-        """After a step's synchronisation: per-launch K2 time + algorithmic bytes
-        (K/V rows streamed + Q read + O written, bf16/fp32 elements)."""
+        """After a step's synchronisation: per-launch time + algorithmic bytes.
+        K2: K/V rows streamed + Q read + O written.  GEMM: weights + X read +
+        fp32 Y written (read too when accumulating), for the live rows."""
         if self.attn_timer is None:
             self._pending_events.clear()
             return
         elt = 2 if self.tdtype != self.torch.float32 else 4
-        for e0, e1, role, M in self._pending_events:
+        for e0, e1, role, M, kind, K, N, acc in self._pending_events:
             kv, rows = keys.get(role, (0, M))
-            self.attn_timer.append({"ms": e0.elapsed_time(e1), "role": role,
-                                    "bytes": kv * 2 * self.H * elt + 2 * rows * self.H * elt})
+            if kind == "attn":
+                nbytes = kv * 2 * self.H * elt + 2 * rows * self.H * elt
+            else:
+                rows = min(rows, M) if M else rows
+                nbytes = K * N * elt + rows * K * elt + rows * N * 4 * (2 if acc else 1)
+            self.attn_timer.append({"ms": e0.elapsed_time(e1), "role": role, "kind": kind, "bytes": nbytes})
         self._pending_events.clear()
+
+    def _gemm_ws(self, M, live, N, K, X, W, Y, ldy, acc: int, phases=None) -> None:
+        """One weight-streaming projection Y (+)= X[M,K] W[K,N] (X, W row-major,
+        contiguous), optionally with in-kernel prologue/tail phases."""
+        st = self.stream()
+        if phases is None:
+            launch = lambda: self._call("propd_gemm_ws", M, live, N, K, ptr(X), K, ptr(W), N, ptr(Y), ldy, acc, 0, st)
+        else:
+            launch = lambda: self._call("propd_gemm_ws_ph", M, live, N, K, ptr(X), K, ptr(W), N, ptr(Y), ldy, acc, 0,
+                                        phases, st)
+        self._timed("gemm", launch, M, K, N, bool(acc))
+
+    def _attention(self, rt: Rows, qkv, l: int, mask, n_tmpl: int, W: int, ctx, ws) -> None:
+        """K2 over the rows of `rt` for layer l (Q = columns [0, H) of qkv)."""
+        H, M = self.H, rt.M
+        ws_bytes = 0 if ws is None else ws.numel()
+        self._timed("attn", lambda: self._call(
+            "propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax, self.n_slots,
+            rt.max_rows, rt.max_keys, ptr(qkv), qkv.shape[1], ptr(self.kcache[l]), ptr(self.vcache[l]),
+            ptr(rt.seq_slot), ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx),
+            H, ptr(ws), ws_bytes, self.stream()), M)
 
     def _run_layers_phased(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
         """Blocks l0..l1-1 as five launches per layer (bf16, <= 128 rows):
@@ -332,56 +361,40 @@ class B200Backend:
         GEMM (adds into x) -> W_1 GEMM [prologue LN(x)] -> W_2 GEMM [prologue
         GELU(acc), adds into x].  The prologues/tails meet at in-kernel grid
         barriers while the weight ring keeps streaming (propd_ws_phases)."""
-        torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
+        torch, T, H = self.torch, self.tdtype, self.H
         self._flush(x, pending)
         M = rt.M
         ws = self._workspace(M, rt.B)
-        ws_bytes = 0 if ws is None else ws.numel()
         acc1, acc2, live, bar = self._acc, self._acc2, ptr(rt.live), ptr(self._bar)
         h = torch.empty(M, H, device=self.device, dtype=T)
         ctx = torch.empty(M, H, device=self.device, dtype=T)
         qkv = torch.empty(M, 3 * H, device=self.device, dtype=T)
         g = torch.empty(M, 4 * H, device=self.device, dtype=T)
         ln = dict(pro_mode=_lib.PRO_LN, pro_src=ptr(x), pro_ld=H, pro_dst=ptr(h), pro_ldd=H, pro_cols=H, bar=bar)
+        gelu = _lib.WsPhases(pro_mode=_lib.PRO_GELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g), pro_ldd=4 * H,
+                             pro_cols=4 * H, bar=bar)
         for l in range(l0, l1):
-            kc, vc = self.kcache[l], self.vcache[l]
-            ph = _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A, dh=self.dh,
-                               Lmax=self.Lmax, row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node),
-                               seq_slot=ptr(rt.seq_slot), seq_len=ptr(self.seq_len), kcache=ptr(kc), vcache=ptr(vc),
-                               **ln)
-            self._call("propd_gemm_ws_ph", M, live, 3 * H, H, ptr(h), H, ptr(self.w.wqkv[l]), 3 * H, ptr(acc1), 3 * H,
-                       1, 0, ph, st)
-            if self.attn_timer is not None:
-                ev0 = self._timing_event()
-                ev0.record()
-            self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
-                       self.n_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
-                       ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
-                       ptr(ws), ws_bytes, st)
-            if self.attn_timer is not None:
-                ev1 = self._timing_event()
-                ev1.record()
-                self._events_sink().append((ev0, ev1, self._role, M))
-            self._call("propd_gemm_ws", M, live, H, H, ptr(ctx), H, ptr(self.w.wo[l]), H, ptr(x), H, 1, 0, st)
-            self._call("propd_gemm_ws_ph", M, live, 4 * H, H, ptr(h), H, ptr(self.w.w1[l]), 4 * H, ptr(acc2), 4 * H,
-                       1, 0, _lib.WsPhases(**ln), st)
-            ph = _lib.WsPhases(pro_mode=_lib.PRO_GELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g), pro_ldd=4 * H,
-                               pro_cols=4 * H, bar=bar)
-            self._call("propd_gemm_ws_ph", M, live, H, 4 * H, ptr(g), 4 * H, ptr(self.w.w2[l]), H, ptr(x), H, 1, 0,
-                       ph, st)
+            qkv_phases = _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A, dh=self.dh,
+                                       Lmax=self.Lmax, row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node),
+                                       seq_slot=ptr(rt.seq_slot), seq_len=ptr(self.seq_len),
+                                       kcache=ptr(self.kcache[l]), vcache=ptr(self.vcache[l]), **ln)
+            self._gemm_ws(M, live, 3 * H, H, h, self.w.wqkv[l], acc1, 3 * H, 1, qkv_phases)
+            self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
+            self._gemm_ws(M, live, H, H, ctx, self.w.wo[l], x, H, 1)
+            self._gemm_ws(M, live, 4 * H, H, h, self.w.w1[l], acc2, 4 * H, 1, _lib.WsPhases(**ln))
+            self._gemm_ws(M, live, H, 4 * H, g, self.w.w2[l], x, H, 1, gelu)
         return None
 
     def _run_layers_ws(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
-        """Same blocks with the weight-streaming tcgen05 projections (bf16,
-        <= 128 rows): QKV / W1 accumulate into an fp32 scratch that the finish
-        kernels turn into bf16 operands (K/V go straight into the cache, GELU is
-        applied on the way); W_o and W_2 accumulate into the residual stream x."""
+        """Same blocks with separate LN / finish kernels between the
+        weight-streaming projections (H > 4096, or ws_phases off): QKV / W1
+        accumulate into an fp32 scratch that the finish kernels turn into bf16
+        operands (K/V straight into the cache, GELU on the way); W_o and W_2
+        accumulate into the residual stream x."""
         torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
         M = rt.M
         ws = self._workspace(M, rt.B)
-        ws_bytes = 0 if ws is None else ws.numel()
-        acc = self._acc
-        live = ptr(rt.live)
+        acc, live = self._acc, ptr(rt.live)
         h = torch.empty(M, H, device=self.device, dtype=T)
         ctx = torch.empty(M, H, device=self.device, dtype=T)
         qkv = torch.empty(M, 3 * H, device=self.device, dtype=T)
@@ -390,25 +403,15 @@ class B200Backend:
             self._call("propd_add_ln", self.code, M, live, H, ptr(x), ptr(pending), ptr(h), None, None, st)
             pending = None
             kc, vc = self.kcache[l], self.vcache[l]
-            self._call("propd_gemm_ws", M, live, 3 * H, H, ptr(h), H, ptr(self.w.wqkv[l]), 3 * H, ptr(acc), 3 * H, 1, 0, st)
+            self._gemm_ws(M, live, 3 * H, H, h, self.w.wqkv[l], acc, 3 * H, 1)
             self._call("propd_qkv_finish", M, live, self.A, self.dh, self.Lmax, ptr(acc), 3 * H, ptr(qkv), 3 * H,
                        ptr(rt.row_seq), ptr(rt.row_node), ptr(rt.seq_slot), ptr(self.seq_len), ptr(kc), ptr(vc), st)
-            if self.attn_timer is not None:
-                ev0 = self._timing_event()
-                ev0.record()
-            self._call("propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax,
-                       self.n_slots, rt.max_rows, rt.max_keys, ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(rt.seq_slot),
-                       ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx), H,
-                       ptr(ws), ws_bytes, st)
-            if self.attn_timer is not None:
-                ev1 = self._timing_event()
-                ev1.record()
-                self._events_sink().append((ev0, ev1, self._role, M))
-            self._call("propd_gemm_ws", M, live, H, H, ptr(ctx), H, ptr(self.w.wo[l]), H, ptr(x), H, 1, 0, st)
+            self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
+            self._gemm_ws(M, live, H, H, ctx, self.w.wo[l], x, H, 1)
             self._call("propd_add_ln", self.code, M, live, H, ptr(x), None, ptr(h), None, None, st)
-            self._call("propd_gemm_ws", M, live, 4 * H, H, ptr(h), H, ptr(self.w.w1[l]), 4 * H, ptr(acc), 4 * H, 1, 0, st)
+            self._gemm_ws(M, live, 4 * H, H, h, self.w.w1[l], acc, 4 * H, 1)
             self._call("propd_gelu_finish", M, live, 4 * H, ptr(acc), 4 * H, ptr(g), 4 * H, st)
-            self._call("propd_gemm_ws", M, live, H, 4 * H, ptr(g), 4 * H, ptr(self.w.w2[l]), H, ptr(x), H, 1, 0, st)
+            self._gemm_ws(M, live, H, 4 * H, g, self.w.w2[l], x, H, 1)
         return None
 
     def _proj_f32(self, X, Wt, N, live=None):
@@ -416,12 +419,11 @@ class B200Backend:
         (rows >= *live, when given, are left unwritten)."""
         torch = self.torch
         M = X.shape[0]
-        live = ptr(live)
         if self.use_gws and M <= 128 and N % 128 == 0 and X.dtype == torch.bfloat16:
             out = torch.empty(M, N, device=self.device, dtype=torch.float32)
-            self._call("propd_gemm_ws", M, live, N, self.H, ptr(X), self.H, ptr(Wt), N, ptr(out), N, 0, 0, self.stream())
+            self._gemm_ws(M, ptr(live), N, self.H, X, Wt, out, N, 0)
             return out
-        out = torch.mm(X, Wt)
+        out = self._timed("gemm", lambda: torch.mm(X, Wt), M, self.H, N)
         return out if out.dtype == torch.float32 else out.float()
 
     def _flush(self, x, pending):
@@ -688,7 +690,7 @@ class B200Backend:
             return fn()
         # graphs with K2 timing event nodes are kept apart from clean ones
         # (an event node between two kernels also breaks their PDL overlap)
-        key = key + (self.attn_timer is not None,)
+        key = key + (self.attn_timer is not None, self.timeline is not None)
         ent = self._graphs.get(key)
         if ent is None:
             torch = self.torch

@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
     }
     cluster_sync_all();  // peers may still read this CTA's state
   }
-  if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait);
+  if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait, 2);
 }
 
 template <int ROWS>

@@ -488,7 +488,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncwarp();
     cluster_combine(smem, p.nsplit, nrows, r0, a, p.out, p.ldout);
   }
-  if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait);
+  if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait, 2);
 }
 
 // ------------------------------------------------------------------ host --

@@ -63,8 +63,9 @@ inline int launch_pdl(const char* what, void (*kern)(Exp...), dim3 grid, dim3 bl
 // ---- development trace (scripts/kernel_timeline.py) ----
 // When a trace buffer is installed (propd_debug_timeline), instrumented kernels
 // append one record per CTA: [tag, cta, smid, t_entry, t_after_pdl_wait,
-// t_main_done, t_exit] (globaltimer ns); buf[0] is the record counter, records
-// start at buf[8].  tag = host launch sequence number.  Off (NULL) normally.
+// t_main_done, t_exit] (globaltimer ns); buf[0] is the record counter, buf[1]
+// the capacity in records, records
+// start at buf[8].  tag = host launch sequence number, slot 7 = kernel kind.  Off (NULL) normally.
 extern unsigned long long* g_dbg_trace;
 extern unsigned int g_dbg_tag;
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -77,11 +78,13 @@ __device__ __forceinline__ unsigned int smid() {
   asm volatile("mov.u32 %0, %smid;" : "=r"(s));
   return s;
 }
+// kind: 1 = weight-streaming GEMM, 2 = attention (record slot 7)
 __device__ __forceinline__ void trace_record(unsigned long long* buf, unsigned int tag, unsigned long long t0,
-                                             unsigned long long t1, unsigned long long t2) {
+                                             unsigned long long t1, unsigned long long t2, unsigned int kind = 0) {
   if (buf == nullptr) return;
   const unsigned long long t3 = gtimer();
   const unsigned long long i = atomicAdd(buf, 1ull);
+  if (i >= buf[1]) return;  // capacity (records) in buf[1]
   unsigned long long* r = buf + 8 + i * 8;
   r[0] = tag;
   r[1] = blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
@@ -90,6 +93,7 @@ __device__ __forceinline__ void trace_record(unsigned long long* buf, unsigned i
   r[4] = t1;
   r[5] = t2;
   r[6] = t3;
+  r[7] = kind;
 }
 
 // ---- element conversion ----

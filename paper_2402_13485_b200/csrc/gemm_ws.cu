@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     __syncwarp();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
   }
-  if (p.trace && threadIdx.x == 0) trace_record(p.trace, p.tag, t_entry, s_t[0], s_t[1]);
+  if (p.trace && threadIdx.x == 0) trace_record(p.trace, p.tag, t_entry, s_t[0], s_t[1], 1);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

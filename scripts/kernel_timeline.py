@@ -48,6 +48,7 @@ for _ in range(3):
     be._run_layers(x.clone(), rt, 0, args.layers, td["mask"], n, tmpl.words)
 torch.cuda.synchronize()
 buf = torch.zeros(8 + 8 * 200000, device=dev, dtype=torch.int64)
+buf[1] = 200000
 lib.propd_debug_timeline(ctypes.c_void_p(buf.data_ptr()))
 be._run_layers(x.clone(), rt, 0, args.layers, td["mask"], n, tmpl.words)
 torch.cuda.synchronize()
