@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA graphs")
+    ap.add_argument("--planted", action="store_true",
+                    help="planted acceptance (SURVEY f3): draft head 0 := LM head, so depth-1 nodes are accepted")
     ap.add_argument("--sync-rows", action="store_true",
                     help="size the post-prune layers on the host (one mid-step sync) instead of on the device")
     return ap.parse_args()
@@ -196,6 +198,8 @@ def cpu_reference(args, steps: int, warmup: int):
                       ("w2", (4 * H, H)))} for _ in range(Ly)],
          "w_lm": rng.standard_normal((H, V)) * s, "w_early": rng.standard_normal((H, V)) * s,
          "w_draft": rng.standard_normal((4, H, V)) * s}
+    if args.planted:
+        w["w_draft"][0] = w["w_lm"]
     model = op.TinyModel(cfg, weights=w)
     prune = op.PruneCfg(layer=1, topk=50) if args.mode in ("prune_only", "propd_full") else None
     ecfg = op.EngineCfg(mode=args.mode, draft_heads=4, draft_topk=args.topk, prune=prune,
@@ -236,6 +240,8 @@ def run_b200(args, rank: int, world: int, group):
     B = args.batch
     be = B200Backend(cfg, dtype="bf16", device=dev, random_device_init=True, max_slots=B + 1, max_tree=4 * args.topk,
                      kv_len=cfg.max_positions, attn_impl=args.attn_impl, use_graphs=not args.no_graphs)
+    if args.planted:
+        be.plant_draft_head(0)
     eng = DecodeEngine(be, engine_cfg(args), None, group=group)
     states = be.synthetic_states(B, args.kv, seed=1000 + rank)
     seqs = [_Seq(st, st.committed[:], rank * B + i) for i, st in enumerate(states)]
@@ -467,7 +473,8 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights, random KV/prompt state)",
-        "config": {"workload": "configs[1]: Vicuna-7B-shape random-init bf16, ProPD pruned+dynamic tree",
+        "config": {"workload": "configs[1]: Vicuna-7B-shape random-init bf16, ProPD pruned+dynamic tree"
+                               + (", planted draft head 0 (accepts depth-1 nodes)" if args.planted else ""),
                    "model": "vicuna-7b-shape (32L, 4096, 32x128, V32000, 4 draft heads)", "layers": args.layers,
                    "batch_per_gpu": args.batch, "global_batch": args.batch * world, "kv": args.kv,
                    "mode": args.mode, "draft_topk": args.topk, "prune": "layer 4, top-K 50",

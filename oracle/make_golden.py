@@ -18,6 +18,9 @@ It imports the unmodified reference package `treedecode` from
                                       C1 model (TinyTransformer seed 17) + prompts
   tests/golden/forward_cases.npz      forward_tree logits (fp64) for random trees,
                                       pruned and unpruned, on two model configs
+  tests/golden/cli_run_tiny/          the reference CLI's run outputs for configs/run_tiny.json
+                                      (transcripts, metrics.jsonl, summary.csv, plan_events.jsonl)
+  tests/golden/cli_sweep_tiny/        the reference CLI's sweep.csv (mode x batch)
   tests/golden/gate_numbers.json      worked-number anchors (mask text, verify walks,
                                       prune cases, selection curves)
 """
@@ -226,6 +229,22 @@ def main() -> None:
     gate = {"fig_mask": format_mask(make_mask(fig)), "walks": walks, "prunes": prunes,
             "selections": sel_cases, "grid_4_3": [list(p) for p in grid_candidates(4, 3)]}
     (OUT / "gate_numbers.json").write_text(json.dumps(gate))
+
+    # 6. the reference CLI's own output files (cli.py:27-73) -------------------
+    import shutil
+
+    from treedecode import cli as tcli
+
+    cli_dir = OUT / "cli_run_tiny"
+    shutil.rmtree(cli_dir, ignore_errors=True)
+    shutil.copy(REF_PKG / "configs" / "run_tiny.json", OUT / "run_tiny_config.json")
+    assert tcli.main(["run", "--config", str(OUT / "run_tiny_config.json"), "--out-dir", str(cli_dir),
+                      "--verbose"]) == 0
+    sweep_cfg = json.loads((REF_PKG / "configs" / "run_tiny.json").read_text())
+    sweep_cfg["sweep"] = {"mode": ["static_tree", "propd_full"], "batch": [2, 4]}
+    (OUT / "sweep_tiny_config.json").write_text(json.dumps(sweep_cfg, indent=2))
+    assert tcli.main(["sweep", "--config", str(OUT / "sweep_tiny_config.json"), "--axis", "mode", "--axis", "batch",
+                      "--out-dir", str(OUT / "cli_sweep_tiny")]) == 0
     print(f"golden fixtures written to {OUT}")
 
 

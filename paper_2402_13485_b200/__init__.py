@@ -9,12 +9,12 @@ is the batched decode loop with the reference's run()/metrics surface
 
 from .config import (MODES, VICUNA_7B_SHAPE, VICUNA_33B_SHAPE, EngineConfig, PruneConfig, SchedulerConfig,
                      TinyTransformerConfig)
-from .planning import CostModel, HeadPredictions, InsufficientDataError, choose_size, grid_candidates
+from .planning import CostModel, HeadPredictions, InsufficientDataError, LatencyModel, choose_size, grid_candidates
 from .tree import TreeTemplate
 
 __all__ = [
     "MODES", "VICUNA_7B_SHAPE", "VICUNA_33B_SHAPE", "EngineConfig", "PruneConfig", "SchedulerConfig",
-    "TinyTransformerConfig", "CostModel", "HeadPredictions", "InsufficientDataError", "choose_size",
+    "TinyTransformerConfig", "CostModel", "HeadPredictions", "InsufficientDataError", "LatencyModel", "choose_size",
     "grid_candidates", "TreeTemplate", "B200Backend", "DecodeEngine",
 ]
 

@@ -201,6 +201,17 @@ class B200Backend:
         self._pending_events: list = []
         self._role = "eager"
 
+    def plant_draft_head(self, d: int = 0) -> None:
+        """Planted-acceptance harness: draft head d := the LM
+        head, so its top-1 is the model's own next-token argmax.  With random
+        weights acceptance is otherwise ~0 (out/run_tiny/summary.csv:2); with
+        head 0 planted every step accepts the depth-1 node, which exercises
+        the accept walk, the KV compaction and multi-token commits at scale."""
+        V = self.V
+        if not 0 <= d < self.config.draft_heads:
+            raise ValueError("draft head index out of range")
+        self.w.w_draft[:, d * V:(d + 1) * V].copy_(self.w.w_lm)
+
     # ------------------------------------------------------------------ API
     @property
     def vocab_size(self) -> int:

@@ -166,3 +166,27 @@ def should_replan(snap: RuntimeSnapshot, cfg) -> bool:
     return (abs(snap.batch - snap.planned_batch) >= cfg.resize_batch_delta
             or abs(snap.mean_seqlen - snap.planned_seqlen) >= cfg.resize_seqlen_delta
             or snap.iterations_since_plan >= cfg.replan_period)
+
+
+class LatencyModel:
+    """Seeded simulated iteration clock (backends.py:568-603): the engine's
+    time source for reproducible tree sizing in parity runs,
+    t = c0_base + c0_batch B + c0_seqlen S + (c1_base + c1_batch B) rows
+    + U(-noise, noise)."""
+
+    def __init__(self, c0_base: float = 1.0, c0_batch: float = 0.0, c0_seqlen: float = 0.0, c1_base: float = 0.05,
+                 c1_batch: float = 0.0, noise: float = 0.0, seed: int = 0) -> None:
+        if noise < 0.0:
+            raise ValueError("noise amplitude must be non-negative")
+        self.c0 = (float(c0_base), float(c0_batch), float(c0_seqlen))
+        self.c1 = (float(c1_base), float(c1_batch))
+        self.noise = float(noise)
+        self._rng = np.random.default_rng(seed)
+
+    def iteration_time(self, rows: float, batch: int = 1, seqlen: float = 0.0) -> float:
+        t = (self.c0[0] + self.c0[1] * batch + self.c0[2] * seqlen) + (self.c1[0] + self.c1[1] * batch) * float(rows)
+        if self.noise > 0.0:
+            t += float(self._rng.uniform(-self.noise, self.noise))
+        if t <= 0.0:
+            raise ValueError("latency coefficients produced a non-positive time")
+        return float(t)

@@ -261,3 +261,35 @@ def test_sync_free_post_prune_pass_matches_synced_pass():
     assert (ra == rb).mean() >= 0.95
     if np.array_equal(ra, rb):
         assert np.array_equal(a.committed, b.committed) and np.array_equal(a.acc_len, b.acc_len)
+
+
+@pytest.mark.parametrize("mode", ["static_tree", "propd_full"])
+def test_planted_acceptance_matches_oracle(mode):
+    """Planted-acceptance harness: draft head 0 := the LM head on the same seeded weights for
+    the B200 backend and the oracle, so every step accepts depth-1 nodes (multi-token commits, in-place KV
+    compaction, acceptance statistics away from zero) — transcripts, metrics and P stay identical."""
+    from paper_2402_13485_b200.weights import seeded_weights
+
+    mc = op.TinyCfg(layers=4, hidden=64, heads=4, vocab=256, draft_heads=4, max_positions=160, seed=11)
+    w = seeded_weights(TinyTransformerConfig(**mc.__dict__))
+    w["w_draft"] = w["w_draft"].copy()
+    w["w_draft"][0] = w["w_lm"]
+    ecfg = op.EngineCfg(mode=mode, draft_heads=4, draft_topk=3, prune=op.PruneCfg(layer=2, topk=24),
+                        scheduler=op.SchedCfg(replan_period=8, size_candidates=(1, 2, 4, 8, 12)))
+    prompts = op.synthetic_prompts(256, 6, 7, 3)
+    clock = dict(c0_base=3.0, c1_base=0.05, noise=0.02, seed=5)
+    ref = op.Engine(op.TinyModel(mc, weights=w), ecfg, op.Clock(**clock)).run(prompts, 24, batch_size=3)
+    be = B200Backend(TinyTransformerConfig(**mc.__dict__), dtype="fp32", max_slots=8, weights=w)
+    res = DecodeEngine(be, product_cfg(ecfg, mode), op.Clock(**clock)).run(prompts, 24, batch_size=3)
+    assert res.transcripts == ref["transcripts"]
+    assert [m.to_json() for m in res.metrics] == ref["metrics"]
+    assert res.summary.mean_accepted >= 0.9  # depth-1 accepted (almost) every step
+
+
+def test_plant_draft_head_copies_lm_head():
+    be = B200Backend(TinyTransformerConfig(layers=1, hidden=128, heads=1, vocab=512, draft_heads=3),
+                     dtype="bf16", random_device_init=True, max_slots=2)
+    be.plant_draft_head(1)
+    assert torch.equal(be.w.w_draft[:, 512:1024], be.w.w_lm)
+    with pytest.raises(ValueError, match="out of range"):
+        be.plant_draft_head(3)
