@@ -185,6 +185,20 @@ int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, fl
 /* out = bf16(tanh-GELU(acc)) for acc[M, N] fp32; acc re-zeroed. */
 int propd_gelu_finish(int M, const int32_t* rows_dev, int N, float* acc, int ldacc, void* out, int ldout, void* stream);
 
+/* ---- probability statistics (probability pruning, typical acceptance) ----
+ * stats[r] = (log-sum-exp, entropy) in fp64 of z = logits[idx ? idx[r] : r] / temp
+ * (fp32 rows of width V, row stride ld); rows_dev as above. */
+int propd_row_lse(int R, const int32_t* rows_dev, int V, int ld, const float* logits, const int32_t* idx,
+                  double temp, double* stats, void* stream);
+/* Probability-based early pruning (the reference disables
+ * it, pruning.py:76-82; definition = oracle probability_prune):
+ * member[b*n+i] = depth-1, or sum over the path of (l_parent[token] - lse_parent)
+ * >= log_tau, summed top-down in fp64.  early_stats = propd_row_lse of the
+ * early rows (temp 1); row layout as propd_early_member. */
+int propd_early_prob_member(int B, int n, int P, int V, double log_tau, const float* early_logits,
+                            const double* early_stats, const int32_t* parent, const int32_t* parent_slot,
+                            const int32_t* tokens, uint8_t* member, void* stream);
+
 /* ---- K3: early prune (pruning.py:40-66, backends.py:320-327) ----
  * early_logits: fp32 [R, V], one row per (sequence, parent-slot): row
  * b*P + parent_slot[p] holds the early head output of node p of sequence b.
@@ -203,6 +217,30 @@ int propd_prune_compact(int B, int n, const int32_t* parent, const uint8_t* memb
                         int32_t* new_row_off, int32_t* node_row, int32_t* surv_cnt, int32_t* total,
                         void* stream);
 
+/* Typical acceptance for propd_verify_commit_ex (definition = oracle
+ * typical_verify): candidate x is typical under row p = softmax(logits / T)
+ * iff log p(x) > min(log_eps, log_alpha - H(p)); accepted = typical and parent
+ * accepted (depth 1: under the root row); the path to the deepest accepted
+ * node (ties: lowest index) is committed, bonus = its row argmax.
+ * row_logits/row_stats: the tree pass's LM rows (survivor order) and their
+ * propd_row_lse; root_logits: per sequence SLOT (stride root_ld), root_stats:
+ * per batch entry; depth: template depths. */
+typedef struct propd_typical {
+  const float* row_logits;
+  int ld;
+  const double* row_stats;
+  const float* root_logits;
+  int root_ld;
+  const double* root_stats;
+  double log_eps, log_alpha, temperature;
+  const int32_t* depth;
+} propd_typical;
+int propd_verify_commit_ex(int dtype, int B, int n, int D, int kmax, int layers, int A, int dh, int Lmax,
+                           int64_t layer_stride, const int32_t* parent, const int32_t* tokens, const uint8_t* alive,
+                           const int32_t* node_row, const int32_t* row_argmax, const int32_t* root,
+                           const int32_t* draft_tok, const int32_t* seq_slot, int32_t* seq_len, void* kcache,
+                           void* vcache, int32_t* acc_node, int32_t* acc_surv, int32_t* acc_len, int32_t* bonus,
+                           int32_t* committed, int8_t* ranks, const propd_typical* typical, void* stream);
 /* ---- K5: greedy accept + in-place KV compaction (verification.py:30-53,
  * backends.py:337-348) ----
  * Walks each sequence's (pruned) tree from root[slot]; accepted nodes

@@ -213,8 +213,11 @@ class TinyModel:
             if prune_callback is not None and prune_layer == li + 1:
                 early = x @ self.w["w_early"]
                 kk = min(early_topk, self.cfg.vocab)
-                order = np.argsort(-early, axis=1, kind="stable")[:, :kk]
-                surv = [int(s) for s in prune_callback([r.tolist() for r in order])]
+                if getattr(prune_callback, "wants_logits", False):  # probability-based pruning
+                    surv = [int(s) for s in prune_callback(early)]
+                else:
+                    order = np.argsort(-early, axis=1, kind="stable")[:, :kk]
+                    surv = [int(s) for s in prune_callback([r.tolist() for r in order])]
                 vis = subsample_mask(vis, surv)
                 x, keep = x[surv], keep[surv]
         logits = layer_norm(x) @ self.w["w_lm"]
@@ -401,6 +404,7 @@ def format_mask(mask: np.ndarray) -> str:
 class PruneCfg:
     layer: int = 4
     topk: int = 50
+    threshold: float | None = None  # probability-based pruning (probability_prune) when set
 
 
 def prune(tree: Tree, early_lists, cfg: PruneCfg):
@@ -422,6 +426,82 @@ def prune(tree: Tree, early_lists, cfg: PruneCfg):
         alive[i] = True if nd.parent == ROOT else bool(alive[nd.parent] and nd.token in sets[nd.parent])
     surv = tuple(int(i) for i in np.flatnonzero(alive))
     return surv, (0.0 if n == 0 else 1.0 - len(surv) / n)
+
+
+def row_lse_entropy(logits, temperature: float = 1.0):
+    """Per row of z = logits / T: log-sum-exp and entropy H = lse - sum(p z) (fp64)."""
+    z = np.asarray(logits, dtype=np.float64) / float(temperature)
+    m = z.max(axis=1, keepdims=True)
+    e = np.exp(z - m)
+    s = e.sum(axis=1, keepdims=True)
+    lse = (m + np.log(s))[:, 0]
+    H = lse - (e * z).sum(axis=1) / s[:, 0]
+    return lse, H
+
+
+def probability_prune(tree: Tree, early_logits, threshold: float):
+    """Probability-based early pruning (the reference ships
+    only top-K and disables this entry point, pruning.py:76-82 -- parity
+    unpinned, this restatement is the definition the B200 kernel follows): a
+    node survives iff it has depth 1, or its parent survives and the marginal
+    path probability prod p_early(token | parent row) >= threshold.  Terms are
+    summed top-down in log space in fp64.  Returns (survivors, rate)."""
+    n = len(tree)
+    early = np.asarray(early_logits, dtype=np.float64)
+    lse, _ = row_lse_entropy(early)
+    log_tau = math.log(threshold)
+    logp = np.zeros(n)
+    alive = np.zeros(n, dtype=bool)
+    for i, nd in enumerate(tree.nodes):
+        if nd.parent == ROOT:
+            alive[i] = True
+        else:
+            logp[i] = logp[nd.parent] + (early[nd.parent, nd.token] - lse[nd.parent])
+            alive[i] = bool(alive[nd.parent] and logp[i] >= log_tau)
+    surv = tuple(int(i) for i in np.flatnonzero(alive))
+    return surv, (0.0 if n == 0 else 1.0 - len(surv) / n)
+
+
+def typical_verify(tree: Tree, node_logits, root_logits, epsilon: float, alpha: float, temperature: float = 1.0):
+    """Typical acceptance (Medusa-style; named by the north star, absent from
+    the reference -- parity unpinned, this restatement is the definition the
+    B200 kernel follows): with p = softmax(logits / T) of the accepting row,
+    candidate token x is typical iff log p(x) > min(log eps, log alpha - H(p)).
+    A node is accepted iff it is typical under its parent's row (depth 1:
+    under the root row = the last committed token's logits) and its parent is
+    accepted.  The path to the deepest accepted node (ties: lowest index) is
+    committed; the bonus is the argmax of that node's row (root row if none).
+    Returns (accepted, bonus)."""
+    n = len(tree)
+    rows = np.asarray(node_logits, dtype=np.float64)
+    root = np.asarray(root_logits, dtype=np.float64)[None, :]
+    lse, H = row_lse_entropy(rows, temperature) if n else (np.zeros(0), np.zeros(0))
+    rlse, rH = row_lse_entropy(root, temperature)
+    le = math.log(epsilon)
+    la = math.log(alpha)
+
+    def typical(z_row, lse_r, H_r, tok):
+        return (z_row[tok] / temperature - lse_r) > min(le, la - H_r)
+
+    acc = np.zeros(n, dtype=bool)
+    for i, nd in enumerate(tree.nodes):
+        if nd.parent == ROOT:
+            acc[i] = typical(root[0], rlse[0], rH[0], nd.token)
+        else:
+            acc[i] = bool(acc[nd.parent] and typical(rows[nd.parent], lse[nd.parent], H[nd.parent], nd.token))
+    depths = tree.depths
+    best, best_d = -1, 0
+    for i in range(n):
+        if acc[i] and int(depths[i]) > best_d:
+            best, best_d = i, int(depths[i])
+    if best < 0:
+        return (), int(np.argmax(root[0]))
+    chain = []
+    j = best
+    while j != ROOT:
+        chain.append(j)
+        j = tree.nodes[j].parent
+    return tuple(reversed(chain)), int(np.argmax(rows[best]))
 
 
 def verify(tree: Tree, node_argmax, root_argmax: int):
@@ -649,6 +729,10 @@ class EngineCfg:
     include_bonus_in_speed: bool = False
     probe_rounds: int = 1
     eos_token: int | None = None
+    acceptance: str = "greedy"  # or "typical" (typical_verify)
+    typical_epsilon: float = 0.09
+    typical_alpha: float = 0.3
+    typical_temperature: float = 1.0
 
     uses_tree = property(lambda self: self.mode != "autoregressive")
     uses_prune = property(lambda self: self.mode in ("prune_only", "propd_full"))
@@ -755,8 +839,13 @@ class Engine:
 
                 def on_early(lists, _t=tree, _b=box):
                     _b["lists"] = lists
-                    _b["dec"] = prune(_t, lists, cfg.prune)
+                    if cfg.prune.threshold is not None:
+                        _b["dec"] = probability_prune(_t, lists, cfg.prune.threshold)
+                    else:
+                        _b["dec"] = prune(_t, lists, cfg.prune)
                     return _b["dec"][0]
+
+                on_early.wants_logits = cfg.prune.threshold is not None
 
                 fwd = self.b.forward_tree(st, tree.tokens, positions, mask, prune_layer=cfg.prune.layer,
                                           early_topk=cfg.prune.topk, prune_callback=on_early)
@@ -764,11 +853,16 @@ class Engine:
                 vtree = restrict(tree, surv)
                 subsample_mask(mask, surv)
                 rates.append(rate)
-                rec["early_lists"] = box["lists"]
+                rec["early_lists"] = (box["lists"] if cfg.prune.threshold is None
+                                      else np.argsort(-box["lists"], axis=1, kind="stable")[:, :4].tolist())
             else:
                 fwd = self.b.forward_tree(st, tree.tokens, positions, mask)
                 vtree = tree
-            accepted, bonus = verify(vtree, fwd.argmax, root)
+            if cfg.acceptance == "typical":
+                accepted, bonus = typical_verify(vtree, fwd.logits, st.last_logits, cfg.typical_epsilon,
+                                                 cfg.typical_alpha, cfg.typical_temperature)
+            else:
+                accepted, bonus = verify(vtree, fwd.argmax, root)
             self.b.commit(st, accepted, bonus)
             newly = [vtree.nodes[i].token for i in accepted] + [bonus]
             n_tok += self._absorb(s, newly, max_tokens)

@@ -45,6 +45,10 @@ SIGNATURES = {
     "propd_qkv_finish": [I, P, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
     "propd_gelu_finish": [I, P, I, P, I, P, I, P],
     "propd_early_member": [I, I, I, I, I, P, P, P, P, P, P],
+    "propd_row_lse": [I, P, I, I, P, P, c_double, P, P],
+    "propd_early_prob_member": [I, I, I, I, c_double, P, P, P, P, P, P, P],
+    "propd_verify_commit_ex": [I, I, I, I, I, I, I, I, I, L, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P,
+                               "typical", P],
     "propd_prune_compact": [I, I, P, P, P, P, P, P, P, P, P, P, P],
     "propd_verify_commit": [I, I, I, I, I, I, I, I, I, L, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "propd_kv_compact": [I, I, I, I, I, I, I, L, P, P, P, P, P, P, P],
@@ -68,6 +72,14 @@ class WsPhases(ctypes.Structure):
                 ("kcache", P), ("vcache", P), ("bar", P)]
 
 
+class Typical(ctypes.Structure):
+    """propd_typical (include/propd.h): typical-acceptance inputs of propd_verify_commit_ex."""
+
+    _fields_ = [("row_logits", P), ("ld", c_int), ("row_stats", P), ("root_logits", P), ("root_ld", c_int),
+                ("root_stats", P), ("log_eps", c_double), ("log_alpha", c_double), ("temperature", c_double),
+                ("depth", P)]
+
+
 class PropdError(RuntimeError):
     """A libpropd call returned a nonzero status."""
 
@@ -87,7 +99,8 @@ def load():
     lib = ctypes.CDLL(LIB_PATH)
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
-        fn.argtypes = [ctypes.POINTER(WsPhases) if a == "phases" else a for a in argtypes]
+        structs = {"phases": WsPhases, "typical": Typical}
+        fn.argtypes = [ctypes.POINTER(structs[a]) if isinstance(a, str) else a for a in argtypes]
         fn.restype = _RESTYPES.get(name, c_int)
     if lib.propd_abi_version() != ABI_VERSION:
         raise ImportError(f"libpropd ABI {lib.propd_abi_version()} != expected {ABI_VERSION}; rebuild")

@@ -19,6 +19,7 @@ final LN'd hidden of that row (the draft heads' input).
 
 from __future__ import annotations
 
+import math
 import weakref
 from dataclasses import dataclass, field
 
@@ -729,7 +730,7 @@ class B200Backend:
         self._pending_events.extend(ent[3])
         return ent[1]
 
-    def _bonus_program(self, seq_slot, bonus, B: int, max_keys: int):
+    def _bonus_program(self, seq_slot, bonus, B: int, max_keys: int, keep_logits: bool = False):
         """One committed row per sequence at position seq_len (backends.py:239-259
         for the bonus token): K/V append, hidden/root update, seq_len += 1."""
         torch, st = self.torch, self.stream()
@@ -750,6 +751,8 @@ class B200Backend:
         self._call("propd_add_ln", self.code, B, None, self.H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
         logits, am = self._lm_argmax(hfin)
         self.hidden.index_copy_(0, seq_slot.long(), hfin)
+        if keep_logits:  # the next step's root row (typical acceptance)
+            self.last_logits.index_copy_(0, seq_slot.long(), logits)
         self._call("propd_scatter_i32", B, ptr(seq_slot), ptr(am), ptr(self.root), st)
         self._call("propd_seq_advance", B, ptr(seq_slot), ptr(self.seq_len), None, 1, st)
 
@@ -808,8 +811,14 @@ class B200Backend:
             xp = torch.empty(B * Pn, H, device=dev, dtype=self.tdtype)
             self._call("propd_gather_rows", self.code, B * Pn, H, ptr(x), ptr(par), ptr(xp), st)
             early = self._proj_f32(xp, self.w.w_early, V)
-            self._call("propd_early_member", B, n, Pn, V, min(prune.topk, V), ptr(early), ptr(td["parent"]),
-                       ptr(td["parent_slot"]), ptr(o["tokens"]), ptr(member), st)
+            if getattr(prune, "threshold", None) is not None:  # probability-based (marginal path probability)
+                est = torch.empty(B * Pn, 2, device=dev, dtype=torch.float64)
+                self._call("propd_row_lse", B * Pn, None, V, V, ptr(early), None, 1.0, ptr(est), st)
+                self._call("propd_early_prob_member", B, n, Pn, V, math.log(prune.threshold), ptr(early), ptr(est),
+                           ptr(td["parent"]), ptr(td["parent_slot"]), ptr(o["tokens"]), ptr(member), st)
+            else:
+                self._call("propd_early_member", B, n, Pn, V, min(prune.topk, V), ptr(early), ptr(td["parent"]),
+                           ptr(td["parent_slot"]), ptr(o["tokens"]), ptr(member), st)
         o["alive"] = torch.empty(M, device=dev, dtype=torch.uint8)
         # compacted row tables sized for the worst case + pad entry
         cap = max(M, self._s_bucket(M))
@@ -820,7 +829,7 @@ class B200Backend:
                    ptr(o["total"]), st)
         return o
 
-    def _part_b(self, B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows=False):
+    def _part_b(self, B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows=False, accept=None):
         torch, st, cfg = self.torch, self.stream(), self.config
         n, D, H = len(tmpl), cfg.draft_heads, self.H
         dev = self.device
@@ -842,17 +851,30 @@ class B200Backend:
         live = a["total"] if (prune is not None and device_rows) else None
         hfin = torch.empty(S, H, device=dev, dtype=self.tdtype)
         self._call("propd_add_ln", self.code, S, ptr(live), H, ptr(x), ptr(pending), ptr(hfin), None, None, st)
-        _, row_argmax = self._lm_argmax(hfin, live)
+        row_logits, row_argmax = self._lm_argmax(hfin, live)
         i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
         o = {"acc_node": i32(B * D), "acc_surv": i32(B * D), "acc_len": i32(B), "bonus": i32(B),
              "committed": i32(B * (D + 1)), "ranks": torch.empty(B, D, device=dev, dtype=torch.int8),
              "row_argmax": row_argmax, "root_before": self.root.index_select(0, seq_slot.long())}
-        self._call("propd_verify_commit", self.code, B, n, D, k, cfg.layers, self.A, self.dh, self.Lmax,
+        typ = None
+        if accept is not None:  # typical acceptance: softmax statistics of the tree rows and the root rows
+            eps, alpha, temp = accept
+            V = self.V
+            rst = torch.empty(S, 2, device=dev, dtype=torch.float64)
+            self._call("propd_row_lse", S, ptr(live), V, V, ptr(row_logits), None, float(temp), ptr(rst), st)
+            o["root_stats"] = torch.empty(B, 2, device=dev, dtype=torch.float64)
+            self._call("propd_row_lse", B, None, V, V, ptr(self.last_logits), ptr(seq_slot), float(temp),
+                       ptr(o["root_stats"]), st)
+            o["row_stats"] = rst
+            typ = _lib.Typical(row_logits=ptr(row_logits), ld=V, row_stats=ptr(rst), root_logits=ptr(self.last_logits),
+                               root_ld=V, root_stats=ptr(o["root_stats"]), log_eps=math.log(eps),
+                               log_alpha=math.log(alpha), temperature=float(temp), depth=ptr(td["depth"]))
+        self._call("propd_verify_commit_ex", self.code, B, n, D, k, cfg.layers, self.A, self.dh, self.Lmax,
                    self.layer_stride, ptr(td["parent"]), ptr(a["tokens"]), ptr(alive), ptr(node_row),
                    ptr(row_argmax), ptr(self.root), ptr(a["draft_tok"]), ptr(seq_slot), ptr(self.seq_len),
                    ptr(self.kcache), ptr(self.vcache), ptr(o["acc_node"]), ptr(o["acc_surv"]), ptr(o["acc_len"]),
-                   ptr(o["bonus"]), ptr(o["committed"]), ptr(o["ranks"]), st)
-        self._bonus_program(seq_slot, o["bonus"], B, kb)
+                   ptr(o["bonus"]), ptr(o["committed"]), ptr(o["ranks"]), typ, st)
+        self._bonus_program(seq_slot, o["bonus"], B, kb, keep_logits=accept is not None)
         return o
 
     @staticmethod
@@ -875,7 +897,7 @@ class B200Backend:
         return hb
 
     def step_tree(self, states, tmpl: TreeTemplate, k: int, prune=None, trace: bool = False,
-                  stats=None) -> StepOutput:
+                  stats=None, accept=None) -> StepOutput:
         """One batched ProPD tree iteration on the device (engine.py:243-303):
         K4a draft -> K1 tree embed -> layers 1..p -> K3 early prune + row
         compaction -> layers p+1..Ly on survivors -> LM argmax -> K5 accept +
@@ -898,7 +920,8 @@ class B200Backend:
         if ("par_rows", B) not in td:
             rows = (np.arange(B, dtype=np.int32)[:, None] * n + tmpl.parent_nodes[None, :]).reshape(-1)
             td[("par_rows", B)] = self.torch.from_numpy(np.ascontiguousarray(rows)).to(self.device)
-        pkey = (prune.layer, prune.topk) if prune is not None else None
+        pkey = (prune.layer, prune.topk, getattr(prune, "threshold", None), accept) if prune is not None else (
+            None, accept)
         self._role = "tree"
         a = self._run(("A", B, tmpl.paths, k, pkey, kb), lambda: self._part_a(B, tmpl, k, prune, slot_buf, kb))
         # Layers > p run on the survivors.  When every projection of that pass
@@ -916,7 +939,7 @@ class B200Backend:
             S_pad = self._s_bucket(S) if self.use_graphs else S
         self._role = "tree_pruned"
         b = self._run(("B", B, tmpl.paths, k, pkey, kb, S_pad, device_rows),
-                      lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows))
+                      lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows, accept))
         if stats is not None:  # single process: replay this batch's records right away (K4)
             P, counts, alpha, order_dev, lcurve_dev = stats
             self.stats_replay_select(b["ranks"], B, P, counts, alpha, order_dev, lcurve_dev)

@@ -132,7 +132,9 @@ def build_engine_config(cfg: dict) -> EngineConfig:
                             scheduler=sched, static_tree=static, acceptance_alpha=s["acceptance_alpha"],
                             cost_alpha=s["cost_alpha"], cost_staleness=s["cost_staleness"],
                             include_bonus_in_speed=s["include_bonus_in_speed"], probe_rounds=s["probe_rounds"],
-                            eos_token=s["eos_token"])
+                            eos_token=s["eos_token"], acceptance=s.get("acceptance", "greedy"),
+                            typical_epsilon=s.get("typical_epsilon", 0.09), typical_alpha=s.get("typical_alpha", 0.3),
+                            typical_temperature=s.get("typical_temperature", 1.0))
     except (TypeError, ValueError) as exc:
         raise ConfigError(f"engine: {exc}") from exc
 

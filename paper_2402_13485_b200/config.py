@@ -49,14 +49,22 @@ VICUNA_33B_SHAPE = dict(layers=60, hidden=6656, heads=52, vocab=32000, draft_hea
 
 @dataclass(frozen=True)
 class PruneConfig:
+    """Top-K early pruning (pruning.py:22-30, 40-66); with `threshold` set,
+    probability-based pruning instead: a node survives iff its marginal path
+    probability under the early head is >= threshold (the
+    reference disables this criterion, pruning.py:76-82)."""
+
     layer: int = 4
     topk: int = 50
+    threshold: float | None = None
 
     def __post_init__(self) -> None:
         if self.layer < 1:
             raise ValueError("prune layer must be >= 1")
         if self.topk < 1:
             raise ValueError("prune top-K must be >= 1")
+        if self.threshold is not None and not 0.0 < self.threshold <= 1.0:
+            raise ValueError("prune threshold must lie in (0, 1]")
 
 
 @dataclass(frozen=True)
@@ -87,8 +95,18 @@ class EngineConfig:
     include_bonus_in_speed: bool = False
     probe_rounds: int = 1
     eos_token: int | None = None
+    # "greedy" (verification.py:30-53) or "typical": candidate x accepted iff
+    # log p(x) > min(log epsilon, log alpha - H(p)), p = softmax(logits / T)
+    acceptance: str = "greedy"
+    typical_epsilon: float = 0.09
+    typical_alpha: float = 0.3
+    typical_temperature: float = 1.0
 
     def __post_init__(self) -> None:
+        if self.acceptance not in ("greedy", "typical"):
+            raise ValueError("acceptance must be 'greedy' or 'typical'")
+        if not (self.typical_epsilon > 0 and self.typical_alpha > 0 and self.typical_temperature > 0):
+            raise ValueError("typical acceptance parameters must be positive")
         if self.mode not in MODES:
             raise ValueError(f"unknown mode {self.mode!r}; expected one of {MODES}")
         if self.draft_heads < 1 or self.draft_topk < 1:

@@ -135,6 +135,63 @@ __device__ void compact_rows(int len, const int* acc, int slot, int L, int layer
   }
 }
 
+// Typical acceptance (oracle typical_verify): candidate token x of a node is
+// typical under its parent's row p = softmax(z), z = logits / T, iff
+// z[x] - lse > min(log eps, log alpha - H); a node is accepted iff typical and
+// its parent accepted (depth 1: under the root row); the path to the deepest
+// accepted node (ties: lowest index) is committed, bonus = that row's argmax.
+// Evaluated level by level by one warp (parents precede children in the
+// canonical order and depth <= D).
+__device__ __forceinline__ bool typical_ok(const float* row, int tok, const double* st, const propd_typical& t) {
+  const double lp = __dsub_rn(__ddiv_rn((double)row[tok], t.temperature), st[0]);
+  return lp > fmin(t.log_eps, __dsub_rn(t.log_alpha, st[1]));
+}
+
+__device__ int typical_walk(int b, int slot, int n, int D, const int32_t* parent, const int32_t* tokens,
+                            const uint8_t* alive, const int32_t* node_row, const propd_typical& t, int* s_acc,
+                            uint8_t* s_ok, int lane) {
+  for (int i = lane; i < n; i += 32) s_ok[i] = 0;
+  __syncwarp();
+  for (int d = 1; d <= D; ++d) {
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      if (i < n && t.depth[i] == d && (alive == nullptr || alive[b * n + i])) {
+        const int p = parent[i];
+        bool ok;
+        if (p < 0) {
+          ok = typical_ok(t.root_logits + (size_t)slot * t.root_ld, tokens[b * n + i], t.root_stats + 2 * b, t);
+        } else if (s_ok[p]) {
+          const int r = node_row ? node_row[b * n + p] : b * n + p;
+          ok = typical_ok(t.row_logits + (size_t)r * t.ld, tokens[b * n + i], t.row_stats + 2 * r, t);
+        } else {
+          ok = false;
+        }
+        s_ok[i] = ok ? 1 : 0;
+      }
+    }
+    __syncwarp();
+  }
+  // deepest accepted node, ties -> lowest index
+  int best = -1, best_d = 0;
+  for (int i = lane; i < n; i += 32)
+    if (s_ok[i] && t.depth[i] > best_d) {
+      best = i;
+      best_d = t.depth[i];
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int ob = __shfl_xor_sync(0xffffffffu, best, o), od = __shfl_xor_sync(0xffffffffu, best_d, o);
+    if (od > best_d || (od == best_d && ob >= 0 && (best < 0 || ob < best))) {
+      best = ob;
+      best_d = od;
+    }
+  }
+  if (lane == 0)
+    for (int j = best, k = best_d - 1; j >= 0; j = parent[j], --k) s_acc[k] = j;
+  __syncwarp();
+  return best;
+}
+
 template <typename T>
 __global__ void verify_commit_kernel(int n, int D, int kmax, int layers, int A, int dh, int Lmax, int64_t layer_stride,
                                      const int32_t* __restrict__ parent, const int32_t* __restrict__ tokens,
@@ -142,9 +199,11 @@ __global__ void verify_commit_kernel(int n, int D, int kmax, int layers, int A, 
                                      const int32_t* __restrict__ row_argmax, const int32_t* __restrict__ root,
                                      const int32_t* __restrict__ draft_tok, const int32_t* __restrict__ seq_slot,
                                      int32_t* seq_len, T* kc, T* vc, int32_t* acc_node, int32_t* acc_surv,
-                                     int32_t* acc_len, int32_t* bonus, int32_t* committed, int8_t* ranks) {
+                                     int32_t* acc_len, int32_t* bonus, int32_t* committed, int8_t* ranks,
+                                     propd_typical typ) {
   __shared__ int s_acc[MAX_D];
   __shared__ int s_len, s_L;
+  __shared__ uint8_t s_ok[1024];
   const int b = blockIdx.x;
   const int slot = seq_slot[b];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -152,7 +211,14 @@ __global__ void verify_commit_kernel(int n, int D, int kmax, int layers, int A, 
     const int L = seq_len[slot];
     int target = root[slot];
     int cur = -1, len = 0;
-    for (int step = 0; step < D; ++step) {
+    if (typ.depth != nullptr) {  // typical acceptance: the walk fills s_acc, D steps skipped below
+      const int best = typical_walk(b, slot, n, D, parent, tokens, alive, node_row, typ, s_acc, s_ok, lane);
+      if (best >= 0) {
+        len = typ.depth[best];
+        target = row_argmax[node_row ? node_row[b * n + best] : b * n + best];
+      }
+    }
+    for (int step = 0; step < D && typ.depth == nullptr; ++step) {
       int found = -1;
       for (int base = 0; base < n; base += 32) {
         const int i = base + lane;
@@ -345,13 +411,28 @@ int propd_verify_commit(int dtype, int B, int n, int D, int kmax, int layers, in
                         const int32_t* draft_tok, const int32_t* seq_slot, int32_t* seq_len, void* kcache,
                         void* vcache, int32_t* acc_node, int32_t* acc_surv, int32_t* acc_len, int32_t* bonus,
                         int32_t* committed, int8_t* ranks, void* stream) {
+  return propd_verify_commit_ex(dtype, B, n, D, kmax, layers, A, dh, Lmax, layer_stride, parent, tokens, alive,
+                                node_row, row_argmax, root, draft_tok, seq_slot, seq_len, kcache, vcache, acc_node,
+                                acc_surv, acc_len, bonus, committed, ranks, nullptr, stream);
+}
+
+int propd_verify_commit_ex(int dtype, int B, int n, int D, int kmax, int layers, int A, int dh, int Lmax,
+                           int64_t layer_stride, const int32_t* parent, const int32_t* tokens, const uint8_t* alive,
+                           const int32_t* node_row, const int32_t* row_argmax, const int32_t* root,
+                           const int32_t* draft_tok, const int32_t* seq_slot, int32_t* seq_len, void* kcache,
+                           void* vcache, int32_t* acc_node, int32_t* acc_surv, int32_t* acc_len, int32_t* bonus,
+                           int32_t* committed, int8_t* ranks, const propd_typical* typical, void* stream) {
   if (B == 0) return 0;
   PROPD_REQUIRE(D >= 1 && D <= MAX_D, "verify_commit: D=%d outside 1..%d", D, MAX_D);
+  PROPD_REQUIRE(typical == nullptr || (n <= 1024 && typical->depth && typical->row_logits && typical->row_stats &&
+                                       typical->root_logits && typical->root_stats),
+                "verify_commit: typical acceptance needs depth, row and root logits + statistics (n <= 1024)");
   return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
     PROPD_REQUIRE((dh * (int)sizeof(T)) % 16 == 0, "verify_commit: dh*sizeof must be a multiple of 16");
     verify_commit_kernel<T><<<B, 256, 0, as_stream(stream)>>>(
         n, D, kmax, layers, A, dh, Lmax, layer_stride, parent, tokens, alive, node_row, row_argmax, root, draft_tok,
-        seq_slot, seq_len, (T*)kcache, (T*)vcache, acc_node, acc_surv, acc_len, bonus, committed, ranks);
+        seq_slot, seq_len, (T*)kcache, (T*)vcache, acc_node, acc_surv, acc_len, bonus, committed, ranks,
+        typical ? *typical : propd_typical{});
     return check_launch("verify_commit");
   });
 }

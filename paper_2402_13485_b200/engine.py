@@ -200,8 +200,10 @@ class DecodeEngine:
         stats = None
         if self.group is None:  # single process: the backend replays the records in the step's batch
             stats = (self._P, self._counts, cfg.acceptance_alpha, self._order_dev, self._lcurve_dev)
+        accept = ((cfg.typical_epsilon, cfg.typical_alpha, cfg.typical_temperature)
+                  if cfg.acceptance == "typical" else None)
         out = self.backend.step_tree(states, tmpl, cfg.draft_topk, prune, trace=self.trace is not None,
-                                     stats=stats) if active else None
+                                     stats=stats, accept=accept) if active else None
         if stats is not None:
             self._order, self._lcurve = out.order, out.lcurve
         else:

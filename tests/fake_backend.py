@@ -39,7 +39,7 @@ class OracleBatchBackend:
             out.append(tok)
         return np.array(out)
 
-    def step_tree(self, states, tmpl, k, prune=None, trace=False, stats=None):
+    def step_tree(self, states, tmpl, k, prune=None, trace=False, stats=None, accept=None):
         D = self.cfg.draft_heads
         B = len(states)
         committed = np.full((B, D + 1), -1, dtype=np.int32)

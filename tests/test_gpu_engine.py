@@ -293,3 +293,28 @@ def test_plant_draft_head_copies_lm_head():
     assert torch.equal(be.w.w_draft[:, 512:1024], be.w.w_lm)
     with pytest.raises(ValueError, match="out of range"):
         be.plant_draft_head(3)
+
+
+@pytest.mark.parametrize("threshold,acceptance", [(0.01, "greedy"), (None, "typical"), (0.02, "typical")])
+def test_probability_prune_and_typical_acceptance_match_oracle(threshold, acceptance):
+    """propd_full with probability-based pruning and/or typical acceptance on the device == the oracle engine
+    with the same criteria (oracle probability_prune / typical_verify): transcripts and per-iteration metrics."""
+    mc = op.TinyCfg(layers=4, hidden=64, heads=4, vocab=256, draft_heads=4, max_positions=160, seed=11)
+    ecfg = op.EngineCfg(mode="propd_full", draft_heads=4, draft_topk=3,
+                        prune=op.PruneCfg(layer=2, topk=24, threshold=threshold), acceptance=acceptance,
+                        typical_epsilon=0.3, typical_alpha=0.5,
+                        scheduler=op.SchedCfg(replan_period=8, size_candidates=(1, 2, 4, 8, 12)))
+    prompts = op.synthetic_prompts(256, 6, 7, 3)
+    clock = dict(c0_base=3.0, c1_base=0.05, noise=0.02, seed=5)
+    ref = op.Engine(op.TinyModel(mc), ecfg, op.Clock(**clock)).run(prompts, 24, batch_size=3)
+    pcfg = EngineConfig(mode="propd_full", draft_heads=4, draft_topk=3,
+                        prune=PruneConfig(layer=2, topk=24, threshold=threshold),
+                        scheduler=SchedulerConfig(replan_period=8, size_candidates=(1, 2, 4, 8, 12)),
+                        acceptance=acceptance, typical_epsilon=0.3, typical_alpha=0.5)
+    for graphs in (False, True):
+        be = tiny_backend(mc, use_graphs=graphs)
+        res = DecodeEngine(be, pcfg, op.Clock(**clock)).run(prompts, 24, batch_size=3)
+        assert res.transcripts == ref["transcripts"]
+        assert [m.to_json() for m in res.metrics] == ref["metrics"]
+    if acceptance == "typical":
+        assert ref["summary"]["mean_accepted"] > 0.3

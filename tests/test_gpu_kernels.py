@@ -498,3 +498,134 @@ def test_phased_layers_match_separate_kernels(rows, live):
     assert (ka - kb).abs().max().item() <= 3e-2 * max(1.0, ka.abs().max().item())
     assert (va - vb).abs().max().item() <= 3e-2 * max(1.0, va.abs().max().item())
     assert be._bar.abs().max().item() == 0 and be._acc.abs().max().item() == 0 and be._acc2.abs().max().item() == 0
+
+
+# --------------------------------------------------------------- probability pruning / typical acceptance
+def test_row_lse_matches_oracle():
+    rng = np.random.default_rng(5)
+    x = (rng.normal(size=(6, 3000)) * 3).astype(np.float32)
+    x[2, :] = 0.0
+    d = torch.from_numpy(x).to(DEV)
+    for temp in (1.0, 0.7):
+        st_ = torch.empty(6, 2, device=DEV, dtype=torch.float64)
+        call("propd_row_lse", 6, None, 3000, 3000, ptr(d), None, temp, ptr(st_), st())
+        lse, H = op.row_lse_entropy(x.astype(np.float64), temp)
+        got = st_.cpu().numpy()
+        assert np.allclose(got[:, 0], lse, rtol=1e-13, atol=1e-12)
+        assert np.allclose(got[:, 1], H, rtol=1e-11, atol=1e-11)
+
+
+@pytest.mark.parametrize("tau", [0.5, 0.02, 1e-4])
+def test_probability_prune_matches_oracle(tau):
+    """Survivor sets of probability-based pruning == oracle probability_prune on the same fp32 early logits."""
+    rng = np.random.default_rng(int(1 / tau))
+    tmpl = TreeTemplate.from_paths(op.grid_candidates(4, 8))
+    n, B, V = len(tmpl), 3, 300
+    Pn = len(tmpl.parent_nodes)
+    tok = rng.integers(0, V, size=(B, n)).astype(np.int32)
+    early = (rng.normal(size=(B, Pn, V)) * 2.5).astype(np.float32)
+    for b in range(B):  # make some candidates likely so deep nodes survive
+        for i in range(n):
+            par = int(tmpl.parent[i])
+            if par >= 0 and rng.random() < 0.5:
+                early[b, tmpl.parent_slot[par], tok[b, i]] += 6.0
+    d_early = torch.from_numpy(early.reshape(B * Pn, V)).to(DEV)
+    est = torch.empty(B * Pn, 2, device=DEV, dtype=torch.float64)
+    call("propd_row_lse", B * Pn, None, V, V, ptr(d_early), None, 1.0, ptr(est), st())
+    member = torch.empty(B * n, device=DEV, dtype=torch.uint8)
+    td = tmpl.device(DEV)
+    d_tok = torch.from_numpy(tok.reshape(-1)).to(DEV)
+    call("propd_early_prob_member", B, n, Pn, V, float(np.log(tau)), ptr(d_early), ptr(est), ptr(td["parent"]),
+         ptr(td["parent_slot"]), ptr(d_tok), ptr(member), st())
+    mem = member.view(B, n).cpu().numpy().astype(bool)
+    for b in range(B):
+        tree = op.Tree(tuple(op.Node(int(tok[b, i]), int(tmpl.parent[i]), int(tmpl.depth[i]), int(tmpl.rank[i]),
+                                     1.0) for i in range(n)), 0)
+        rows = np.zeros((n, V))
+        for i in tmpl.parent_nodes:
+            rows[i] = early[b, tmpl.parent_slot[i]]
+        surv, _ = op.probability_prune(tree, rows, tau)
+        alive = np.zeros(n, dtype=bool)
+        for i in range(n):  # device closure: member and parent alive
+            par = int(tmpl.parent[i])
+            alive[i] = mem[b, i] and (par < 0 or alive[par])
+        assert tuple(np.flatnonzero(alive)) == surv
+
+
+@pytest.mark.parametrize("eps,alpha,temp", [(0.09, 0.3, 1.0), (0.3, 0.5, 0.7), (1e-3, 0.01, 1.0)])
+def test_typical_acceptance_matches_oracle(eps, alpha, temp):
+    """Typical-acceptance walk of verify_commit_ex (accepted path, bonus, committed tokens, KV compaction
+    source slots) == oracle typical_verify on the same fp32 logits, over pruned trees."""
+    rng = np.random.default_rng(int(eps * 1000) + 7)
+    tmpl = TreeTemplate.from_paths(op.grid_candidates(4, 6))
+    n, B, V, D, k = len(tmpl), 4, 200, 4, 6
+    A, dh, layers, Lmax = 2, 16, 2, 64
+    tok = rng.integers(0, V, size=(B, n)).astype(np.int32)
+    alive = np.ones((B, n), dtype=np.uint8)
+    alive[1, 7:] = 0
+    alive[2, 3:] = 0
+    for b in range(B):
+        for i in range(n):
+            par = int(tmpl.parent[i])
+            if par >= 0 and not alive[b, par]:
+                alive[b, i] = 0
+    node_row = -np.ones((B, n), dtype=np.int32)
+    S = 0
+    for b in range(B):
+        for i in range(n):
+            if alive[b, i]:
+                node_row[b, i] = S
+                S += 1
+    row_logits = (rng.normal(size=(S, V)) * 1.5).astype(np.float32)
+    root_logits = (rng.normal(size=(B, V)) * 1.5).astype(np.float32)
+    for b in range(B):  # boost some children so acceptance goes deep
+        root_logits[b, tok[b, 0]] += 5.0
+        for i in range(n):
+            par = int(tmpl.parent[i])
+            if par >= 0 and alive[b, i] and rng.random() < 0.6:
+                row_logits[node_row[b, par], tok[b, i]] += 5.0
+    dl = lambda a: keep(torch.from_numpy(np.ascontiguousarray(a)).to(DEV))  # inline temporaries stay alive
+    d_rows, d_root = dl(row_logits), dl(root_logits)
+    slots = np.arange(B, dtype=np.int32)
+    rst = torch.empty(S, 2, device=DEV, dtype=torch.float64)
+    call("propd_row_lse", S, None, V, V, ptr(d_rows), None, temp, ptr(rst), st())
+    rootst = torch.empty(B, 2, device=DEV, dtype=torch.float64)
+    call("propd_row_lse", B, None, V, V, ptr(d_root), ptr(i32(slots)), temp, ptr(rootst), st())
+    row_argmax = dl(row_logits.argmax(1).astype(np.int32))
+    root = dl(root_logits.argmax(1).astype(np.int32))
+    draft = dl(rng.integers(0, V, size=(B, D, k)).astype(np.int32))
+    seq_len = dl(np.full(B, 10, dtype=np.int32))
+    kc = torch.randn(layers, B, A, Lmax, dh, device=DEV)
+    vc = torch.randn_like(kc)
+    outs = {name: torch.empty(sz, device=DEV, dtype=torch.int32)
+            for name, sz in (("acc_node", B * D), ("acc_surv", B * D), ("acc_len", B), ("bonus", B),
+                             ("committed", B * (D + 1)))}
+    ranks = torch.empty(B, D, device=DEV, dtype=torch.int8)
+    td = tmpl.device(DEV)
+    typ = _lib.Typical(row_logits=ptr(d_rows), ld=V, row_stats=ptr(rst), root_logits=ptr(d_root), root_ld=V,
+                       root_stats=ptr(rootst), log_eps=float(np.log(eps)), log_alpha=float(np.log(alpha)),
+                       temperature=temp, depth=ptr(td["depth"]))
+    call("propd_verify_commit_ex", _lib.F32, B, n, D, k, layers, A, dh, Lmax, B * A * Lmax * dh, ptr(td["parent"]),
+         ptr(dl(tok.reshape(-1))), ptr(dl(alive.reshape(-1))), ptr(dl(node_row.reshape(-1))), ptr(row_argmax),
+         ptr(root), ptr(draft), ptr(i32(slots)), ptr(seq_len), ptr(kc), ptr(vc), ptr(outs["acc_node"]),
+         ptr(outs["acc_surv"]), ptr(outs["acc_len"]), ptr(outs["bonus"]), ptr(outs["committed"]), ptr(ranks), typ,
+         st())
+    torch.cuda.synchronize()
+    got = {k_: v.cpu().numpy() for k_, v in outs.items()}
+    deep = 0
+    for b in range(B):
+        surv = [i for i in range(n) if alive[b, i]]
+        full = op.Tree(tuple(op.Node(int(tok[b, i]), int(tmpl.parent[i]), int(tmpl.depth[i]), int(tmpl.rank[i]),
+                                     1.0) for i in range(n)), 0)
+        vtree = op.restrict(full, surv)
+        acc, bonus = op.typical_verify(vtree, row_logits[[node_row[b, i] for i in surv]], root_logits[b], eps,
+                                       alpha, temp)
+        L = int(got["acc_len"][b])
+        assert L == len(acc)
+        assert list(got["acc_surv"][b * D: b * D + L]) == list(acc)
+        assert list(got["acc_node"][b * D: b * D + L]) == [surv[a] for a in acc]
+        assert int(got["bonus"][b]) == bonus
+        assert list(got["committed"][b * (D + 1): b * (D + 1) + L + 1]) == [vtree.nodes[a].token for a in acc] + [
+            bonus]
+        deep = max(deep, L)
+    assert deep >= 2  # the cases exercise multi-node paths
