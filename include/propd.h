@@ -177,6 +177,29 @@ typedef struct propd_ws_phases {
 } propd_ws_phases;
 int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
                      float* Y, int ldy, int accumulate, int max_split, const propd_ws_phases* phases, void* stream);
+/* Chain of up to 4 dependent weight-streaming projections in ONE persistent
+ * launch (all CTAs co-resident), e.g. W_o -> W_1 -> W_2 -> QKV of the next
+ * layer: the weight tiles of all jobs stream back to back through one ring
+ * while the jobs' X operands become ready at grid barriers.  Per job: Y (+)=
+ * X.W as propd_gemm_ws; pro_mode (PROPD_PRO_LN / _GELU) produces X from
+ * pro_src in a prologue (as propd_ws_phases; pro_cols = K); tail_qkv finishes
+ * the job's QKV accumulator with `tail` (tail_q / cache tables as
+ * propd_ws_phases).  bar: >= 32 zeroed uint32 (left zeroed). */
+typedef struct propd_chain_job {
+  int N, K;
+  const void* X;
+  int ldx;
+  const void* W;
+  int ldw;
+  float* Y;
+  int ldy, accumulate;
+  int pro_mode;
+  float* pro_src;
+  int pro_ld, pro_cols;
+  int tail_qkv;
+} propd_chain_job;
+int propd_gemm_chain(int M, const int32_t* rows_dev, int njobs, const propd_chain_job* jobs,
+                     const propd_ws_phases* tail, uint32_t* bar, void* stream);
 /* acc[M, 3H] fp32 -> qkv bf16 [M, 3H] and K/V rows into the layer cache
  * (slot seq_len[seq_slot[row_seq[m]]] + row_node[m]); acc re-zeroed. */
 int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,

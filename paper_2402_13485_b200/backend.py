@@ -180,7 +180,13 @@ class B200Backend:
         self.ws_phases = self.use_gws and cfg.hidden <= 4096
         if self.ws_phases:
             self._acc2 = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32)
-            self._bar = torch.zeros(4, device=dev, dtype=torch.int32)
+            self._bar = torch.zeros(32, device=dev, dtype=torch.int32)
+        # one persistent launch per layer for W_o -> W_1 -> W_2 -> next QKV
+        # (propd_gemm_chain): parity-tested but measured slower than the
+        # five-launch layer at 1-34 rows (each phase boundary still costs two
+        # grid barriers plus the prologue, which the ring does not cover), so
+        # off by default
+        self.ws_chain = False
         self.device_rows = True  # sync-free post-prune pass when it fits the weight-streaming GEMMs
         self._graphs: dict = {}
         self._templates: dict = {}
@@ -283,6 +289,8 @@ class B200Backend:
         """Blocks l0..l1-1 over the rows of `rt` (backends.py:202-237).  Returns
         the last MLP output not yet added to the residual stream x."""
         if self.use_gws and rt.M <= 128:
+            if self.ws_chain:
+                return self._run_layers_chain(x, rt, l0, l1, mask, n_tmpl, W, pending)
             if self.ws_phases:
                 return self._run_layers_phased(x, rt, l0, l1, mask, n_tmpl, W, pending)
             return self._run_layers_ws(x, rt, l0, l1, mask, n_tmpl, W, pending)
@@ -306,9 +314,10 @@ class B200Backend:
         return pending
 
     # ------------------------------------------------- per-launch timing (bench)
-    def _timed(self, kind: str, launch, M: int = 0, K: int = 0, N: int = 0, acc: bool = False):
+    def _timed(self, kind: str, launch, M: int = 0, K: int = 0, N: int = 0, acc: bool = False, shapes=None):
         """Run `launch` bracketed by CUDA events when the bench's kernel timer
-        is on (kind "attn": K2; "gemm": a projection [M,K] x [K,N])."""
+        is on (kind "attn": K2; "gemm": projections [M,K] x [K,N], one or a
+        chain given as `shapes` = [(K, N, accumulate), ...])."""
         if self.attn_timer is None:
             return launch()
         ev0 = self._timing_event()
@@ -316,7 +325,7 @@ class B200Backend:
         out = launch()
         ev1 = self._timing_event()
         ev1.record()
-        self._events_sink().append((ev0, ev1, self._role, M, kind, K, N, acc))
+        self._events_sink().append((ev0, ev1, self._role, M, kind, shapes or [(K, N, acc)]))
         return out
 
     def _timing_event(self):
@@ -336,13 +345,13 @@ class B200Backend:
             self._pending_events.clear()
             return
         elt = 2 if self.tdtype != self.torch.float32 else 4
-        for e0, e1, role, M, kind, K, N, acc in self._pending_events:
+        for e0, e1, role, M, kind, shapes in self._pending_events:
             kv, rows = keys.get(role, (0, M))
             if kind == "attn":
                 nbytes = kv * 2 * self.H * elt + 2 * rows * self.H * elt
             else:
                 rows = min(rows, M) if M else rows
-                nbytes = K * N * elt + rows * K * elt + rows * N * 4 * (2 if acc else 1)
+                nbytes = sum(K * N * elt + rows * K * elt + rows * N * 4 * (2 if acc else 1) for K, N, acc in shapes)
             self.attn_timer.append({"ms": e0.elapsed_time(e1), "role": role, "kind": kind, "bytes": nbytes})
         self._pending_events.clear()
 
@@ -366,6 +375,53 @@ class B200Backend:
             rt.max_rows, rt.max_keys, ptr(qkv), qkv.shape[1], ptr(self.kcache[l]), ptr(self.vcache[l]),
             ptr(rt.seq_slot), ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx),
             H, ptr(ws), ws_bytes, self.stream()), M)
+
+    def _run_layers_chain(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
+        """Blocks l0..l1-1 as two launches per layer (bf16, <= 128 rows): K2,
+        then one persistent propd_gemm_chain launch W_o -> [LN] W_1 -> [GELU]
+        W_2 -> [LN] QKV(next layer) -> [finish] whose weight stream runs
+        across the phase boundaries.  The pass starts with a 1-job chain for
+        the first QKV."""
+        torch, T, H = self.torch, self.tdtype, self.H
+        self._flush(x, pending)
+        M = rt.M
+        ws = self._workspace(M, rt.B)
+        acc1, acc2, live, bar = self._acc, self._acc2, ptr(rt.live), ptr(self._bar)
+        h = torch.empty(M, H, device=self.device, dtype=T)
+        ctx = torch.empty(M, H, device=self.device, dtype=T)
+        qkv = torch.empty(M, 3 * H, device=self.device, dtype=T)
+        g = torch.empty(M, 4 * H, device=self.device, dtype=T)
+        J = _lib.ChainJob
+
+        def qkv_job(l):
+            return J(N=3 * H, K=H, X=ptr(h), ldx=H, W=ptr(self.w.wqkv[l]), ldw=3 * H, Y=ptr(acc1), ldy=3 * H,
+                     accumulate=1, pro_mode=_lib.PRO_LN, pro_src=ptr(x), pro_ld=H, pro_cols=H, tail_qkv=1)
+
+        def tail(l):
+            return _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A, dh=self.dh,
+                                 Lmax=self.Lmax, row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node),
+                                 seq_slot=ptr(rt.seq_slot), seq_len=ptr(self.seq_len), kcache=ptr(self.kcache[l]),
+                                 vcache=ptr(self.vcache[l]))
+
+        def chain(jobs, tail_ph, shapes):
+            arr = (J * len(jobs))(*jobs)
+            self._timed("gemm", lambda: self._call("propd_gemm_chain", M, live, len(jobs), arr, tail_ph, bar,
+                                                   self.stream()), M, shapes=shapes)
+
+        chain([qkv_job(l0)], tail(l0), [(H, 3 * H, True)])
+        for l in range(l0, l1):
+            self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
+            jobs = [J(N=H, K=H, X=ptr(ctx), ldx=H, W=ptr(self.w.wo[l]), ldw=H, Y=ptr(x), ldy=H, accumulate=1),
+                    J(N=4 * H, K=H, X=ptr(h), ldx=H, W=ptr(self.w.w1[l]), ldw=4 * H, Y=ptr(acc2), ldy=4 * H,
+                      accumulate=1, pro_mode=_lib.PRO_LN, pro_src=ptr(x), pro_ld=H, pro_cols=H),
+                    J(N=H, K=4 * H, X=ptr(g), ldx=4 * H, W=ptr(self.w.w2[l]), ldw=H, Y=ptr(x), ldy=H, accumulate=1,
+                      pro_mode=_lib.PRO_GELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_cols=4 * H)]
+            shapes = [(H, H, True), (H, 4 * H, True), (4 * H, H, True)]
+            if l + 1 < l1:
+                jobs.append(qkv_job(l + 1))
+                shapes.append((H, 3 * H, True))
+            chain(jobs, tail(l + 1) if l + 1 < l1 else None, shapes)
+        return None
 
     def _run_layers_phased(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
         """Blocks l0..l1-1 as five launches per layer (bf16, <= 128 rows):

@@ -364,9 +364,13 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   (void)ws;
   (void)ws_bytes;
   if (max_rows_per_seq > 4 || W > 4 || (ldqkv % 8) != 0) return 0;
-  // splits per (sequence, head): enough CTAs for ~2 per SM, one cluster each
+  // splits per (sequence, head), one cluster each: enough CTAs for ~2 per SM
+  // at small batch; at large batch (>= one wave of pairs) the split count
+  // whose last wave is fullest (measured: 2 splits at B=32 x 32 heads)
   const int pairs = B * A;
-  int nsplit = (2 * 148 + pairs - 1) / pairs;
+  const int slots = 2 * propd_num_sms();
+  int nsplit = (slots + pairs - 1) / pairs;
+  if (pairs >= slots) nsplit = wave_split(pairs, slots, 2);
   const int cap = (max_keys + dec::CHUNK - 1) / dec::CHUNK;
   if (nsplit > cap) nsplit = cap;
   if (nsplit > dec::MAX_SPLIT) nsplit = dec::MAX_SPLIT;

@@ -554,9 +554,11 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   const int mtiles = (max_rows_per_seq + tc2::BM - 1) / tc2::BM;
   const int ctas = B * A * mtiles;
   const int nblk_max = (max_keys + tc2::BN - 1) / tc2::BN;
-  int nsplit = 148 / ctas;  // one wave of one CTA per SM
+  // key splits per row tile (one cluster each, <= 8): one wave of one CTA
+  // per SM at small batch (more, shorter splits measured slower at B=8-16)
+  int nsplit = propd_num_sms() / ctas;
   if (nsplit > nblk_max) nsplit = nblk_max;
-  if (nsplit > tc2::MAX_SPLIT) nsplit = tc2::MAX_SPLIT;  // the splits of a row tile form one cluster
+  if (nsplit > tc2::MAX_SPLIT) nsplit = tc2::MAX_SPLIT;
   if (nsplit < 1) nsplit = 1;
   (void)ws;
   (void)ws_bytes;

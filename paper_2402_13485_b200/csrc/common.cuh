@@ -96,6 +96,31 @@ __device__ __forceinline__ void trace_record(unsigned long long* buf, unsigned i
   r[7] = kind;
 }
 
+// ---- key-split count of a split-KV attention launch ----
+// units = (sequence, head, row-tile) work items, slots = co-resident CTAs of
+// the kernel on the device.  If every unit can get max_split splits within
+// one wave, take as many as fit (latency-bound small batches); otherwise the
+// split count in [1, max_split] whose grid fills its last wave best
+// (>= 95 %, else the best fill), so large batches do not lose a partial wave.
+inline int wave_split(int units, int slots, int max_split) {
+  if (max_split < 1) return 1;
+  if (units * max_split <= slots) return max_split;
+  if (2 * units <= slots) return slots / units;  // one wave, as many splits as fit
+  int best = 1;
+  double best_eff = 0.0;
+  for (int ns = 1; ns <= max_split; ++ns) {
+    const long long ctas = (long long)units * ns;
+    const long long waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots);
+    if (eff >= 0.95) return ns;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = ns;
+    }
+  }
+  return best;
+}
+
 // ---- element conversion ----
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
