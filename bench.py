@@ -41,7 +41,9 @@ def parse():
     ap.add_argument("--kv", type=int, default=1024, help="KV length (synthetic prompt state)")
     ap.add_argument("--mode", default="propd_full")
     ap.add_argument("--topk", type=int, default=16, help="draft top-k per head (tree grid = 4 x topk)")
-    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--shape", default="7b", choices=["7b", "33b"],
+                    help="Vicuna-7B shape (configs[1-2]) or Vicuna-33B shape (configs[3]: 60 x 6656, 52 heads)")
+    ap.add_argument("--layers", type=int, default=None, help="override the shape's layer count")
     ap.add_argument("--attn-impl", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -54,10 +56,12 @@ def parse():
 
 
 def model_cfg(args):
-    from paper_2402_13485_b200 import TinyTransformerConfig
+    from paper_2402_13485_b200 import VICUNA_7B_SHAPE, VICUNA_33B_SHAPE, TinyTransformerConfig
 
-    return TinyTransformerConfig(layers=args.layers, hidden=4096, heads=32, vocab=32000, draft_heads=4,
-                                 max_positions=args.kv + 5 * (2 * args.steps + args.warmup + 100), seed=0)
+    shape = dict(VICUNA_7B_SHAPE if args.shape == "7b" else VICUNA_33B_SHAPE)
+    if args.layers is not None:
+        shape["layers"] = args.layers
+    return TinyTransformerConfig(**shape, max_positions=args.kv + 5 * (2 * args.steps + args.warmup + 100), seed=0)
 
 
 def engine_cfg(args):
@@ -178,8 +182,8 @@ def ncu_traffic(kind: str, args) -> dict:
 def cpu_reference(args, steps: int, warmup: int):
     """The reference algorithm on host cores: oracle/treedecode_port (the
     fp64 numpy restatement of treedecode, pinned to the real reference by
-    tests/golden) at the 7B width with 2 of 32 layers, tree mode, batch 1;
-    per-step time extrapolated x16 to 32 layers (stated in `sample`)."""
+    tests/golden) at the model width with 2 of its layers, tree mode, batch
+    1; per-step time extrapolated to all layers (stated in `sample`)."""
     import numpy as np
 
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
@@ -188,7 +192,9 @@ def cpu_reference(args, steps: int, warmup: int):
     cores = os.cpu_count()
     Ly = 2
     kv = args.kv
-    cfg = op.TinyCfg(layers=Ly, hidden=4096, heads=32, vocab=32000, draft_heads=4, max_positions=kv + 64, seed=0)
+    full = model_cfg(args)
+    cfg = op.TinyCfg(layers=Ly, hidden=full.hidden, heads=full.heads, vocab=full.vocab, draft_heads=4,
+                     max_positions=kv + 64, seed=0)
     rng = np.random.default_rng(0)
     H, V = cfg.hidden, cfg.vocab
     s = 1.0 / np.sqrt(H)
@@ -217,11 +223,13 @@ def cpu_reference(args, steps: int, warmup: int):
             times.append(dt)
             toks += m["tokens_committed"]
             acc += m["mean_accepted"]
-    per_step = sum(times) / len(times) * (32 / Ly)
-    value = toks / (sum(times) * (32 / Ly))
-    sample = (f"oracle/treedecode_port (fp64 numpy restatement of the reference) at 7B width, {Ly} of 32 layers, "
-              f"batch 1, KV {kv}, {steps} decode steps after {warmup} warm-up; time x{32 // Ly} to 32 layers "
-              f"(extrapolated); OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS')}")
+    Lf = full.layers
+    per_step = sum(times) / len(times) * (Lf / Ly)
+    value = toks / (sum(times) * (Lf / Ly))
+    sample = (f"oracle/treedecode_port (fp64 numpy restatement of the reference) at {args.shape.upper()} width "
+              f"({full.hidden}), {Ly} of {Lf} layers, batch 1, KV {kv}, {steps} decode steps after {warmup} warm-up; "
+              f"time x{Lf // Ly} to {Lf} layers (extrapolated); "
+              f"OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS')}")
     return {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample,
             "ms_per_step": per_step * 1e3, "accepted_len_per_step": acc / max(1, steps)}
 
@@ -301,7 +309,7 @@ def run_b200(args, rank: int, world: int, group):
     tokens = sum(m.tokens_committed for m in metrics)  # engine metrics are already global
     hbm, peak_kind = peaks()
     kernels = {}
-    for kind in ("gemm", "attn"):
+    for kind in ("gemm", "attn", "cublas"):
         rs = [r for r in attn if r.get("kind", "attn") == kind]
         k_ms, k_bytes = sum(r["ms"] for r in rs), sum(r["bytes"] for r in rs)
         kernels[kind] = {"launches": len(rs), "ms_total": k_ms, "bytes": k_bytes,
@@ -457,8 +465,9 @@ def main():
     a = kern["attn"]
     dom = max(kern, key=lambda k: kern[k]["ms_total"])  # the kernel family with the largest share of the step
     d = kern[dom]
-    names = {"gemm": "weight-streaming tcgen05 projections (propd_gemm_ws) + cuBLAS above 128 rows",
-             "attn": "K2 tree-masked verification attention (tc2 tcgen05 / streaming decode kernel)"}
+    names = {"gemm": "weight-streaming tcgen05 projections (propd_gemm_ws, <= 128 rows)",
+             "attn": "K2 tree-masked verification attention (tc2 tcgen05 / streaming decode kernel)",
+             "cublas": "cuBLAS projections (torch.mm, > 128 rows)"}
     traffic = ncu_traffic(dom, args)
     line = {
         "metric": METRIC,
@@ -473,19 +482,22 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights, random KV/prompt state)",
-        "config": {"workload": "configs[1]: Vicuna-7B-shape random-init bf16, ProPD pruned+dynamic tree"
+        "config": {"workload": ("configs[1]: Vicuna-7B-shape" if args.shape == "7b" else "configs[3]: Vicuna-33B-shape")
+                               + " random-init bf16, ProPD pruned+dynamic tree"
                                + (", planted draft head 0 (accepts depth-1 nodes)" if args.planted else ""),
-                   "model": "vicuna-7b-shape (32L, 4096, 32x128, V32000, 4 draft heads)", "layers": args.layers,
+                   "model": ("vicuna-7b-shape (32L, 4096, 32x128, V32000, 4 draft heads)" if args.shape == "7b"
+                             else "vicuna-33b-shape (60L, 6656, 52x128, V32000, 4 draft heads)"),
+                   "layers": model_cfg(args).layers,
                    "batch_per_gpu": args.batch, "global_batch": args.batch * world, "kv": args.kv,
                    "mode": args.mode, "draft_topk": args.topk, "prune": "layer 4, top-K 50",
                    "parallelism": f"dp{world} (sequence-sharded replicas)",
-                   "l2": "inputs larger than L2 (14.8 GB of weights stream every step)"},
+                   "l2": f"inputs larger than L2 ({res['weights_bytes'] / 1e9:.1f} GB of weights stream every step)"},
         "accepted_len_per_step": sum(x.mean_accepted for x in m) / K,
         "tree_size_mean": sum(x.tree_size for x in m) / K,
         "prune_rate_mean": sum(x.prune_rate for x in m) / K,
         "verify_attention_ms_per_step": a["verify_ms_total"] / K,
         "attention_ms_per_step": a["ms_total"] / K,
-        "projection_ms_per_step": kern["gemm"]["ms_total"] / K,
+        "projection_ms_per_step": (kern["gemm"]["ms_total"] + kern["cublas"]["ms_total"]) / K,
         "roofline": roofline_line(dom, names[dom], d, res["in_step"], traffic, K, ms),
         "roofline_by_kernel": {k: {"achieved": v["achieved_gbs"], "frac": v["achieved_gbs"] / v["peak"],
                                    "ms_per_step": v["ms_total"] / K, "launches_per_step": v["launches"] / K,

@@ -301,23 +301,24 @@ class B200Backend:
         ctx = torch.empty(M, H, device=self.device, dtype=T)
         for l in range(l0, l1):
             self._call("propd_add_ln", self.code, M, None, H, ptr(x), ptr(pending), ptr(h), None, None, st)
-            qkv = self._timed("gemm", lambda: torch.mm(h, self.w.wqkv[l]), M, H, 3 * H)
+            qkv = self._timed("cublas", lambda: torch.mm(h, self.w.wqkv[l]), M, H, 3 * H)
             kc, vc = self.kcache[l], self.vcache[l]
             self._call("propd_kv_append", self.code, M, self.A, self.dh, self.Lmax, ptr(qkv), 3 * H,
                        ptr(rt.row_seq), ptr(rt.row_node), ptr(rt.seq_slot), ptr(self.seq_len), ptr(kc), ptr(vc), st)
             self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
-            o = self._timed("gemm", lambda: torch.mm(ctx, self.w.wo[l]), M, H, H)
+            o = self._timed("cublas", lambda: torch.mm(ctx, self.w.wo[l]), M, H, H)
             self._call("propd_add_ln", self.code, M, None, H, ptr(x), ptr(o), ptr(h), None, None, st)
-            g = self._timed("gemm", lambda: torch.mm(h, self.w.w1[l]), M, H, 4 * H)
+            g = self._timed("cublas", lambda: torch.mm(h, self.w.w1[l]), M, H, 4 * H)
             self._call("propd_gelu", self.code, g.numel(), ptr(g), st)
-            pending = self._timed("gemm", lambda: torch.mm(g, self.w.w2[l]), M, 4 * H, H)
+            pending = self._timed("cublas", lambda: torch.mm(g, self.w.w2[l]), M, 4 * H, H)
         return pending
 
     # ------------------------------------------------- per-launch timing (bench)
     def _timed(self, kind: str, launch, M: int = 0, K: int = 0, N: int = 0, acc: bool = False, shapes=None):
         """Run `launch` bracketed by CUDA events when the bench's kernel timer
-        is on (kind "attn": K2; "gemm": projections [M,K] x [K,N], one or a
-        chain given as `shapes` = [(K, N, accumulate), ...])."""
+        is on (kind "attn": K2; "gemm": weight-streaming projections [M,K] x
+        [K,N], one or a chain given as `shapes` = [(K, N, accumulate), ...];
+        "cublas": torch.mm above 128 rows)."""
         if self.attn_timer is None:
             return launch()
         ev0 = self._timing_event()
@@ -491,7 +492,7 @@ class B200Backend:
             out = torch.empty(M, N, device=self.device, dtype=torch.float32)
             self._gemm_ws(M, ptr(live), N, self.H, X, Wt, out, N, 0)
             return out
-        out = self._timed("gemm", lambda: torch.mm(X, Wt), M, self.H, N)
+        out = self._timed("cublas", lambda: torch.mm(X, Wt), M, self.H, N)
         return out if out.dtype == torch.float32 else out.float()
 
     def _flush(self, x, pending):

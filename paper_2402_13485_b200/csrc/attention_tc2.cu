@@ -287,41 +287,57 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       const uint32_t id_s = idesc_bf16(false, BN, 128), id_o = idesc_bf16(true, 128, 128);
       const uint32_t q_addr = smem_u32(smem + SMEM_Q);
-      auto issue_pv = [&](int jj) {
-        const int g = jj & 1, i = jj >> 1, st = jj % VS;
-        const int sb = g * 2 + (i & 1);
-        mbar_wait(&p_full[g], i & 1, 12);
-        mbar_wait(&v_full[st], (jj / VS) & 1, 18);
-        tc_after_sync();
-        const uint32_t p_tmem = tmem + 256 + 64 * sb;  // P (bf16 pairs) over its S buffer
-        const uint32_t v_addr = smem_u32(smem + SMEM_V + st * KV_TILE);
+      // Event loop: S_j = Q K_j^T is issued as soon as K_j has landed and its
+      // S buffer is free (PV_{j-4}, the previous user of the buffer, issued),
+      // O_g += P_j V_j as soon as P_j and V_j are ready; so S runs up to four
+      // blocks ahead and each softmax group finds its next S already computed.
+      // Every barrier is polled in phase order (no phase is ever skipped).
+      int ns = 0, np = 0;
+      uint32_t idle = 0;
+      while (np < nblk) {
+        bool prog = false;
+        if (ns < nblk && ns < np + 4 && mbar_try(&k_full[ns % KS], (ns / KS) & 1)) {
+          const int st = ns % KS;
+          tc_after_sync();
+          const int sb = (ns & 1) * 2 + ((ns >> 1) & 1);
+          const uint32_t k_addr = smem_u32(smem + SMEM_K + st * KV_TILE);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t bd = sw128_desc(v_addr + kk * 2048, KV_HALF, 1024);
-          mma_bf16_ts(tmem + g * 128, p_tmem + 8 * kk, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {  // K = dh 128 in steps of 16
+            const uint64_t ad = sw128_desc(q_addr + (kk >> 2) * HALF + (kk & 3) * 32, 16, 1024);
+            const uint64_t bd = sw128_desc(k_addr + (kk >> 2) * KV_HALF + (kk & 3) * 32, 16, 1024);
+            mma_bf16(tmem + 256 + 64 * sb, ad, bd, id_s, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&s_full[sb]);
+          mma_commit(&k_empty[st]);  // K is only needed by S: release its stage now
+          if (ns < 24) TR2(26 + ns);
+          ++ns;
+          prog = true;
         }
-        if (jj < 24) TR2(98 + jj);
-        mma_commit(&v_empty[st]);
-        mma_commit(&o_done[g]);
-      };
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j % KS;
-        mbar_wait(&k_full[st], (j / KS) & 1, 13);
-        tc_after_sync();
-        const int sb = (j & 1) * 2 + ((j >> 1) & 1);
-        const uint32_t k_addr = smem_u32(smem + SMEM_K + st * KV_TILE);
+        if (np < ns) {
+          const int g = np & 1, i = np >> 1, st = np % VS;
+          if (mbar_try(&p_full[g], i & 1) && mbar_try(&v_full[st], (np / VS) & 1)) {
+            tc_after_sync();
+            const int sb = g * 2 + (i & 1);
+            const uint32_t p_tmem = tmem + 256 + 64 * sb;  // P (bf16 pairs) over its S buffer
+            const uint32_t v_addr = smem_u32(smem + SMEM_V + st * KV_TILE);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // K = dh 128 in steps of 16
-          const uint64_t ad = sw128_desc(q_addr + (kk >> 2) * HALF + (kk & 3) * 32, 16, 1024);
-          const uint64_t bd = sw128_desc(k_addr + (kk >> 2) * KV_HALF + (kk & 3) * 32, 16, 1024);
-          mma_bf16(tmem + 256 + 64 * sb, ad, bd, id_s, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < BN / 16; ++kk) {
+              const uint64_t bd = sw128_desc(v_addr + kk * 2048, KV_HALF, 1024);
+              mma_bf16_ts(tmem + g * 128, p_tmem + 8 * kk, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
+            }
+            if (np < 24) TR2(98 + np);
+            mma_commit(&v_empty[st]);
+            mma_commit(&o_done[g]);
+            ++np;
+            prog = true;
+          }
         }
-        mma_commit(&s_full[sb]);
-        mma_commit(&k_empty[st]);  // K is only needed by S: release its stage now
-        if (j < 24) TR2(26 + j);
-        if (j > 0) issue_pv(j - 1);
+        if (prog) {
+          idle = 0;
+        } else if (++idle > (1u << 28)) {
+          mbar_timeout(12, (uint32_t)np);
+        }
       }
-      issue_pv(nblk - 1);
     }
   } else {
     // ================= softmax warpgroups =================
