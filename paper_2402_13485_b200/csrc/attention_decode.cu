@@ -370,7 +370,7 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   const int pairs = B * A;
   const int slots = 2 * propd_num_sms();
   int nsplit = (slots + pairs - 1) / pairs;
-  if (pairs >= slots) nsplit = wave_split(pairs, slots, 2);
+  if (2 * pairs > slots) nsplit = wave_split(pairs, slots, 2);
   const int cap = (max_keys + dec::CHUNK - 1) / dec::CHUNK;
   if (nsplit > cap) nsplit = cap;
   if (nsplit > dec::MAX_SPLIT) nsplit = dec::MAX_SPLIT;
