@@ -58,8 +58,8 @@ def parse():
 def model_cfg(args):
     from paper_2402_13485_b200 import VICUNA_7B_SHAPE, VICUNA_33B_SHAPE, TinyTransformerConfig
 
-    shape = dict(VICUNA_7B_SHAPE if args.shape == "7b" else VICUNA_33B_SHAPE)
-    if args.layers is not None:
+    shape = dict(VICUNA_7B_SHAPE if getattr(args, "shape", "7b") == "7b" else VICUNA_33B_SHAPE)
+    if getattr(args, "layers", None) is not None:
         shape["layers"] = args.layers
     return TinyTransformerConfig(**shape, max_positions=args.kv + 5 * (2 * args.steps + args.warmup + 100), seed=0)
 

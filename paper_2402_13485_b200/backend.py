@@ -746,11 +746,17 @@ class B200Backend:
             t = torch.from_numpy(host).to(self.device)
             self._keepalive.append(t)
             return t
-        buf = self._slot_static.get(B)
-        if buf is None:
-            buf = self._slot_static[B] = torch.empty(B + 1, device=self.device, dtype=torch.int32)
-        pin = torch.from_numpy(host).pin_memory()
-        buf.copy_(pin, non_blocking=True)
+        ent = self._slot_static.get(B)
+        if ent is None:
+            ent = self._slot_static[B] = [torch.empty(B + 1, device=self.device, dtype=torch.int32),
+                                          torch.empty(B + 1, dtype=torch.int32).pin_memory(), None]
+        buf, pin, last = ent
+        key = host.tobytes()
+        if key != last:  # the active set changed: stage it (graphs read the device buffer)
+            self.torch.cuda.current_stream(self.device).synchronize()  # the pinned buffer may still be in flight
+            pin.numpy()[:] = host
+            buf.copy_(pin, non_blocking=True)
+            ent[2] = key
         return buf
 
     def _run(self, key, fn):
