@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA graphs")
     ap.add_argument("--planted", action="store_true",
                     help="planted acceptance (SURVEY f3): draft head 0 := LM head, so depth-1 nodes are accepted")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend under torchrun (gloo + --same-device: a multi-rank dry run on 1 GPU)")
+    ap.add_argument("--same-device", action="store_true", help="every rank on cuda:0 (multi-rank dry run)")
     ap.add_argument("--sync-rows", action="store_true",
                     help="size the post-prune layers on the host (one mid-step sync) instead of on the device")
     return ap.parse_args()
@@ -235,6 +238,26 @@ def cpu_reference(args, steps: int, warmup: int):
 
 
 # ---------------------------------------------------------------- B200 arm
+def local_device(args):
+    import torch
+
+    return torch.device("cuda", 0 if args.same_device else int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def all_max(value: float, group, dev) -> float:
+    """Max over ranks (identity without a process group); fp64 on the
+    backend's device (NCCL: the GPU, gloo: host)."""
+    if group is None:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+
+    where = dev if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=where)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
 def run_b200(args, rank: int, world: int, group):
     import numpy as np
     import torch
@@ -242,7 +265,7 @@ def run_b200(args, rank: int, world: int, group):
     from paper_2402_13485_b200 import B200Backend, DecodeEngine
     from paper_2402_13485_b200.engine import _Seq
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = local_device(args)
     torch.cuda.set_device(dev)
     cfg = model_cfg(args)
     B = args.batch
@@ -260,12 +283,15 @@ def run_b200(args, rank: int, world: int, group):
         # untimed priming: run until no new CUDA graph has been captured for 6
         # consecutive steps (every tree size / survivor-row bucket seen so far
         # has its graphs)
+        # has its graphs).  Under torchrun the decision is collective (every
+        # rank runs the same number of steps: the steps contain collectives)
         stable, n = 0, 0
         while stable < 6 and n < 48:
             n_graphs = len(be._graphs)
             eng._step(seqs, 10 ** 9)
             n += 1
-            stable = stable + 1 if len(be._graphs) == n_graphs else 0
+            changed = all_max(float(len(be._graphs) != n_graphs), group, dev)
+            stable = stable + 1 if changed == 0.0 else 0
         return n
 
     primed = prime()
@@ -302,10 +328,7 @@ def run_b200(args, rank: int, world: int, group):
     attn = be.attn_timer
     be.attn_timer = None
     in_step = timeline_region(be, eng, seqs, prime, dev)
-    if group is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=group)
-        ms = float(t.item())
+    ms = all_max(ms, group, dev)
     tokens = sum(m.tokens_committed for m in metrics)  # engine metrics are already global
     hbm, peak_kind = peaks()
     kernels = {}
@@ -404,10 +427,7 @@ def run_e2e(args, be, eng, rank, world, group):
     res = eng.run(prompts, max_tokens, batch_size=n_prompts)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    if group is not None:
-        t = torch.tensor([dt], dtype=torch.float64, device=be.device)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX, group=group)
-        dt = float(t.item())
+    dt = all_max(dt, group, be.device)
     toks = sum(len(t) for t in res.transcripts)
     h2d = sum(len(p) for p in prompts) * 4
     return {"value": toks / dt, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / max(1, res.summary.iterations)),
@@ -440,8 +460,8 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_device(args))
+        dist.init_process_group(args.dist_backend)
         group = dist.group.WORLD
     res = run_b200(args, rank, world, group)
     if rank != 0:
