@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA graphs")
+    ap.add_argument("--acceptance", default="greedy", choices=["greedy", "typical"])
+    ap.add_argument("--prune-threshold", type=float, default=None,
+                    help="probability-based pruning (marginal path probability >= threshold) instead of top-K 50")
     ap.add_argument("--planted", action="store_true",
                     help="planted acceptance (SURVEY f3): draft head 0 := LM head, so depth-1 nodes are accepted")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -70,10 +73,12 @@ def model_cfg(args):
 def engine_cfg(args):
     from paper_2402_13485_b200 import EngineConfig, PruneConfig, SchedulerConfig
 
-    prune = PruneConfig(layer=4, topk=50) if args.mode in ("prune_only", "propd_full") else None
+    threshold = getattr(args, "prune_threshold", None)
+    prune = PruneConfig(layer=4, topk=50, threshold=threshold) if args.mode in ("prune_only", "propd_full") else None
     sizes = tuple(s for s in (1, 2, 4, 8, 16, 32, 64) if s <= 4 * args.topk)
     return EngineConfig(mode=args.mode, draft_heads=4, draft_topk=args.topk, prune=prune,
-                        scheduler=SchedulerConfig(replan_period=16, size_candidates=sizes))
+                        scheduler=SchedulerConfig(replan_period=16, size_candidates=sizes),
+                        acceptance=getattr(args, "acceptance", "greedy"))
 
 
 class ClockSampler:
@@ -509,7 +514,10 @@ def main():
                              else "vicuna-33b-shape (60L, 6656, 52x128, V32000, 4 draft heads)"),
                    "layers": model_cfg(args).layers,
                    "batch_per_gpu": args.batch, "global_batch": args.batch * world, "kv": args.kv,
-                   "mode": args.mode, "draft_topk": args.topk, "prune": "layer 4, top-K 50",
+                   "mode": args.mode, "draft_topk": args.topk,
+                   "prune": ("layer 4, top-K 50" if args.prune_threshold is None
+                             else f"layer 4, path probability >= {args.prune_threshold}"),
+                   "acceptance": args.acceptance,
                    "parallelism": f"dp{world} (sequence-sharded replicas)",
                    "l2": f"inputs larger than L2 ({res['weights_bytes'] / 1e9:.1f} GB of weights stream every step)"},
         "accepted_len_per_step": sum(x.mean_accepted for x in m) / K,
