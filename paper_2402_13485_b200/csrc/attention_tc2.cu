@@ -12,10 +12,13 @@
 //     and P V reads its A operand straight from TMEM);
 //   - two softmax warpgroups (A: even blocks, B: odd blocks), each with its
 //     own TMEM accumulator O_g, running max/sum and P buffer, so two blocks
-//     are in softmax at once; the MMA thread interleaves S_j = Q K_j^T
-//     (M=128, N=64) and O_g += P_g V_j (M=128, N=128, K=64);
-//   - the two partial softmax states are merged in-kernel at the end
-//     (same algebra as the split-KV combine).
+//     are in softmax at once; the MMA thread is an event loop that issues
+//     S_j = Q K_j^T (M=128, N=64) as soon as K_j and an S buffer are free
+//     (up to four blocks ahead) and O_g += P_g V_j (M=128, N=128, K=64) as
+//     soon as P_j and V_j are ready;
+//   - the two partial softmax states are merged in-kernel at the end; the key
+//     splits of one (sequence, head, row tile) are one thread-block cluster
+//     and are merged through distributed shared memory (no combine launch).
 // Warp roles (352 threads): warp 0 TMA (K), warp 10 TMA (V), warp 1 TMEM
 // alloc + MMA issue, warps 2-5 group A, warps 6-9 group B.
 #include <unordered_map>
@@ -23,10 +26,6 @@
 #include "tc_common.cuh"
 
 namespace propd {
-
-template <typename T>
-__global__ void attn_combine_kernel(int A, int dh, int nsplit, const float* __restrict__ part_o,
-                                    const float* __restrict__ part_ml, T* __restrict__ out, int ldout);
 
 namespace tc2 {
 using namespace propd::tc;
@@ -57,8 +56,6 @@ struct Args {
   int n_tmpl, W, A, Lmax;
   float scale_log2;
   int split_len, nsplit, mtiles;
-  float* part_o;
-  float* part_ml;
   __nv_bfloat16* out;
   int ldout;
   unsigned long long* trace;  // debug: per-block event timestamps of CTA (0,0,0)
@@ -596,8 +593,6 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   p.split_len = blocks_per_split * tc2::BN;
   p.nsplit = nsplit;
   p.mtiles = mtiles;
-  p.part_o = nullptr;
-  p.part_ml = nullptr;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
   p.trace = g_trace2;
