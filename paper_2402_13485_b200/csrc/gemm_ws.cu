@@ -285,24 +285,38 @@ __global__ void __launch_bounds__(THREADS, 2)
     if (p.trace && threadIdx.x == 64) s_t[1] = gtimer();
     const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
     const int nchunk = (M + 31) >> 5;
+    // Each warp owns a [32 features x 32 tokens] block per chunk (TMEM lane =
+    // feature).  It is transposed through a private shared-memory tile (the
+    // stage ring is idle after the last MMA) so that every thread stores /
+    // reduces 4 consecutive features of one token with one 16-byte operation:
+    // 4x fewer L2 reductions on the split-K tail of every projection.
+    float* tile = reinterpret_cast<float*>(smem) + q4 * (32 * 36);  // [token][36] (16-byte aligned rows)
+    const int tq = lane >> 3, fq = (lane & 7) * 4;                 // read side: token quarter, feature quad
 #pragma unroll 1
     for (int c = 0; c < nchunk; ++c) {
       uint32_t rr[32];
       TMEM_LD32(lane_addr + c * 32, rr);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int t = c * 32 + i;
+      for (int i = 0; i < 32; ++i) tile[i * 36 + lane] = __uint_as_float(rr[i]);
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int tl = it * 4 + tq, t = c * 32 + tl;
         if (t < M) {
-          float* dst = p.Y + (size_t)t * p.ldy + f;
-          const float v = __uint_as_float(rr[i]);
+          const float4 v = *reinterpret_cast<const float4*>(tile + tl * 36 + fq);
+          float* dst = p.Y + (size_t)t * p.ldy + n0 + q4 * 32 + fq;
           if (p.accumulate)
-            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst), "f"(v) : "memory");
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
+                         "f"(v.w)
+                         : "memory");
           else
-            *dst = v;
+            *reinterpret_cast<float4*>(dst) = v;
         }
       }
+      __syncwarp();
     }
+    (void)f;
     if (p.ph.tail_mode != PROPD_TAIL_NONE) {  // every CTA's reduction lands, then the tile rows are finished
       __threadfence();
       epi_sync();
@@ -766,6 +780,9 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
                      float* Y, int ldy, int accumulate, int max_split, const propd_ws_phases* ph, void* stream) {
   PROPD_REQUIRE(M >= 1 && M <= 128, "gemm_ws: M=%d outside 1..128", M);
   PROPD_REQUIRE(N % gws::BF == 0 && K % gws::BK == 0, "gemm_ws: N=%d must be a multiple of 128, K=%d of 64", N, K);
+  PROPD_REQUIRE((ph != nullptr && ph->tail_mode == PROPD_TAIL_NONE && Y == nullptr) ||
+                    (ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0),
+                "gemm_ws: Y must be 16-byte aligned with ldy %% 4 == 0 (vector stores / reductions)");
   const int mp = ((M + 15) / 16) * 16;
   CUtensorMap wm, xm;
   PROPD_REQUIRE(gws::map2d(&wm, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw, 64) &&
