@@ -203,6 +203,7 @@ class B200Backend:
         self.launches = 0  # libpropd kernel launches issued (bench accounting)
         self.attn_timer = None  # list -> per-launch {ms, bytes, role, kind} of K2 / GEMM launches (bench)
         self.timeline = None  # device trace buffer while kernels record per-CTA timelines (bench)
+        self.mark_only = False  # with attn_timer: record only the verify-pass markers
         self._capturing = False
         self._capture_events: list = []
         self._pending_events: list = []
@@ -319,7 +320,7 @@ class B200Backend:
         is on (kind "attn": K2; "gemm": weight-streaming projections [M,K] x
         [K,N], one or a chain given as `shapes` = [(K, N, accumulate), ...];
         "cublas": torch.mm above 128 rows)."""
-        if self.attn_timer is None:
+        if self.attn_timer is None or self.mark_only:
             return launch()
         ev0 = self._timing_event()
         ev0.record()
@@ -328,6 +329,17 @@ class B200Backend:
         ev1.record()
         self._events_sink().append((ev0, ev1, self._role, M, kind, shapes or [(K, N, acc)]))
         return out
+
+    def _mark(self, name: str) -> None:
+        """Marker (an event node when captured) bracketing the verify pass:
+        tree embed .. verify/commit, without draft and bonus.  Recorded in the
+        per-launch timing region and in the marks-only region (`mark_only`:
+        two event nodes per step, the PDL chain otherwise intact)."""
+        if self.attn_timer is None:
+            return
+        ev = self._timing_event()
+        ev.record()
+        self._events_sink().append((ev, None, name, 0, "mark", None))
 
     def _timing_event(self):
         torch = self.torch
@@ -346,7 +358,16 @@ class B200Backend:
             self._pending_events.clear()
             return
         elt = 2 if self.tdtype != self.torch.float32 else 4
+        begin = None
         for e0, e1, role, M, kind, shapes in self._pending_events:
+            if kind == "mark":  # verify-pass markers: K1 .. K5 of the tree pass
+                if role == "verify_begin":
+                    begin = e0
+                elif begin is not None:
+                    self.attn_timer.append({"ms": begin.elapsed_time(e0), "role": "tree", "kind": "verify",
+                                            "bytes": 0})
+                    begin = None
+                continue
             kv, rows = keys.get(role, (0, M))
             if kind == "attn":
                 nbytes = kv * 2 * self.H * elt + 2 * rows * self.H * elt
@@ -765,7 +786,7 @@ class B200Backend:
             return fn()
         # graphs with K2 timing event nodes are kept apart from clean ones
         # (an event node between two kernels also breaks their PDL overlap)
-        key = key + (self.attn_timer is not None, self.timeline is not None)
+        key = key + (self.attn_timer is not None, self.mark_only, self.timeline is not None)
         ent = self._graphs.get(key)
         if ent is None:
             torch = self.torch
@@ -851,6 +872,7 @@ class B200Backend:
         seq_slot = slot_buf[:B]
         o = {}
         o["draft_tok"], _ = self._draft_dev(seq_slot, B, k)
+        self._mark("verify_begin")
         M = B * n
         i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
         o["tokens"], o["positions"] = i32(M), i32(M)
@@ -937,6 +959,7 @@ class B200Backend:
                    ptr(row_argmax), ptr(self.root), ptr(a["draft_tok"]), ptr(seq_slot), ptr(self.seq_len),
                    ptr(self.kcache), ptr(self.vcache), ptr(o["acc_node"]), ptr(o["acc_surv"]), ptr(o["acc_len"]),
                    ptr(o["bonus"]), ptr(o["committed"]), ptr(o["ranks"]), typ, st)
+        self._mark("verify_end")
         self._bonus_program(seq_slot, o["bonus"], B, kb, keep_logits=accept is not None)
         return o
 

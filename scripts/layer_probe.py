@@ -72,7 +72,7 @@ def run(skip):
 floor = 402653184 / 6543.1e9 * 1e6
 print(f"rows {n}, kv {args.kv}: weight floor {floor:.1f} us/layer")
 if "--unfused" in sys.argv:
-    be.ws_phases = be.ws_chain = False
+    be.ws_phases = False
 for label, skip in [("full layer", set()), ("no attention", {"propd_tree_attention"}),
                     ("no add_ln", {"propd_add_ln"}), ("no finish", {"propd_qkv_finish", "propd_gelu_finish"}),
                     ("GEMMs only", {"propd_tree_attention", "propd_add_ln", "propd_qkv_finish", "propd_gelu_finish"})]:
