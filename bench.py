@@ -136,12 +136,33 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def tensor_peak():
+    """Dense bf16 TFLOP/s for kernels timed inside a long step (sustained),
+    and the burst figure beside it."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return (float(p["bf16_tflops_sustained"]), float(p["bf16_tflops"]),
+                "measured sustained (MEASURED_PEAKS.json bf16_tflops_sustained; burst beside it)")
+    except Exception:
+        return 1800.0, 1800.0, "fallback (B200_PROFILING.md)"
+
+
 def roofline_line(dom: str, name: str, d: dict, ts: dict, traffic: dict, K: int, ms: float) -> dict:
     """Roofline of the dominant kernel family.  achieved = its algorithmic
     bytes per step / its busy device time per step inside the PDL-chained
     step (per-CTA globaltimer records, one traced step).  CUDA events around
     each launch (the event-bracketed region) serialise the chained launches
     and add each launch's ramp, so they are reported beside it."""
+    tpk, tburst, tpk_kind = tensor_peak()
+    if d.get("flops", 0) / (tpk * 1e12) > d["bytes"] / (d["peak"] * 1e9) and d["ms_total"] > 0:
+        # compute-bound family (cuBLAS at hundreds of rows): the tensor roofline
+        ach = d["flops"] / (d["ms_total"] * 1e-3) / 1e12
+        return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": tpk, "unit": "TFLOP/s",
+                "frac": ach / tpk, "burst_peak": tburst, "burst_frac": ach / tburst,
+                "traffic": traffic.get("bytes_per_launch"), "peak_kind": tpk_kind,
+                "launches_per_step": d["launches"] / K, "avg_launch_us": d["avg_launch_us"],
+                "share_of_step": d["ms_total"] / ms, "timer": "CUDA events per launch (timing region)"}
     ev = {"events_achieved": d["achieved_gbs"], "events_frac": d["achieved_gbs"] / d["peak"],
           "events_avg_launch_us": d["avg_launch_us"]}
     busy = ts.get(dom, {}).get("busy_ms")
@@ -350,7 +371,8 @@ def run_b200(args, rank: int, world: int, group):
     for kind in ("gemm", "attn", "cublas"):
         rs = [r for r in attn if r.get("kind", "attn") == kind]
         k_ms, k_bytes = sum(r["ms"] for r in rs), sum(r["bytes"] for r in rs)
-        kernels[kind] = {"launches": len(rs), "ms_total": k_ms, "bytes": k_bytes,
+        k_flops = sum(r.get("flops", 0) for r in rs)
+        kernels[kind] = {"launches": len(rs), "ms_total": k_ms, "bytes": k_bytes, "flops": k_flops,
                          "achieved_gbs": k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0,
                          "avg_launch_us": k_ms / max(1, len(rs)) * 1e3, "peak": hbm, "peak_kind": peak_kind}
     kernels["attn"]["verify_ms_total"] = sum(r["ms"] for r in attn
@@ -541,6 +563,7 @@ def main():
         "projection_ms_per_step": (kern["gemm"]["ms_total"] + kern["cublas"]["ms_total"]) / K,
         "roofline": roofline_line(dom, names[dom], d, res["in_step"], traffic, K, ms),
         "roofline_by_kernel": {k: {"achieved": v["achieved_gbs"], "frac": v["achieved_gbs"] / v["peak"],
+                                   "tflops": (v["flops"] / (v["ms_total"] * 1e-3) / 1e12) if v["ms_total"] > 0 else 0.0,
                                    "ms_per_step": v["ms_total"] / K, "launches_per_step": v["launches"] / K,
                                    "avg_launch_us": v["avg_launch_us"]} for k, v in kern.items()},
         "in_step": in_step_view(res["in_step"], kern, K),

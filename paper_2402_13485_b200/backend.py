@@ -369,12 +369,15 @@ class B200Backend:
                     begin = None
                 continue
             kv, rows = keys.get(role, (0, M))
+            flops = 0
             if kind == "attn":
                 nbytes = kv * 2 * self.H * elt + 2 * rows * self.H * elt
             else:
                 rows = min(rows, M) if M else rows
                 nbytes = sum(K * N * elt + rows * K * elt + rows * N * 4 * (2 if acc else 1) for K, N, acc in shapes)
-            self.attn_timer.append({"ms": e0.elapsed_time(e1), "role": role, "kind": kind, "bytes": nbytes})
+                flops = sum(2 * rows * K * N for K, N, _ in shapes)
+            self.attn_timer.append({"ms": e0.elapsed_time(e1), "role": role, "kind": kind, "bytes": nbytes,
+                                    "flops": flops})
         self._pending_events.clear()
 
     def _gemm_ws(self, M, live, N, K, X, W, Y, ldy, acc: int, phases=None) -> None:
