@@ -391,28 +391,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       mx *= scale;
-      if (i > 0) {  // this group's previous PV finished: P_g free, O_g stable
-        mbar_wait(&o_done[g], (i - 1) & 1, 15);
-        tc_after_sync();
-      }
       float corr = 1.f;
       const bool grow = mx > m_ref + 8.f;
       if (grow) {
         corr = ex2(m_ref - mx);
         l_sum *= corr;
         m_ref = mx;
-      }
-      if (i > 0 && __any_sync(0xffffffffu, grow)) {  // warp-collective O_g rescale
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t rr[32];
-          TMEM_LD32(o_addr + c * 32, rr);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 32; ++k) rr[k] = __float_as_uint(__uint_as_float(rr[k]) * corr);
-          TMEM_ST32(o_addr + c * 32, rr);
-        }
-        tmem_wait_st();
       }
       const float mneg = m_ref == -INFINITY ? 0.f : -m_ref;
       float ls8[8];
@@ -427,7 +411,25 @@ __global__ void __launch_bounds__(THREADS, 1)
         __nv_bfloat162 v2 = __floats2bfloat162_rn(pp.x, pp.y);
         pk[k2] = *reinterpret_cast<uint32_t*>(&v2);
       }
-      TMEM_ST32(lane_addr + 256 + 64 * sb, pk);
+      TMEM_ST32(lane_addr + 256 + 64 * sb, pk);  // P_i goes to its own S buffer: no conflict with PV_{i-1}
+      // Only now wait for this group's previous PV (it overlapped the exp
+      // work above): O_g must be stable before a rescale, and the phase of
+      // every PV is observed in order.
+      if (i > 0) {
+        mbar_wait(&o_done[g], (i - 1) & 1, 15);
+        tc_after_sync();
+      }
+      if (i > 0 && __any_sync(0xffffffffu, grow)) {  // warp-collective O_g rescale
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t rr[32];
+          TMEM_LD32(o_addr + c * 32, rr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) rr[k] = __float_as_uint(__uint_as_float(rr[k]) * corr);
+          TMEM_ST32(o_addr + c * 32, rr);
+        }
+      }
       tmem_wait_st();
       l_sum += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
       tc_before_sync();
