@@ -23,8 +23,8 @@ namespace propd {
 namespace dec {
 using namespace propd::tc;
 
-constexpr int DH = 128, THREADS = 128, KB = 8;  // keys per half-warp batch
 constexpr int CHUNK = 64, RING = 3, MAX_SPLIT = 8;
+constexpr int DH = 128, NW = 8, THREADS = 32 * NW, KB = CHUNK / (2 * NW);  // keys per half-warp batch
 
 struct Args {
   const __nv_bfloat16* qkv;
@@ -89,8 +89,8 @@ template <int ROWS>
 struct Smem {
   __nv_bfloat16 k[RING][CHUNK * DH];
   __nv_bfloat16 v[RING][CHUNK * DH];
-  float red_m[4][ROWS], red_l[4][ROWS];
-  float red_o[4][ROWS][DH];
+  float red_m[NW][ROWS], red_l[NW][ROWS];
+  float red_o[NW][ROWS][DH];
   float part_m[ROWS], part_l[ROWS];  // this split's merged state (read by the cluster)
   float part_o[ROWS][DH];
   uint64_t full[RING];
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
   auto issue = [&](int c) {
     const int st = c % RING;
     const int key0 = k_begin + c * CHUNK;
-    const int nk = min(CHUNK, p.Lmax - key0);  // whole chunk unless the tile ends
+    const int nk = min(CHUNK, k_end - key0);  // the split's last chunk loads only its own keys
     const uint32_t bytes = (uint32_t)nk * DH * 2;
     mbar_expect_tx(&sm.full[st], 2 * bytes);
     bulk_load(sm.k[st], p.kc + (tile + key0) * DH, bytes, &sm.full[st]);
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
   for (int c = 0; c < nchunk; ++c) {
     const int st = c % RING;
     mbar_wait(&sm.full[st], (c / RING) & 1, 41);
-    // warp w: keys [16w, 16w + 16) of the chunk, half-warp h: 8 of them
+    // warp w: keys [2KB w, 2KB (w + 1)) of the chunk, half-warp h: KB of them
     const int kc0 = warp * 2 * KB + half * KB;
     uint4 kr[KB], vr[KB];
 #pragma unroll
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
     __syncthreads();  // every warp is done with stage st
     if (threadIdx.x == 0 && c + RING < nchunk) issue(c + RING);
   }
-  // merge the two half-warps (same dims, different keys), then the 4 warps
+  // merge the two half-warps (same dims, different keys), then the warps
 #pragma unroll
   for (int r = 0; r < ROWS; ++r)
 #pragma unroll
@@ -244,17 +244,18 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
     }
   }
   __syncthreads();
+  const unsigned long long t_loop = p.tl ? gtimer() : 0ull;
   const int nsplit = (int)cluster_nrank();
   for (int idx = threadIdx.x; idx < ROWS * DH; idx += THREADS) {
     const int r = idx / DH, d = idx - r * DH;
     if (r >= nrows) continue;
     float mx = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) mx = fmaxf(mx, sm.red_m[w][r]);
+    for (int w = 0; w < NW; ++w) mx = fmaxf(mx, sm.red_m[w][r]);
     float lsum = 0.f, acc = 0.f;
     if (mx != -INFINITY) {
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
+      for (int w = 0; w < NW; ++w) {
         const float f = sm.red_m[w][r] == -INFINITY ? 0.f : ex2(sm.red_m[w][r] - mx);
         lsum += sm.red_l[w][r] * f;
         acc += sm.red_o[w][r][d] * f;
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
     }
     cluster_sync_all();  // peers may still read this CTA's state
   }
-  if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait, 2);
+  if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_loop, 2);
 }
 
 template <int ROWS>
@@ -376,7 +377,9 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   if (nsplit > dec::MAX_SPLIT) nsplit = dec::MAX_SPLIT;
   if (nsplit < 1) nsplit = 1;
   int split_len = (max_keys + nsplit - 1) / nsplit;
-  split_len = ((split_len + dec::CHUNK - 1) / dec::CHUNK) * dec::CHUNK;
+  // any multiple of 16 keys: chunks start at the split's first key and the
+  // last one loads only the keys left, so splits stay balanced across SMs
+  split_len = ((split_len + 15) / 16) * 16;
   nsplit = (max_keys + split_len - 1) / split_len;
   dec::Args p{};
   p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);

@@ -27,6 +27,7 @@ ap.add_argument("--kv", type=int, default=1024)
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--show", type=int, default=2, help="layers to print")
 ap.add_argument("--unfused", action="store_true")
+ap.add_argument("--per-cta", action="store_true", help="attention: per-CTA phase percentiles")
 ap.add_argument("--chain", action="store_true", help="one persistent chain launch per layer (propd_gemm_chain)")
 args = ap.parse_args()
 
@@ -71,5 +72,8 @@ for tg in tags:
     print(f"{tg:4d} {len(r):5d} {us(r[:, 3].min()):8.1f} {us(r[:, 3].max()):8.1f} {us(r[:, 4].max()):8.1f} "
           f"{us(r[:, 5].max()):8.1f} {us(r[:, 6].min()):8.1f} {us(r[:, 6].max()):8.1f} {gap:6.1f}")
     prev_exit = us(r[:, 6].max())
+    if args.per_cta and r[0, 7] == 2:  # attention: per-CTA wait -> loop end -> exit
+        q = lambda v: " ".join(f"{x:5.2f}" for x in np.percentile(v / 1e3, [0, 50, 90, 100]))
+        print(f"      per-CTA wait->main [p0 p50 p90 max] {q(r[:, 5] - r[:, 4])}   main->exit {q(r[:, 6] - r[:, 5])}")
 span = (rec[:, 6].max() - t_ref) / 1e3
 print(f"span {span:.1f} us for {args.layers} layers = {span / args.layers:.1f} us/layer")
