@@ -231,6 +231,10 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
                        const int32_t* seq_len, const int32_t* row_off, const int32_t* row_node, const uint64_t* mask,
                        int n_tmpl, int W, void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st,
                        bool* handled);
+int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
+                       int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
+                       const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
+                       void* out, int ldout, cudaStream_t st, bool force, bool* handled);
 static int g_tc_version = 2;  // auto-dispatch target for multi-row bf16 dh=128 launches
 
 int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
@@ -268,6 +272,13 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
                                   workspace_bytes, st, &handled);
     if (e || handled) return e;
     PROPD_REQUIRE(impl != 3, "tree_attention: decode kernel cannot serve this shape");
+  }
+  if (impl == 5 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {  // <= 32 rows: transposed kernel
+    bool handled = false;
+    int e = attention_tct_bf16(B, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
+                               seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, st, impl == 5, &handled);
+    if (e || handled) return e;
+    PROPD_REQUIRE(impl != 5, "tree_attention: transposed tcgen05 kernel serves <= 32 rows per sequence");
   }
   if (impl == 4 || (impl == 0 && dtype == PROPD_BF16 && dh == 128 && g_tc_version == 2)) {
     bool handled = false;

@@ -126,10 +126,17 @@ def torch_tree_attention(q, kc, vc, slots, lens, row_off, row_node, mask_bool, A
     ("bf16", 128, 4, [512, 77, 1000], "grid43", 0),
     ("bf16", 128, 3, [4096, 200], "full44", 0),
     ("bf16", 128, 2, [130, 2000, 7, 900], "chain", 0),
+    # transposed kernel (<= 32 rows per sequence): cluster splits at B=1, ragged lengths, 32-node tree
+    ("bf16", 128, 4, [512, 77, 1000], "grid43", 5),
+    ("bf16", 128, 2, [130, 2000, 7, 900], "chain", 5),
+    ("bf16", 128, 32, [1030], "grid43", 5),
+    ("bf16", 128, 8, [1, 64, 4096], "grid48", 5),
+    ("bf16", 128, 32, [3000], "grid48", 0),
 ])
 def test_tree_attention_vs_torch(dtype, dh, A, lens, paths, impl):
     rng = np.random.default_rng(dh * 7 + len(lens))
-    universe = {"grid43": op.grid_candidates(4, 3), "full33": op.complete_tree_paths(3, 3),
+    universe = {"grid43": op.grid_candidates(4, 3), "grid48": op.grid_candidates(4, 8),
+                "full33": op.complete_tree_paths(3, 3),
                 "full44": op.complete_tree_paths(4, 4)[:200], "chain": [(1,) * d for d in range(1, 5)]}[paths]
     tmpl = TreeTemplate.from_paths(universe)
     n = len(tmpl)
@@ -188,6 +195,42 @@ def test_decode_attention_cluster_combine(A, lens, rows):
     err = (out.float() - ref).abs().max().item()
     assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
     del rng
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_tree_attention_tct_pruned_rows(causal):
+    """Transposed kernel (impl 5) on a compacted survivor subset of a 32-node tree (rows = surviving nodes,
+    row_node = their template indices), with the tree mask or causal (mask = NULL)."""
+    dh, A = 128, 4
+    H = A * dh
+    lens = [700, 3, 1500]
+    B = len(lens)
+    tmpl = TreeTemplate.from_paths(op.grid_candidates(4, 8))
+    n = len(tmpl)
+    keep = [[0, 1, 2, 8, 9, 20, 31], [0, 5], list(range(0, 32, 3))]
+    Lmax = max(lens) + n + 8
+    kc = torch.randn(B, A, Lmax, dh, device=DEV).bfloat16()
+    vc = torch.randn(B, A, Lmax, dh, device=DEV).bfloat16()
+    row_off = [0]
+    for k in keep:
+        row_off.append(row_off[-1] + len(k))
+    row_node = [i for k in keep for i in k]
+    M = row_off[-1]
+    qkv = torch.randn(M, 3 * H, device=DEV).bfloat16()
+    slots = [2, 0, 1]
+    seq_len = torch.zeros(B, dtype=torch.int32, device=DEV)
+    for b, s_ in enumerate(slots):
+        seq_len[s_] = lens[b]
+    mask = None if causal else torch.from_numpy(tmpl.mask_bits.view(np.int64)).to(DEV)
+    out = torch.zeros(M, H, device=DEV, dtype=torch.bfloat16)
+    call("propd_tree_attention", _lib.BF16, 5, B, M, A, dh, Lmax, B, max(len(k) for k in keep), max(lens) + n,
+         ptr(qkv), 3 * H, ptr(kc), ptr(vc), ptr(i32(slots)), ptr(seq_len), ptr(i32(row_off)), ptr(i32(row_node)),
+         None if causal else ptr(mask), n, tmpl.words, ptr(out), H, None, 0, st())
+    torch.cuda.synchronize()
+    ref = torch_tree_attention(qkv[:, :H], kc, vc, slots, lens, row_off, row_node, None if causal else tmpl.mask(),
+                               A, dh)
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
 
 
 def test_tree_attention_causal_and_pruned_rows():
