@@ -273,12 +273,12 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
     if (e || handled) return e;
     PROPD_REQUIRE(impl != 3, "tree_attention: decode kernel cannot serve this shape");
   }
-  if (impl == 5 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {  // <= 32 rows: transposed kernel
+  if (impl == 5 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {  // <= 64 rows: transposed kernel
     bool handled = false;
     int e = attention_tct_bf16(B, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
                                seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, st, impl == 5, &handled);
     if (e || handled) return e;
-    PROPD_REQUIRE(impl != 5, "tree_attention: transposed tcgen05 kernel serves <= 32 rows per sequence");
+    PROPD_REQUIRE(impl != 5, "tree_attention: transposed tcgen05 kernel serves <= 64 rows per sequence");
   }
   if (impl == 4 || (impl == 0 && dtype == PROPD_BF16 && dh == 128 && g_tc_version == 2)) {
     bool handled = false;

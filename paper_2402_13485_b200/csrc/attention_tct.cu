@@ -1,4 +1,4 @@
-// K2 for trees of <= 32 rows per (sequence, head): the transposed tcgen05
+// K2 for trees of <= 64 rows per (sequence, head): the transposed tcgen05
 // kernel ("tcT").  Reference semantics as attention_tc2.cu (backends.py:216-233).
 //
 // Why transposed: with M = 128 query rows per MMA (tc2) a pruned tree of ~20
@@ -13,15 +13,16 @@
 //   O^T  += V_j^T P_j^T (M = 128 dims, N = 32 rows, K = 128 keys; A = V_j
 //                        MN-major straight from the same TMA tile, B = P^T
 //                        K-major written by the softmax warps)
-// so each MMA is 4x smaller (N = 32), Q is 8 KB, and the softmax of a block
-// is spread over four warps (TMEM lane = key: warp q owns keys 32q..32q+31 of
-// the block, 32 row values per thread).  Row maxima / sums are lane
+// so each MMA is 4x (2x at 64 rows) smaller, Q is 8-16 KB, and the softmax of
+// a block is spread over four warps (TMEM lane = key: warp q owns keys
+// 32q..32q+31 of the block, 32 row values per thread and 32-row half).  Row maxima / sums are lane
 // transposes: a 5-step butterfly leaves lane l with row l's maximum over the
 // warp's keys, one named barrier merges the four warps.  l stays as per-thread
 // partial sums (one per row) until the end.
 //
-// Warp roles (224 threads): warp 0 TMA K, warp 6 TMA V, warp 1 TMEM alloc +
-// MMA issue (event loop), warps 2-5 softmax.  Key splits of one (sequence,
+// Warp roles: warp 0 TMA K, warp 1 TMEM alloc + MMA issue (event loop), one
+// softmax warpgroup per 32-row half (warps 2-5, 6-9), then the V TMA warp
+// (224 threads at 32 rows, 352 at 64).  Key splits of one (sequence,
 // head) form a thread-block cluster merged through distributed shared memory.
 #include <unordered_map>
 
@@ -31,39 +32,44 @@ namespace propd {
 namespace tct {
 using namespace propd::tc;
 
-constexpr int NR = 32;    // query rows per tile (N of both MMAs)
 constexpr int BK = 128;   // keys per block (M of S^T)
 constexpr int DH = 128;
 constexpr int KS = 3, VS = 3;  // K / V ring stages (32 KB each)
 constexpr int NSB = 4;         // S^T buffers in TMEM (S runs up to NSB blocks ahead of PV)
-constexpr int NPB = 2;         // P^T buffers in shared memory
-constexpr int THREADS = 224;
 constexpr int MAX_SPLIT = 8;
-
 constexpr int KV_HALF = BK * 128;     // [128 keys x 64 dims] SW128 = 16 KB
 constexpr int KV_TILE = 2 * KV_HALF;  // 32 KB
-constexpr int Q_HALF = NR * 128;      // [32 rows x 64 dims] = 4 KB
-constexpr int P_HALF = NR * 128;      // [32 rows x 64 keys] = 4 KB
-constexpr int P_TILE = 2 * P_HALF;
 
-constexpr int SMEM_K = 0;
-constexpr int SMEM_V = SMEM_K + KS * KV_TILE;
-constexpr int SMEM_Q = SMEM_V + VS * KV_TILE;
-constexpr int SMEM_P = SMEM_Q + 2 * Q_HALF;
-constexpr int SMEM_RED = SMEM_P + NPB * P_TILE;    // [2][4][32] floats: block-max exchange (double buffered)
-constexpr int SMEM_LRED = SMEM_RED + 2 * 4 * 32 * 4;  // [4][32] floats: final row sums
-constexpr int SMEM_MASK = SMEM_LRED + 4 * 32 * 4;  // [32 rows][4] u64 tree visibility words
-constexpr int SMEM_BAR = SMEM_MASK + NR * 4 * 8;
-constexpr int SMEM_TOTAL = SMEM_BAR + 256;
-// cluster combine state parks in the idle K ring after the main loop
-constexpr int SMEM_PO = SMEM_K;               // [32 rows][128] fp32
-constexpr int SMEM_PM = SMEM_PO + NR * DH * 4;  // [32] m (log2 domain)
-constexpr int SMEM_PL = SMEM_PM + NR * 4;       // [32] l
-static_assert(SMEM_PL + NR * 4 <= SMEM_V, "partial state must fit in the K ring");
-static_assert(SMEM_TOTAL <= 227 * 1024, "shared memory");
-
-// TMEM: O^T [0, 32), S^T buffers 32 + 32 * b
-constexpr uint32_t TMEM_COLS = 256, O_COL = 0, S_COL = 32;
+// Shared-memory / TMEM plan for NR query rows per tile (32 or 64).
+template <int NR_>
+struct Cfg {
+  static constexpr int NR = NR_;
+  static constexpr int NH = NR / 32;             // softmax warpgroups, one per 32-row half
+  static constexpr int NPB = NR == 32 ? 2 : 1;   // P^T buffers (one at 64 rows: shared memory)
+  static constexpr int VWARP = 2 + 4 * NH;       // V producer warp (after the softmax warps)
+  static constexpr int THREADS = 32 * (VWARP + 1);
+  static constexpr int Q_HALF = NR * 128;        // [NR rows x 64 dims]
+  static constexpr int P_HALF = NR * 128;        // [NR rows x 64 keys]
+  static constexpr int P_TILE = 2 * P_HALF;
+  static constexpr int SMEM_K = 0;
+  static constexpr int SMEM_V = SMEM_K + KS * KV_TILE;
+  static constexpr int SMEM_Q = SMEM_V + VS * KV_TILE;
+  static constexpr int SMEM_P = SMEM_Q + 2 * Q_HALF;
+  // [NH][2][4 warps][32] floats: block-max exchange per group (double
+  // buffered; the final row sums reuse the buffer the last block left idle)
+  static constexpr int SMEM_RED = SMEM_P + NPB * P_TILE;
+  static constexpr int SMEM_NODE = SMEM_RED + NH * 2 * 4 * 32 * 4;  // [NR] template node of each row
+  static constexpr int SMEM_BAR = SMEM_NODE + NR * 4;
+  static constexpr int SMEM_TOTAL = SMEM_BAR + 192;
+  // cluster combine state parks in the idle K ring after the main loop
+  static constexpr int SMEM_PO = SMEM_K;              // [NR rows][128] fp32
+  static constexpr int SMEM_PM = SMEM_PO + NR * DH * 4;  // [NR] m (log2 domain)
+  static constexpr int SMEM_PL = SMEM_PM + NR * 4;       // [NR] l
+  static_assert(SMEM_PL + NR * 4 <= SMEM_V, "partial state must fit in the K ring");
+  static_assert(SMEM_TOTAL <= 227 * 1024, "shared memory");
+  // TMEM: O^T [0, NR), S^T buffers NR + NR * b
+  static constexpr uint32_t O_COL = 0, S_COL = NR, TMEM_COLS = NR == 32 ? 256 : 512;
+};
 
 struct Args {
   const __nv_bfloat16* qkv;
@@ -113,6 +119,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 // Merge the key splits of one (sequence, head): rank q finishes rows
 // [q * ceil(nrows / splits), ...) from every rank's parked (O, m, l).
+template <class C>
 __device__ __forceinline__ void cluster_combine(const uint8_t* smem, int nsplit, int nrows, int r0, int a,
                                                 __nv_bfloat16* out, int ldout) {
   cl_sync();
@@ -123,9 +130,9 @@ __device__ __forceinline__ void cluster_combine(const uint8_t* smem, int nsplit,
 #pragma unroll
   for (int q = 0; q < MAX_SPLIT; ++q) {
     const uint32_t rk = q < nsplit ? q : 0;
-    po[q] = cl_map(smem_u32(smem + SMEM_PO), rk);
-    pm[q] = cl_map(smem_u32(smem + SMEM_PM), rk);
-    pl[q] = cl_map(smem_u32(smem + SMEM_PL), rk);
+    po[q] = cl_map(smem_u32(smem + C::SMEM_PO), rk);
+    pm[q] = cl_map(smem_u32(smem + C::SMEM_PM), rk);
+    pl[q] = cl_map(smem_u32(smem + C::SMEM_PL), rk);
   }
   for (int e = threadIdx.x; e < (re - rb) * (DH / 4); e += blockDim.x) {
     const int r = rb + e / (DH / 4), d4 = (e % (DH / 4)) * 4;
@@ -158,10 +165,29 @@ __device__ __forceinline__ void cluster_combine(const uint8_t* smem, int nsplit,
   cl_sync();  // peers may still be reading this CTA's state
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+// Butterfly transpose-reduce of 32 per-lane values: lane l ends with the
+// reduction over the warp's 32 lanes of value index l (in t[0]).
+template <bool MAX>
+__device__ __forceinline__ void lane_transpose_reduce(float (&t)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = up ? t[i] : t[i + o];
+      const float keep = up ? t[i + o] : t[i];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, o);
+      t[i] = MAX ? fmaxf(keep, recv) : keep + recv;
+    }
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
     attn_tct_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, Args p) {
+  constexpr int NR = C::NR, NH = C::NH, NPB = C::NPB;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SMEM_BAR);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
   uint64_t* k_full = bars;
   uint64_t* k_empty = k_full + KS;
   uint64_t* v_full = k_empty + KS;
@@ -170,9 +196,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* p_full = s_full + NSB;   // [NPB]
   uint64_t* pv_done = p_full + NPB;  // [NPB]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + NPB);
-  float* red = reinterpret_cast<float*>(smem + SMEM_RED);
-  float* lred = reinterpret_cast<float*>(smem + SMEM_LRED);
-  uint64_t* rmask = reinterpret_cast<uint64_t*>(smem + SMEM_MASK);
+  float* red = reinterpret_cast<float*>(smem + C::SMEM_RED);
+  int* rnode = reinterpret_cast<int*>(smem + C::SMEM_NODE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned long long t_entry = p.tl ? gtimer() : 0ull;
@@ -191,15 +216,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (nblk == 0) {  // no keys in this split: an empty state for the cluster combine
     if (p.nsplit > 1) {
       for (int r = threadIdx.x; r < NR; r += blockDim.x) {
-        reinterpret_cast<float*>(smem + SMEM_PM)[r] = -INFINITY;
-        reinterpret_cast<float*>(smem + SMEM_PL)[r] = 0.f;
+        reinterpret_cast<float*>(smem + C::SMEM_PM)[r] = -INFINITY;
+        reinterpret_cast<float*>(smem + C::SMEM_PL)[r] = 0.f;
       }
       __syncthreads();
-      cluster_combine(smem, p.nsplit, nrows, r0, a, p.out, p.ldout);
+      cluster_combine<C>(smem, p.nsplit, nrows, r0, a, p.out, p.ldout);
     }
     return;
   }
 
+  // live 32-row halves: a 64-row launch whose sequence has <= 32 surviving
+  // rows runs N = 32 MMAs and one softmax group (row capacities are host
+  // upper bounds; the survivor counts live on the device)
+  const int live_h = NH == 1 ? 1 : (nrows + 31) >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
@@ -211,21 +240,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int i = 0; i < NSB; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < NPB; ++i) {
-      mbar_init(&p_full[i], 128);
+      mbar_init(&p_full[i], 128 * live_h);
       mbar_init(&pv_done[i], 1);
     }
     fence_barrier_init();
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  {  // Q rows -> SW128 K-major [32 rows x 128 dims] (rows past nrows zero)
+  {  // Q rows -> SW128 K-major [NR rows x 128 dims] (rows past nrows zero)
     const __nv_bfloat16* qbase = p.qkv + a * DH;
-    for (int i = threadIdx.x; i < NR * 16; i += THREADS) {
+    for (int i = threadIdx.x; i < NR * 16; i += C::THREADS) {
       const int r = i >> 4, c = i & 15;
-      uint8_t* dst = smem + SMEM_Q + (c >> 3) * Q_HALF + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
+      uint8_t* dst =
+          smem + C::SMEM_Q + (c >> 3) * C::Q_HALF + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
       if (r < nrows)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
                      "l"(qbase + (size_t)(r0 + r) * p.ldq + c * 8)
@@ -233,21 +263,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       else
         *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
     }
-    // tree visibility words per row (causal when no mask: nodes 0..node)
-    for (int i = threadIdx.x; i < NR * 4; i += THREADS) {
-      const int r = i >> 2, w = i & 3;
-      uint64_t m = 0ull;
-      if (r < nrows && w < max(p.W, 1)) {
-        const int node = p.row_node[r0 + r];
-        if (p.mask != nullptr) {
-          m = w < p.W ? p.mask[(size_t)node * p.W + w] : 0ull;
-        } else {
-          const int nb = node + 1 - 64 * w;
-          m = nb >= 64 ? ~0ull : (nb <= 0 ? 0ull : ((1ull << nb) - 1ull));
-        }
-      }
-      rmask[i] = m;
-    }
+    for (int r = threadIdx.x; r < NR; r += C::THREADS) rnode[r] = r < nrows ? p.row_node[r0 + r] : 0;
     asm volatile("cp.async.wait_all;" ::: "memory");
   }
   fence_proxy_async();
@@ -258,15 +274,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   pdl_trigger();  // after the TMEM allocation (see common.cuh)
   const size_t row_base = ((size_t)slot * p.A + a) * p.Lmax;
 
-  if (warp == 0 || warp == 6) {
-    // ================= TMA producers: warp 0 streams K, warp 6 streams V =================
+  if (warp == 0 || warp == C::VWARP) {
+    // ================= TMA producers: warp 0 streams K, warp VWARP streams V =================
     if (lane == 0) {
       const bool isk = warp == 0;
       const int NS = isk ? KS : VS;
       uint64_t* full = isk ? k_full : v_full;
       uint64_t* empty = isk ? k_empty : v_empty;
       const CUtensorMap* map = isk ? &kmap : &vmap;
-      uint8_t* ring = smem + (isk ? SMEM_K : SMEM_V);
+      uint8_t* ring = smem + (isk ? C::SMEM_K : C::SMEM_V);
       for (int j = 0; j < nblk; ++j) {
         const int st = j % NS;
         mbar_wait(&empty[st], ((j / NS) & 1) ^ 1, isk ? 61 : 67);
@@ -280,9 +296,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     // ================= MMA issuer =================
     if (lane == 0) {
-      const uint32_t id_s = idesc_bf16(false, NR, BK);
-      const uint32_t id_o = idesc_bf16(false, NR, DH) | (1u << 15);  // A = V^T read MN-major from the V tile
-      const uint32_t q_addr = smem_u32(smem + SMEM_Q);
+      const uint32_t nn = 32u * live_h;
+      const uint32_t id_s = idesc_bf16(false, nn, BK);
+      const uint32_t id_o = idesc_bf16(false, nn, DH) | (1u << 15);  // A = V^T read MN-major from the V tile
+      const uint32_t q_addr = smem_u32(smem + C::SMEM_Q);
       int ns = 0, np = 0;
       uint32_t idle = 0;
       while (np < nblk) {
@@ -290,12 +307,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (ns < nblk && ns < np + NSB && mbar_try(&k_full[ns % KS], (ns / KS) & 1)) {
           const int st = ns % KS;
           tc_after_sync();
-          const uint32_t k_addr = smem_u32(smem + SMEM_K + st * KV_TILE);
+          const uint32_t k_addr = smem_u32(smem + C::SMEM_K + st * KV_TILE);
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk) {
             const uint64_t ad = sw128_desc(k_addr + (kk >> 2) * KV_HALF + (kk & 3) * 32, 16, 1024);
-            const uint64_t bd = sw128_desc(q_addr + (kk >> 2) * Q_HALF + (kk & 3) * 32, 16, 1024);
-            mma_bf16(tmem + S_COL + NR * (ns % NSB), ad, bd, id_s, kk > 0 ? 1u : 0u);
+            const uint64_t bd = sw128_desc(q_addr + (kk >> 2) * C::Q_HALF + (kk & 3) * 32, 16, 1024);
+            mma_bf16(tmem + C::S_COL + NR * (ns % NSB), ad, bd, id_s, kk > 0 ? 1u : 0u);
           }
           mma_commit(&s_full[ns % NSB]);
           mma_commit(&k_empty[st]);
@@ -306,13 +323,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int st = np % VS, pb = np % NPB;
           if (mbar_try(&p_full[pb], (np / NPB) & 1) && mbar_try(&v_full[st], (np / VS) & 1)) {
             tc_after_sync();
-            const uint32_t v_addr = smem_u32(smem + SMEM_V + st * KV_TILE);
-            const uint32_t p_addr = smem_u32(smem + SMEM_P + pb * P_TILE);
+            const uint32_t v_addr = smem_u32(smem + C::SMEM_V + st * KV_TILE);
+            const uint32_t p_addr = smem_u32(smem + C::SMEM_P + pb * C::P_TILE);
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
               const uint64_t ad = sw128_desc(v_addr + kk * 2048, KV_HALF, 1024);
-              const uint64_t bd = sw128_desc(p_addr + (kk >> 2) * P_HALF + (kk & 3) * 32, 16, 1024);
-              mma_bf16(tmem + O_COL, ad, bd, id_o, (np > 0 || kk > 0) ? 1u : 0u);
+              const uint64_t bd = sw128_desc(p_addr + (kk >> 2) * C::P_HALF + (kk & 3) * 32, 16, 1024);
+              mma_bf16(tmem + C::O_COL, ad, bd, id_o, (np > 0 || kk > 0) ? 1u : 0u);
             }
             mma_commit(&v_empty[st]);
             mma_commit(&pv_done[pb]);
@@ -327,56 +344,56 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
-  } else if (warp <= 5) {
-    // ================= softmax: warp q owns keys 32q..32q+31 of each block =================
-    const int q = warp & 3;
+  } else if (warp < C::VWARP && (NH == 1 || ((warp - 2) >> 2) < live_h)) {
+    // ============ softmax: group h = rows 32h..32h+31, warp q owns keys 32q..32q+31 of each block ============
+    const int h = NH == 1 ? 0 : (warp - 2) >> 2, q = warp & 3;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     const float scale = p.scale_log2;
-    float m_ref = -INFINITY;  // running reference max of row `lane` (log2 domain; same in every warp)
-    float lpart[NR];          // this thread's key-lane partial row sums
+    float m_ref = -INFINITY;  // running reference max of row 32h + lane (log2 domain; same in the group's warps)
+    float lpart[32];          // this thread's key-lane partial sums of rows 32h..32h+31
 #pragma unroll
-    for (int n = 0; n < NR; ++n) lpart[n] = 0.f;
+    for (int n = 0; n < 32; ++n) lpart[n] = 0.f;
     const int kin = (q & 1) * 32 + (lane & ~1);  // even key of this lane pair within its 64-key half
     const int pchunk = kin >> 3, pbyte = (kin & 7) * 2;
     const bool odd = lane & 1;
+    float* red_g = red + h * 256;
     for (int j = 0; j < nblk; ++j) {
       const int sb = j % NSB, pb = j % NPB;
-      float v[NR];
       mbar_wait(&s_full[sb], (j / NSB) & 1, 63);
       tc_after_sync();
-      TMEM_LD32(lane_base + S_COL + NR * sb, reinterpret_cast<uint32_t*>(v));
-      tmem_wait_ld();
-      // visibility of key `key` for each row
       const int key = k_begin + j * BK + q * 32 + lane;
+      float v[32];
+      TMEM_LD32(lane_base + C::S_COL + NR * sb + 32 * h, reinterpret_cast<uint32_t*>(v));
+      tmem_wait_ld();
+      // visibility of key `key` for rows 32h + n
       if (key >= k_end) {
 #pragma unroll
-        for (int n = 0; n < NR; ++n) v[n] = -INFINITY;
+        for (int n = 0; n < 32; ++n) v[n] = -INFINITY;
       } else if (key >= L) {
-        const int t = key - L;
+        const int t = key - L;  // tree node index of this key
 #pragma unroll
-        for (int n = 0; n < NR; ++n)
-          v[n] = (n < nrows && ((rmask[n * 4 + (t >> 6)] >> (t & 63)) & 1ull)) ? v[n] * scale : -INFINITY;
+        for (int n = 0; n < 32; ++n) {
+          const int r = 32 * h + n;
+          bool vis = r < nrows;
+          if (vis) {
+            const int node = rnode[r];
+            vis = p.mask != nullptr ? ((__ldg(p.mask + (size_t)node * p.W + (t >> 6)) >> (t & 63)) & 1ull) != 0
+                                    : t <= node;
+          }
+          v[n] = vis ? v[n] * scale : -INFINITY;
+        }
       } else {
 #pragma unroll
-        for (int n = 0; n < NR; ++n) v[n] = n < nrows ? v[n] * scale : -INFINITY;
+        for (int n = 0; n < 32; ++n) v[n] = 32 * h + n < nrows ? v[n] * scale : -INFINITY;
       }
-      // block maximum of every row: butterfly transpose (lane l ends with row l) + 4-warp merge
-      float t[NR];
+      // block maximum of every row: butterfly transpose (lane l ends with row 32h + l) + 4-warp merge
+      float tr[32];
 #pragma unroll
-      for (int n = 0; n < NR; ++n) t[n] = v[n];
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < o; ++i) {
-          const float send = up ? t[i] : t[i + o];
-          const float keep = up ? t[i + o] : t[i];
-          t[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, o));
-        }
-      }
-      float* rb = red + (j & 1) * 128;
-      rb[q * 32 + lane] = t[0];
-      named_sync(1, 128);
+      for (int n = 0; n < 32; ++n) tr[n] = v[n];
+      lane_transpose_reduce<true>(tr, lane);
+      float* rb = red_g + (j & 1) * 128;
+      rb[q * 32 + lane] = tr[0];
+      named_sync(1 + h, 128);
       const float bm = fmaxf(fmaxf(rb[lane], rb[32 + lane]), fmaxf(rb[64 + lane], rb[96 + lane]));
       // lazy rescale: move the reference only when the block max exceeds it by > 2^8
       const bool grow = bm > m_ref + 8.f;
@@ -388,40 +405,38 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool any_grow = __any_sync(0xffffffffu, grow);
       const float mneg = m_ref == -INFINITY ? 0.f : -m_ref;
 #pragma unroll
-      for (int n = 0; n < NR; n += 2) {
+      for (int n = 0; n < 32; n += 2) {
         const float2 pp = ex2x2(v[n] + __shfl_sync(0xffffffffu, mneg, n), v[n + 1] + __shfl_sync(0xffffffffu, mneg, n + 1));
         v[n] = pp.x;
         v[n + 1] = pp.y;
       }
       if (any_grow) {
 #pragma unroll
-        for (int n = 0; n < NR; ++n) lpart[n] *= __shfl_sync(0xffffffffu, corr, n);
+        for (int n = 0; n < 32; ++n) lpart[n] *= __shfl_sync(0xffffffffu, corr, n);
       }
 #pragma unroll
-      for (int n = 0; n < NR; ++n) lpart[n] += v[n];
-      // P^T (K-major [32 rows x 128 keys], SW128): lane pairs exchange so each
-      // stores one 4-byte word (keys 2i, 2i+1) for 16 rows
-      if (j >= NPB) {  // PV_{j-NPB} has finished reading this buffer
-        mbar_wait(&pv_done[pb], ((j / NPB) - 1) & 1, 64);
-      }
-      uint8_t* pbase = smem + SMEM_P + pb * P_TILE + (q >> 1) * P_HALF;
+      for (int n = 0; n < 32; ++n) lpart[n] += v[n];
+      // P^T (K-major [NR rows x 128 keys], SW128): lane pairs exchange so
+      // each stores one 4-byte word (keys 2i, 2i+1) for 16 rows
+      if (j >= NPB) mbar_wait(&pv_done[pb], ((j / NPB) - 1) & 1, 64);  // PV_{j-NPB} has read this buffer
+      uint8_t* pbase = smem + C::SMEM_P + pb * C::P_TILE + (q >> 1) * C::P_HALF;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float send = odd ? v[i] : v[16 + i];
         const float recv = __shfl_xor_sync(0xffffffffu, send, 1);
-        const int n = odd ? 16 + i : i;
+        const int n = 32 * h + (odd ? 16 + i : i);
         const uint32_t w = odd ? pack_bf16(recv, v[16 + i]) : pack_bf16(v[i], recv);
         *reinterpret_cast<uint32_t*>(pbase + (n >> 3) * 1024 + (n & 7) * 128 + ((pchunk ^ (n & 7)) << 4) + pbyte) = w;
       }
-      if (any_grow && j > 0) {  // O^T rows (TMEM columns) whose reference moved: rescale after PV_{j-1}
+      if (any_grow && j > 0) {  // O^T columns (rows) whose reference moved: rescale after PV_{j-1}
         mbar_wait(&pv_done[(j - 1) % NPB], ((j - 1) / NPB) & 1, 65);
         tc_after_sync();
         uint32_t o[32];
-        TMEM_LD32(lane_base + O_COL, o);
+        TMEM_LD32(lane_base + C::O_COL + 32 * h, o);
         tmem_wait_ld();
 #pragma unroll
-        for (int n = 0; n < NR; ++n) o[n] = __float_as_uint(__uint_as_float(o[n]) * __shfl_sync(0xffffffffu, corr, n));
-        TMEM_ST32(lane_base + O_COL, o);
+        for (int n = 0; n < 32; ++n) o[n] = __float_as_uint(__uint_as_float(o[n]) * __shfl_sync(0xffffffffu, corr, n));
+        TMEM_ST32(lane_base + C::O_COL + 32 * h, o);
         tmem_wait_st();
       }
       fence_proxy_async();  // P^T stores -> visible to the tensor core
@@ -429,39 +444,32 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_arrive(&p_full[pb]);
     }
     // ---- epilogue: row sums, then O^T (lane = dim) -> rows ----
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const bool up = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < o; ++i) {
-        const float send = up ? lpart[i] : lpart[i + o];
-        const float keep = up ? lpart[i + o] : lpart[i];
-        lpart[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
+    lane_transpose_reduce<false>(lpart, lane);
+    float* lred = red_g + (nblk & 1) * 128;  // the exchange buffer the last block did not use
     lred[q * 32 + lane] = lpart[0];
     mbar_wait(&pv_done[(nblk - 1) % NPB], ((nblk - 1) / NPB) & 1, 66);
     tc_after_sync();
-    named_sync(1, 128);
-    const float lrow = (lred[lane] + lred[32 + lane]) + (lred[64 + lane] + lred[96 + lane]);  // row `lane`
-    uint32_t o[32];
-    TMEM_LD32(lane_base + O_COL, o);
-    tmem_wait_ld();
+    named_sync(1 + h, 128);
+    const float lrow = (lred[lane] + lred[32 + lane]) + (lred[64 + lane] + lred[96 + lane]);  // row 32h + lane
     const int d = q * 32 + lane;
+    uint32_t o[32];
+    TMEM_LD32(lane_base + C::O_COL + 32 * h, o);
+    tmem_wait_ld();
     if (p.nsplit == 1) {
       const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
 #pragma unroll
-      for (int n = 0; n < NR; ++n) {
+      for (int n = 0; n < 32; ++n) {
         const float f = __shfl_sync(0xffffffffu, inv, n);
-        if (n < nrows) p.out[(size_t)(r0 + n) * p.ldout + a * DH + d] = __float2bfloat16_rn(__uint_as_float(o[n]) * f);
+        if (32 * h + n < nrows)
+          p.out[(size_t)(r0 + 32 * h + n) * p.ldout + a * DH + d] = __float2bfloat16_rn(__uint_as_float(o[n]) * f);
       }
     } else {  // park the unnormalised state; the K ring is idle (every S has completed)
-      float* po = reinterpret_cast<float*>(smem + SMEM_PO);
+      float* po = reinterpret_cast<float*>(smem + C::SMEM_PO);
 #pragma unroll
-      for (int n = 0; n < NR; ++n) po[n * DH + d] = __uint_as_float(o[n]);
+      for (int n = 0; n < 32; ++n) po[(32 * h + n) * DH + d] = __uint_as_float(o[n]);
       if (q == 0) {
-        reinterpret_cast<float*>(smem + SMEM_PM)[lane] = m_ref;
-        reinterpret_cast<float*>(smem + SMEM_PL)[lane] = lrow;
+        reinterpret_cast<float*>(smem + C::SMEM_PM)[32 * h + lane] = m_ref;
+        reinterpret_cast<float*>(smem + C::SMEM_PL)[32 * h + lane] = lrow;
       }
     }
   }
@@ -470,9 +478,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_after_sync();
   if (warp == 1) {
     __syncwarp();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
   }
-  if (p.nsplit > 1) cluster_combine(smem, p.nsplit, nrows, r0, a, p.out, p.ldout);
+  if (p.nsplit > 1) cluster_combine<C>(smem, p.nsplit, nrows, r0, a, p.out, p.ldout);
   if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_wait, 2);
 }
 
@@ -526,13 +534,52 @@ static bool tct_enabled() {
   return v == 1;
 }
 
+template <class C>
+static int tct_launch(const CUtensorMap& km, const CUtensorMap& vm, const tct::Args& p, int nsplit, int A, int B,
+                      cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tct::attn_tct_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_TOTAL);
+    if (e != cudaSuccess) return fail("prepare(tcT): %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nsplit, A, B);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (nsplit > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = nsplit;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tct::attn_tct_kernel<C>, km, vm, p);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail("tree_attention(tcT): %s", cudaGetErrorString(e));
+  }
+  return check_launch("tree_attention(tcT)");
+}
+
 int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
                        int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                        const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                        void* out, int ldout, cudaStream_t st, bool force, bool* handled) {
   *handled = false;
   if (!force && !tct_enabled()) return 0;
-  if (n_slots <= 0 || max_rows_per_seq > tct::NR || W > 4 || (ldqkv % 8) != 0) return 0;
+  if (n_slots <= 0 || max_rows_per_seq > 64 || W > 4 || (ldqkv % 8) != 0) return 0;
   CUtensorMap km, vm;
   const uint64_t rows = (uint64_t)n_slots * A * Lmax;
   if (!tct::kv_map128(&km, kc, rows) || !tct::kv_map128(&vm, vc, rows)) return 0;
@@ -566,41 +613,9 @@ int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq
   p.ldout = ldout;
   p.tl = g_dbg_trace;
   p.tag = g_dbg_tag++;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tct::attn_tct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tct::SMEM_TOTAL);
-    if (e != cudaSuccess) return fail("prepare(tcT): %s", cudaGetErrorString(e));
-    attr = true;
-  }
   *handled = true;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nsplit, A, B);
-  cfg.blockDim = dim3(tct::THREADS);
-  cfg.dynamicSmemBytes = tct::SMEM_TOTAL;
-  cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  int na = 0;
-  if (nsplit > 1) {
-    at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = nsplit;
-    at[na].val.clusterDim.y = 1;
-    at[na].val.clusterDim.z = 1;
-    ++na;
-  }
-  if (pdl_enabled()) {
-    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  cfg.attrs = at;
-  cfg.numAttrs = na;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tct::attn_tct_kernel, km, vm, p);
-  if (e != cudaSuccess) {
-    (void)cudaGetLastError();
-    return fail("tree_attention(tcT): %s", cudaGetErrorString(e));
-  }
-  return check_launch("tree_attention(tcT)");
+  return max_rows_per_seq <= 32 ? tct_launch<tct::Cfg<32>>(km, vm, p, nsplit, A, B, st)
+                                : tct_launch<tct::Cfg<64>>(km, vm, p, nsplit, A, B, st);
 }
 
 }  // namespace propd

@@ -132,10 +132,14 @@ def torch_tree_attention(q, kc, vc, slots, lens, row_off, row_node, mask_bool, A
     ("bf16", 128, 32, [1030], "grid43", 5),
     ("bf16", 128, 8, [1, 64, 4096], "grid48", 5),
     ("bf16", 128, 32, [3000], "grid48", 0),
+    ("bf16", 128, 2, [1500, 64], "full33", 5),
+    ("bf16", 128, 8, [1, 64, 4096], "grid416", 5),
+    ("bf16", 128, 32, [1030], "grid416", 0),
 ])
 def test_tree_attention_vs_torch(dtype, dh, A, lens, paths, impl):
     rng = np.random.default_rng(dh * 7 + len(lens))
     universe = {"grid43": op.grid_candidates(4, 3), "grid48": op.grid_candidates(4, 8),
+                "grid416": op.grid_candidates(4, 16),
                 "full33": op.complete_tree_paths(3, 3),
                 "full44": op.complete_tree_paths(4, 4)[:200], "chain": [(1,) * d for d in range(1, 5)]}[paths]
     tmpl = TreeTemplate.from_paths(universe)
@@ -197,17 +201,22 @@ def test_decode_attention_cluster_combine(A, lens, rows):
     del rng
 
 
-@pytest.mark.parametrize("causal", [False, True])
-def test_tree_attention_tct_pruned_rows(causal):
-    """Transposed kernel (impl 5) on a compacted survivor subset of a 32-node tree (rows = surviving nodes,
-    row_node = their template indices), with the tree mask or causal (mask = NULL)."""
+@pytest.mark.parametrize("causal,big", [(False, False), (True, False), (False, True), (True, True)])
+def test_tree_attention_tct_pruned_rows(causal, big):
+    """Transposed kernel (impl 5) on a compacted survivor subset of a tree (rows = surviving nodes, row_node =
+    their template indices), with the tree mask or causal (mask = NULL); big: a 200-node template (4 mask words)
+    with up to 64 surviving rows (the 64-row variant)."""
     dh, A = 128, 4
     H = A * dh
     lens = [700, 3, 1500]
     B = len(lens)
-    tmpl = TreeTemplate.from_paths(op.grid_candidates(4, 8))
+    if big:
+        tmpl = TreeTemplate.from_paths(op.complete_tree_paths(4, 4)[:200])
+        keep = [list(range(0, 200, 4))[:50], [0, 3, 150, 199], list(range(5, 69))]
+    else:
+        tmpl = TreeTemplate.from_paths(op.grid_candidates(4, 8))
+        keep = [[0, 1, 2, 8, 9, 20, 31], [0, 5], list(range(0, 32, 3))]
     n = len(tmpl)
-    keep = [[0, 1, 2, 8, 9, 20, 31], [0, 5], list(range(0, 32, 3))]
     Lmax = max(lens) + n + 8
     kc = torch.randn(B, A, Lmax, dh, device=DEV).bfloat16()
     vc = torch.randn(B, A, Lmax, dh, device=DEV).bfloat16()
