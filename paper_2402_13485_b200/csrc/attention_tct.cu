@@ -580,6 +580,12 @@ int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq
   *handled = false;
   if (!force && !tct_enabled()) return 0;
   if (n_slots <= 0 || max_rows_per_seq > 64 || W > 4 || (ldqkv % 8) != 0) return 0;
+  // > 32-row capacity with few 128-key blocks per SM (B=1-4 at KV <= 2K) is
+  // latency-bound, where the row-major tc2 kernel's shorter per-block chain
+  // wins (measured: 11.2 vs 14.7 us at B=1/KV 512, 22.2 vs 25.0 at B=4/KV 1K)
+  if (!force && max_rows_per_seq > 32 &&
+      (long long)B * A * ((max_keys + 127) / 128) < 16LL * propd_num_sms())
+    return 0;
   CUtensorMap km, vm;
   const uint64_t rows = (uint64_t)n_slots * A * Lmax;
   if (!tct::kv_map128(&km, kc, rows) || !tct::kv_map128(&vm, vc, rows)) return 0;
