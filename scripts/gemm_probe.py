@@ -30,7 +30,7 @@ def bench(fn, reps=20):
     return e0.elapsed_time(e1) * 1e3 / reps
 
 
-for M in (1, 16, 48):
+for M in tuple(int(m) for m in os.environ.get("ROWS", "1,16,48").split(",")):
     for name, N, K, acc in shapes:
         X = torch.randn(M, K, device="cuda").bfloat16()
         W = torch.randn(K, N, device="cuda").bfloat16()
