@@ -424,7 +424,8 @@ def timeline_region(be, eng, seqs, prime, dev):
     rec = buf[8: 8 + 8 * n].view(n, 8).cpu().numpy()
     out = {"step_ms": t0.elapsed_time(t1), "records": n}
     for kind, name in ((1, "gemm"), (2, "attn")):
-        r = rec[rec[:, 7] == kind]
+        # kind 4 = the transposed attention kernel (same release / exit columns)
+        r = rec[(rec[:, 7] == kind) | ((rec[:, 7] == 4) if kind == 2 else False)]
         if len(r) == 0:
             continue
         spans = []

@@ -72,6 +72,10 @@ for tg in tags:
     print(f"{tg:4d} {len(r):5d} {us(r[:, 3].min()):8.1f} {us(r[:, 3].max()):8.1f} {us(r[:, 4].max()):8.1f} "
           f"{us(r[:, 5].max()):8.1f} {us(r[:, 6].min()):8.1f} {us(r[:, 6].max()):8.1f} {gap:6.1f}")
     prev_exit = us(r[:, 6].max())
+    if args.per_cta and r[0, 7] == 4:  # tcT: records (first S, wait, loop end, exit)
+        q = lambda v: " ".join(f"{x:5.2f}" for x in np.percentile(v / 1e3, [0, 50, 90, 100]))
+        print(f"      tcT per-CTA [p0 p50 p90 max] wait->S0 {q(r[:, 3] - r[:, 4])}  S0->loop end {q(r[:, 5] - r[:, 3])}"
+              f"  ->exit {q(r[:, 6] - r[:, 5])}")
     if args.per_cta and r[0, 7] == 2:  # attention: per-CTA wait -> loop end -> exit
         q = lambda v: " ".join(f"{x:5.2f}" for x in np.percentile(v / 1e3, [0, 50, 90, 100]))
         print(f"      per-CTA wait->main [p0 p50 p90 max] {q(r[:, 5] - r[:, 4])}   main->exit {q(r[:, 6] - r[:, 5])}")
