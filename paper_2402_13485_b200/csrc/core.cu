@@ -226,18 +226,46 @@ __global__ void gather_rows_kernel(int H, const float* __restrict__ src, const i
 }
 
 // First maximum per row (numpy argmax semantics).
-__global__ void argmax_rows_kernel(int V, int ld, const float* __restrict__ logits, int32_t* __restrict__ out,
-                                   const int32_t* __restrict__ rows_dev) {
+// First maximum of each row.  The scan is latency-bound (one row per CTA,
+// ~20 rows at batch 1), so every thread keeps 4 float4 loads in flight; each
+// thread still visits its indices in increasing order, so "first max" per
+// thread plus the (value, lower index) reduction is the first max of the row.
+__device__ __forceinline__ void argmax_take(float t, int v, float& best, int& bi) {
+  if (t > best) {
+    best = t;
+    bi = v;
+  }
+}
+__global__ void __launch_bounds__(512) argmax_rows_kernel(int V, int ld, const float* __restrict__ logits,
+                                                            int32_t* __restrict__ out,
+                                                            const int32_t* __restrict__ rows_dev) {
   __shared__ float sv[32];
   __shared__ int si[32];
   if (rows_dev && (int)blockIdx.x >= *rows_dev) return;
   const float* x = logits + (size_t)blockIdx.x * ld;
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) {
-    float t = x[v];
-    if (t > best) { best = t; bi = v; }  // strided scan visits v in increasing order
+  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(logits) & 15) == 0);
+  const int V4 = vec ? (V >> 2) : 0;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  constexpr int U = 4;
+  for (int base = threadIdx.x; base < V4; base += U * blockDim.x) {
+    float4 f[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * blockDim.x;
+      f[u] = i < V4 ? __ldg(x4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = 4 * (base + u * blockDim.x);
+      argmax_take(f[u].x, v, best, bi);
+      argmax_take(f[u].y, v + 1, best, bi);
+      argmax_take(f[u].z, v + 2, best, bi);
+      argmax_take(f[u].w, v + 3, best, bi);
+    }
   }
+  for (int v = 4 * V4 + threadIdx.x; v < V; v += blockDim.x) argmax_take(x[v], v, best, bi);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     float ov = __shfl_xor_sync(0xffffffffu, best, o);
@@ -264,13 +292,30 @@ __global__ void argmax_rows_kernel(int V, int ld, const float* __restrict__ logi
 // Stable descending top-k: radix select on the unique 64-bit key
 // (float_key(x) << 32) | ~index, then bitonic sort of the k winners.
 constexpr int TOPK_MAX = 1024;
+// The row is staged once in shared memory when it fits (every radix pass
+// re-reads it; V = 32000 is 125 KB), read from global memory otherwise.
+constexpr int TOPK_SMEM_MAX = 48 * 1024;  // floats staged (192 KB)
 __global__ void __launch_bounds__(512) topk_rows_kernel(int V, int ld, int k, const float* __restrict__ logits,
                                                           int32_t* __restrict__ out_idx, float* __restrict__ out_val) {
   __shared__ unsigned hist[256];
   __shared__ unsigned long long cand[TOPK_MAX];
   __shared__ unsigned long long s_prefix;
   __shared__ int s_shift, s_need, s_done, s_cnt;
-  const float* x = logits + (size_t)blockIdx.x * ld;
+  extern __shared__ float4 row_s[];
+  const float* xg = logits + (size_t)blockIdx.x * ld;
+  const float* x = xg;
+  if (V <= TOPK_SMEM_MAX) {
+    float* rs = reinterpret_cast<float*>(row_s);
+    if (((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(logits) & 15) == 0)) {
+      const float4* g4 = reinterpret_cast<const float4*>(xg);
+      for (int i = threadIdx.x; i < (V >> 2); i += blockDim.x) row_s[i] = __ldg(g4 + i);
+      for (int v = 4 * (V >> 2) + threadIdx.x; v < V; v += blockDim.x) rs[v] = xg[v];
+    } else {
+      for (int v = threadIdx.x; v < V; v += blockDim.x) rs[v] = xg[v];
+    }
+    x = rs;
+    __syncthreads();
+  }
   auto key_of = [&](int v) -> unsigned long long {
     return ((unsigned long long)float_key(x[v]) << 32) | (unsigned long long)(0xffffffffu - (unsigned)v);
   };
@@ -496,14 +541,22 @@ int propd_gather_rows(int dtype, int M, int H, const float* src, const int32_t* 
 int propd_argmax_rows(int M, const int32_t* rows_dev, int V, int ld, const float* logits, int32_t* out, void* stream) {
   if (M == 0) return 0;
   PROPD_REQUIRE(V > 0 && ld >= V, "argmax_rows: bad V=%d ld=%d", V, ld);
-  argmax_rows_kernel<<<M, 256, 0, as_stream(stream)>>>(V, ld, logits, out, rows_dev);
+  argmax_rows_kernel<<<M, 512, 0, as_stream(stream)>>>(V, ld, logits, out, rows_dev);
   return check_launch("argmax_rows");
 }
 
 int propd_topk_rows(int R, int V, int ld, int k, const float* logits, int32_t* out_idx, float* out_val, void* stream) {
   if (R == 0) return 0;
   PROPD_REQUIRE(k >= 1 && k <= TOPK_MAX && k <= V, "topk_rows: k=%d outside 1..min(%d, V=%d)", k, TOPK_MAX, V);
-  topk_rows_kernel<<<R, 512, 0, as_stream(stream)>>>(V, ld, k, logits, out_idx, out_val);
+  const int smem = V <= TOPK_SMEM_MAX ? V * 4 : 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(topk_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         TOPK_SMEM_MAX * 4);
+    if (e != cudaSuccess) return fail("topk_rows: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  topk_rows_kernel<<<R, 512, smem, as_stream(stream)>>>(V, ld, k, logits, out_idx, out_val);
   return check_launch("topk_rows");
 }
 

@@ -32,9 +32,32 @@ __global__ void early_member_kernel(int n, int P, int V, int topk, const float* 
   const int t = tokens[m];
   const float target = row[t];
   int cnt = 0;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) {
-    const float x = row[v];
-    cnt += (x > target) || (x == target && v < t);
+  // latency-bound scan (one parent row per CTA): 4 float4 loads in flight per thread
+  if ((V & 3) == 0 && (reinterpret_cast<uintptr_t>(early) & 15) == 0) {
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int V4 = V >> 2;
+    constexpr int U = 4;
+    for (int base = threadIdx.x; base < V4; base += U * blockDim.x) {
+      float4 f[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * blockDim.x;
+        f[u] = i < V4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = 4 * (base + u * blockDim.x);
+        cnt += (f[u].x > target) || (f[u].x == target && v < t);
+        cnt += (f[u].y > target) || (f[u].y == target && v + 1 < t);
+        cnt += (f[u].z > target) || (f[u].z == target && v + 2 < t);
+        cnt += (f[u].w > target) || (f[u].w == target && v + 3 < t);
+      }
+    }
+  } else {
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+      const float x = row[v];
+      cnt += (x > target) || (x == target && v < t);
+    }
   }
   cnt = warp_isum(cnt);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

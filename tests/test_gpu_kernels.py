@@ -44,7 +44,7 @@ def keep(t):
 
 
 # --------------------------------------------------------------- top-k / argmax
-@pytest.mark.parametrize("V,k", [(256, 3), (256, 24), (32000, 64), (32000, 1), (1000, 1000), (64, 64)])
+@pytest.mark.parametrize("V,k", [(256, 3), (256, 24), (32000, 64), (32000, 1), (1000, 1000), (64, 64), (50001, 7)])
 def test_topk_matches_stable_argsort(V, k):
     rng = np.random.default_rng(V + k)
     x = rng.normal(size=(7, V)).astype(np.float32)
@@ -61,15 +61,20 @@ def test_topk_matches_stable_argsort(V, k):
     assert np.array_equal(val.cpu().numpy(), np.take_along_axis(x, ref, axis=1))
 
 
-def test_argmax_first_max():
-    rng = np.random.default_rng(1)
-    x = rng.normal(size=(9, 32000)).astype(np.float32)
-    x[0, [5, 77, 31999]] = 100.0
+@pytest.mark.parametrize("V,ld", [(32000, 32000), (32001, 32001), (5000, 5003), (3, 4)])
+def test_argmax_first_max(V, ld):
+    """First maximum (lowest index on ties), vectorised rows (ld % 4 == 0) and scalar ones."""
+    rng = np.random.default_rng(V)
+    x = rng.normal(size=(9, ld)).astype(np.float32)
+    x[0, [min(5, V - 1), min(77, V - 1), V - 1]] = 100.0
     x[1] = 0.0
+    x[2, V - 1] = 50.0
+    x[3, :V] = np.round(x[3, :V])  # coarse ties
+    x[:, V:] = 1e9  # padding past V is never a candidate
     dx = torch.from_numpy(x).to(DEV)
     out = torch.empty(9, dtype=torch.int32, device=DEV)
-    call("propd_argmax_rows", 9, None, 32000, 32000, ptr(dx), ptr(out), st())
-    assert np.array_equal(out.cpu().numpy(), np.argmax(x, axis=1))
+    call("propd_argmax_rows", 9, None, V, ld, ptr(dx), ptr(out), st())
+    assert np.array_equal(out.cpu().numpy(), np.argmax(x[:, :V], axis=1))
 
 
 def test_rows_dev_skips_padded_rows():
