@@ -225,8 +225,7 @@ __global__ void gather_rows_kernel(int H, const float* __restrict__ src, const i
   for (int h = threadIdx.x; h < H; h += blockDim.x) d[h] = from_f<T>(s[h]);
 }
 
-// First maximum per row (numpy argmax semantics).
-// First maximum of each row.  The scan is latency-bound (one row per CTA,
+// First maximum of each row (numpy argmax semantics).  The scan is latency-bound (one row per CTA,
 // ~20 rows at batch 1), so every thread keeps 4 float4 loads in flight; each
 // thread still visits its indices in increasing order, so "first max" per
 // thread plus the (value, lower index) reduction is the first max of the row.
