@@ -555,13 +555,15 @@ static bool kv_map128(CUtensorMap* m, const void* base, uint64_t rows) {
 
 }  // namespace tct
 
-static bool tct_enabled() {
+// PROPD_TCT: 0 = never (tc2 for every multi-row launch), 2 = whenever the
+// shape fits (no latency heuristic), unset / other = auto
+static int tct_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PROPD_TCT");
-    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+    v = (e != nullptr && e[0] == '0') ? 0 : ((e != nullptr && e[0] == '2') ? 2 : 1);
   }
-  return v == 1;
+  return v;
 }
 
 template <class C>
@@ -608,12 +610,12 @@ int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq
                        const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                        void* out, int ldout, cudaStream_t st, bool force, bool* handled) {
   *handled = false;
-  if (!force && !tct_enabled()) return 0;
+  if (!force && tct_mode() == 0) return 0;
   if (n_slots <= 0 || max_rows_per_seq > 64 || W > 4 || (ldqkv % 8) != 0) return 0;
   // > 32-row capacity with few 128-key blocks per SM (B=1-4 at KV <= 2K) is
   // latency-bound, where the row-major tc2 kernel's shorter per-block chain
   // wins (measured: 11.2 vs 14.7 us at B=1/KV 512, 22.2 vs 25.0 at B=4/KV 1K)
-  if (!force && max_rows_per_seq > 32 &&
+  if (!force && tct_mode() != 2 && max_rows_per_seq > 32 &&
       (long long)B * A * ((max_keys + 127) / 128) < 16LL * propd_num_sms())
     return 0;
   CUtensorMap km, vm;
