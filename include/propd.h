@@ -113,9 +113,11 @@ int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, 
  * `workspace` must hold propd_attn_workspace_bytes(...) bytes.
  * impl: 0 = auto, 1 = CUDA-core split-KV kernel, 2 = tcgen05/TMA kernel v1
  * (128-key blocks, one softmax warpgroup), 4 = tcgen05/TMA kernel v2 (64-key
- * blocks, 4-stage ring, two softmax warpgroups; auto for > 4 rows), 3 =
- * streaming decode kernel (<= 4 rows per sequence; auto for the bonus pass).
- * impls 2-4 need bf16 and dh = 128.  n_slots = number of [A, Lmax, dh] slot blocks in the
+ * blocks, 6+6-stage K/V rings, two softmax warpgroups; auto for > 64 rows and
+ * for latency-bound > 32-row launches), 5 = transposed tcgen05 kernel
+ * (S^T = K Q^T, O^T += V^T P^T, keys on the MMA M dimension; <= 64 rows per
+ * sequence; auto for 5..64 rows), 3 = streaming decode kernel (<= 4 rows per
+ * sequence; auto for the bonus pass).  impls 2-5 need bf16 and dh = 128.  n_slots = number of [A, Lmax, dh] slot blocks in the
  * cache layer (bounds of the TMA tensor map). */
 int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits);
 int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int n_slots,
