@@ -25,6 +25,7 @@ ap.add_argument("--kv", type=int, default=4096)
 ap.add_argument("--rows", type=int, default=20)
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--impl", type=int, default=0)
+ap.add_argument("--cap", type=int, default=0, help="row capacity passed as max_rows_per_seq (default: --rows)")
 args = ap.parse_args()
 
 dev = torch.device("cuda:0")
@@ -53,7 +54,7 @@ def run(rows, impl):
     st = torch.cuda.current_stream().cuda_stream
 
     def launch():
-        call("propd_tree_attention", _lib.BF16, impl, B, M, A, dh, Lmax, B, rows, L + n, ptr(qkv), 3 * H, ptr(kc),
+        call("propd_tree_attention", _lib.BF16, impl, B, M, A, dh, Lmax, B, max(rows, args.cap), L + n, ptr(qkv), 3 * H, ptr(kc),
              ptr(vc), ptr(slots), ptr(lens), ptr(row_off), ptr(row_node), ptr(mask), n, tmpl.words, ptr(out), H,
              ptr(ws), wsb, torch.cuda.current_stream().cuda_stream)
 
