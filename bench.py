@@ -195,15 +195,16 @@ def in_step_view(ts: dict, kern: dict, K: int) -> dict:
 
 
 def ncu_traffic(kind: str, args) -> dict:
-    """DRAM bytes of one launch of the dominant kernel from a committed
-    `ncu --set full` capture of this bench configuration (profiles/), if any."""
+    """DRAM bytes of one launch of the dominant kernel from a committed ncu
+    capture (dram__bytes_read/write) of this bench configuration
+    (profiles/ncu_traffic.json), if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
             table = json.load(fh)
     except Exception:
         return {}
-    key = f"{kind}:b{args.batch}:kv{args.kv}:{args.mode}"
+    key = f"{kind}:b{args.batch}:kv{args.kv}:{args.mode}" + ("" if args.shape == "7b" else f":{args.shape}")
     return table.get(key, {})
 
 
