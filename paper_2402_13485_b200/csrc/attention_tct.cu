@@ -205,7 +205,6 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   static_assert(8 * (2 * KS + 2 * VS + NSB + 2 * C::NPB) + 4 <= 176, "barrier block");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned long long t_entry = p.tl ? gtimer() : 0ull;
   // independent of the predecessor: barriers, tensor-map prefetch
   if (threadIdx.x == 0) {
     for (int i = 0; i < KS; ++i) {
@@ -511,7 +510,6 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   if (p.nsplit > 1) cluster_combine<C>(smem, p.nsplit, nrows, r0, a, p.out, p.ldout);
   // kind 4: (first S seen, dependency release, softmax loop end, exit)
   if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, s_t[0], t_wait, s_t[1], 4);
-  (void)t_entry;
 }
 
 // ------------------------------------------------------------------ host --
