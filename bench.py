@@ -186,8 +186,12 @@ def in_step_view(ts: dict, kern: dict, K: int) -> dict:
     busy ms per step and the algorithmic bytes of one step over that time."""
     out = {"step_ms": ts.get("step_ms"), "note": "one traced step; busy = union of [release, last exit] per launch"}
     for k in ("gemm", "attn"):
-        if k in ts and ts[k]["busy_ms"] > 0:
-            bytes_step = kern[k]["bytes"] / K
+        if k in ts and ts[k]["busy_ms"] > 0 and kern[k]["launches"] > 0:
+            # bytes of the traced step itself: exact for the GEMMs (shape in
+            # the trace record), the timed steps' bytes per launch x the traced
+            # launch count for attention (which projections run weight-streaming
+            # vs cuBLAS follows each step's data-dependent survivor count)
+            bytes_step = ts[k].get("bytes") or kern[k]["bytes"] / kern[k]["launches"] * ts[k]["launches"]
             gbs = bytes_step / (ts[k]["busy_ms"] * 1e-3) / 1e9
             out[k] = {"busy_ms": ts[k]["busy_ms"], "launches": ts[k]["launches"], "achieved": gbs,
                       "frac": gbs / kern[k]["peak"]}
@@ -424,15 +428,21 @@ def timeline_region(be, eng, seqs, prime, dev):
     n = min(int(buf[0].item()), cap)
     rec = buf[8: 8 + 8 * n].view(n, 8).cpu().numpy()
     out = {"step_ms": t0.elapsed_time(t1), "records": n}
+    kinds = rec[:, 7] & 0xFF
     for kind, name in ((1, "gemm"), (2, "attn")):
         # kind 4 = the transposed attention kernel (same release / exit columns)
-        r = rec[(rec[:, 7] == kind) | ((rec[:, 7] == 4) if kind == 2 else False)]
+        r = rec[(kinds == kind) | ((kinds == 4) if kind == 2 else False)]
         if len(r) == 0:
             continue
         spans = []
+        nbytes = 0
         for tag in np.unique(r[:, 0]):
             g = r[r[:, 0] == tag]
             spans.append((int(g[:, 4].min()), int(g[:, 6].max())))
+            if kind == 1:  # the GEMM's shape rides in the kind word (gemm_ws.cu): its algorithmic bytes
+                w = int(g[0, 7])
+                N, Kd, M, acc = ((w >> 8) & 0xFFFF) * 128, ((w >> 24) & 0xFFFF) * 64, (w >> 40) & 0xFFFF, (w >> 56) & 1
+                nbytes += Kd * N * 2 + M * Kd * 2 + M * N * 4 * (2 if acc else 1)
         spans.sort()
         busy, cur0, cur1 = 0, None, None
         for a, b in spans:
@@ -444,6 +454,8 @@ def timeline_region(be, eng, seqs, prime, dev):
                 cur1 = max(cur1, b)
         busy += cur1 - cur0
         out[name] = {"launches": len(spans), "busy_ms": busy / 1e6}
+        if kind == 1:
+            out[name]["bytes"] = nbytes
     return out
 
 

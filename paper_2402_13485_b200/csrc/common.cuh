@@ -78,9 +78,11 @@ __device__ __forceinline__ unsigned int smid() {
   asm volatile("mov.u32 %0, %smid;" : "=r"(s));
   return s;
 }
-// kind: 1 = weight-streaming GEMM, 2 = attention (record slot 7)
+// kind (record slot 7, low byte): 1 = weight-streaming GEMM, 2 = attention, 4 = transposed attention;
+// GEMM records carry their shape above it (gemm_ws.cu: N / 128, K / 64, live rows, accumulate)
 __device__ __forceinline__ void trace_record(unsigned long long* buf, unsigned int tag, unsigned long long t0,
-                                             unsigned long long t1, unsigned long long t2, unsigned int kind = 0) {
+                                             unsigned long long t1, unsigned long long t2,
+                                             unsigned long long kind = 0) {
   if (buf == nullptr) return;
   const unsigned long long t3 = gtimer();
   const unsigned long long i = atomicAdd(buf, 1ull);
