@@ -25,7 +25,7 @@ else:
 rows = []
 for B, kv in points:
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--shape", args.shape, "--batch", str(B), "--kv", str(kv),
-           "--steps", "5", "--no-e2e", "--no-cpu-baseline"]
+           "--steps", "10", "--no-e2e", "--no-cpu-baseline"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     try:
         d = json.loads(r.stdout.strip().splitlines()[-1])
@@ -35,10 +35,12 @@ for B, kv in points:
         continue
     ins = d.get("in_step", {})
     frac = lambda k: f"{ins[k]['frac']:.2f}" if isinstance(ins.get(k), dict) else "-"
+    cap = d.get("cuda_graphs", {}).get("captures_in_timed_region", 0)
     rows.append(f"| {B} | {kv} | {d['value']:.1f} | {d['ms_per_step']:.2f} | {d.get('verify_ms_per_step', 0):.2f} | "
-                f"{frac('gemm')} | {frac('attn')} | {d['clocks']['sm_mhz']:.0f} {','.join(d['clocks']['reasons'])} |")
+                f"{d.get('tree_size_mean', 0):.1f} | {frac('gemm')} | {frac('attn')} | "
+                f"{d['clocks']['sm_mhz']:.0f} {','.join(d['clocks']['reasons'])} | {cap} |")
     print(rows[-1], flush=True)
-hdr = (f"| batch | KV | tok/s | ms/step | verify ms/step | GEMM frac (in-step) | K2 frac (in-step) | SM MHz, throttle |\n"
-       "|---|---|---|---|---|---|---|---|\n")
+hdr = ("| batch | KV | tok/s | ms/step | verify ms/step | mean tree size | GEMM frac (in-step) | K2 frac (in-step) | "
+       "SM MHz, throttle | graph captures in timed steps |\n|---|---|---|---|---|---|---|---|---|---|\n")
 with open(os.path.join(ROOT, args.out), "w") as fh:
     fh.write(hdr + "\n".join(rows) + "\n")
