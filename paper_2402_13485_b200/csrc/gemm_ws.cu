@@ -335,7 +335,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   if (p.trace && threadIdx.x == 0)  // shape in the kind word: bench.py computes this launch's algorithmic bytes
     trace_record(p.trace, p.tag, t_entry, s_t[0], s_t[1],
                  1ull | ((unsigned long long)(p.N / BF) << 8) | ((unsigned long long)(p.K / BK) << 24) |
-                     ((unsigned long long)M << 40) | ((unsigned long long)(p.accumulate ? 1 : 0) << 56));
+                     ((unsigned long long)M << 40) | ((unsigned long long)(p.accumulate ? 1 : 0) << 56) |
+                     ((unsigned long long)STAGES << 57));  // W stages prefetched before the dependency release
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
