@@ -233,10 +233,18 @@ def cpu_reference(args, steps: int, warmup: int):
     1; per-step time extrapolated to all layers (stated in `sample`)."""
     import numpy as np
 
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+    # all host threads: torchrun exports OMP_NUM_THREADS=1 to every rank, which
+    # OpenBLAS would otherwise pick up for the reference arm at N > 1
+    cores = os.cpu_count()
+    os.environ["OPENBLAS_NUM_THREADS"] = str(cores)
+    os.environ["OMP_NUM_THREADS"] = str(cores)
     from oracle import treedecode_port as op
 
-    cores = os.cpu_count()
+    try:  # numpy may already be loaded (threads fixed at load): resize its BLAS pool
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(cores)
+    except Exception:
+        pass
     Ly = 2
     kv = args.kv
     full = model_cfg(args)
