@@ -10,9 +10,12 @@ bonus pass, on-device statistics replay) over the whole batch.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N>1: launched by torchrun, one rank per GPU, sequences sharded (weak
-scaling: --batch is per GPU), one NCCL all-gather of acceptance records per
-step.  `value` = committed tokens of all ranks / max-over-ranks device time.
+N>1: bench.py re-launches itself under torchrun (one rank per GPU, NCCL),
+sequences sharded (weak scaling: --batch is per GPU), one all-gather of the
+per-step record table per step.  `value` = committed tokens of all ranks /
+max-over-ranks device time.  At N=1 the line also carries `sweep`: the
+north-star grid (configs[2]: B 1-64 x KV 1024/4096, static Medusa tree vs
+ProPD at B=1) measured in the same process.
 """
 
 from __future__ import annotations
@@ -21,6 +24,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -29,9 +33,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode tokens/sec @ batch 1-64 (7B shape); accepted len/step; verify ms/step"
+SIZES = (1, 2, 4, 8, 16, 32, 64)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -47,6 +52,10 @@ def parse():
     ap.add_argument("--attn-impl", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the north-star grid (N=1 only)")
+    ap.add_argument("--sweep-points", default="1:1024:propd_full,1:1024:static_tree,1:4096,8:1024,8:4096,32:1024,"
+                                               "32:4096,64:4096",
+                    help="B:KV[:mode] points of the in-process sweep")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA graphs")
     ap.add_argument("--acceptance", default="greedy", choices=["greedy", "typical"])
     ap.add_argument("--prune-threshold", type=float, default=None,
@@ -58,25 +67,30 @@ def parse():
     ap.add_argument("--same-device", action="store_true", help="every rank on cuda:0 (multi-rank dry run)")
     ap.add_argument("--sync-rows", action="store_true",
                     help="size the post-prune layers on the host (one mid-step sync) instead of on the device")
-    return ap.parse_args()
+    ap.add_argument("--ref-tree-sizes", default="64,64,64,32,32",
+                    help="reference arm: per-step tree sizes (cycled) it is pinned to; the default is the schedule "
+                         "the B200 arm's dynamic plan settles into at configs[1] (mean 51.2 nodes)")
+    return ap.parse_args(argv)
 
 
-def model_cfg(args):
+def model_cfg(args, kv_cap: int | None = None):
     from paper_2402_13485_b200 import VICUNA_7B_SHAPE, VICUNA_33B_SHAPE, TinyTransformerConfig
 
     shape = dict(VICUNA_7B_SHAPE if getattr(args, "shape", "7b") == "7b" else VICUNA_33B_SHAPE)
     if getattr(args, "layers", None) is not None:
         shape["layers"] = args.layers
-    return TinyTransformerConfig(**shape, max_positions=args.kv + 5 * (2 * args.steps + args.warmup + 100), seed=0)
+    kv = args.kv if kv_cap is None else kv_cap
+    return TinyTransformerConfig(**shape, max_positions=kv + 5 * (2 * args.steps + args.warmup + 110), seed=0)
 
 
-def engine_cfg(args):
+def engine_cfg(args, mode=None):
     from paper_2402_13485_b200 import EngineConfig, PruneConfig, SchedulerConfig
 
+    mode = mode or args.mode
     threshold = getattr(args, "prune_threshold", None)
-    prune = PruneConfig(layer=4, topk=50, threshold=threshold) if args.mode in ("prune_only", "propd_full") else None
-    sizes = tuple(s for s in (1, 2, 4, 8, 16, 32, 64) if s <= 4 * args.topk)
-    return EngineConfig(mode=args.mode, draft_heads=4, draft_topk=args.topk, prune=prune,
+    prune = PruneConfig(layer=4, topk=50, threshold=threshold) if mode in ("prune_only", "propd_full") else None
+    sizes = tuple(s for s in SIZES if s <= 4 * args.topk)
+    return EngineConfig(mode=mode, draft_heads=4, draft_topk=args.topk, prune=prune,
                         scheduler=SchedulerConfig(replan_period=16, size_candidates=sizes),
                         acceptance=getattr(args, "acceptance", "greedy"))
 
@@ -137,8 +151,7 @@ def peaks():
 
 
 def tensor_peak():
-    """Dense bf16 TFLOP/s for kernels timed inside a long step (sustained),
-    and the burst figure beside it."""
+    """Dense bf16 TFLOP/s for kernels timed inside a long step (sustained), and the burst figure."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
@@ -148,76 +161,12 @@ def tensor_peak():
         return 1800.0, 1800.0, "fallback (B200_PROFILING.md)"
 
 
-def roofline_line(dom: str, name: str, d: dict, ts: dict, traffic: dict, K: int, ms: float) -> dict:
-    """Roofline of the dominant kernel family.  achieved = its algorithmic
-    bytes per step / its busy device time per step inside the PDL-chained
-    step (per-CTA globaltimer records, one traced step).  CUDA events around
-    each launch (the event-bracketed region) serialise the chained launches
-    and add each launch's ramp, so they are reported beside it."""
-    tpk, tburst, tpk_kind = tensor_peak()
-    if d.get("flops", 0) / (tpk * 1e12) > d["bytes"] / (d["peak"] * 1e9) and d["ms_total"] > 0:
-        # compute-bound family (cuBLAS at hundreds of rows): the tensor roofline
-        ach = d["flops"] / (d["ms_total"] * 1e-3) / 1e12
-        return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": tpk, "unit": "TFLOP/s",
-                "frac": ach / tpk, "burst_peak": tburst, "burst_frac": ach / tburst,
-                "traffic": traffic.get("bytes_per_launch"), "peak_kind": tpk_kind,
-                "launches_per_step": d["launches"] / K, "avg_launch_us": d["avg_launch_us"],
-                "share_of_step": d["ms_total"] / ms, "timer": "CUDA events per launch (timing region)"}
-    ev = {"events_achieved": d["achieved_gbs"], "events_frac": d["achieved_gbs"] / d["peak"],
-          "events_avg_launch_us": d["avg_launch_us"]}
-    busy = ts.get(dom, {}).get("busy_ms")
-    if busy:
-        # the traced step's bytes inside the [release, exit] windows (GEMM:
-        # the prefetched weight stages excluded, see in_step_view)
-        ach = ts[dom]["achieved"] if "achieved" in ts.get(dom, {}) else (d["bytes"] / K) / (busy * 1e-3) / 1e9
-        base = {"achieved": ach, "frac": ach / d["peak"], "avg_launch_us": busy * 1e3 / max(1, ts[dom]["launches"]),
-                "share_of_step": busy / (ms / K),
-                "timer": "device globaltimer per CTA: union of [dependency release, last CTA exit] per launch"}
-        if ts[dom].get("frac_incl_prefetch") is not None:
-            ev["frac_incl_prefetch"] = ts[dom]["frac_incl_prefetch"]
-            ev["prefetch_note"] = ("weight stages streamed before each launch's dependency release (PDL prologue) "
-                                   "are excluded from `achieved`; counted inside the windows they give this frac")
-    else:
-        base = {"achieved": d["achieved_gbs"], "frac": d["achieved_gbs"] / d["peak"],
-                "avg_launch_us": d["avg_launch_us"], "share_of_step": d["ms_total"] / ms, "timer": "CUDA events"}
-    return {"kernel": name, "bound": "hbm", "achieved": base["achieved"], "peak": d["peak"], "unit": "GB/s",
-            "frac": base["frac"], "traffic": traffic.get("bytes_per_launch"), "traffic_note": traffic.get("note"),
-            "peak_kind": d["peak_kind"], "launches_per_step": d["launches"] / K,
-            "avg_launch_us": base["avg_launch_us"], "share_of_step": base["share_of_step"], "timer": base["timer"],
-            **ev}
-
-
-def in_step_view(ts: dict, kern: dict, K: int) -> dict:
-    """Kernel families inside the PDL-chained step (globaltimer records):
-    busy ms per step and the algorithmic bytes of one step over that time."""
-    out = {"step_ms": ts.get("step_ms"), "note": "one traced step; busy = union of [release, last exit] per launch"}
-    for k in ("gemm", "attn"):
-        if k in ts and ts[k]["busy_ms"] > 0 and kern[k]["launches"] > 0:
-            # bytes of the traced step itself: exact for the GEMMs (shape in
-            # the trace record), the timed steps' bytes per launch x the traced
-            # launch count for attention (which projections run weight-streaming
-            # vs cuBLAS follows each step's data-dependent survivor count)
-            bytes_step = ts[k].get("bytes") or kern[k]["bytes"] / kern[k]["launches"] * ts[k]["launches"]
-            gbs = bytes_step / (ts[k]["busy_ms"] * 1e-3) / 1e9
-            out[k] = {"busy_ms": ts[k]["busy_ms"], "launches": ts[k]["launches"], "achieved": gbs,
-                      "frac": gbs / kern[k]["peak"]}
-            if ts[k].get("prefetch_bytes"):
-                # the weight stages each launch streams while its predecessor
-                # drains are excluded above (conservative: assumes they landed
-                # before the release); counted in the window they would give
-                full = (bytes_step + ts[k]["prefetch_bytes"]) / (ts[k]["busy_ms"] * 1e-3) / 1e9
-                out[k]["prefetch_bytes"] = ts[k]["prefetch_bytes"]
-                out[k]["frac_incl_prefetch"] = full / kern[k]["peak"]
-    return out
-
-
 def ncu_traffic(kind: str, args) -> dict:
     """DRAM bytes of one launch of the dominant kernel from a committed ncu
     capture (dram__bytes_read/write) of this bench configuration
     (profiles/ncu_traffic.json), if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        with open(path) as fh:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             table = json.load(fh)
     except Exception:
         return {}
@@ -226,15 +175,21 @@ def ncu_traffic(kind: str, args) -> dict:
 
 
 # ---------------------------------------------------------------- CPU reference arm
-def cpu_reference(args, steps: int, warmup: int):
-    """The reference algorithm on host cores: oracle/treedecode_port (the
-    fp64 numpy restatement of treedecode, pinned to the real reference by
-    tests/golden) at the model width with 2 of its layers, tree mode, batch
-    1; per-step time extrapolated to all layers (stated in `sample`)."""
+def cpu_reference(args, steps: int, warmup: int, sizes=None):
+    """The reference algorithm on the host cores, on the B200 arm's workload:
+    oracle/treedecode_port (the fp64 numpy restatement of treedecode's
+    DecodeEngine._step, pinned to the real reference by tests/golden) at the
+    model's full width (hidden, heads, vocab), batch --batch, KV --kv, the same
+    mode, pruning (layer 4, top-K 50) and draft grid, with the tree size of
+    every step pinned to `sizes` (the B200 arm's schedule; the dynamic plan's
+    path selection from the running statistics is kept).  Five layers run (4
+    before the prune point, 1 after; one layer's weights shared by all five:
+    values do not change the work) and every block call is timed, so each
+    step is extrapolated to the full depth from MEASURED per-layer times:
+    T = T_step - T_blocks + p * t_pre + (L - p) * t_post + L * t_commit."""
     import numpy as np
 
-    # all host threads: torchrun exports OMP_NUM_THREADS=1 to every rank, which
-    # OpenBLAS would otherwise pick up for the reference arm at N > 1
+    # all host threads: torchrun exports OMP_NUM_THREADS=1 to every rank
     cores = os.cpu_count()
     os.environ["OPENBLAS_NUM_THREADS"] = str(cores)
     os.environ["OMP_NUM_THREADS"] = str(cores)
@@ -245,48 +200,84 @@ def cpu_reference(args, steps: int, warmup: int):
         threadpool_limits(cores)
     except Exception:
         pass
-    Ly = 2
-    kv = args.kv
     full = model_cfg(args)
-    cfg = op.TinyCfg(layers=Ly, hidden=full.hidden, heads=full.heads, vocab=full.vocab, draft_heads=4,
-                     max_positions=kv + 64, seed=0)
+    Lf = full.layers
+    p = 4
+    mode = args.mode
+    prune = op.PruneCfg(layer=p, topk=50, threshold=args.prune_threshold) if mode in ("prune_only",
+                                                                                    "propd_full") else None
+    Ly = p + 1
+    H, V, D = full.hidden, full.vocab, full.draft_heads
+    cfg = op.TinyCfg(layers=Ly, hidden=H, heads=full.heads, vocab=V, draft_heads=D,
+                     max_positions=args.kv + (D + 1) * (steps + warmup) + 8, seed=0)
     rng = np.random.default_rng(0)
-    H, V = cfg.hidden, cfg.vocab
     s = 1.0 / np.sqrt(H)
-    w = {"emb": rng.standard_normal((V, H)) * s, "pos": rng.standard_normal((cfg.max_positions, H)) * s,
-         "blocks": [{k: rng.standard_normal(sh) * s for k, sh in
-                     (("wq", (H, H)), ("wk", (H, H)), ("wv", (H, H)), ("wo", (H, H)), ("w1", (H, 4 * H)),
-                      ("w2", (4 * H, H)))} for _ in range(Ly)],
-         "w_lm": rng.standard_normal((H, V)) * s, "w_early": rng.standard_normal((H, V)) * s,
-         "w_draft": rng.standard_normal((4, H, V)) * s}
-    if args.planted:
-        w["w_draft"][0] = w["w_lm"]
-    model = op.TinyModel(cfg, weights=w)
-    prune = op.PruneCfg(layer=1, topk=50) if args.mode in ("prune_only", "propd_full") else None
-    ecfg = op.EngineCfg(mode=args.mode, draft_heads=4, draft_topk=args.topk, prune=prune,
-                        scheduler=op.SchedCfg(size_candidates=tuple(x for x in (1, 2, 4, 8, 16, 32, 64)
-                                                                    if x <= 4 * args.topk)))
-    eng = op.Engine(model, ecfg, None)
-    prompt = rng.integers(0, V, size=kv).tolist()
-    seqs = [{"state": model.prefill(prompt), "prompt": prompt, "gen": [], "done": False}]
-    times, toks, acc = [], 0, 0.0
+    blk = {k: rng.standard_normal(sh) * s for k, sh in (("wq", (H, H)), ("wk", (H, H)), ("wv", (H, H)),
+                                                         ("wo", (H, H)), ("w1", (H, 4 * H)))}
+    blk["w2"] = rng.standard_normal((4 * H, H)) * (0.5 * s)
+    head = rng.standard_normal((H, V)) * s
+    w = {"emb": np.ascontiguousarray(head.T), "pos": rng.standard_normal((cfg.max_positions, H)) * s,
+         "blocks": [blk] * Ly, "w_lm": head, "w_early": head, "w_draft": [head] * D}
+    log: list = []
+
+    class TimedModel(op.TinyModel):
+        def block(self, x, li, kc, vc, vis):
+            t0 = time.perf_counter()
+            out = super().block(x, li, kc, vc, vis)
+            log.append((li, time.perf_counter() - t0))
+            return out
+
+    model = TimedModel(cfg, weights=w)
+    sizes = list(sizes) if sizes else [4 * args.topk]
+
+    class PinnedEngine(op.Engine):
+        def _plan(self, B, seqlen):  # size pinned per step; paths = the statistics' best nodes (acceptance.py:186-206)
+            if not self.cfg.uses_dynamic:
+                return super()._plan(B, seqlen)
+            size = min(sizes[(self.it - 1) % len(sizes)], self.cfg.draft_heads * self.cfg.draft_topk)
+            return op.select_best_nodes(self.stats, [size])[size][0], False
+
+    ecfg = op.EngineCfg(mode=mode, draft_heads=D, draft_topk=args.topk, prune=prune,
+                        scheduler=op.SchedCfg(size_candidates=tuple(x for x in SIZES if x <= D * args.topk)),
+                        acceptance=args.acceptance)
+    eng = PinnedEngine(model, ecfg, None)
+    prompts = [rng.integers(0, V, size=args.kv).tolist() for _ in range(args.batch)]
+    seqs = [{"state": model.prefill(pr), "prompt": pr, "gen": [], "done": False} for pr in prompts]
+    per_step, toks, acc, tree = [], 0, 0.0, 0.0
     for i in range(warmup + steps):
+        log.clear()
         t0 = time.perf_counter()
         m = eng.step(seqs, 10 ** 9)
         dt = time.perf_counter() - t0
-        if i >= warmup:
-            times.append(dt)
-            toks += m["tokens_committed"]
-            acc += m["mean_accepted"]
-    Lf = full.layers
-    per_step = sum(times) / len(times) * (Lf / Ly)
-    value = toks / (sum(times) * (Lf / Ly))
-    sample = (f"oracle/treedecode_port (fp64 numpy restatement of the reference) at {args.shape.upper()} width "
-              f"({full.hidden}), {Ly} of {Lf} layers, batch 1, KV {kv}, {steps} decode steps after {warmup} warm-up; "
-              f"time x{Lf // Ly} to {Lf} layers (extrapolated); "
-              f"OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS')}")
-    return {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample,
-            "ms_per_step": per_step * 1e3, "accepted_len_per_step": acc / max(1, steps)}
+        if i < warmup:
+            continue
+        # block calls: the tree pass (Ly per sequence, in order) then each commit's extend (Ly)
+        t_blocks = sum(t for _, t in log)
+        per_seq = [log[j: j + 2 * Ly] for j in range(0, len(log), 2 * Ly)]
+        extr = dt - t_blocks
+        for calls in per_seq:
+            tree_calls, commit_calls = calls[:Ly], calls[Ly:]
+            if prune is not None:
+                t_pre = sum(t for _, t in tree_calls[:p]) / p
+                t_post = sum(t for _, t in tree_calls[p:]) / (Ly - p)
+                extr += p * t_pre + (Lf - p) * t_post
+            else:
+                extr += Lf * sum(t for _, t in tree_calls) / Ly
+            extr += Lf * sum(t for _, t in commit_calls) / max(1, len(commit_calls))
+        per_step.append(extr)
+        toks += m["tokens_committed"]
+        acc += m["mean_accepted"]
+        tree += m["tree_size"]
+    total = sum(per_step)
+    sample = (f"oracle/treedecode_port (fp64 numpy restatement of the reference DecodeEngine._step) at "
+              f"{args.shape.upper()} width (hidden {H}, {full.heads} heads, vocab {V}), batch {args.batch}, KV {args.kv}, "
+              f"{mode}" + (f" (prune layer {p}, top-K 50)" if prune is not None else "") +
+              f", tree size pinned per step to {sizes} (the B200 arm's schedule), {steps} steps timed after {warmup} "
+              f"warm-up; {Ly} layers run ({p} before the prune point), every block timed, each step extrapolated to "
+              f"{Lf} layers from the measured per-layer times; OPENBLAS_NUM_THREADS={cores}")
+    return {"value": toks / total, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample,
+            "ms_per_step": total / steps * 1e3, "accepted_len_per_step": acc / steps, "tree_size_mean": tree / steps,
+            "steps": steps}
 
 
 # ---------------------------------------------------------------- B200 arm
@@ -297,8 +288,7 @@ def local_device(args):
 
 
 def all_max(value: float, group, dev) -> float:
-    """Max over ranks (identity without a process group); fp64 on the
-    backend's device (NCCL: the GPU, gloo: host)."""
+    """Max over ranks (identity without a process group)."""
     if group is None:
         return float(value)
     import torch
@@ -310,119 +300,31 @@ def all_max(value: float, group, dev) -> float:
     return float(t.item())
 
 
-def run_b200(args, rank: int, world: int, group):
-    import numpy as np
-    import torch
-
-    from paper_2402_13485_b200 import B200Backend, DecodeEngine
-    from paper_2402_13485_b200.engine import _Seq
-
-    dev = local_device(args)
-    torch.cuda.set_device(dev)
-    cfg = model_cfg(args)
-    B = args.batch
-    be = B200Backend(cfg, dtype="bf16", device=dev, random_device_init=True, max_slots=B + 1, max_tree=4 * args.topk,
-                     kv_len=cfg.max_positions, attn_impl=args.attn_impl, use_graphs=not args.no_graphs)
-    if args.planted:
-        be.plant_draft_head(0)
-    eng = DecodeEngine(be, engine_cfg(args), None, group=group)
-    states = be.synthetic_states(B, args.kv, seed=1000 + rank)
-    seqs = [_Seq(st, st.committed[:], rank * B + i) for i, st in enumerate(states)]
-    if args.sync_rows:
-        be.device_rows = False
-
-    def prime():
-        # untimed priming: run until no new CUDA graph has been captured for 6
-        # consecutive steps (every tree size / survivor-row bucket seen so far
-        # has its graphs)
-        # has its graphs).  Under torchrun the decision is collective (every
-        # rank runs the same number of steps: the steps contain collectives)
-        stable, n = 0, 0
-        while stable < 6 and n < 48:
-            n_graphs = len(be._graphs)
-            eng._step(seqs, 10 ** 9)
-            n += 1
-            changed = all_max(float(len(be._graphs) != n_graphs), group, dev)
-            stable = stable + 1 if changed == 0.0 else 0
-        return n
-
-    primed = prime()
-    for _ in range(args.warmup):
-        eng._step(seqs, 10 ** 9)
-    graphs_before = len(be._graphs)
-    torch.cuda.synchronize()
-    if group is not None:
-        torch.distributed.barrier(group)
-    be.attn_timer = None  # clean timed region: no per-launch event harvesting on the host
-    launches0 = be.launches
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    metrics = []
-    with ClockSampler(dev.index) as clk:
-        t_start.record()
-        for _ in range(args.steps):
-            metrics.append(eng._step(seqs, 10 ** 9))
-        t_end.record()
-        torch.cuda.synchronize()
-        if group is not None:
-            torch.distributed.barrier(group)
-    ms = t_start.elapsed_time(t_end)
-    launches = be.launches - launches0
-    captures_in_timed = len(be._graphs) - graphs_before
-    # second timed region of K steps: per-launch CUDA events around every K2
-    # launch (event nodes inside separately captured graphs), harvested after
-    # each step
-    be.attn_timer = []
-    prime()
-    be.attn_timer = []
-    for _ in range(args.steps):
-        eng._step(seqs, 10 ** 9)
-    torch.cuda.synchronize()
-    attn = be.attn_timer
-    be.attn_timer = None
-    # third region: only the two verify-pass markers per step (the PDL chain
-    # stays intact elsewhere): "verify ms/step" of BASELINE's metric
-    be.attn_timer, be.mark_only = [], True
-    prime()
-    be.attn_timer = []
-    for _ in range(args.steps):
-        eng._step(seqs, 10 ** 9)
-    torch.cuda.synchronize()
-    verify = [r["ms"] for r in be.attn_timer if r.get("kind") == "verify"]
-    be.attn_timer, be.mark_only = None, False
-    in_step = timeline_region(be, eng, seqs, prime, dev)
-    ms = all_max(ms, group, dev)
-    tokens = sum(m.tokens_committed for m in metrics)  # engine metrics are already global
-    hbm, peak_kind = peaks()
-    kernels = {}
-    for kind in ("gemm", "attn", "cublas"):
-        rs = [r for r in attn if r.get("kind", "attn") == kind]
-        k_ms, k_bytes = sum(r["ms"] for r in rs), sum(r["bytes"] for r in rs)
-        k_flops = sum(r.get("flops", 0) for r in rs)
-        kernels[kind] = {"launches": len(rs), "ms_total": k_ms, "bytes": k_bytes, "flops": k_flops,
-                         "achieved_gbs": k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0,
-                         "avg_launch_us": k_ms / max(1, len(rs)) * 1e3, "peak": hbm, "peak_kind": peak_kind}
-    kernels["attn"]["verify_ms_total"] = sum(r["ms"] for r in attn
-                                             if r.get("kind", "attn") == "attn" and r["role"].startswith("tree"))
-    out = {
-        "ms": ms, "tokens": tokens, "metrics": metrics, "launches": launches, "clock": clk.summary(),
-        "kernels": kernels, "in_step": in_step, "verify_ms": sum(verify) / max(1, len(verify)),
-        "weights_bytes": be.w.nbytes(), "priming_steps": primed, "captures_in_timed": captures_in_timed,
-    }
-    for st in states:  # free the synthetic sequences' cache slots for the e2e run
-        be.release(st)
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(args, be, eng, rank, world, group)
-    out["e2e"] = e2e
-    return out
+def attn_step_bytes(be, m, prune_layer) -> float:
+    """Algorithmic K2 bytes of one engine step from its metrics:
+    per layer and sequence 2 (L_b + r_b) H elt of cache + tree K/V read plus
+    r_b H elt of Q read and O written; tree pass r = n (layers <= p) / |S_b|
+    (layers > p), bonus pass r = 1 over L_b + acc_b + 1 keys."""
+    H, Ly = be.H, be.num_layers
+    elt = 2 if be.tdtype != be.torch.float32 else 4
+    B, n = m.batch, m.tree_size
+    L0 = m.mean_seqlen * B
+    f = lambda keys, rows: (2 * keys + 2 * rows) * H * elt
+    if n == 0:  # autoregressive
+        return Ly * f(L0 + B, B)
+    p = prune_layer if prune_layer is not None else Ly
+    S = m.mean_survivors * B
+    tree = p * f(L0 + B * n, B * n) + (Ly - p) * f(L0 + B * n, S)
+    return tree + Ly * f(L0 + m.mean_accepted * B + B, B)
 
 
-def timeline_region(be, eng, seqs, prime, dev):
-    """One more step with per-CTA globaltimer records (graphs captured with
-    the trace on): busy time of each kernel family inside the PDL-chained
-    step = union over its launches of [first dependency release, last CTA
-    exit].  Unlike the event-bracketed region this keeps the programmatic
-    overlap between launches, so it is the in-step view of the same kernels."""
+def timeline_step(be, eng, seqs, prime, dev, prune_layer):
+    """One step with per-CTA globaltimer records (graphs captured with the
+    trace on): busy time of each kernel family inside the PDL-chained step =
+    union over its launches of [dependency release, last CTA exit]; GEMM bytes
+    from the shapes in the trace records (weight stages streamed before a
+    launch's release are left out of its window's bytes: conservative),
+    attention bytes from the step's metrics."""
     import ctypes
 
     import numpy as np
@@ -440,7 +342,7 @@ def timeline_region(be, eng, seqs, prime, dev):
         buf[0] = 0
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
-        eng._step(seqs, 10 ** 9)
+        m = eng._step(seqs, 10 ** 9)
         t1.record()
         torch.cuda.synchronize()
     finally:
@@ -450,27 +352,25 @@ def timeline_region(be, eng, seqs, prime, dev):
     rec = buf[8: 8 + 8 * n].view(n, 8).cpu().numpy()
     out = {"step_ms": t0.elapsed_time(t1), "records": n}
     kinds = rec[:, 7] & 0xFF
+    hbm, _ = peaks()
     for kind, name in ((1, "gemm"), (2, "attn")):
         # kind 4 = the transposed attention kernel (same release / exit columns)
         r = rec[(kinds == kind) | ((kinds == 4) if kind == 2 else False)]
         if len(r) == 0:
             continue
         spans = []
-        nbytes = npre = 0
+        nbytes = 0
         for tag in np.unique(r[:, 0]):
             g = r[r[:, 0] == tag]
             spans.append((int(g[:, 4].min()), int(g[:, 6].max())))
-            if kind == 1:  # the GEMM's shape rides in the kind word (gemm_ws.cu): its algorithmic bytes
+            if kind == 1:  # the GEMM's shape rides in the kind word (gemm_ws.cu)
                 w = int(g[0, 7])
                 N, Kd, M, acc = ((w >> 8) & 0xFFFF) * 128, ((w >> 24) & 0xFFFF) * 64, (w >> 40) & 0xFFFF, (w >> 56) & 1
                 stages = (w >> 57) & 7
-                # weight stages each CTA streamed before its dependency release
-                # (outside the [release, exit] window): not counted in the window
                 ctas, tiles = len(g), max(1, N // 128)
                 per = -(-(Kd // 64) // max(1, ctas // tiles))
                 pre = ctas * min(stages, per) * 128 * 64 * 2
                 nbytes += Kd * N * 2 + M * Kd * 2 + M * N * 4 * (2 if acc else 1) - pre
-                npre += pre
         spans.sort()
         busy, cur0, cur1 = 0, None, None
         for a, b in spans:
@@ -481,59 +381,306 @@ def timeline_region(be, eng, seqs, prime, dev):
             else:
                 cur1 = max(cur1, b)
         busy += cur1 - cur0
-        out[name] = {"launches": len(spans), "busy_ms": busy / 1e6}
-        if kind == 1:
-            out[name]["bytes"] = nbytes  # streamed inside the windows
-            out[name]["prefetch_bytes"] = npre  # streamed before the dependency release (PDL prologue)
+        if kind == 2:
+            nbytes = attn_step_bytes(be, m, prune_layer)
+        busy_ms = busy / 1e6
+        gbs = nbytes / (busy_ms * 1e-3) / 1e9 if busy_ms > 0 else 0.0
+        out[name] = {"launches": len(spans), "busy_ms": busy_ms, "bytes": nbytes, "achieved": gbs, "frac": gbs / hbm,
+                     "share_of_step": busy_ms / out["step_ms"]}
+    return out
+
+
+def prime_fn(be, eng, seqs, group, dev):
+    def prime():
+        # untimed: run until no new CUDA graph has been captured for 6
+        # consecutive steps.  Under torchrun the decision is collective (every
+        # rank runs the same number of steps: the steps contain a collective)
+        stable, n = 0, 0
+        while stable < 6 and n < 48:
+            n_graphs = len(be._graphs)
+            eng._step(seqs, 10 ** 9)
+            n += 1
+            changed = all_max(float(len(be._graphs) != n_graphs), group, dev)
+            stable = stable + 1 if changed == 0.0 else 0
+        return n
+    return prime
+
+
+def timed_steps(be, eng, seqs, K, group, dev):
+    """K steps bracketed by a barrier + synchronize, CUDA events on the launch stream."""
+    import torch
+
+    torch.cuda.synchronize()
+    if group is not None:
+        torch.distributed.barrier(group)
+    launches0, graphs0 = be.launches, len(be._graphs)
+    stream = torch.cuda.current_stream(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    metrics = []
+    with ClockSampler(dev.index) as clk:
+        t0.record(stream)
+        for _ in range(K):
+            metrics.append(eng._step(seqs, 10 ** 9))
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if group is not None:
+            torch.distributed.barrier(group)
+    return {"ms": all_max(t0.elapsed_time(t1), group, dev), "metrics": metrics, "clock": clk.summary(),
+            "launches": be.launches - launches0, "captures": len(be._graphs) - graphs0}
+
+
+def verify_ms(be, eng, seqs, prime, K):
+    """BASELINE's verify ms/step: two event nodes per step bracketing the tree
+    pass (K1 -> layers -> K3 -> LM argmax -> K5) in otherwise unmodified graphs."""
+    import torch
+
+    be.attn_timer, be.mark_only = [], True
+    try:
+        prime()
+        be.attn_timer = []
+        for _ in range(K):
+            eng._step(seqs, 10 ** 9)
+        torch.cuda.synchronize()
+        v = [r["ms"] for r in be.attn_timer if r.get("kind") == "verify"]
+    finally:
+        be.attn_timer, be.mark_only = None, False
+    return sum(v) / max(1, len(v))
+
+
+def run_b200(args, rank: int, world: int, group):
+    import torch
+
+    from paper_2402_13485_b200 import B200Backend, DecodeEngine
+    from paper_2402_13485_b200.engine import _Seq
+
+    dev = local_device(args)
+    torch.cuda.set_device(dev)
+    cfg = model_cfg(args)
+    B = args.batch
+    be = B200Backend(cfg, dtype="bf16", device=dev, random_device_init=True, max_slots=B + 1, max_tree=4 * args.topk,
+                     kv_len=cfg.max_positions, attn_impl=args.attn_impl, use_graphs=not args.no_graphs)
+    if args.planted:
+        be.plant_draft_head(0)
+    ecfg = engine_cfg(args)
+    eng = DecodeEngine(be, ecfg, None, group=group)
+    states = be.synthetic_states(B, args.kv, seed=1000 + rank)
+    seqs = [_Seq(st, st.committed[:], rank * B + i) for i, st in enumerate(states)]
+    if group is not None:  # the engine's multi-rank view of this synthetic batch
+        from paper_2402_13485_b200.engine import _Global
+
+        eng._glob = _Global([s.prompt for _ in range(world) for s in seqs], world)
+    if args.sync_rows:
+        be.device_rows = False
+    prime = prime_fn(be, eng, seqs, group, dev)
+    primed = prime()
+    for _ in range(args.warmup):
+        eng._step(seqs, 10 ** 9)
+    be.attn_timer = None  # clean timed region: no per-launch event harvesting on the host
+    main = timed_steps(be, eng, seqs, args.steps, group, dev)
+    # second region of K steps: CUDA events around every K2 / GEMM launch
+    # (event nodes inside separately captured graphs, each launch serialised)
+    be.attn_timer = []
+    prime()
+    be.attn_timer = []
+    for _ in range(args.steps):
+        eng._step(seqs, 10 ** 9)
+    torch.cuda.synchronize()
+    events = be.attn_timer
+    be.attn_timer = None
+    vms = verify_ms(be, eng, seqs, prime, args.steps)
+    prune_layer = ecfg.prune.layer if ecfg.uses_prune else None
+    in_step = timeline_step(be, eng, seqs, prime, dev, prune_layer)
+    hbm, peak_kind = peaks()
+    kernels = {}
+    for kind in ("gemm", "attn", "cublas"):
+        rs = [r for r in events if r.get("kind", "attn") == kind]
+        k_ms, k_bytes = sum(r["ms"] for r in rs), sum(r["bytes"] for r in rs)
+        k_flops = sum(r.get("flops", 0) for r in rs)
+        kernels[kind] = {"launches": len(rs), "ms_total": k_ms, "bytes": k_bytes, "flops": k_flops,
+                         "achieved_gbs": k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0,
+                         "avg_launch_us": k_ms / max(1, len(rs)) * 1e3, "peak": hbm, "peak_kind": peak_kind}
+    out = {"main": main, "kernels": kernels, "in_step": in_step, "verify_ms": vms, "priming_steps": primed,
+           "streamed_bytes": be.w.streamed_bytes_per_step(prune=ecfg.uses_prune)}
+    for st in states:  # free the synthetic sequences' cache slots for the e2e run
+        be.release(st)
+    eng._glob = None
+    out["e2e"] = None if args.no_e2e else run_e2e(args, be, eng, rank, world, group)
+    del be, eng, states, seqs
+    torch.cuda.empty_cache()
     return out
 
 
 def run_e2e(args, be, eng, rank, world, group):
     """End-to-end through the public API: DecodeEngine.run(prompts) from host
-    token lists (H2D of prompts, batched prefill, decode, D2H of tokens)."""
+    token lists at the same KV length as `value` (H2D of the prompts, batched
+    prefill, decode of 64 new tokens per sequence, per-step D2H of the step's
+    results), wall clock, max over ranks."""
     import numpy as np
     import torch
 
     rng = np.random.default_rng(7)
     n_prompts = args.batch * world
-    kv = min(args.kv, 512)
-    prompts = [rng.integers(0, be.V, size=kv).tolist() for _ in range(n_prompts)]
-    max_tokens = 8
-    eng.run(prompts[: world], 2, batch_size=world)  # warm path
+    prompts = [rng.integers(0, be.V, size=args.kv).tolist() for _ in range(n_prompts)]
+    max_tokens = 64
+    eng.run([p[: args.kv] for p in prompts[:world]], 2, batch_size=world)  # warm path (prefill at this length)
     torch.cuda.synchronize()
     if group is not None:
         torch.distributed.barrier(group)
+    graphs0 = len(be._graphs)
     t0 = time.perf_counter()
     res = eng.run(prompts, max_tokens, batch_size=n_prompts)
     torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    dt = all_max(dt, group, be.device)
+    dt = all_max(time.perf_counter() - t0, group, be.device)
     toks = sum(len(t) for t in res.transcripts)
-    h2d = sum(len(p) for p in prompts) * 4
-    return {"value": toks / dt, "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / max(1, res.summary.iterations)),
-            "d2h_bytes_per_step": int(n_prompts * (4 + 1) * 4 * 3), "what": (
-                f"DecodeEngine.run of {n_prompts} prompts x {kv} tokens, {max_tokens} new tokens each, "
-                "wall clock incl. prefill, H2D of prompts and per-step D2H of committed tokens")}
+    iters = max(1, res.summary.iterations)
+    D, G = 4, 4 * args.topk
+    hb = be._host.get((args.batch, D, G))
+    d2h = sum(t.numel() * t.element_size() for t in hb.values()) if hb else 0
+    return {"value": toks / dt, "unit": "tokens/s",
+            "h2d_bytes_per_step": int(sum(len(p) for p in prompts) * 4 / iters),
+            "d2h_bytes_per_step": int(d2h * world),
+            "captures": len(be._graphs) - graphs0,
+            "what": (f"DecodeEngine.run of {n_prompts} prompts x {args.kv} tokens (host lists), {max_tokens} new "
+                     "tokens each, wall clock incl. H2D of the prompts, batched prefill, decode and the per-step D2H "
+                     f"of each step's results ({iters} iterations)")}
+
+
+def run_sweep(args, dev):
+    """The north-star grid in this process (configs[2]; static tree vs ProPD at
+    B=1, configs[1]): one backend sized for the largest point, a fresh synthetic
+    batch per point; tok/s from a clean timed region, verify ms from the marker
+    region, K2 / GEMM in-step roofline fractions from one traced step."""
+    import torch
+
+    from paper_2402_13485_b200 import B200Backend, DecodeEngine
+    from paper_2402_13485_b200.engine import _Seq
+
+    pts = []
+    for spec in args.sweep_points.split(","):
+        f = spec.split(":")
+        pts.append((int(f[0]), int(f[1]), f[2] if len(f) > 2 else "propd_full"))
+    K = 5
+    kv_max, b_max = max(p[1] for p in pts), max(p[0] for p in pts)
+    margin = 5 * (3 * 48 + 3 * K + 8)
+    import copy
+
+    sargs = copy.copy(args)
+    sargs.steps, sargs.warmup = K, 0
+    cfg = model_cfg(sargs, kv_cap=kv_max)
+    cfg = type(cfg)(**{**cfg.__dict__, "max_positions": kv_max + margin})
+    be = B200Backend(cfg, dtype="bf16", device=dev, random_device_init=True, max_slots=b_max,
+                     max_tree=4 * args.topk, kv_len=cfg.max_positions, use_graphs=True)
+    rows = []
+    for B, kv, mode in pts:
+        t_start = time.perf_counter()
+        row = {"batch": B, "kv": kv, "mode": mode}
+        try:
+            ecfg = engine_cfg(args, mode)
+            eng = DecodeEngine(be, ecfg, None)
+            states = be.synthetic_states(B, kv, seed=B * 7919 + kv)
+            seqs = [_Seq(st, st.committed[:], i) for i, st in enumerate(states)]
+            prime = prime_fn(be, eng, seqs, None, dev)
+            prime()
+            r = timed_steps(be, eng, seqs, K, None, dev)
+            m = r["metrics"]
+            vms = verify_ms(be, eng, seqs, prime, 3)
+            ins = timeline_step(be, eng, seqs, prime, dev, ecfg.prune.layer if ecfg.uses_prune else None)
+            row.update({"tok_s": sum(x.tokens_committed for x in m) / (r["ms"] * 1e-3), "ms_per_step": r["ms"] / K,
+                        "verify_ms_per_step": vms, "accepted_len_per_step": sum(x.mean_accepted for x in m) / K,
+                        "tree_size_mean": sum(x.tree_size for x in m) / K,
+                        "k2_frac_in_step": ins.get("attn", {}).get("frac"),
+                        "gemm_frac_in_step": ins.get("gemm", {}).get("frac"),
+                        "k2_share_of_step": ins.get("attn", {}).get("share_of_step"),
+                        "clocks": r["clock"], "captures_in_timed_region": r["captures"]})
+            for st in states:
+                be.release(st)
+        except Exception as exc:  # a point that does not fit is reported, not fatal
+            row["error"] = f"{type(exc).__name__}: {exc}"[:200]
+            torch.cuda.synchronize()
+        row["wall_s"] = round(time.perf_counter() - t_start, 1)
+        rows.append(row)
+    del be
+    torch.cuda.empty_cache()
+    return {"points": rows, "steps_per_point": K,
+            "note": ("B200 arm, same process and kernels as `value`: 7B shape, random init, tok/s = committed tokens / "
+                     "device time of 5 steps after graph priming; K2 / GEMM fractions of the measured copy peak inside "
+                     "one traced step (union of [dependency release, last CTA exit] per launch); static_tree = the "
+                     "full 64-node Medusa grid without pruning")}
+
+
+def roofline(res, args) -> dict:
+    """Roofline of the kernel family with the largest busy share of the traced step."""
+    ins = res["in_step"]
+    fam = {k: v for k, v in ins.items() if isinstance(v, dict)}
+    dom = max(fam, key=lambda k: fam[k]["busy_ms"])
+    d = fam[dom]
+    hbm, peak_kind = peaks()
+    ev = res["kernels"].get(dom, {})
+    names = {"gemm": "weight-streaming tcgen05 projections (propd_gemm_ws, <= 128 rows)",
+             "attn": "K2 tree-masked verification attention (tcgen05 tcT / tc2 kernels + streaming decode kernel)"}
+    out = {"kernel": names[dom], "bound": "hbm", "achieved": d["achieved"], "peak": hbm, "unit": "GB/s",
+           "frac": d["achieved"] / hbm, "traffic": ncu_traffic(dom, args).get("bytes_per_launch"),
+           "traffic_note": ncu_traffic(dom, args).get("note"), "peak_kind": peak_kind,
+           "launches_per_step": d["launches"], "avg_launch_us": d["busy_ms"] * 1e3 / max(1, d["launches"]),
+           "share_of_step": d["share_of_step"],
+           "algorithmic_bytes_per_step": d["bytes"],
+           "timer": "device globaltimer per CTA: union of [dependency release, last CTA exit] per launch, one step"}
+    if ev.get("launches"):
+        out["events_achieved"] = ev["achieved_gbs"]
+        out["events_frac"] = ev["achieved_gbs"] / hbm
+        out["events_avg_launch_us"] = ev["avg_launch_us"]
+        out["events_note"] = "CUDA events around each launch (serialises the PDL chain; ramp included)"
+    return out
+
+
+def reference_line(args):
+    ref = cpu_reference(args, args.steps, args.warmup, [int(x) for x in args.ref_tree_sizes.split(",")])
+    return {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "n_gpus": args.gpus, "steps": ref["steps"],
+            "warmup": args.warmup, "ms_per_step": ref["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (random-init weights and prompts)",
+            "impl": "reference",
+            "config": config_block(args, 1),
+            "accepted_len_per_step": ref["accepted_len_per_step"], "tree_size_mean": ref["tree_size_mean"],
+            "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def config_block(args, world):
+    shape7 = args.shape == "7b"
+    return {"workload": ("configs[1]: Vicuna-7B-shape" if shape7 else "configs[3]: Vicuna-33B-shape")
+                        + f" random-init bf16, batch {args.batch}/GPU, KV {args.kv}, {args.mode}"
+                        + (", planted draft head 0 (accepts depth-1 nodes)" if args.planted else ""),
+            "model": ("vicuna-7b-shape (32L, 4096, 32x128, V32000, 4 draft heads)" if shape7
+                      else "vicuna-33b-shape (60L, 6656, 52x128, V32000, 4 draft heads)"),
+            "batch_per_gpu": args.batch, "global_batch": args.batch * world, "kv": args.kv, "mode": args.mode,
+            "draft_topk": args.topk,
+            "prune": ("layer 4, top-K 50" if args.prune_threshold is None
+                      else f"layer 4, path probability >= {args.prune_threshold}"),
+            "acceptance": args.acceptance, "parallelism": f"dp{world} (sequence-sharded replicas)",
+            "l2": "inputs larger than L2 (14.8 GB of weights stream twice per step)"}
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 outside torchrun: run this script under torchrun, one rank per GPU."""
+    import random
+
+    port = str(29600 + random.randint(0, 3000))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
-        if rank != 0:
-            return
-        ref = cpu_reference(args, max(1, min(args.steps, 3)), min(args.warmup, 1))
-        line = {"metric": METRIC, "value": ref["value"], "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ref["ms_per_step"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "impl": "reference",
-                "config": {"workload": "configs[1]: Vicuna-7B-shape, batch 1, ProPD pruned+dynamic tree (CPU sample)",
-                           "batch": 1, "kv": args.kv, "mode": args.mode, "draft_topk": args.topk},
-                "accepted_len_per_step": ref["accepted_len_per_step"],
-                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": ref["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        if rank == 0:  # the CPU path: rank 0 alone, every host thread
+            print(json.dumps(reference_line(args)))
         return
     group = None
     if world > 1:
@@ -544,34 +691,30 @@ def main():
         dist.init_process_group(args.dist_backend)
         group = dist.group.WORLD
     res = run_b200(args, rank, world, group)
+    sweep = None
+    if world == 1 and not args.no_sweep:
+        sweep = run_sweep(args, local_device(args))
     if rank != 0:
         if group is not None:
             import torch.distributed as dist
 
             dist.destroy_process_group()
         return
+    main_r = res["main"]
+    m, ms, K = main_r["metrics"], main_r["ms"], args.steps
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        try:
-            cpu = cpu_reference(args, 1, 0)
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        try:  # the reference arm's measurement on this arm's own tree-size schedule
+            steps = min(K, 4)
+            c = cpu_reference(args, steps, 1, [x.tree_size for x in m[:steps]])
+            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc}"}
-    m = res["metrics"]
-    ms = res["ms"]
-    K = args.steps
     kern = res["kernels"]
-    a = kern["attn"]
-    dom = max(kern, key=lambda k: kern[k]["ms_total"])  # the kernel family with the largest share of the step
-    d = kern[dom]
-    names = {"gemm": "weight-streaming tcgen05 projections (propd_gemm_ws, <= 128 rows)",
-             "attn": "K2 tree-masked verification attention (tc2 tcgen05 / streaming decode kernel)",
-             "cublas": "cuBLAS projections (torch.mm, > 128 rows)"}
-    traffic = ncu_traffic(dom, args)
     line = {
         "metric": METRIC,
-        "value": res["tokens"] / (ms * 1e-3),
+        "value": main_r["metrics"] and sum(x.tokens_committed for x in m) / (ms * 1e-3),
         "unit": "tokens/s",
         "n_gpus": world,
         "steps": K,
@@ -582,40 +725,29 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (random-init weights, random KV/prompt state)",
-        "config": {"workload": ("configs[1]: Vicuna-7B-shape" if args.shape == "7b" else "configs[3]: Vicuna-33B-shape")
-                               + " random-init bf16, ProPD pruned+dynamic tree"
-                               + (", planted draft head 0 (accepts depth-1 nodes)" if args.planted else ""),
-                   "model": ("vicuna-7b-shape (32L, 4096, 32x128, V32000, 4 draft heads)" if args.shape == "7b"
-                             else "vicuna-33b-shape (60L, 6656, 52x128, V32000, 4 draft heads)"),
-                   "layers": model_cfg(args).layers,
-                   "batch_per_gpu": args.batch, "global_batch": args.batch * world, "kv": args.kv,
-                   "mode": args.mode, "draft_topk": args.topk,
-                   "prune": ("layer 4, top-K 50" if args.prune_threshold is None
-                             else f"layer 4, path probability >= {args.prune_threshold}"),
-                   "acceptance": args.acceptance,
-                   "parallelism": f"dp{world} (sequence-sharded replicas)",
-                   "l2": f"inputs larger than L2 ({res['weights_bytes'] / 1e9:.1f} GB of weights stream every step)"},
+        "config": config_block(args, world),
         "accepted_len_per_step": sum(x.mean_accepted for x in m) / K,
         "tree_size_mean": sum(x.tree_size for x in m) / K,
+        "tree_sizes": [x.tree_size for x in m],
         "prune_rate_mean": sum(x.prune_rate for x in m) / K,
         "verify_ms_per_step": res["verify_ms"],
         "verify_ms_note": ("tree pass K1 -> layers -> K3 -> LM argmax -> K5 (excludes draft heads and the bonus pass): "
                            "two CUDA event nodes per step in otherwise unmodified graphs, mean over K steps"),
-        "verify_attention_ms_per_step": a["verify_ms_total"] / K,
-        "attention_ms_per_step": a["ms_total"] / K,
-        "projection_ms_per_step": (kern["gemm"]["ms_total"] + kern["cublas"]["ms_total"]) / K,
-        "roofline": roofline_line(dom, names[dom], d, in_step_view(res["in_step"], kern, K), traffic, K, ms),
+        "roofline": roofline(res, args),
         "roofline_by_kernel": {k: {"achieved": v["achieved_gbs"], "frac": v["achieved_gbs"] / v["peak"],
                                    "tflops": (v["flops"] / (v["ms_total"] * 1e-3) / 1e12) if v["ms_total"] > 0 else 0.0,
                                    "ms_per_step": v["ms_total"] / K, "launches_per_step": v["launches"] / K,
                                    "avg_launch_us": v["avg_launch_us"]} for k, v in kern.items()},
-        "in_step": in_step_view(res["in_step"], kern, K),
-        "step_weight_gbs": res["weights_bytes"] * 2 / (ms / K * 1e-3) / 1e9,
-        "gpu_launches": res["launches"],
-        "cuda_graphs": {"priming_steps": res["priming_steps"], "captures_in_timed_region": res["captures_in_timed"]},
-        "clocks": res["clock"],
+        "in_step": res["in_step"],
+        "step_weight_gbs": res["streamed_bytes"] / (ms / K * 1e-3) / 1e9,
+        "step_weight_note": ("weight bytes streamed per step (layers + LM head twice, early head, draft heads; the "
+                             "embedding / position tables are gathered) / ms_per_step"),
+        "gpu_launches": main_r["launches"],
+        "cuda_graphs": {"priming_steps": res["priming_steps"], "captures_in_timed_region": main_r["captures"]},
+        "clocks": main_r["clock"],
         "cpu_baseline": cpu,
         "e2e": res["e2e"],
+        "sweep": sweep,
     }
     print(json.dumps(line))
     if group is not None:

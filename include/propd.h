@@ -44,8 +44,19 @@ const char* propd_last_error(void);
 int propd_abi_version(void);
 /* Number of SMs of the current device (0 if no device). */
 int propd_num_sms(void);
-/* One-time kernel attribute setup; call before capturing CUDA graphs. */
+/* One-time kernel attribute setup and occupancy queries (the weight-streaming
+ * GEMM's grid barriers are only launched when every CTA can be co-resident);
+ * call before capturing CUDA graphs. */
 int propd_prepare(void);
+/* Largest grid of a weight-streaming launch with in-kernel phases (grid
+ * barriers) whose CTAs are all resident at once on this device: resident CTAs
+ * per SM (computed from the kernel's resources, confirmed by a bounded probe
+ * launch in propd_prepare) x SMs.  0 if the probe failed to run. */
+int propd_gemm_ws_barrier_ctas(void);
+/* Measurement hook (bench.py in-step view): install (buf) or remove (NULL) a
+ * device buffer that receives one timeline record per CTA of the GEMM and
+ * attention kernels (layout in csrc/common.cuh).  Off by default. */
+int propd_debug_timeline(void* buf);
 
 /* ---- K1: tree materialisation (token_tree.py:125-170, engine.py:260) ----
  * For sequence b and template node i (row m = b*n + i):
@@ -111,13 +122,12 @@ int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, 
  * beyond L_b + n_tmpl are never visible).
  * q = columns [0,H) of qkv.  out[m, a*dh:(a+1)*dh] = softmax(q k^T / sqrt(dh)) v.
  * `workspace` must hold propd_attn_workspace_bytes(...) bytes.
- * impl: 0 = auto, 1 = CUDA-core split-KV kernel, 2 = tcgen05/TMA kernel v1
- * (128-key blocks, one softmax warpgroup), 4 = tcgen05/TMA kernel v2 (64-key
+ * impl: 0 = auto, 1 = CUDA-core split-KV kernel, 4 = tcgen05/TMA row-major kernel (64-key
  * blocks, 6+6-stage K/V rings, two softmax warpgroups; auto for > 64 rows and
  * for latency-bound > 32-row launches), 5 = transposed tcgen05 kernel
  * (S^T = K Q^T, O^T += V^T P^T, keys on the MMA M dimension; <= 64 rows per
  * sequence; auto for 5..64 rows), 3 = streaming decode kernel (<= 4 rows per
- * sequence; auto for the bonus pass).  impls 2-5 need bf16 and dh = 128.  n_slots = number of [A, Lmax, dh] slot blocks in the
+ * sequence; auto for the bonus pass).  impls 3-5 need bf16 and dh = 128.  n_slots = number of [A, Lmax, dh] slot blocks in the
  * cache layer (bounds of the TMA tensor map). */
 int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits);
 int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int n_slots,
@@ -179,29 +189,6 @@ typedef struct propd_ws_phases {
 } propd_ws_phases;
 int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
                      float* Y, int ldy, int accumulate, int max_split, const propd_ws_phases* phases, void* stream);
-/* Chain of up to 4 dependent weight-streaming projections in ONE persistent
- * launch (all CTAs co-resident), e.g. W_o -> W_1 -> W_2 -> QKV of the next
- * layer: the weight tiles of all jobs stream back to back through one ring
- * while the jobs' X operands become ready at grid barriers.  Per job: Y (+)=
- * X.W as propd_gemm_ws; pro_mode (PROPD_PRO_LN / _GELU) produces X from
- * pro_src in a prologue (as propd_ws_phases; pro_cols = K); tail_qkv finishes
- * the job's QKV accumulator with `tail` (tail_q / cache tables as
- * propd_ws_phases).  bar: >= 32 zeroed uint32 (left zeroed). */
-typedef struct propd_chain_job {
-  int N, K;
-  const void* X;
-  int ldx;
-  const void* W;
-  int ldw;
-  float* Y;
-  int ldy, accumulate;
-  int pro_mode;
-  float* pro_src;
-  int pro_ld, pro_cols;
-  int tail_qkv;
-} propd_chain_job;
-int propd_gemm_chain(int M, const int32_t* rows_dev, int njobs, const propd_chain_job* jobs,
-                     const propd_ws_phases* tail, uint32_t* bar, void* stream);
 /* acc[M, 3H] fp32 -> qkv bf16 [M, 3H] and K/V rows into the layer cache
  * (slot seq_len[seq_slot[row_seq[m]]] + row_node[m]); acc re-zeroed. */
 int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,

@@ -12,7 +12,7 @@ import os
 from ctypes import c_double, c_int, c_int64, c_void_p
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpropd.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 F32 = 0
 BF16 = 1
@@ -27,6 +27,8 @@ SIGNATURES = {
     "propd_abi_version": [],
     "propd_num_sms": [],
     "propd_prepare": [],
+    "propd_gemm_ws_barrier_ctas": [],
+    "propd_debug_timeline": [P],
     "propd_pad_rows": [I, I, I, P, P, P, P, P, P],
     "propd_tree_embed": [I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "propd_embed_rows": [I, I, I, P, P, P, P, P, P],
@@ -42,7 +44,6 @@ SIGNATURES = {
     "propd_tree_attention": [I, I, I, I, I, I, I, I, I, I, P, I, P, P, P, P, P, P, P, I, I, P, I, P, L, P],
     "propd_gemm_ws": [I, P, I, I, P, I, P, I, P, I, I, I, P],
     "propd_gemm_ws_ph": [I, P, I, I, P, I, P, I, P, I, I, I, "phases", P],
-    "propd_gemm_chain": [I, P, I, "chain", "phases", P, P],
     "propd_qkv_finish": [I, P, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
     "propd_gelu_finish": [I, P, I, P, I, P, I, P],
     "propd_early_member": [I, I, I, I, I, P, P, P, P, P, P],
@@ -73,14 +74,6 @@ class WsPhases(ctypes.Structure):
                 ("kcache", P), ("vcache", P), ("bar", P)]
 
 
-class ChainJob(ctypes.Structure):
-    """propd_chain_job (include/propd.h): one projection of a propd_gemm_chain launch."""
-
-    _fields_ = [("N", c_int), ("K", c_int), ("X", P), ("ldx", c_int), ("W", P), ("ldw", c_int), ("Y", P),
-                ("ldy", c_int), ("accumulate", c_int), ("pro_mode", c_int), ("pro_src", P), ("pro_ld", c_int),
-                ("pro_cols", c_int), ("tail_qkv", c_int)]
-
-
 class Typical(ctypes.Structure):
     """propd_typical (include/propd.h): typical-acceptance inputs of propd_verify_commit_ex."""
 
@@ -108,7 +101,7 @@ def load():
     lib = ctypes.CDLL(LIB_PATH)
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
-        structs = {"phases": WsPhases, "typical": Typical, "chain": ChainJob}
+        structs = {"phases": WsPhases, "typical": Typical}
         fn.argtypes = [ctypes.POINTER(structs[a]) if isinstance(a, str) else a for a in argtypes]
         fn.restype = _RESTYPES.get(name, c_int)
     if lib.propd_abi_version() != ABI_VERSION:

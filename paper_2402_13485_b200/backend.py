@@ -114,6 +114,7 @@ class StepOutput:
     acc_surv: np.ndarray  # [B, D] accepted indices into the pruned tree
     surv_cnt: np.ndarray  # [B]
     ranks_dev: object  # device int8 [B, D] acceptance records
+    ranks: np.ndarray | None = None  # host copy of the records (multi-rank step table)
     trace: dict | None = None
     order: np.ndarray | None = None  # selection order after this step's stats replay (single process)
     lcurve: np.ndarray | None = None
@@ -177,16 +178,14 @@ class B200Backend:
         self._acc = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32) if self.use_gws else None
         # in-kernel prologue/tail phases (LN, GELU, QKV finish) between the
         # weight-streaming projections: five launches per layer
-        self.ws_phases = self.use_gws and cfg.hidden <= 4096
+        call("propd_prepare")
+        # the phases meet at grid barriers: only when the split-K grids (<= 2
+        # CTAs per SM) are confirmed co-resident on this device
+        self.ws_phases = (self.use_gws and cfg.hidden <= 4096 and
+                          self.lib.propd_gemm_ws_barrier_ctas() >= 2 * self.lib.propd_num_sms())
         if self.ws_phases:
             self._acc2 = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32)
             self._bar = torch.zeros(32, device=dev, dtype=torch.int32)
-        # one persistent launch per layer for W_o -> W_1 -> W_2 -> next QKV
-        # (propd_gemm_chain): parity-tested but measured slower than the
-        # five-launch layer at 1-34 rows (each phase boundary still costs two
-        # grid barriers plus the prologue, which the ring does not cover), so
-        # off by default
-        self.ws_chain = False
         self.device_rows = True  # sync-free post-prune pass when it fits the weight-streaming GEMMs
         self._graphs: dict = {}
         self._templates: dict = {}
@@ -197,7 +196,6 @@ class B200Backend:
         self._len = [0] * self.max_slots  # host mirror of seq_len
         self._free = list(range(self.max_slots - 1, -1, -1))
         self._ws = torch.empty(0, device=dev, dtype=torch.uint8)
-        call("propd_prepare")
         self._one_mask = torch.ones(1, device=dev, dtype=torch.int64)  # single-node template {0}
         self._keepalive: list = []
         self.launches = 0  # libpropd kernel launches issued (bench accounting)
@@ -273,8 +271,13 @@ class B200Backend:
         return t
 
     def _workspace(self, M: int, B: int) -> object:
-        """Split-KV partials for one attention launch.  Under graph capture a
-        fresh (graph-owned) buffer per launch; eagerly a grown shared one."""
+        """Split-KV partials for one attention launch of the CUDA-core kernel
+        (fp32 parity mode, head dims != 128).  The bf16 dh = 128 kernels
+        combine their key splits through DSMEM and need none.  Under graph
+        capture a fresh (graph-owned) buffer per launch; eagerly a grown
+        shared one."""
+        if self.tdtype == self.torch.bfloat16 and self.dh == 128:
+            return None
         splits = min(64, -(-(4 * 148) // max(1, B * self.A)))
         if splits <= 1:
             return None
@@ -290,8 +293,6 @@ class B200Backend:
         """Blocks l0..l1-1 over the rows of `rt` (backends.py:202-237).  Returns
         the last MLP output not yet added to the residual stream x."""
         if self.use_gws and rt.M <= 128:
-            if self.ws_chain:
-                return self._run_layers_chain(x, rt, l0, l1, mask, n_tmpl, W, pending)
             if self.ws_phases:
                 return self._run_layers_phased(x, rt, l0, l1, mask, n_tmpl, W, pending)
             return self._run_layers_ws(x, rt, l0, l1, mask, n_tmpl, W, pending)
@@ -400,53 +401,6 @@ class B200Backend:
             rt.max_rows, rt.max_keys, ptr(qkv), qkv.shape[1], ptr(self.kcache[l]), ptr(self.vcache[l]),
             ptr(rt.seq_slot), ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx),
             H, ptr(ws), ws_bytes, self.stream()), M)
-
-    def _run_layers_chain(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
-        """Blocks l0..l1-1 as two launches per layer (bf16, <= 128 rows): K2,
-        then one persistent propd_gemm_chain launch W_o -> [LN] W_1 -> [GELU]
-        W_2 -> [LN] QKV(next layer) -> [finish] whose weight stream runs
-        across the phase boundaries.  The pass starts with a 1-job chain for
-        the first QKV."""
-        torch, T, H = self.torch, self.tdtype, self.H
-        self._flush(x, pending)
-        M = rt.M
-        ws = self._workspace(M, rt.B)
-        acc1, acc2, live, bar = self._acc, self._acc2, ptr(rt.live), ptr(self._bar)
-        h = torch.empty(M, H, device=self.device, dtype=T)
-        ctx = torch.empty(M, H, device=self.device, dtype=T)
-        qkv = torch.empty(M, 3 * H, device=self.device, dtype=T)
-        g = torch.empty(M, 4 * H, device=self.device, dtype=T)
-        J = _lib.ChainJob
-
-        def qkv_job(l):
-            return J(N=3 * H, K=H, X=ptr(h), ldx=H, W=ptr(self.w.wqkv[l]), ldw=3 * H, Y=ptr(acc1), ldy=3 * H,
-                     accumulate=1, pro_mode=_lib.PRO_LN, pro_src=ptr(x), pro_ld=H, pro_cols=H, tail_qkv=1)
-
-        def tail(l):
-            return _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A, dh=self.dh,
-                                 Lmax=self.Lmax, row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node),
-                                 seq_slot=ptr(rt.seq_slot), seq_len=ptr(self.seq_len), kcache=ptr(self.kcache[l]),
-                                 vcache=ptr(self.vcache[l]))
-
-        def chain(jobs, tail_ph, shapes):
-            arr = (J * len(jobs))(*jobs)
-            self._timed("gemm", lambda: self._call("propd_gemm_chain", M, live, len(jobs), arr, tail_ph, bar,
-                                                   self.stream()), M, shapes=shapes)
-
-        chain([qkv_job(l0)], tail(l0), [(H, 3 * H, True)])
-        for l in range(l0, l1):
-            self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
-            jobs = [J(N=H, K=H, X=ptr(ctx), ldx=H, W=ptr(self.w.wo[l]), ldw=H, Y=ptr(x), ldy=H, accumulate=1),
-                    J(N=4 * H, K=H, X=ptr(h), ldx=H, W=ptr(self.w.w1[l]), ldw=4 * H, Y=ptr(acc2), ldy=4 * H,
-                      accumulate=1, pro_mode=_lib.PRO_LN, pro_src=ptr(x), pro_ld=H, pro_cols=H),
-                    J(N=H, K=4 * H, X=ptr(g), ldx=4 * H, W=ptr(self.w.w2[l]), ldw=H, Y=ptr(x), ldy=H, accumulate=1,
-                      pro_mode=_lib.PRO_GELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_cols=4 * H)]
-            shapes = [(H, H, True), (H, 4 * H, True), (4 * H, H, True)]
-            if l + 1 < l1:
-                jobs.append(qkv_job(l + 1))
-                shapes.append((H, 3 * H, True))
-            chain(jobs, tail(l + 1) if l + 1 < l1 else None, shapes)
-        return None
 
     def _run_layers_phased(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
         """Blocks l0..l1-1 as five launches per layer (bf16, <= 128 rows):
@@ -748,19 +702,22 @@ class B200Backend:
     # The batched step is organised as two device programs so that each can
     # be captured once in a CUDA graph and replayed (the per-step host cost
     # is then a few copies and two graph launches):
-    #   part A  (B, tree, key bucket)        draft -> K1 -> layers 1..p
+    #   part A  (B, tree)                    draft -> K1 -> layers 1..p
     #           [-> early head -> K3 membership + closure/compaction]
-    #   part B  (B, tree, S_pad, key bucket) layers p+1..Ly on the S
+    #   part B  (B, tree, S_pad)             layers p+1..Ly on the S
     #           surviving rows padded to S_pad (pad rows form one extra
     #           scratch "sequence"), LM argmax, K5 accept + KV compaction,
     #           bonus pass.
     # Between them the host reads the survivor count S (the one mid-step sync).
     # Without pruning part A runs all layers and part B starts at the LM head.
 
-    def _key_bucket(self, need: int) -> int:
-        """Attention launch geometry (key range) is captured in the graph:
-        round the largest per-sequence key count up to a 256-key bucket."""
-        return min(self.Lmax, ((need + 255) // 256) * 256)
+    def _key_bound(self, need: int) -> int:
+        """Key bound of an attention launch.  The kernels place their key-split
+        boundaries from each sequence's device length, so a captured graph
+        stays valid as sequences grow: graphs are launched with the cache
+        capacity (no KV-length term in the graph keys), eager passes with the
+        exact bound."""
+        return self.Lmax if self.use_graphs else min(self.Lmax, need)
 
     def _slot_buf(self, B: int, slots):
         """Device int32 [B+1] = active slots + the scratch slot (pad rows)."""
@@ -850,7 +807,7 @@ class B200Backend:
         if max(lens) + 1 > self.config.max_positions:
             raise ValueError("sequence exceeds max_positions")
         slot_buf = self._slot_buf(B, [s.slot for s in states])
-        kb = self._key_bucket(max(lens) + 1)
+        kb = self._key_bound(max(lens) + 1)
 
         def program():
             seq_slot = slot_buf[:B]
@@ -859,7 +816,7 @@ class B200Backend:
             return bonus
 
         self._role = "bonus"
-        bonus = self._run(("ar", B, kb), program)
+        bonus = self._run(("ar", B), program)
         out = bonus.cpu().numpy()
         self._harvest({"bonus": (sum(lens) + B, B)})
         for s, t in zip(states, out):
@@ -874,7 +831,7 @@ class B200Backend:
         td = tmpl.device(dev)
         seq_slot = slot_buf[:B]
         o = {}
-        o["draft_tok"], _ = self._draft_dev(seq_slot, B, k)
+        o["draft_tok"], o["draft_val"] = self._draft_dev(seq_slot, B, k)
         self._mark("verify_begin")
         M = B * n
         i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
@@ -899,6 +856,7 @@ class B200Backend:
             xp = torch.empty(B * Pn, H, device=dev, dtype=self.tdtype)
             self._call("propd_gather_rows", self.code, B * Pn, H, ptr(x), ptr(par), ptr(xp), st)
             early = self._proj_f32(xp, self.w.w_early, V)
+            o["early"] = early
             if getattr(prune, "threshold", None) is not None:  # probability-based (marginal path probability)
                 est = torch.empty(B * Pn, 2, device=dev, dtype=torch.float64)
                 self._call("propd_row_lse", B * Pn, None, V, V, ptr(early), None, 1.0, ptr(est), st)
@@ -943,7 +901,8 @@ class B200Backend:
         i32 = lambda m: torch.empty(m, device=dev, dtype=torch.int32)
         o = {"acc_node": i32(B * D), "acc_surv": i32(B * D), "acc_len": i32(B), "bonus": i32(B),
              "committed": i32(B * (D + 1)), "ranks": torch.empty(B, D, device=dev, dtype=torch.int8),
-             "row_argmax": row_argmax, "root_before": self.root.index_select(0, seq_slot.long())}
+             "row_argmax": row_argmax, "row_logits": row_logits,
+             "root_before": self.root.index_select(0, seq_slot.long())}
         typ = None
         if accept is not None:  # typical acceptance: softmax statistics of the tree rows and the root rows
             eps, alpha, temp = accept
@@ -982,6 +941,7 @@ class B200Backend:
             pin = lambda n, dt: torch.empty(n, dtype=dt).pin_memory()
             hb = self._host[key] = {"committed": pin(B * (D + 1), torch.int32), "acc_len": pin(B, torch.int32),
                                     "acc_surv": pin(B * D, torch.int32), "surv_cnt": pin(B, torch.int32),
+                                    "ranks": pin(B * D, torch.int8),
                                     "order": pin(G, torch.int32), "lcurve": pin(G, torch.float64)}
         return hb
 
@@ -998,13 +958,16 @@ class B200Backend:
         if tmpl.max_depth > D:
             raise ValueError("tree deeper than the draft heads")
         lens = [self._len[s.slot] for s in states]
-        if max(lens) + tmpl.max_depth + 1 > cfg.max_positions:
-            raise ValueError("sequence exceeds max_positions")
+        # forward_tree's bound (backends.py:308-309): positions L + depth - 1 < max_positions
+        if max(lens) + tmpl.max_depth > cfg.max_positions:
+            raise ValueError("tree positions must follow the committed context")
+        if max(lens) + n > self.Lmax:  # tree rows live at cache slots L + node
+            raise ValueError(f"KV cache capacity {self.Lmax} exceeded (kv_len too small for this tree)")
         # captured graphs hold the template's device pointers: the backend owns
         # one canonical template per tree shape for its whole lifetime
         tmpl = self._templates.setdefault(tmpl.paths, tmpl)
         slot_buf = self._slot_buf(B, [s.slot for s in states])
-        kb = self._key_bucket(max(lens) + n + D + 1)
+        kb = self._key_bound(max(lens) + n + D + 1)
         td = tmpl.device(self.device)  # host->device uploads happen outside any capture
         if ("par_rows", B) not in td:
             rows = (np.arange(B, dtype=np.int32)[:, None] * n + tmpl.parent_nodes[None, :]).reshape(-1)
@@ -1012,7 +975,7 @@ class B200Backend:
         pkey = (prune.layer, prune.topk, getattr(prune, "threshold", None), accept) if prune is not None else (
             None, accept)
         self._role = "tree"
-        a = self._run(("A", B, tmpl.paths, k, pkey, kb), lambda: self._part_a(B, tmpl, k, prune, slot_buf, kb))
+        a = self._run(("A", B, tmpl.paths, k, pkey), lambda: self._part_a(B, tmpl, k, prune, slot_buf, kb))
         # Layers > p run on the survivors.  When every projection of that pass
         # is a weight-streaming GEMM (<= 128 rows), part B is launched for the
         # padded capacity and the GEMMs read the live row count on the device
@@ -1027,7 +990,7 @@ class B200Backend:
             S = int(a["total"].item())  # mid-step sync: row count of layers > p
             S_pad = self._s_bucket(S) if self.use_graphs else S
         self._role = "tree_pruned"
-        b = self._run(("B", B, tmpl.paths, k, pkey, kb, S_pad, device_rows),
+        b = self._run(("B", B, tmpl.paths, k, pkey, S_pad, device_rows),
                       lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows, accept))
         if stats is not None:  # single process: replay this batch's records right away (K4)
             P, counts, alpha, order_dev, lcurve_dev = stats
@@ -1037,6 +1000,7 @@ class B200Backend:
         hb["committed"].copy_(b["committed"], non_blocking=True)
         hb["acc_len"].copy_(b["acc_len"], non_blocking=True)
         hb["acc_surv"].copy_(b["acc_surv"], non_blocking=True)
+        hb["ranks"].copy_(b["ranks"].view(-1), non_blocking=True)
         if prune is not None:
             hb["surv_cnt"].copy_(a["surv_cnt"], non_blocking=True)
         if stats is not None:
@@ -1046,7 +1010,7 @@ class B200Backend:
         out = StepOutput(hb["committed"].numpy().reshape(B, D + 1).copy(), hb["acc_len"].numpy().copy(),
                          hb["acc_surv"].numpy().reshape(B, D).copy(),
                          hb["surv_cnt"].numpy().copy() if prune is not None else np.full(B, n, dtype=np.int32),
-                         b["ranks"])
+                         b["ranks"], hb["ranks"].numpy().reshape(B, D).copy())
         if stats is not None:
             out.order = hb["order"].numpy().copy()
             out.lcurve = hb["lcurve"].numpy().copy()
@@ -1054,6 +1018,11 @@ class B200Backend:
         S_real = int(out.surv_cnt.sum())
         self._harvest({"tree": (L0 + B * n, B * n), "tree_pruned": (L0 + B * n, S_real),
                        "bonus": (L0 + int(out.acc_len.sum()) + B, B)})
+        for L, acc in zip(lens, out.acc_len):
+            # commit's bound (backends.py:247-248): the accepted chain + bonus
+            # must fit; the reference raises from commit, so does this step
+            if L + int(acc) + 1 > cfg.max_positions:
+                raise ValueError("sequence exceeds max_positions")
         for s, row, acc in zip(states, out.committed, out.acc_len):
             new = [int(t) for t in row[: acc + 1]]
             s.committed.extend(new)
@@ -1064,7 +1033,11 @@ class B200Backend:
             out.trace = {"tokens": a["tokens"].view(B, n).cpu().numpy(),
                          "positions": a["positions"].view(B, n).cpu().numpy(),
                          "draft_tokens": a["draft_tok"].cpu().numpy(), "root": b["root_before"].cpu().numpy(),
-                         "alive": alive, "node_row": node_row, "row_argmax": b["row_argmax"].cpu().numpy()}
+                         "alive": alive, "node_row": node_row, "row_argmax": b["row_argmax"].cpu().numpy(),
+                         # values behind the decisions (parity checks against the fp64 oracle)
+                         "draft_val": a["draft_val"].cpu().numpy(),
+                         "row_logits": b["row_logits"][:S_real].cpu().numpy(),
+                         "early": a["early"].cpu().numpy() if "early" in a else None}
         return out
 
     def stats_replay_select(self, ranks_dev, S: int, P, counts, alpha, order, lcurve) -> None:

@@ -165,7 +165,10 @@ def run_once(cfg: dict):
     vocab = (b["tiny"] if b["kind"] == "tiny" else b["b200"]).get("vocab", TinyTransformerConfig().vocab)
     ecfg, latency = build_engine_config(cfg), build_latency(cfg)  # validate before touching the device
     prompts = build_prompts(cfg, vocab)
-    backend = build_backend(cfg, max_slots=len(prompts) + 1)
+    # the engine holds one batch chunk at a time and frees its slots after it
+    # (the backend adds its own scratch slot for padded rows)
+    bs = w["batch_size"]
+    backend = build_backend(cfg, max_slots=len(prompts) if bs is None else min(max(1, int(bs)), len(prompts)))
     engine = DecodeEngine(backend, ecfg, latency)
     result = engine.run(prompts, w["max_tokens"], batch_size=w["batch_size"])
     return engine, result

@@ -220,12 +220,6 @@ static int choose_splits(int B, int A, int max_keys, int max_splits) {
   return want < 1 ? 1 : want;
 }
 
-int attention_tc_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
-                      int ldqkv,
-                      const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
-                      const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
-                      void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled);
-
 int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys,
                        const void* qkv, int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot,
                        const int32_t* seq_len, const int32_t* row_off, const int32_t* row_node, const uint64_t* mask,
@@ -235,7 +229,6 @@ int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq
                        int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                        const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                        void* out, int ldout, cudaStream_t st, bool force, bool* handled);
-static int g_tc_version = 2;  // auto-dispatch target for multi-row bf16 dh=128 launches
 
 int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
                           int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
@@ -248,7 +241,20 @@ using namespace propd;
 
 static constexpr int kMaxSplits = 64;
 
+namespace propd {
+int attention_tc2_prepare();
+int gemm_ws_prepare();
+int gemm_ws_barrier_ctas();
+}  // namespace propd
+
 extern "C" {
+
+int propd_prepare(void) {  // one-time function attributes + occupancy queries (before any graph capture)
+  if (int e = propd::attention_tc2_prepare()) return e;
+  return propd::gemm_ws_prepare();
+}
+
+int propd_gemm_ws_barrier_ctas(void) { return propd::gemm_ws_barrier_ctas(); }
 
 int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits) {
   if (max_splits <= 0 || max_splits > kMaxSplits) max_splits = kMaxSplits;
@@ -280,21 +286,13 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
     if (e || handled) return e;
     PROPD_REQUIRE(impl != 5, "tree_attention: transposed tcgen05 kernel serves <= 64 rows per sequence");
   }
-  if (impl == 4 || (impl == 0 && dtype == PROPD_BF16 && dh == 128 && g_tc_version == 2)) {
+  if (impl == 4 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {
     bool handled = false;
     int e = attention_tc2_bf16(B, M, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache,
                                seq_slot, seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, workspace,
                                workspace_bytes, st, &handled);
     if (e || handled) return e;
     PROPD_REQUIRE(impl != 4, "tree_attention: tcgen05 v2 kernel cannot serve this shape");
-  }
-  if (impl == 2 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {
-    bool handled = false;
-    int e = attention_tc_bf16(B, M, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
-                              seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, workspace, workspace_bytes,
-                              st, &handled);
-    if (e || handled) return e;
-    PROPD_REQUIRE(impl != 2, "tree_attention: tcgen05 kernel cannot serve this shape");
   }
   AttnArgs p{};
   p.qkv = qkv;

@@ -38,7 +38,6 @@ struct Args {
   const uint64_t* mask;
   int n_tmpl, W, A, Lmax;
   float scale_log2;
-  int split_len;
   __nv_bfloat16* out;
   int ldout;
   unsigned long long* tl;  // development timeline (common.cuh)
@@ -117,8 +116,12 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
   const int r0 = p.row_off[b];
   const int nrows = min(ROWS, p.row_off[b + 1] - r0);
   const int nkeys = L + p.n_tmpl;
-  const int k_begin = s * p.split_len;
-  const int k_end = nrows > 0 ? min(nkeys, k_begin + p.split_len) : k_begin;
+  // split boundaries from this sequence's device length (16-key multiples;
+  // launch geometry independent of the KV length)
+  const int nspl = (int)gridDim.x;
+  const int split_len = (((nkeys + nspl - 1) / nspl + 15) / 16) * 16;
+  const int k_begin = s * split_len;
+  const int k_end = nrows > 0 ? min(nkeys, k_begin + split_len) : k_begin;
   const int nchunk = k_end > k_begin ? (k_end - k_begin + CHUNK - 1) / CHUNK : 0;
   const size_t tile = ((size_t)slot * p.A + a) * p.Lmax;  // first cache row of this (sequence, head)
   auto issue = [&](int c) {
@@ -376,10 +379,10 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   if (nsplit > cap) nsplit = cap;
   if (nsplit > dec::MAX_SPLIT) nsplit = dec::MAX_SPLIT;
   if (nsplit < 1) nsplit = 1;
-  int split_len = (max_keys + nsplit - 1) / nsplit;
-  // any multiple of 16 keys: chunks start at the split's first key and the
-  // last one loads only the keys left, so splits stay balanced across SMs
-  split_len = ((split_len + 15) / 16) * 16;
+  // boundaries: any multiple of 16 keys from the device length (chunks start
+  // at the split's first key and the last one loads only the keys left, so
+  // splits stay balanced across SMs); no split empty at max_keys
+  const int split_len = (((max_keys + nsplit - 1) / nsplit + 15) / 16) * 16;
   nsplit = (max_keys + split_len - 1) / split_len;
   dec::Args p{};
   p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
@@ -396,7 +399,6 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   p.A = A;
   p.Lmax = Lmax;
   p.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
-  p.split_len = split_len;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
   p.tl = g_dbg_trace;

@@ -55,25 +55,12 @@ struct Args {
   const uint64_t* mask;
   int n_tmpl, W, A, Lmax;
   float scale_log2;
-  int split_len, nsplit, mtiles;
+  int nsplit, mtiles;  // key splits per row tile; boundaries from the device length
   __nv_bfloat16* out;
   int ldout;
-  unsigned long long* trace;  // debug: per-block event timestamps of CTA (0,0,0)
   unsigned long long* tl;     // development timeline (common.cuh)
   unsigned int tag;
 };
-
-__device__ __forceinline__ unsigned long long gtime2() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-// trace slots: [0] start, [1] setup done; per block j < 24: 2+j: TMA issued,
-// 26+j: S issued, 50+j: softmax start (S seen), 74+j: P arrive, 98+j: PV issued
-#define TR2(k)                                                                                 \
-  do {                                                                                         \
-    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) p.trace[k] = gtime2(); \
-  } while (0)
 
 // Bits [t0, t0+32) of a row's visibility over tree nodes (0 outside [0, 64W)).
 __device__ __forceinline__ uint32_t tree_bits32(const uint64_t* mrow, int W, int node, int t0) {
@@ -184,7 +171,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   float* ml = reinterpret_cast<float*>(smem + SMEM_ML);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) TR2(0);
   const unsigned long long t_entry = p.tl ? gtimer() : 0ull;
   pdl_wait();
   const unsigned long long t_wait = p.tl ? gtimer() : 0ull;
@@ -196,8 +182,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int nrows = min(BM, p.row_off[b + 1] - r0);
   if (nrows <= 0) return;
   const int nkeys = L + p.n_tmpl;
-  const int k_begin = s * p.split_len;
-  const int k_end = min(nkeys, k_begin + p.split_len);
+  // split boundaries from this sequence's device length (BN-key multiples;
+  // launch geometry independent of the KV length)
+  const int split_len = (((nkeys + BN - 1) / BN + p.nsplit - 1) / p.nsplit) * BN;
+  const int k_begin = s * split_len;
+  const int k_end = min(nkeys, k_begin + split_len);
   const int nblk = k_end > k_begin ? (k_end - k_begin + BN - 1) / BN : 0;
   if (nblk == 0) {  // no keys in this split: contribute an empty state to the cluster combine
     if (p.nsplit > 1) {
@@ -256,7 +245,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();  // after the TMEM allocation (see common.cuh)
-  if (threadIdx.x == 0) TR2(1);
   const size_t row_base = ((size_t)slot * p.A + a) * p.Lmax;
 
   if (warp == 0 || warp == 10) {
@@ -276,7 +264,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint8_t* d = ring + st * KV_TILE;
         tma_load_2d(d, map, &full[st], 0, row);
         tma_load_2d(d + KV_HALF, map, &full[st], 64, row);
-        if (isk && j < 24) TR2(2 + j);
       }
     }
   } else if (warp == 1) {
@@ -306,7 +293,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           mma_commit(&s_full[sb]);
           mma_commit(&k_empty[st]);  // K is only needed by S: release its stage now
-          if (ns < 24) TR2(26 + ns);
           ++ns;
           prog = true;
         }
@@ -322,7 +308,6 @@ __global__ void __launch_bounds__(THREADS, 1)
               const uint64_t bd = sw128_desc(v_addr + kk * 2048, KV_HALF, 1024);
               mma_bf16_ts(tmem + g * 128, p_tmem + 8 * kk, bd, id_o, (i > 0 || kk > 0) ? 1u : 0u);
             }
-            if (np < 24) TR2(98 + np);
             mma_commit(&v_empty[st]);
             mma_commit(&o_done[g]);
             ++np;
@@ -358,7 +343,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       float sv[64];
       mbar_wait(&s_full[sb], (i >> 1) & 1, 14);
       tc_after_sync();
-      if (j < 24 && lane == 0 && q4 == 0) TR2(50 + j);
       {
         uint32_t* rv = reinterpret_cast<uint32_t*>(sv);
         TMEM_LD32(lane_addr + 256 + 64 * sb, rv);
@@ -434,7 +418,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       l_sum += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
       tc_before_sync();
       mbar_arrive(&p_full[g]);
-      if (j < 24 && lane == 0 && q4 == 0) TR2(74 + j);
     }
     // ---- epilogue: merge the two groups' (m, l, O) and write ----
     if (warp_live && nb > 0) {
@@ -548,7 +531,6 @@ static bool kv_map64(CUtensorMap* m, const void* base, uint64_t rows) {
 
 }  // namespace tc2
 
-unsigned long long* g_trace2 = nullptr;
 
 int attention_tc2_prepare() {
   cudaError_t e = cudaFuncSetAttribute(tc2::attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -592,12 +574,10 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   p.A = A;
   p.Lmax = Lmax;
   p.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
-  p.split_len = blocks_per_split * tc2::BN;
   p.nsplit = nsplit;
   p.mtiles = mtiles;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;
-  p.trace = g_trace2;
   p.tl = g_dbg_trace;
   p.tag = g_dbg_tag++;
   static bool attr = false;
@@ -638,69 +618,3 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
 }
 
 }  // namespace propd
-
-extern "C" int propd_debug_trace2(void* buf) {  // development aid: per-block timeline of one v2 CTA
-  propd::g_trace2 = reinterpret_cast<unsigned long long*>(buf);
-  return 0;
-}
-
-// ---------------------------------------------------------------------------
-// Development probe: stream K and V blocks of 64 keys through the same TMA
-// rings with no compute (consumer releases stages on arrival), to measure the
-// TMA streaming ceiling of this access pattern.
-namespace propd {
-namespace tc2 {
-__global__ void __launch_bounds__(128, 1) tma_stream_kernel(const __grid_constant__ CUtensorMap kmap,
-                                                            const __grid_constant__ CUtensorMap vmap, int units,
-                                                            int nblk, int Lmax, int box_split) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int NS = 6;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * 2 * KV_TILE);
-  uint64_t* empty = full + 8;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 8; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
-    const size_t row_base = (size_t)u * Lmax;
-    const int jbase = ((u - blockIdx.x) / gridDim.x) * nblk;
-    if (warp == 0 && lane == 0) {
-      for (int j = 0; j < nblk; ++j) {
-        const int jj = jbase + j, st = jj % NS;
-        mbar_wait(&empty[st], ((jj / NS) & 1) ^ 1, 21);
-        mbar_expect_tx(&full[st], 2 * KV_TILE);
-        const int row = (int)(row_base + j * BN);
-        uint8_t* d = smem + st * 2 * KV_TILE;
-        tma_load_2d(d, &kmap, &full[st], 0, row);
-        tma_load_2d(d + KV_HALF, &kmap, &full[st], 64, row);
-        tma_load_2d(d + KV_TILE, &vmap, &full[st], 0, row);
-        tma_load_2d(d + KV_TILE + KV_HALF, &vmap, &full[st], 64, row);
-      }
-    } else if (warp == 1 && lane == 0) {
-      for (int j = 0; j < nblk; ++j) {
-        const int jj = jbase + j, st = jj % NS;
-        mbar_wait(&full[st], (jj / NS) & 1, 22);
-        mbar_arrive(&empty[st]);
-      }
-    }
-  }
-  (void)box_split;
-}
-}  // namespace tc2
-}  // namespace propd
-
-extern "C" int propd_debug_tma_stream(const void* kc, const void* vc, int n_slots, int A, int Lmax, int nblk,
-                                      int grid, void* stream) {
-  CUtensorMap km, vm;
-  const uint64_t rows = (uint64_t)n_slots * A * Lmax;
-  if (!propd::tc2::kv_map64(&km, kc, rows) || !propd::tc2::kv_map64(&vm, vc, rows)) return propd::fail("map");
-  const int smem = 6 * 2 * propd::tc2::KV_TILE + 256;
-  cudaFuncSetAttribute(propd::tc2::tma_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  propd::tc2::tma_stream_kernel<<<grid, 128, smem, (cudaStream_t)stream>>>(km, vm, n_slots * A, nblk, Lmax, 0);
-  return propd::check_launch("tma_stream");
-}

@@ -82,7 +82,7 @@ struct Args {
   const uint64_t* mask;
   int n_tmpl, W, A, Lmax;
   float scale_log2;
-  int split_len, nsplit;
+  int nsplit;  // key splits per (sequence, head); boundaries from the device length
   __nv_bfloat16* out;
   int ldout;
   unsigned long long* tl;  // development timeline (common.cuh)
@@ -231,8 +231,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   const int nrows = min(NR, p.row_off[b + 1] - r0);
   if (nrows <= 0) return;  // uniform over the cluster (same sequence)
   const int nkeys = L + p.n_tmpl;
-  const int k_begin = s * p.split_len;
-  const int k_end = min(nkeys, k_begin + p.split_len);
+  // split boundaries from this sequence's device length (64-key multiples):
+  // the launch geometry does not depend on the KV length, so captured graphs
+  // stay valid as sequences grow
+  const int split_len = ((((nkeys + 63) >> 6) + p.nsplit - 1) / p.nsplit) * 64;
+  const int k_begin = s * split_len;
+  const int k_end = min(nkeys, k_begin + split_len);
   const int nblk = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
   if (nblk == 0) {  // no keys in this split: an empty state for the cluster combine
     if (p.nsplit > 1) {
@@ -628,8 +632,8 @@ int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq
   if (nsplit > nh) nsplit = nh;
   if (nsplit > tct::MAX_SPLIT) nsplit = tct::MAX_SPLIT;
   if (nsplit < 1) nsplit = 1;
-  const int split_len = ((nh + nsplit - 1) / nsplit) * 64;
-  nsplit = (max_keys + split_len - 1) / split_len;
+  const int per = (nh + nsplit - 1) / nsplit;  // 64-key units per split at max_keys
+  nsplit = (nh + per - 1) / per;               // no split empty at max_keys
   tct::Args p{};
   p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
   p.ldq = ldqkv;
@@ -643,7 +647,6 @@ int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq
   p.A = A;
   p.Lmax = Lmax;
   p.scale_log2 = 1.4426950408889634f / sqrtf(128.f);
-  p.split_len = split_len;
   p.nsplit = nsplit;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.ldout = ldout;

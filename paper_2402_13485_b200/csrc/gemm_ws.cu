@@ -386,19 +386,148 @@ static bool map2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols
   return true;
 }
 
+// ---- co-residency of the grid-barrier launches ----
+// The in-kernel grid barriers need every CTA of the launch resident at once.
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor cannot decide it: for any
+// kernel that executes tcgen05.alloc it reports 1 CTA per SM (measured on
+// B200: a probe kernel with this kernel's footprint reports 1 with the
+// allocation and 2 without, and 296 of them are co-resident either way).  So
+// the resident count is computed from the kernel's resources (shared memory
+// incl. static + the per-CTA reservation, registers at the per-warp
+// allocation granularity, threads, TMEM columns, the per-SM CTA limit) and,
+// once per process, confirmed by a probe kernel with the largest variant's
+// footprint that allocates the same TMEM columns and spins (bounded by the
+// global timer, so it cannot hang) until every CTA of that grid has arrived.
+// If the probe does not see them all, barrier launches are limited to one
+// CTA per SM (the host then runs the layers without in-kernel phases).
+constexpr int TMEM_COLS = 128;
+
+__global__ void __launch_bounds__(THREADS, 2) coresidency_probe_kernel(unsigned* ctr, unsigned n, int* ok) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  if (threadIdx.x == 0) {
+    smem_raw[0] = 1;
+    atomicAdd(ctr, 1u);
+    const unsigned long long t0 = gtimer();
+    while (ld_acquire(ctr) < n) {
+      if (gtimer() - t0 > 20000000ull) {  // 20 ms: not all co-resident
+        atomicExch(ok, 0);
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(slot), "r"(TMEM_COLS));
+}
+
+static int resident_per_sm(const void* fn, int dyn_smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp pr{};
+  cudaFuncAttributes fa{};
+  if (cudaGetDeviceProperties(&pr, dev) != cudaSuccess || cudaFuncGetAttributes(&fa, fn) != cudaSuccess) return -1;
+  const int per_cta_smem = dyn_smem + (int)fa.sharedSizeBytes + (int)pr.reservedSharedMemPerBlock;
+  const int warps = (THREADS + 31) / 32;
+  const int regs_per_warp = ((fa.numRegs + 7) / 8) * 8 * 32;
+  int n = (int)pr.sharedMemPerMultiprocessor / per_cta_smem;
+  n = min(n, pr.regsPerMultiprocessor / (regs_per_warp * warps));
+  n = min(n, pr.maxThreadsPerMultiProcessor / THREADS);
+  n = min(n, 512 / TMEM_COLS);
+  n = min(n, pr.maxBlocksPerMultiProcessor);
+  return n;
+}
+
+// One-time function attributes (maximum dynamic shared memory, maximum
+// shared-memory carveout for two CTAs per SM) and the resident CTAs per SM
+// (< 0 = error, message set).
 template <int MP>
-static int launch(const CUtensorMap& wm, const CUtensorMap& xm, Args p, dim3 grid, cudaStream_t st) {
+static int prepare_mp() {
   constexpr int smem = stages_for(MP) * (A_BYTES + MP * 128) + 256 + 1024;
-  static bool attr = false;
-  if (!attr) {
+  static int occ = -1;
+  if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(gemm_ws_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    // two CTAs per SM need the maximum shared-memory carveout
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_ws_kernel<MP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return fail("gemm_ws: %s", cudaGetErrorString(e));
-    attr = true;
+    if (e != cudaSuccess) {
+      fail("gemm_ws: %s", cudaGetErrorString(e));
+      return -1;
+    }
+    occ = resident_per_sm(reinterpret_cast<const void*>(gemm_ws_kernel<MP>), smem);
+    if (occ < 1) {
+      fail("gemm_ws: resource query failed");
+      return -1;
+    }
   }
+  return occ;
+}
+
+static int occupancy(int mp) {
+  switch (mp) {
+    case 16: return prepare_mp<16>();
+    case 32: return prepare_mp<32>();
+    case 48: return prepare_mp<48>();
+    case 64: return prepare_mp<64>();
+    case 80: return prepare_mp<80>();
+    case 96: return prepare_mp<96>();
+    case 112: return prepare_mp<112>();
+    default: return prepare_mp<128>();
+  }
+}
+
+// Resident CTAs per SM confirmed by the probe (0 = not probed yet).
+static int g_probe_per_sm = 0;
+
+static int run_probe() {
+  if (g_probe_per_sm > 0) return 0;
+  int max_smem = 0, per_sm = 1 << 30;
+  for (int mp = 16; mp <= 128; mp += 16) {
+    const int o = occupancy(mp);
+    if (o < 0) return 1;
+    per_sm = min(per_sm, o);
+    // + 1 KB for the static shared memory of gemm_ws_kernel (timeline scratch, reductions)
+    max_smem = max(max_smem, stages_for(mp) * (A_BYTES + mp * 128) + 256 + 1024 + 1024);
+  }
+  const int n = per_sm * propd_num_sms();
+  cudaError_t e = cudaFuncSetAttribute(coresidency_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(coresidency_probe_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  unsigned* ctr = nullptr;
+  int* ok = nullptr;
+  int h_ok = 1;
+  if (e == cudaSuccess) e = cudaMalloc(&ctr, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMalloc(&ok, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(ctr, 0, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemcpy(ok, &h_ok, sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    coresidency_probe_kernel<<<n, THREADS, max_smem>>>(ctr, (unsigned)n, ok);
+    e = cudaDeviceSynchronize();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(&h_ok, ok, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(ctr);
+  cudaFree(ok);
+  if (e != cudaSuccess) return fail("gemm_ws co-residency probe: %s", cudaGetErrorString(e));
+  g_probe_per_sm = h_ok ? per_sm : 1;
+  return 0;
+}
+
+template <int MP>
+static int launch(const CUtensorMap& wm, const CUtensorMap& xm, Args p, dim3 grid, cudaStream_t st) {
+  constexpr int smem = stages_for(MP) * (A_BYTES + MP * 128) + 256 + 1024;
+  if (prepare_mp<MP>() < 0) return 1;
   return launch_pdl("gemm_ws", gemm_ws_kernel<MP>, grid, dim3(THREADS), smem, st, wm, xm, p);
 }
 
@@ -416,302 +545,6 @@ static void split_k(int N, int K, int accumulate, int max_split, int* split_out,
   const int per = (kb + split - 1) / split;
   *split_out = (kb + per - 1) / per;
   *per_out = per;
-}
-
-// ---- spread grid barrier: arrivals are fire-and-forget reductions over 16
-// counters (16 L2 slices instead of one hot line), one warp polls their sum
-// against a cumulative target; the counters are re-armed by the last CTA to
-// leave the kernel (kernel_exit_rearm).
-constexpr int SPREAD = 16;
-__device__ __forceinline__ void spread_arrive(unsigned* ctr, int cta) {
-  __threadfence();
-  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr + (cta & (SPREAD - 1))) : "memory");
-}
-__device__ __forceinline__ void spread_wait(const unsigned* ctr, unsigned target, int lane) {  // one full warp
-  while (true) {
-    unsigned v = lane < SPREAD ? ld_acquire(ctr + lane) : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (v >= target) break;
-    __nanosleep(20);
-  }
-}
-// last CTA out zeroes `n` counters (after every CTA has passed every barrier)
-__device__ __forceinline__ void kernel_exit_rearm(unsigned* ctr, int n, unsigned* exit_ctr, unsigned ncta) {
-  __threadfence();
-  if (atomicAdd(exit_ctr, 1u) == ncta - 1) {
-    for (int i = 0; i < n; ++i) ctr[i] = 0u;
-    *exit_ctr = 0u;
-    __threadfence();
-  }
-}
-
-__global__ void barrier_bench_kernel(unsigned* bar, int iters, int impl) {
-  const int lane = threadIdx.x & 31;
-  for (int i = 0; i < iters; ++i) {
-    if (impl == 0) {
-      if (threadIdx.x == 0) grid_barrier(bar + 2 * (i & 7), gridDim.x);
-    } else {
-      if (threadIdx.x == 0) spread_arrive(bar + 64, blockIdx.x);
-      if (threadIdx.x < 32) spread_wait(bar + 64, (unsigned)(gridDim.x * (i + 1)), lane);
-    }
-    __syncthreads();
-  }
-  if (impl != 0 && threadIdx.x == 0) kernel_exit_rearm(bar + 64, SPREAD, bar + 96, gridDim.x);
-}
-
-// ------------------------------------------------------------------ chain
-// Several dependent projections of one layer in ONE persistent launch (all
-// CTAs co-resident): W_o -> [LN] W_1 -> [GELU] W_2 -> [LN] QKV(next layer)
-// -> [finish].  Roles: warp 0 streams the weight tiles of every job back to
-// back through the ring and never waits for a dependency (weights are
-// immutable), warp 6 loads each job's X tiles once that job's operand is
-// ready, warp 1 issues tcgen05.mma, warps 2-5 drain the accumulator (split-K
-// reductions into Y) and run the prologue / tail phases between the jobs at
-// grid barriers.  The HBM weight stream therefore keeps flowing across the
-// phase boundaries that separate kernels would turn into launch gaps.
-constexpr int CHAIN_MAX = 4, CHAIN_THREADS = 224;
-
-struct ChainJob {
-  int N, K, tiles, split, per;
-  float* Y;
-  int ldy, accumulate;
-  int pro_mode;  // PROPD_PRO_*: this job's X is produced from pro_src in a prologue phase
-  float* pro_src;
-  int pro_ld, pro_cols;
-  __nv_bfloat16* pro_dst;
-  int pro_ldd;
-  int tail;  // QKV finish after this job (tables in ChainArgs::tailph)
-};
-
-struct ChainArgs {
-  int M, njobs;
-  const int32_t* m_dev;
-  ChainJob job[CHAIN_MAX];
-  propd_ws_phases tailph;
-  unsigned* bar;  // 2 counters per barrier: A_j = 4j, B_j = 4j + 2, tail = 4 CHAIN_MAX
-  unsigned long long* trace;
-  unsigned int tag;
-};
-
-template <int MP>
-__global__ void __launch_bounds__(CHAIN_THREADS, 2)
-    chain_kernel(const __grid_constant__ CUtensorMap w0, const __grid_constant__ CUtensorMap w1,
-                 const __grid_constant__ CUtensorMap w2, const __grid_constant__ CUtensorMap w3,
-                 const __grid_constant__ CUtensorMap x0, const __grid_constant__ CUtensorMap x1,
-                 const __grid_constant__ CUtensorMap x2, const __grid_constant__ CUtensorMap x3, ChainArgs p) {
-  constexpr int STAGES = stages_for(MP);
-  constexpr int B_BYTES = MP * 128;
-  constexpr int STAGE = A_BYTES + B_BYTES;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
-  uint64_t* empty = full + STAGES;
-  uint64_t* acc_full = empty + STAGES;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
-  __shared__ int s_xready[CHAIN_MAX];
-  const unsigned long long t_entry = p.trace ? gtimer() : 0ull;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta = blockIdx.x, ncta = gridDim.x;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], 2);  // W producer + X producer
-      mbar_init(&empty[i], 1);
-    }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 128);
-    for (int j = 0; j < CHAIN_MAX; ++j) s_xready[j] = 0;
-    fence_barrier_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(128));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_before_sync();
-  __syncthreads();
-  tc_after_sync();
-  const uint32_t tmem = *tmem_slot;
-  pdl_trigger();  // after the TMEM allocation (see common.cuh)
-  const CUtensorMap* wm[CHAIN_MAX] = {&w0, &w1, &w2, &w3};
-  const CUtensorMap* xm[CHAIN_MAX] = {&x0, &x1, &x2, &x3};
-  unsigned long long t_wait = 0ull;
-  if (warp == 0) {
-    // ---- weight producer: no dependency on earlier kernels, never waits
-    if (lane == 0) {
-      int g = 0;
-      for (int j = 0; j < p.njobs; ++j) {
-        const ChainJob& J = p.job[j];
-        if (cta >= J.tiles * J.split) continue;
-        const int tile = cta % J.tiles, kb0 = (cta / J.tiles) * J.per;
-        const int nkb = min(J.per, J.K / BK - kb0);
-        for (int t = 0; t < nkb; ++t, ++g) {
-          const int st = g % STAGES;
-          mbar_wait(&empty[st], ((g / STAGES) & 1) ^ 1, 51);
-          mbar_expect_tx(&full[st], A_BYTES);
-          uint8_t* a = smem + st * STAGE;
-          const int k = (kb0 + t) * BK;
-          tma_load_2d(a, wm[j], &full[st], tile * BF, k);
-          tma_load_2d(a + A_BYTES / 2, wm[j], &full[st], tile * BF + 64, k);
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 6) {
-    // ---- X producer: each job's operand once it is ready
-    pdl_wait();
-    if (lane == 0) {
-      const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
-      const int nbox = max(1, (M + 15) >> 4);
-      int g = 0;
-      for (int j = 0; j < p.njobs; ++j) {
-        const ChainJob& J = p.job[j];
-        if (cta >= J.tiles * J.split) continue;
-        while (*reinterpret_cast<volatile int*>(&s_xready[j]) == 0) __nanosleep(32);
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes of the prologue -> TMA reads
-        const int kb0 = (cta / J.tiles) * J.per;
-        const int nkb = min(J.per, J.K / BK - kb0);
-        for (int t = 0; t < nkb; ++t, ++g) {
-          const int st = g % STAGES;
-          mbar_wait(&empty[st], ((g / STAGES) & 1) ^ 1, 52);
-          mbar_expect_tx(&full[st], nbox * 2048);
-          uint8_t* b = smem + st * STAGE + A_BYTES;
-          for (int i = 0; i < nbox; ++i) tma_load_2d(b + i * 2048, xm[j], &full[st], (kb0 + t) * BK, i * 16);
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    // ---- MMA issuer
-    pdl_wait();
-    if (lane == 0) {
-      const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
-      const int nbox = max(1, (M + 15) >> 4);
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(nbox * 2) << 17) |
-                             ((128u >> 4) << 24);
-      int g = 0, jw = 0;
-      for (int j = 0; j < p.njobs; ++j) {
-        const ChainJob& J = p.job[j];
-        if (cta >= J.tiles * J.split) continue;
-        if (jw > 0) {  // the epilogue has drained the previous job's accumulator
-          mbar_wait(acc_empty, (jw - 1) & 1, 53);
-          tc_after_sync();
-        }
-        const int kb0 = (cta / J.tiles) * J.per;
-        const int nkb = min(J.per, J.K / BK - kb0);
-        for (int t = 0; t < nkb; ++t, ++g) {
-          const int st = g % STAGES;
-          mbar_wait(&full[st], (g / STAGES) & 1, 54);
-          tc_after_sync();
-          const uint32_t a = smem_u32(smem + st * STAGE);
-          const uint32_t b = a + A_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = sw128_desc(a + kk * 2048, A_BYTES / 2, 1024);
-            const uint64_t bd = sw128_desc(b + kk * 32, 16, 1024);
-            mma_bf16(tmem, ad, bd, idesc, (t > 0 || kk > 0) ? 1u : 0u);
-          }
-          mma_commit(&empty[st]);
-        }
-        mma_commit(acc_full);
-        ++jw;
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---- epilogue + phase workers (warps 2-5)
-    pdl_wait();
-    t_wait = p.trace ? gtimer() : 0ull;
-    const int tid = threadIdx.x - 64;
-    const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
-    const int q4 = warp & 3;
-    int jw = 0;
-    for (int j = 0; j < p.njobs; ++j) {
-      const ChainJob& J = p.job[j];
-      if (J.pro_mode != PROPD_PRO_NONE) {
-        if (j > 0) {  // the previous job's reductions have landed everywhere
-          __threadfence();
-          epi_sync();
-          if (tid == 0) grid_barrier(p.bar + 4 * j, (unsigned)ncta);
-          epi_sync();
-        }
-        propd_ws_phases ph{};
-        ph.pro_mode = J.pro_mode;
-        ph.pro_src = J.pro_src;
-        ph.pro_ld = J.pro_ld;
-        ph.pro_dst = J.pro_dst;
-        ph.pro_ldd = J.pro_ldd;
-        ph.pro_cols = J.pro_cols;
-        prologue_phase(ph, M, tid, cta, ncta);
-        __threadfence();
-        epi_sync();
-        if (tid == 0) grid_barrier(p.bar + 4 * j + 2, (unsigned)ncta);
-        epi_sync();
-      }
-      if (tid == 0) *reinterpret_cast<volatile int*>(&s_xready[j]) = 1;
-      if (cta < J.tiles * J.split) {
-        const int f = (cta % J.tiles) * BF + q4 * 32 + lane;
-        mbar_wait(acc_full, jw & 1, 55);
-        tc_after_sync();
-        const uint32_t lane_addr = tmem + ((uint32_t)(q4 * 32) << 16);
-        const int nchunk = (M + 31) >> 5;
-#pragma unroll 1
-        for (int c = 0; c < nchunk; ++c) {
-          uint32_t rr[32];
-          TMEM_LD32(lane_addr + c * 32, rr);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int t = c * 32 + i;
-            if (t < M) {
-              float* dst = J.Y + (size_t)t * J.ldy + f;
-              const float v = __uint_as_float(rr[i]);
-              if (J.accumulate)
-                asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst), "f"(v) : "memory");
-              else
-                *dst = v;
-            }
-          }
-        }
-        tc_before_sync();
-        mbar_arrive(acc_empty);
-        ++jw;
-      }
-      if (J.tail) {
-        __threadfence();
-        epi_sync();
-        if (tid == 0) grid_barrier(p.bar + 4 * CHAIN_MAX, (unsigned)ncta);
-        epi_sync();
-        tail_phase(J.Y, J.ldy, p.tailph, M, tid, cta, ncta);
-      }
-    }
-  }
-  tc_before_sync();
-  __syncthreads();
-  tc_after_sync();
-  if (warp == 1) {
-    __syncwarp();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
-  }
-  if (p.trace && threadIdx.x == 64) trace_record(p.trace, p.tag, t_entry, t_wait, t_wait, 1);
-}
-
-template <int MP>
-static int launch_chain(const CUtensorMap* wms, const CUtensorMap* xms, const ChainArgs& p, int grid,
-                        cudaStream_t st) {
-  constexpr int smem = stages_for(MP) * (A_BYTES + MP * 128) + 256 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(chain_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(chain_kernel<MP>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return fail("gemm_chain: %s", cudaGetErrorString(e));
-    attr = true;
-  }
-  return launch_pdl("gemm_chain", chain_kernel<MP>, dim3(grid), dim3(CHAIN_THREADS), smem, st, wms[0], wms[1],
-                    wms[2], wms[3], xms[0], xms[1], xms[2], xms[3], p);
 }
 
 // ------------------------------------------------------------------ finish
@@ -769,6 +602,10 @@ __global__ void gelu_finish_kernel(int N, float* __restrict__ acc, int ldacc, __
 }
 
 }  // namespace gws
+
+// every weight-streaming variant's attributes + occupancy, before any graph capture
+int gemm_ws_prepare() { return gws::run_probe(); }
+int gemm_ws_barrier_ctas() { return gws::run_probe() ? 0 : gws::g_probe_per_sm * propd_num_sms(); }
 }  // namespace propd
 
 using namespace propd;
@@ -797,10 +634,19 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
   gws::split_k(N, K, accumulate, max_split, &split, &per);
   gws::Args p{M, N, K, per, ldy, mp, rows_dev, Y, accumulate, g_dbg_trace, g_dbg_tag++, {}};
   if (ph != nullptr && (ph->pro_mode != PROPD_PRO_NONE || ph->tail_mode != PROPD_TAIL_NONE)) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    PROPD_REQUIRE(tiles * split <= 2 * sms, "gemm_ws: %d CTAs cannot all be co-resident for the grid barrier",
-                  tiles * split);
+    // the grid barriers need every CTA resident at once: checked against the
+    // occupancy the runtime reports for this kernel variant (a launch that
+    // could not be co-resident fails here instead of hanging the device)
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int occ = gws::occupancy(mp);
+    PROPD_REQUIRE(occ > 0, "gemm_ws: occupancy query failed");
+    if (int e = gws::run_probe()) return e;
+    if (gws::g_probe_per_sm < occ) occ = gws::g_probe_per_sm;
+    PROPD_REQUIRE(tiles * split <= occ * sms,
+                  "gemm_ws: %d CTAs cannot all be co-resident for the grid barrier (%d per SM x %d SMs)",
+                  tiles * split, occ, sms);
     PROPD_REQUIRE(ph->bar != nullptr, "gemm_ws: phases need the barrier counters");
     PROPD_REQUIRE(ph->pro_mode == PROPD_PRO_NONE ||
                       (ph->pro_src && ph->pro_dst == X && ph->pro_ldd == ldx && ph->pro_cols == K && K <= 4096 * 4),
@@ -824,80 +670,6 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
     case 112: return gws::launch<112>(wm, xm, p, grid, st);
     default: return gws::launch<128>(wm, xm, p, grid, st);
   }
-}
-
-int propd_gemm_chain(int M, const int32_t* rows_dev, int njobs, const propd_chain_job* jobs,
-                     const propd_ws_phases* tail, uint32_t* bar, void* stream) {
-  PROPD_REQUIRE(M >= 1 && M <= 128, "gemm_chain: M=%d outside 1..128", M);
-  PROPD_REQUIRE(njobs >= 1 && njobs <= gws::CHAIN_MAX, "gemm_chain: %d jobs outside 1..%d", njobs, gws::CHAIN_MAX);
-  PROPD_REQUIRE(bar != nullptr, "gemm_chain: needs the barrier counters");
-  const int mp = ((M + 15) / 16) * 16;
-  CUtensorMap wms[gws::CHAIN_MAX], xms[gws::CHAIN_MAX];
-  gws::ChainArgs p{};
-  p.M = M;
-  p.njobs = njobs;
-  p.m_dev = rows_dev;
-  p.bar = bar;
-  p.trace = g_dbg_trace;
-  p.tag = g_dbg_tag++;
-  int grid = 0;
-  for (int j = 0; j < njobs; ++j) {
-    const propd_chain_job& c = jobs[j];
-    PROPD_REQUIRE(c.N % gws::BF == 0 && c.K % gws::BK == 0, "gemm_chain: job %d N=%d K=%d", j, c.N, c.K);
-    PROPD_REQUIRE(gws::map2d(&wms[j], c.W, (uint64_t)c.K, (uint64_t)c.N, (uint64_t)c.ldw, 64) &&
-                      gws::map2d(&xms[j], c.X, (uint64_t)M, (uint64_t)c.K, (uint64_t)c.ldx, 16),
-                  "gemm_chain: tensor map encode failed");
-    PROPD_REQUIRE(c.pro_mode == PROPD_PRO_NONE || (c.pro_src && c.pro_cols == c.K && (c.pro_mode != PROPD_PRO_LN ||
-                                                                                      c.K <= 4096)),
-                  "gemm_chain: job %d prologue must produce its X operand (LN rows <= 4096)", j);
-    PROPD_REQUIRE(!c.tail_qkv || (c.accumulate && tail && c.N == 3 * tail->A * tail->dh && tail->tail_q &&
-                                  tail->kcache && tail->vcache && tail->row_seq && tail->row_node && tail->seq_slot &&
-                                  tail->seq_len),
-                  "gemm_chain: QKV tail needs an accumulating N = 3H job and the cache tables");
-    int split, per;
-    gws::split_k(c.N, c.K, c.accumulate, 0, &split, &per);
-    gws::ChainJob& J = p.job[j];
-    J.N = c.N;
-    J.K = c.K;
-    J.tiles = c.N / gws::BF;
-    J.split = split;
-    J.per = per;
-    J.Y = c.Y;
-    J.ldy = c.ldy;
-    J.accumulate = c.accumulate;
-    J.pro_mode = c.pro_mode;
-    J.pro_src = c.pro_src;
-    J.pro_ld = c.pro_ld;
-    J.pro_cols = c.pro_cols;
-    J.pro_dst = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(c.X));
-    J.pro_ldd = c.ldx;
-    J.tail = c.tail_qkv;
-    grid = max(grid, J.tiles * split);
-  }
-  for (int j = njobs; j < gws::CHAIN_MAX; ++j) {
-    wms[j] = wms[0];
-    xms[j] = xms[0];
-  }
-  if (tail) p.tailph = *tail;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  PROPD_REQUIRE(grid <= 2 * sms, "gemm_chain: %d CTAs cannot all be co-resident", grid);
-  cudaStream_t st = as_stream(stream);
-  switch (mp) {
-    case 16: return gws::launch_chain<16>(wms, xms, p, grid, st);
-    case 32: return gws::launch_chain<32>(wms, xms, p, grid, st);
-    case 48: return gws::launch_chain<48>(wms, xms, p, grid, st);
-    case 64: return gws::launch_chain<64>(wms, xms, p, grid, st);
-    case 80: return gws::launch_chain<80>(wms, xms, p, grid, st);
-    case 96: return gws::launch_chain<96>(wms, xms, p, grid, st);
-    case 112: return gws::launch_chain<112>(wms, xms, p, grid, st);
-    default: return gws::launch_chain<128>(wms, xms, p, grid, st);
-  }
-}
-
-int propd_debug_barrier_bench(int ctas, int iters, uint32_t* bar, int impl, void* stream) {  // development aid
-  gws::barrier_bench_kernel<<<ctas, 128, 0, as_stream(stream)>>>(bar, iters, impl);
-  return check_launch("barrier_bench");
 }
 
 int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,

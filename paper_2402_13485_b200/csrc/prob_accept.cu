@@ -10,7 +10,7 @@
 
 namespace propd {
 
-constexpr int MAX_PATH = 16;  // tree depth bound (draft heads)
+constexpr int MAX_PATH = 32;  // tree depth bound = MAX_D draft heads (prune_verify.cu)
 
 // Per row of z = logits / temp: stats[r] = (log-sum-exp, entropy) in fp64.
 // idx (nullable) gathers rows: row r reads logits[idx[r]].

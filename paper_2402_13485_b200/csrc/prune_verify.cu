@@ -15,58 +15,93 @@
 namespace propd {
 
 // ---------------------------------------------------------------- K3 ------
-// One CTA per (sequence, node).  Counting rank: number of vocabulary entries
-// that a stable descending argsort would place before the child's token.
-__global__ void early_member_kernel(int n, int P, int V, int topk, const float* __restrict__ early,
-                                    const int32_t* __restrict__ parent, const int32_t* __restrict__ parent_slot,
-                                    const int32_t* __restrict__ tokens, uint8_t* __restrict__ member) {
-  __shared__ int red[32];
-  const int m = blockIdx.x;
-  const int b = m / n, i = m - b * n;
-  const int par = parent[i];
-  if (par < 0) {
-    if (threadIdx.x == 0) member[m] = 1;
-    return;
-  }
-  const float* row = early + ((size_t)b * P + parent_slot[par]) * V;
-  const int t = tokens[m];
-  const float target = row[t];
-  int cnt = 0;
-  // latency-bound scan (one parent row per CTA): 4 float4 loads in flight per thread
-  if ((V & 3) == 0 && (reinterpret_cast<uintptr_t>(early) & 15) == 0) {
-    const float4* r4 = reinterpret_cast<const float4*>(row);
-    const int V4 = V >> 2;
-    constexpr int U = 4;
-    for (int base = threadIdx.x; base < V4; base += U * blockDim.x) {
-      float4 f[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = base + u * blockDim.x;
-        f[u] = i < V4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int v = 4 * (base + u * blockDim.x);
-        cnt += (f[u].x > target) || (f[u].x == target && v < t);
-        cnt += (f[u].y > target) || (f[u].y == target && v + 1 < t);
-        cnt += (f[u].z > target) || (f[u].z == target && v + 2 < t);
-        cnt += (f[u].w > target) || (f[u].w == target && v + 3 < t);
-      }
-    }
-  } else {
-    for (int v = threadIdx.x; v < V; v += blockDim.x) {
-      const float x = row[v];
-      cnt += (x > target) || (x == target && v < t);
-    }
-  }
-  cnt = warp_isum(cnt);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) red[wid] = cnt;
+// One CTA per (sequence, parent row): the parent's early-logit row is read
+// once and every child of that parent is ranked against it in the same pass.
+// Counting rank of child token t: the number of vocabulary entries a stable
+// descending argsort places before t, #{v: l[v] > l[t]} + #{v < t: l[v] == l[t]};
+// the child is a member iff that rank is < K (the parent's K-th order
+// statistic under the (value desc, index asc) order).  Depth-1 nodes are
+// exempt (pruning.py:60-61) and written by the CTAs of parent row 0.
+constexpr int K3_THREADS = 512, K3_CH = 16, K3_MAXN = 1024;
+__global__ void __launch_bounds__(K3_THREADS) early_member_kernel(int n, int P, int V, int topk,
+                                                                  const float* __restrict__ early,
+                                                                  const int32_t* __restrict__ parent,
+                                                                  const int32_t* __restrict__ parent_slot,
+                                                                  const int32_t* __restrict__ tokens,
+                                                                  uint8_t* __restrict__ member) {
+  __shared__ int s_idx[K3_MAXN];
+  __shared__ int s_cnt;
+  __shared__ int red[K3_THREADS / 32][K3_CH];
+  const int Pe = P > 0 ? P : 1;
+  const int b = blockIdx.x / Pe, j = blockIdx.x - b * Pe;
+  if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
-  if (wid == 0) {
-    int c = lane < (int)(blockDim.x >> 5) ? red[lane] : 0;
-    c = warp_isum(c);
-    if (lane == 0) member[m] = c < topk ? 1 : 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int par = parent[i];
+    if (par < 0) {
+      if (j == 0) member[b * n + i] = 1;
+    } else if (parent_slot[par] == j) {
+      s_idx[atomicAdd(&s_cnt, 1)] = i;
+    }
+  }
+  __syncthreads();
+  const int nc = s_cnt;
+  if (nc == 0) return;
+  const float* row = early + ((size_t)b * P + j) * V;
+  const bool vec = (V & 3) == 0 && (reinterpret_cast<uintptr_t>(early) & 15) == 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < nc; c0 += K3_CH) {  // children in chunks held in registers (one row pass each)
+    float tv[K3_CH];
+    int tk[K3_CH], cnt[K3_CH];
+#pragma unroll
+    for (int c = 0; c < K3_CH; ++c) {
+      const bool live = c0 + c < nc;
+      tk[c] = live ? tokens[b * n + s_idx[c0 + c]] : 0;
+      tv[c] = live ? __ldg(row + tk[c]) : INFINITY;
+      cnt[c] = 0;
+    }
+    if (vec) {
+      const float4* r4 = reinterpret_cast<const float4*>(row);
+      const int V4 = V >> 2;
+      constexpr int U = 2;
+      for (int base = threadIdx.x; base < V4; base += U * blockDim.x) {
+        float4 f[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + u * blockDim.x;
+          f[u] = i < V4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int v = 4 * (base + u * blockDim.x);
+#pragma unroll
+          for (int c = 0; c < K3_CH; ++c) {
+            cnt[c] += (f[u].x > tv[c]) || (f[u].x == tv[c] && v < tk[c]);
+            cnt[c] += (f[u].y > tv[c]) || (f[u].y == tv[c] && v + 1 < tk[c]);
+            cnt[c] += (f[u].z > tv[c]) || (f[u].z == tv[c] && v + 2 < tk[c]);
+            cnt[c] += (f[u].w > tv[c]) || (f[u].w == tv[c] && v + 3 < tk[c]);
+          }
+        }
+      }
+    } else {
+      for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        const float x = row[v];
+#pragma unroll
+        for (int c = 0; c < K3_CH; ++c) cnt[c] += (x > tv[c]) || (x == tv[c] && v < tk[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < K3_CH; ++c) {
+      const int s = warp_isum(cnt[c]);
+      if (lane == 0) red[wid][c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < K3_CH && c0 + (int)threadIdx.x < nc) {
+      int s = 0;
+      for (int w = 0; w < K3_THREADS / 32; ++w) s += red[w][threadIdx.x];
+      member[b * n + s_idx[c0 + threadIdx.x]] = s < topk ? 1 : 0;
+    }
+    __syncthreads();
   }
 }
 
@@ -132,30 +167,42 @@ __global__ void pad_rows_kernel(int B, int S_pad, int pad_seq, const int32_t* __
 // ---------------------------------------------------------------- K5 ------
 constexpr int MAX_D = 32;
 
-// Moves accepted rows j (slot L + node[j]) to L + j for every layer/head.
-// Each thread owns a fixed 16-byte column chunk of one (layer, head) block and
-// walks j upward; since node[j] >= j and node is increasing, dst L+j never
-// aliases a source still to be read (read-before-write per element).
+// Moves accepted rows j (slot L + node[j]) to L + j.  One CTA per (sequence,
+// layer); each thread owns a fixed 16-byte column chunk of one head's block
+// and walks j upward: since node[j] >= j and node is increasing, dst L+j never
+// aliases a source still to be read (read-before-write per element).  seq_len
+// has already been advanced by the accepted count: L = seq_len - acc_len.
 template <typename T>
-__device__ void compact_rows(int len, const int* acc, int slot, int L, int layers, int A, int dh, int Lmax,
-                             int64_t layer_stride, T* kc, T* vc) {
+__global__ void compact_rows_kernel(int D, int A, int dh, int Lmax, int64_t layer_stride,
+                                    const int32_t* __restrict__ seq_slot, const int32_t* __restrict__ seq_len,
+                                    const int32_t* __restrict__ acc_node, const int32_t* __restrict__ acc_len, T* kc,
+                                    T* vc) {
+  __shared__ int s_acc[MAX_D];
+  const int b = blockIdx.x, l = blockIdx.y;
+  const int len = acc_len[b];
   if (len == 0) return;
+  const int slot = seq_slot[b];
+  const int L = seq_len[slot] - len;
+  if (threadIdx.x < len) s_acc[threadIdx.x] = acc_node[b * D + threadIdx.x];
+  __syncthreads();
   constexpr int VEC = 16 / sizeof(T);
   const int chunks = dh / VEC;
-  const int items = layers * A * chunks;
-  for (int w = threadIdx.x; w < items; w += blockDim.x) {
-    const int c = w % chunks;
-    const int la = w / chunks;
-    const int a = la % A, l = la / A;
+  for (int w = threadIdx.x; w < A * chunks; w += blockDim.x) {
+    const int c = w % chunks, a = w / chunks;
     const size_t base = (size_t)l * layer_stride + ((size_t)slot * A + a) * Lmax * dh + (size_t)c * VEC;
     for (int j = 0; j < len; ++j) {
-      const int src = acc[j];
+      const int src = s_acc[j];
       if (src == j) continue;
       const size_t so = base + (size_t)(L + src) * dh, dof = base + (size_t)(L + j) * dh;
       *reinterpret_cast<uint4*>(kc + dof) = *reinterpret_cast<const uint4*>(kc + so);
       *reinterpret_cast<uint4*>(vc + dof) = *reinterpret_cast<const uint4*>(vc + so);
     }
   }
+}
+
+__global__ void advance_by_acc_kernel(int B, const int32_t* seq_slot, int32_t* seq_len, const int32_t* acc_len) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) seq_len[seq_slot[b]] += acc_len[b];
 }
 
 // Typical acceptance (oracle typical_verify): candidate token x of a node is
@@ -215,13 +262,13 @@ __device__ int typical_walk(int b, int slot, int n, int D, const int32_t* parent
   return best;
 }
 
-template <typename T>
-__global__ void verify_commit_kernel(int n, int D, int kmax, int layers, int A, int dh, int Lmax, int64_t layer_stride,
-                                     const int32_t* __restrict__ parent, const int32_t* __restrict__ tokens,
+// One warp per sequence: walk, committed tokens, acceptance records; seq_len
+// advanced by the accepted count (the K/V rows move in compact_rows_kernel).
+__global__ void __launch_bounds__(32) verify_commit_kernel(int n, int D, int kmax, const int32_t* __restrict__ parent, const int32_t* __restrict__ tokens,
                                      const uint8_t* __restrict__ alive, const int32_t* __restrict__ node_row,
                                      const int32_t* __restrict__ row_argmax, const int32_t* __restrict__ root,
                                      const int32_t* __restrict__ draft_tok, const int32_t* __restrict__ seq_slot,
-                                     int32_t* seq_len, T* kc, T* vc, int32_t* acc_node, int32_t* acc_surv,
+                                     int32_t* seq_len, int32_t* acc_node, int32_t* acc_surv,
                                      int32_t* acc_len, int32_t* bonus, int32_t* committed, int8_t* ranks,
                                      propd_typical typ) {
   __shared__ int s_acc[MAX_D];
@@ -296,27 +343,7 @@ __global__ void verify_commit_kernel(int n, int D, int kmax, int layers, int A, 
       }
     }
   }
-  __syncthreads();
-  compact_rows<T>(s_len, s_acc, slot, s_L, layers, A, dh, Lmax, layer_stride, kc, vc);
-  __syncthreads();
-  if (threadIdx.x == 0) seq_len[slot] = s_L + s_len;
-}
-
-template <typename T>
-__global__ void kv_compact_kernel(int D, int layers, int A, int dh, int Lmax, int64_t layer_stride,
-                                  const int32_t* seq_slot, int32_t* seq_len, const int32_t* acc_node,
-                                  const int32_t* acc_len, T* kc, T* vc) {
-  __shared__ int s_acc[MAX_D];
-  __shared__ int s_L;
-  const int b = blockIdx.x;
-  const int slot = seq_slot[b];
-  const int len = acc_len[b];
-  if (threadIdx.x < len) s_acc[threadIdx.x] = acc_node[b * D + threadIdx.x];
-  if (threadIdx.x == 0) s_L = seq_len[slot];
-  __syncthreads();
-  compact_rows<T>(len, s_acc, slot, s_L, layers, A, dh, Lmax, layer_stride, kc, vc);
-  __syncthreads();
-  if (threadIdx.x == 0) seq_len[slot] = s_L + len;
+  if (threadIdx.x == 0) seq_len[slot] = s_L + s_len;  // compaction: compact_rows_kernel (L = seq_len - acc_len)
 }
 
 // ---------------------------------------------------------------- K4 ------
@@ -406,8 +433,9 @@ int propd_early_member(int B, int n, int P, int V, int topk, const float* early_
                        const int32_t* parent_slot, const int32_t* tokens, uint8_t* member, void* stream) {
   if (B == 0 || n == 0) return 0;
   PROPD_REQUIRE(topk >= 1, "early_member: topk must be positive");
-  early_member_kernel<<<B * n, 256, 0, as_stream(stream)>>>(n, P, V, topk, early_logits, parent, parent_slot, tokens,
-                                                            member);
+  PROPD_REQUIRE(n <= K3_MAXN, "early_member: tree of %d nodes > %d", n, K3_MAXN);
+  early_member_kernel<<<B * (P > 0 ? P : 1), K3_THREADS, 0, as_stream(stream)>>>(n, P, V, topk, early_logits, parent,
+                                                                                parent_slot, tokens, member);
   return check_launch("early_member");
 }
 
@@ -439,6 +467,18 @@ int propd_verify_commit(int dtype, int B, int n, int D, int kmax, int layers, in
                                 acc_surv, acc_len, bonus, committed, ranks, nullptr, stream);
 }
 
+// K/V rows of the accepted nodes -> positions L + j (seq_len already advanced)
+static int launch_compact(int dtype, int B, int D, int layers, int A, int dh, int Lmax, int64_t layer_stride,
+                          const int32_t* seq_slot, const int32_t* seq_len, const int32_t* acc_node,
+                          const int32_t* acc_len, void* kcache, void* vcache, cudaStream_t st) {
+  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
+    PROPD_REQUIRE((dh * (int)sizeof(T)) % 16 == 0, "kv compaction: dh*sizeof must be a multiple of 16");
+    compact_rows_kernel<T><<<dim3(B, layers), 256, 0, st>>>(D, A, dh, Lmax, layer_stride, seq_slot, seq_len, acc_node,
+                                                           acc_len, (T*)kcache, (T*)vcache);
+    return check_launch("kv compaction");
+  });
+}
+
 int propd_verify_commit_ex(int dtype, int B, int n, int D, int kmax, int layers, int A, int dh, int Lmax,
                            int64_t layer_stride, const int32_t* parent, const int32_t* tokens, const uint8_t* alive,
                            const int32_t* node_row, const int32_t* row_argmax, const int32_t* root,
@@ -447,17 +487,19 @@ int propd_verify_commit_ex(int dtype, int B, int n, int D, int kmax, int layers,
                            int32_t* committed, int8_t* ranks, const propd_typical* typical, void* stream) {
   if (B == 0) return 0;
   PROPD_REQUIRE(D >= 1 && D <= MAX_D, "verify_commit: D=%d outside 1..%d", D, MAX_D);
+  // acceptance records hold rank + 1 in an int8 (propd_stats_replay_select)
+  PROPD_REQUIRE(kmax >= 1 && kmax <= 127, "verify_commit: draft top-k %d outside 1..127 (int8 acceptance records)",
+                kmax);
   PROPD_REQUIRE(typical == nullptr || (n <= 1024 && typical->depth && typical->row_logits && typical->row_stats &&
                                        typical->root_logits && typical->root_stats),
                 "verify_commit: typical acceptance needs depth, row and root logits + statistics (n <= 1024)");
-  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
-    PROPD_REQUIRE((dh * (int)sizeof(T)) % 16 == 0, "verify_commit: dh*sizeof must be a multiple of 16");
-    verify_commit_kernel<T><<<B, 256, 0, as_stream(stream)>>>(
-        n, D, kmax, layers, A, dh, Lmax, layer_stride, parent, tokens, alive, node_row, row_argmax, root, draft_tok,
-        seq_slot, seq_len, (T*)kcache, (T*)vcache, acc_node, acc_surv, acc_len, bonus, committed, ranks,
-        typical ? *typical : propd_typical{});
-    return check_launch("verify_commit");
-  });
+  cudaStream_t st = as_stream(stream);
+  verify_commit_kernel<<<B, 32, 0, st>>>(n, D, kmax, parent, tokens, alive, node_row, row_argmax, root, draft_tok,
+                                         seq_slot, seq_len, acc_node, acc_surv, acc_len, bonus, committed, ranks,
+                                         typical ? *typical : propd_typical{});
+  if (int e = check_launch("verify_commit")) return e;
+  return launch_compact(dtype, B, D, layers, A, dh, Lmax, layer_stride, seq_slot, seq_len, acc_node, acc_len, kcache,
+                        vcache, st);
 }
 
 int propd_kv_compact(int dtype, int B, int D, int layers, int A, int dh, int Lmax, int64_t layer_stride,
@@ -465,17 +507,17 @@ int propd_kv_compact(int dtype, int B, int D, int layers, int A, int dh, int Lma
                      void* kcache, void* vcache, void* stream) {
   if (B == 0) return 0;
   PROPD_REQUIRE(D >= 1 && D <= MAX_D, "kv_compact: D=%d outside 1..%d", D, MAX_D);
-  return PROPD_DISPATCH_DTYPE(dtype, T, [&] {
-    PROPD_REQUIRE((dh * (int)sizeof(T)) % 16 == 0, "kv_compact: dh*sizeof must be a multiple of 16");
-    kv_compact_kernel<T><<<B, 256, 0, as_stream(stream)>>>(D, layers, A, dh, Lmax, layer_stride, seq_slot, seq_len,
-                                                           acc_node, acc_len, (T*)kcache, (T*)vcache);
-    return check_launch("kv_compact");
-  });
+  cudaStream_t st = as_stream(stream);
+  advance_by_acc_kernel<<<(B + 127) / 128, 128, 0, st>>>(B, seq_slot, seq_len, acc_len);
+  if (int e = check_launch("kv_compact")) return e;
+  return launch_compact(dtype, B, D, layers, A, dh, Lmax, layer_stride, seq_slot, seq_len, acc_node, acc_len, kcache,
+                        vcache, st);
 }
 
 int propd_stats_replay_select(int S, int D, int k, const int8_t* ranks, double alpha, double* P, int64_t* counts,
                               int32_t* order, double* lcurve, void* stream) {
-  PROPD_REQUIRE(D >= 1 && D <= MAX_D && k >= 1 && D * k <= 4096, "stats_replay_select: bad grid D=%d k=%d", D, k);
+  PROPD_REQUIRE(D >= 1 && D <= MAX_D && k >= 1 && k <= 127 && D * k <= 4096,
+                "stats_replay_select: bad grid D=%d k=%d (k <= 127: int8 acceptance records)", D, k);
   const size_t smem = (size_t)(2 * D * k + D + 1) * sizeof(double);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(stats_replay_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -25,6 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .config import EngineConfig
+from .parallel import COL_ACC, COL_FIN, COL_KEPT, COL_RANKS, COL_SURV, global_rows, record_width, step_exchange
 from .planning import (CostModel, InsufficientDataError, RuntimeSnapshot, choose_size, grid_candidates,
                        prewarm_P, should_replan)
 from .tree import TreeTemplate
@@ -98,6 +99,8 @@ class DecodeEngine:
                 raise ValueError("engine draft_heads must match the backend's head count")
             if config.draft_topk >= backend.vocab_size:
                 raise ValueError("draft_topk must be smaller than the vocabulary")
+            if config.draft_topk > 127:  # acceptance records: rank + 1 in an int8 (propd_stats_replay_select)
+                raise ValueError("draft_topk above 127 is not supported by the device acceptance records")
         if config.uses_prune and not 1 <= config.prune.layer < backend.num_layers:
             raise ValueError("prune layer must lie strictly inside the backbone")
         D, k = config.draft_heads, config.draft_topk
@@ -170,10 +173,13 @@ class DecodeEngine:
             states = self.backend.prefill_batch([group[i] for i in mine]) if mine else []
             seqs = [_Seq(st, group[i], lo + i) for st, i in zip(states, mine)]
             active = list(seqs)
-            while self._any_active(active):
+            # multi-rank: every rank tracks the whole chunk from the per-step tables
+            self._glob = _Global(group, world) if self.group is not None else None
+            while self._glob.any_active() if self._glob is not None else active:
                 metrics.append(self._step(active, max_tokens))
                 active = [s for s in seqs if not s.finished]
-            transcripts.extend(self._gather_transcripts(seqs, len(group)))
+            transcripts.extend(self._glob.transcripts if self._glob is not None else [s.generated for s in seqs])
+            self._glob = None
             for s in seqs:
                 self.backend.release(s.state)
         return RunResult(transcripts, prompts, metrics, list(self.plan_events), self._summarize(metrics))
@@ -181,65 +187,103 @@ class DecodeEngine:
     # ------------------------------------------------------------- step
     def _step(self, active: list, max_tokens: int) -> IterationMetrics:
         self._iteration += 1
-        glob = self._global_batch(active)
-        batch, mean_seqlen = glob["batch"], glob["mean_seqlen"]
+        glob = getattr(self, "_glob", None)
+        if glob is not None:
+            batch, mean_seqlen = glob.batch_stats()
+        else:
+            batch, mean_seqlen = len(active), float(np.mean([s.state.length for s in active]))
         wall0 = time.perf_counter() if self.latency is None else 0.0
         cfg = self.config
+        D = cfg.draft_heads
         if not cfg.uses_tree:
             toks = self.backend.step_autoregressive([s.state for s in active]) if active else []
-            committed = sum(self._absorb(s, [int(t)], max_tokens) for s, t in zip(active, toks))
-            committed = self._allsum(committed)
-            t = self._clock(wall0, 1.0, batch, mean_seqlen)
+            kept = [self._absorb(s, [int(t)], max_tokens) for s, t in zip(active, toks)]
+            if glob is None:
+                committed = sum(kept)
+                t = self._clock(wall0, 1.0, batch, mean_seqlen)
+            else:
+                rows = np.zeros((len(active), record_width(D)), dtype=np.int32)
+                rows[:, COL_RANKS + D + 1:] = -1
+                for i, (s, tk) in enumerate(zip(active, toks)):
+                    rows[i, COL_KEPT], rows[i, COL_FIN], rows[i, COL_RANKS + D] = kept[i], int(s.finished), int(tk)
+                hrows, t_wall = self._exchange(rows, wall0)
+                committed = int(hrows[:, COL_KEPT].sum())
+                t = self._clock(wall0, 1.0, batch, mean_seqlen, t_wall)
             return IterationMetrics(self._iteration, batch, mean_seqlen, 0, 0.0, 0.0, 0.0, committed, t, False)
 
         paths, replanned = self._plan(batch, mean_seqlen)
         tmpl = self._template(paths)
-        n = len(tmpl)
+        n = len(tmpl)  # nodes of the built tree (prune rate denominator, pruning.py:65)
+        drafted_n = len(paths)  # the reference's tree size: rows formula, cost.observe (engine.py:252, 290-298)
         prune = cfg.prune if cfg.uses_prune else None
         states = [s.state for s in active]
         stats = None
-        if self.group is None:  # single process: the backend replays the records in the step's batch
+        if glob is None:  # single process: the backend replays the records in the step's batch
             stats = (self._P, self._counts, cfg.acceptance_alpha, self._order_dev, self._lcurve_dev)
         accept = ((cfg.typical_epsilon, cfg.typical_alpha, cfg.typical_temperature)
                   if cfg.acceptance == "typical" else None)
         out = self.backend.step_tree(states, tmpl, cfg.draft_topk, prune, trace=self.trace is not None,
                                      stats=stats, accept=accept) if active else None
-        if stats is not None:
+        kept = []
+        for i, s in enumerate(active):
+            a = int(out.acc_len[i])
+            kept.append(self._absorb(s, [int(t) for t in out.committed[i, : a + 1]], max_tokens))
+            if self.trace is not None:
+                self._emit_trace(s, i, out, tmpl, a)
+        t_wall = None
+        if glob is None:
             self._order, self._lcurve = out.order, out.lcurve
+            acc = out.acc_len.astype(np.int64)
+            surv = out.surv_cnt.astype(np.int64)
+            committed = sum(kept)
         else:
-            ranks, S = self._gather_records(out, len(active))
-            self.backend.stats_replay_select(ranks, S, self._P, self._counts, cfg.acceptance_alpha,
-                                             self._order_dev, self._lcurve_dev)
+            rows = np.zeros((len(active), record_width(D)), dtype=np.int32)
+            if active:
+                rows[:, COL_ACC], rows[:, COL_SURV] = out.acc_len, out.surv_cnt
+                rows[:, COL_KEPT] = kept
+                rows[:, COL_FIN] = [int(s.finished) for s in active]
+                rows[:, COL_RANKS: COL_RANKS + D] = out.ranks
+                rows[:, COL_RANKS + D:] = out.committed
+            hrows, t_wall = self._exchange(rows, wall0)
+            acc = hrows[:, COL_ACC].astype(np.int64)
+            surv = hrows[:, COL_SURV].astype(np.int64)
+            committed = int(hrows[:, COL_KEPT].sum())
             self._pull_selection()
-        acc_total = surv_total = committed = 0
-        rates = []
-        if out is not None:
-            for i, s in enumerate(active):
-                a = int(out.acc_len[i])
-                newly = [int(t) for t in out.committed[i, : a + 1]]
-                committed += self._absorb(s, newly, max_tokens)
-                acc_total += a
-                surv_total += int(out.surv_cnt[i])
-                if prune is not None:
-                    rates.append(1.0 - int(out.surv_cnt[i]) / n)
-                if self.trace is not None:
-                    self._emit_trace(s, i, out, tmpl, a)
-        acc_total, surv_total, committed = self._allsum_vec([acc_total, surv_total, committed])
-        if self.group is not None and prune is not None:
-            from .parallel import all_gather_objects
-
-            rates = [r for part in all_gather_objects(rates, self.group) for r in part]
+        acc_total, surv_total = int(acc.sum()), int(surv.sum())
         surv_mean = surv_total / batch
         if prune is not None:
             p, Ly = prune.layer, self.backend.num_layers
-            rows = (p * n + (Ly - p) * surv_mean) / Ly
+            rows_eff = (p * drafted_n + (Ly - p) * surv_mean) / Ly
+            rates = [1.0 - int(c) / n for c in surv]  # global sequence order
             prune_rate = float(np.mean(rates)) if rates else 0.0  # numpy's pairwise sum, as the reference
         else:
-            rows, prune_rate = float(n), 0.0
-        t = self._clock(wall0, rows, batch, mean_seqlen)
-        self.cost.observe(n, t, now=self._iteration)
-        return IterationMetrics(self._iteration, batch, mean_seqlen, n, surv_mean, prune_rate,
+            rows_eff, prune_rate = float(drafted_n), 0.0
+        t = self._clock(wall0, rows_eff, batch, mean_seqlen, t_wall)
+        self.cost.observe(drafted_n, t, now=self._iteration)
+        return IterationMetrics(self._iteration, batch, mean_seqlen, drafted_n, surv_mean, prune_rate,
                                 acc_total / batch, committed, t, replanned)
+
+    def _exchange(self, rows: np.ndarray, wall0: float):
+        """The step's one collective: every rank's records in global order;
+        replays the acceptance records into P (tree modes) and advances the
+        chunk's global view.  Returns (rows [S, R], max step seconds or None)."""
+        import torch
+
+        glob, D = self._glob, self.config.draft_heads
+        us = 0
+        if self.latency is None:
+            torch.cuda.synchronize(self.backend.device)
+            us = int(min((time.perf_counter() - wall0) * 1e6, 2**31 - 1))
+        table = step_exchange(rows, us, glob.cap, self.group)
+        hrows, step_us, drows = global_rows(table)
+        if self.config.uses_tree:
+            ranks = drows[:, COL_RANKS: COL_RANKS + D].to(torch.int8).to(self.backend.device)
+            if ranks.shape[0] == 0:
+                ranks = torch.zeros(1, D, dtype=torch.int8, device=self.backend.device)
+            self.backend.stats_replay_select(ranks, int(hrows.shape[0]), self._P, self._counts,
+                                             self.config.acceptance_alpha, self._order_dev, self._lcurve_dev)
+        glob.advance(hrows, D)
+        return hrows, (float(step_us.max()) * 1e-6 if self.latency is None else None)
 
     def _emit_trace(self, s, i, out, tmpl, a) -> None:
         tr = out.trace
@@ -320,11 +364,12 @@ class DecodeEngine:
                 break
         return kept
 
-    def _clock(self, wall0: float, rows: float, batch: int, seqlen: float) -> float:
+    def _clock(self, wall0: float, rows: float, batch: int, seqlen: float, t_wall: float | None = None) -> float:
         if self.latency is None:
+            if t_wall is not None:  # multi-rank: the maximum over ranks, from the step table
+                return max(t_wall, 1e-9)
             self.backend.torch.cuda.synchronize(self.backend.device)
-            t = max(time.perf_counter() - wall0, 1e-9)
-            return self._allmax(t)
+            return max(time.perf_counter() - wall0, 1e-9)
         return self.latency.iteration_time(rows, batch=batch, seqlen=seqlen)
 
     def _summarize(self, metrics) -> RunSummary:
@@ -344,69 +389,6 @@ class DecodeEngine:
 
         return dist.get_rank(self.group), dist.get_world_size(self.group)
 
-    def _any_active(self, active) -> bool:
-        if self.group is None:
-            return bool(active)
-        return self._allsum(len(active)) > 0
-
-    def _global_batch(self, active) -> dict:
-        n_local = len(active)
-        len_local = float(sum(s.state.length for s in active))
-        if self.group is None:
-            return {"batch": n_local, "mean_seqlen": float(np.mean([s.state.length for s in active]))}
-        # every rank needs the same (batch, mean_seqlen) for the plan: gather
-        # integer lengths in global order and average them like the reference
-        lens = self._allgather_ints([s.state.length for s in active])
-        return {"batch": len(lens), "mean_seqlen": float(np.mean(lens))}
-
-    def _gather_records(self, out, n_local: int):
-        import torch
-
-        D = self.config.draft_heads
-        local = out.ranks_dev if out is not None else torch.zeros(0, D, dtype=torch.int8, device=self.backend.device)
-        if self.group is None:
-            return local, n_local
-        from .parallel import all_gather_records
-
-        allr = all_gather_records(local, self.group)
-        return allr, allr.shape[0]
-
-    def _allsum(self, v):
-        if self.group is None:
-            return v
-        from .parallel import all_reduce_scalars
-
-        return all_reduce_scalars([v], "sum", self.group)[0]
-
-    def _allsum_vec(self, vals):
-        if self.group is None:
-            return vals
-        from .parallel import all_reduce_scalars
-
-        return all_reduce_scalars(vals, "sum", self.group)
-
-    def _allmax(self, v):
-        if self.group is None:
-            return v
-        from .parallel import all_reduce_scalars
-
-        return all_reduce_scalars([v], "max", self.group)[0]
-
-    def _allgather_ints(self, vals):
-        from .parallel import all_gather_ints
-
-        return all_gather_ints(vals, self.group)
-
-    def _gather_transcripts(self, seqs, n_group: int):
-        if self.group is None:
-            return [s.generated for s in seqs]
-        from .parallel import all_gather_objects
-
-        pieces = all_gather_objects([(s.gid, s.generated) for s in seqs], self.group)
-        merged = sorted((g for part in pieces for g in part), key=lambda t: t[0])
-        return [g for _, g in merged]
-
-
 def _warm_host_math() -> None:
     """The first weighted least-squares fit initialises numpy's BLAS (tens of
     ms); do it once up front instead of inside the first replanned step."""
@@ -421,3 +403,32 @@ def _shard(n: int, rank: int, world: int) -> list:
     lo = (n * rank) // world
     hi = (n * (rank + 1)) // world
     return list(range(lo, hi))
+
+
+class _Global:
+    """Every rank's view of the whole batch chunk in global sequence order
+    (committed lengths, active flags, transcripts), advanced from the step
+    tables alone."""
+
+    def __init__(self, group, world: int) -> None:
+        self.length = [len(p) for p in group]
+        self.active = [True] * len(group)
+        self.transcripts = [[] for _ in group]
+        self.cap = max(1, max(len(_shard(len(group), r, world)) for r in range(world)))
+
+    def any_active(self) -> bool:
+        return any(self.active)
+
+    def batch_stats(self):
+        lens = [L for L, a in zip(self.length, self.active) if a]
+        return len(lens), float(np.mean(lens))
+
+    def advance(self, rows: np.ndarray, D: int) -> None:
+        ids = [i for i, a in enumerate(self.active) if a]
+        if len(ids) != rows.shape[0]:
+            raise RuntimeError(f"step table holds {rows.shape[0]} sequences, {len(ids)} are active")
+        for i, r in zip(ids, rows):
+            acc = int(r[COL_ACC])
+            self.length[i] += acc + 1  # the backend commits the whole chain + bonus (backends.py:337-348)
+            self.transcripts[i].extend(int(t) for t in r[COL_RANKS + D: COL_RANKS + D + acc + 1][: int(r[COL_KEPT])])
+            self.active[i] = not bool(r[COL_FIN])

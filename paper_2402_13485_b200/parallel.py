@@ -1,82 +1,78 @@
 """Multi-GPU plumbing: one model replica per rank, sequences sharded in
-contiguous ranges, and the per-step exchange of acceptance records.
+contiguous ranges, and ONE collective per decode step.
 
-The only data-path collective is `all_gather_records`: each rank contributes
-its [B_r, D] int8 acceptance records (1-based rank of the realized token in
-the head's draft list, -1 miss, 0 unknown depth) and receives the global
-[sum B_r, D] table in rank order, which is global sequence order.  Every
-rank then replays the fp64 statistics update in that order on its own device
-(propd_stats_replay_select), so all replicas hold bit-identical P and plan
-the same tree — the reference's single-process update order
-(engine.py:257-288, acceptance.py:96-113).  Summing float hit counts with an
-all-reduce would not be bit-exact because the EMA is order-dependent.
+Each step every rank contributes a fixed-size int32 table (`step_exchange`):
+a header row [active sequences on this rank, step time in µs] and one row per
+active sequence:
 
-Works over NCCL (CUDA tensors) and gloo (CPU tensors, used by the CPU tests).
+    [acc_len, |survivors|, tokens kept after EOS/max clipping, finished,
+     rank record r_1..r_D, committed tokens c_0..c_D]
+
+where r_d is the 1-based rank of the realized token in head d's draft list
+(-1 miss, 0 depth not reached; acceptance.py:53-57, engine.py:283-288) and
+c_0..c_D the accepted chain + bonus (-1 padded).  One all_gather of the table
+gives every rank the whole step in global sequence order (ranks own
+contiguous, increasing index ranges): every rank replays the fp64 statistics
+update in that order on its own device (propd_stats_replay_select), so the
+replicas hold bit-identical P, plan the same tree and agree with the
+single-process reference (acceptance.py:96-113 applied per sequence in batch
+order, engine.py:257-288).  Batch size, mean sequence length, prune rates,
+metric sums, the wall-clock maximum and the transcripts all follow from the
+same table, so there is no other per-step collective and nothing is pickled.
+A sum of float hit counts would not be bit-exact: the EMA is order-dependent.
+
+Works over NCCL (CUDA tensors) and gloo (CPU tensors; the CPU tests).
 """
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
+HEADER_ACTIVE, HEADER_STEP_US = 0, 1
+COL_ACC, COL_SURV, COL_KEPT, COL_FIN, COL_RANKS = 0, 1, 2, 3, 4
 
-def _dev(group):
+
+def record_width(D: int) -> int:
+    return COL_RANKS + D + D + 1
+
+
+def collective_device(group):
+    """Where the exchanged tensor lives: the current GPU for NCCL, host for gloo."""
     return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
 
 
-def all_gather_records(local: torch.Tensor, group=None) -> torch.Tensor:
-    """Concatenate every rank's [B_r, D] int8 records in rank order."""
-    dev = _dev(group)
+def step_exchange(rows: np.ndarray, step_us: int, cap: int, group) -> torch.Tensor:
+    """All-gather of every rank's [cap + 1, R] int32 step table (header row +
+    up to `cap` sequence rows) -> [world, cap + 1, R] on the collective's device."""
+    dev = collective_device(group)
     world = dist.get_world_size(group)
-    D = local.shape[1]
-    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    sizes = [int(s.item()) for s in sizes]
-    cap = max(max(sizes), 1)
-    buf = torch.zeros(cap, D, dtype=torch.int8, device=dev)
-    if local.shape[0]:
-        buf[: local.shape[0]] = local.to(dev)
-    parts = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf, group=group)
-    out = torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
-    return out.to(local.device)
+    R = rows.shape[1]
+    host = np.zeros((cap + 1, R), dtype=np.int32)
+    host[0, HEADER_ACTIVE] = rows.shape[0]
+    host[0, HEADER_STEP_US] = step_us
+    host[1: 1 + rows.shape[0]] = rows
+    buf = torch.from_numpy(host).to(dev)
+    out = torch.empty(world, cap + 1, R, dtype=torch.int32, device=dev)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, buf, group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), buf, group=group)
+    return out
 
 
-def all_reduce_scalars(vals, op: str, group=None):
-    """Sum/max of a few python scalars across ranks (ints stay ints)."""
-    dev = _dev(group)
-    is_int = [isinstance(v, (int,)) and not isinstance(v, bool) for v in vals]
-    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX, group=group)
-    return [int(round(x)) if i else float(x) for x, i in zip(t.tolist(), is_int)]
-
-
-def all_gather_ints(vals, group=None) -> list:
-    """Concatenation of every rank's int list, in rank order."""
-    dev = _dev(group)
-    local = torch.tensor(list(vals), dtype=torch.int64, device=dev).view(-1, 1)
-    recs = all_gather_records_int64(local, group)
-    return [int(v) for v in recs.view(-1).tolist()]
-
-
-def all_gather_records_int64(local: torch.Tensor, group=None) -> torch.Tensor:
-    dev = _dev(group)
-    world = dist.get_world_size(group)
-    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    sizes = [int(s.item()) for s in sizes]
-    cap = max(max(sizes), 1)
-    buf = torch.zeros(cap, local.shape[1], dtype=torch.int64, device=dev)
-    if local.shape[0]:
-        buf[: local.shape[0]] = local.to(dev)
-    parts = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(parts, buf, group=group)
-    return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
+def global_rows(table: torch.Tensor) -> tuple:
+    """(host [S, R] int32 rows of every active sequence in global order, the
+    per-rank step µs, the device/host tensor of those rows)."""
+    counts = table[:, 0, HEADER_ACTIVE].tolist()
+    parts = [table[r, 1: 1 + n] for r, n in enumerate(counts)]
+    dev_rows = torch.cat(parts, dim=0) if parts else table[:0, 0]
+    return dev_rows.cpu().numpy(), table[:, 0, HEADER_STEP_US].cpu().numpy(), dev_rows
 
 
 def all_gather_objects(obj, group=None) -> list:
+    """Pickled gather (end-of-run use only, never on the per-step path)."""
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, obj, group=group)
     return out

@@ -31,6 +31,15 @@ def seeded_weights(cfg) -> dict:
     return out
 
 
+def _guard_row(pos):
+    """Position table + one zero row at index max_positions: the bonus row of a
+    step whose commit would overflow max_positions reads it (in bounds) before
+    the host raises the reference's "sequence exceeds max_positions"."""
+    import torch
+
+    return torch.cat([pos, torch.zeros(1, pos.shape[1], device=pos.device, dtype=pos.dtype)])
+
+
 class DeviceWeights:
     """Device-resident weights in the GEMM layout of the B200 path:
     wqkv[l] = [wq | wk | wv] (H, 3H), wo (H, H), w1 (H, 4H), w2 (4H, H),
@@ -43,7 +52,7 @@ class DeviceWeights:
         H, V, D = cfg.hidden, cfg.vocab, cfg.draft_heads
         if host is not None:
             t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dtype)
-            self.emb, self.pos = t(host["emb"]), t(host["pos"])
+            self.emb, self.pos = t(host["emb"]), _guard_row(t(host["pos"]))
             self.wqkv = [t(np.concatenate([b["wq"], b["wk"], b["wv"]], axis=1)) for b in host["blocks"]]
             self.wo = [t(b["wo"]) for b in host["blocks"]]
             self.w1 = [t(b["w1"]) for b in host["blocks"]]
@@ -60,13 +69,23 @@ class DeviceWeights:
                 w.normal_(0.0, std, generator=g)
                 return w.to(dtype)
 
-            self.emb, self.pos = rnd(V, H), rnd(cfg.max_positions, H)
+            self.emb, self.pos = rnd(V, H), _guard_row(rnd(cfg.max_positions, H))
             self.wqkv = [rnd(H, 3 * H) for _ in range(cfg.layers)]
             self.wo = [rnd(H, H) for _ in range(cfg.layers)]
             self.w1 = [rnd(H, 4 * H) for _ in range(cfg.layers)]
             self.w2 = [rnd(4 * H, H, 0.5 * s) for _ in range(cfg.layers)]
             self.w_lm, self.w_early = rnd(H, V), rnd(H, V)
             self.w_draft = rnd(H, D * V)
+
+    def streamed_bytes_per_step(self, prune: bool = True) -> int:
+        """Weight bytes one tree step streams from HBM: the layer stack twice
+        (tree pass + bonus pass), the LM head twice, the early head once when
+        pruning, the draft heads once (the embedding and position tables are
+        gathered row by row, not streamed)."""
+        el = self.w_lm.element_size()
+        layers = self.layer_bytes() * self.cfg.layers
+        heads = 2 * self.w_lm.numel() * el + self.w_draft.numel() * el + (self.w_early.numel() * el if prune else 0)
+        return 2 * layers + heads
 
     def nbytes(self) -> int:
         ts = [self.emb, self.pos, self.w_lm, self.w_early, self.w_draft, *self.wqkv, *self.wo, *self.w1, *self.w2]

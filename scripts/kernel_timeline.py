@@ -28,14 +28,12 @@ ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--show", type=int, default=2, help="layers to print")
 ap.add_argument("--unfused", action="store_true")
 ap.add_argument("--per-cta", action="store_true", help="attention: per-CTA phase percentiles")
-ap.add_argument("--chain", action="store_true", help="one persistent chain launch per layer (propd_gemm_chain)")
 args = ap.parse_args()
 
 cfg = TinyTransformerConfig(layers=args.layers, hidden=4096, heads=32, vocab=32000, draft_heads=4,
                             max_positions=args.kv + 256, seed=0)
 be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=2, max_tree=64, kv_len=cfg.max_positions)
 be.ws_phases = not args.unfused
-be.ws_chain = args.chain
 states = be.synthetic_states(1, args.kv)
 dev = be.device
 paths = sorted({(1,) * d for d in range(1, 5)} | {(r,) for r in range(1, 17)} | {(1, r) for r in range(1, 17)})

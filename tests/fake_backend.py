@@ -77,7 +77,7 @@ class OracleBatchBackend:
                 r = pred.rank_of(d + 1, newly[d])
                 ranks[b, d] = r if r is not None else -1
         out = SimpleNamespace(committed=committed, acc_len=acc_len, acc_surv=acc_surv, surv_cnt=surv_cnt,
-                              ranks_dev=torch.from_numpy(ranks), trace=None, order=None, lcurve=None)
+                              ranks_dev=torch.from_numpy(ranks), ranks=ranks, trace=None, order=None, lcurve=None)
         if stats is not None:
             P, counts, alpha, order, lcurve = stats
             self.stats_replay_select(out.ranks_dev, B, P, counts, alpha, order, lcurve)

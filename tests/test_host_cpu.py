@@ -168,12 +168,13 @@ def _gloo_worker(rank, world, port, mode, result_path):
     try:
         from paper_2402_13485_b200 import parallel
 
-        # collectives: records in rank order, scalar reductions, int gathers
-        local = torch.full((rank + 1, 4), rank + 1, dtype=torch.int8)
-        allr = parallel.all_gather_records(local, dist.group.WORLD)
-        assert allr.shape == (3, 4) and allr[:1].eq(1).all() and allr[1:].eq(2).all()
-        assert parallel.all_reduce_scalars([rank + 1, 0.5], "sum") == [3, 1.0]
-        assert parallel.all_gather_ints([rank] * (rank + 1)) == [0, 1, 1]
+        # the one per-step collective: fixed-size tables, rows in rank (= global sequence) order
+        rows = np.full((rank + 1, parallel.record_width(2)), rank + 1, dtype=np.int32)
+        table = parallel.step_exchange(rows, 100 * (rank + 1), 2, dist.group.WORLD)
+        assert tuple(table.shape) == (2, 3, parallel.record_width(2))
+        hrows, step_us, _ = parallel.global_rows(table)
+        assert hrows.shape[0] == 3 and (hrows[:1] == 1).all() and (hrows[1:] == 2).all()
+        assert step_us.tolist() == [100, 200]
         cfg = op.RUN_TINY
         e = cfg["engine"]
         ecfg = EngineConfig(mode=mode, draft_heads=4, draft_topk=3,
