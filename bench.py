@@ -67,9 +67,9 @@ def parse(argv=None):
     ap.add_argument("--same-device", action="store_true", help="every rank on cuda:0 (multi-rank dry run)")
     ap.add_argument("--sync-rows", action="store_true",
                     help="size the post-prune layers on the host (one mid-step sync) instead of on the device")
-    ap.add_argument("--ref-tree-sizes", default="64,64,64,32,32",
+    ap.add_argument("--ref-tree-sizes", default="64,64,64,64,32,32,32,32,32,32,32,32,32,32,32,32,32,32,32,32",
                     help="reference arm: per-step tree sizes (cycled) it is pinned to; the default is the schedule "
-                         "the B200 arm's dynamic plan settles into at configs[1] (mean 51.2 nodes)")
+                         "the B200 arm's dynamic plan ran in its 20 timed steps at configs[1] (mean 38.4 nodes)")
     return ap.parse_args(argv)
 
 
@@ -80,7 +80,11 @@ def model_cfg(args, kv_cap: int | None = None):
     if getattr(args, "layers", None) is not None:
         shape["layers"] = args.layers
     kv = args.kv if kv_cap is None else kv_cap
-    return TinyTransformerConfig(**shape, max_positions=kv + 5 * (2 * args.steps + args.warmup + 110), seed=0)
+    # growth room: every step commits acc + 1 tokens (random init: acc ~ 0; planted: 1) over at most four
+    # priming phases of <= 48 steps, the warm-up and three K-step regions
+    per_step = 3 if getattr(args, "planted", False) else 2
+    return TinyTransformerConfig(**shape, max_positions=kv + per_step * (4 * 48 + 3 * args.steps + args.warmup + 8)
+                                 + 64, seed=0)
 
 
 def engine_cfg(args, mode=None):
@@ -216,8 +220,13 @@ def cpu_reference(args, steps: int, warmup: int, sizes=None):
                                                          ("wo", (H, H)), ("w1", (H, 4 * H)))}
     blk["w2"] = rng.standard_normal((4 * H, H)) * (0.5 * s)
     head = rng.standard_normal((H, V)) * s
-    w = {"emb": np.ascontiguousarray(head.T), "pos": rng.standard_normal((cfg.max_positions, H)) * s,
-         "blocks": [blk] * Ly, "w_lm": head, "w_early": head, "w_draft": [head] * D}
+    # the other [H, V] heads and the embedding: independent column permutations of one draw (the draft and
+    # early heads must not coincide with the LM head, or acceptance would be planted)
+    perm = lambda: np.ascontiguousarray(head[:, rng.permutation(V)])
+    w = {"emb": np.ascontiguousarray(perm().T), "pos": rng.standard_normal((cfg.max_positions, H)) * s,
+         "blocks": [blk] * Ly, "w_lm": head, "w_early": perm(), "w_draft": [perm() for _ in range(D)]}
+    if args.planted:
+        w["w_draft"][0] = head
     log: list = []
 
     class TimedModel(op.TinyModel):
@@ -561,12 +570,9 @@ def run_sweep(args, dev):
         pts.append((int(f[0]), int(f[1]), f[2] if len(f) > 2 else "propd_full"))
     K = 5
     kv_max, b_max = max(p[1] for p in pts), max(p[0] for p in pts)
-    margin = 5 * (3 * 48 + 3 * K + 8)
-    import copy
-
-    sargs = copy.copy(args)
-    sargs.steps, sargs.warmup = K, 0
-    cfg = model_cfg(sargs, kv_cap=kv_max)
+    # per point: <= 3 priming phases of <= 48 steps + K + 3 + 1 steps of ~1 token (random init)
+    margin = 2 * (3 * 48 + K + 4) + 16
+    cfg = model_cfg(args, kv_cap=kv_max)
     cfg = type(cfg)(**{**cfg.__dict__, "max_positions": kv_max + margin})
     be = B200Backend(cfg, dtype="bf16", device=dev, random_device_init=True, max_slots=b_max,
                      max_tree=4 * args.topk, kv_len=cfg.max_positions, use_graphs=True)

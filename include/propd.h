@@ -189,6 +189,33 @@ typedef struct propd_ws_phases {
 } propd_ws_phases;
 int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
                      float* Y, int ldy, int accumulate, int max_split, const propd_ws_phases* phases, void* stream);
+/* ---- projections over many rows (> 128): Y = epilogue(X[M,K] . W[K,N]) ----
+ * (backends.py:217-219, 234-236, 281, 321, 329).  bf16: persistent tcgen05
+ * kernel (128 x 256 tiles, TMA, TMEM double-buffered accumulator; N % 32 == 0,
+ * K % 64 == 0, 16-byte aligned rows); fp32 (parity mode): CUDA-core SGEMM.
+ * rows_dev (nullable): live row count on the device (rows past it untouched).
+ * Epilogue modes:
+ *   STORE_F32  Y fp32 [M, N] = acc          (logits)
+ *   ADD_F32    Y fp32 += acc                 (residual stream: W_o, W_2)
+ *   STORE      Y [M, N] = acc in dtype       (bf16 / fp32 operand)
+ *   GELU       Y = tanh-GELU(acc) in dtype   (W_1)
+ *   QKV        N = 3H: columns < H -> Y (Q operand), K / V columns -> the layer
+ *              cache at slot seq_len[seq_slot[row_seq[m]]] + row_node[m]. */
+enum { PROPD_EPI_STORE = 0, PROPD_EPI_STORE_F32 = 1, PROPD_EPI_ADD_F32 = 2, PROPD_EPI_GELU = 3, PROPD_EPI_QKV = 4 };
+typedef struct propd_gemm_epi {
+  int mode;
+  void* Y;
+  int ldy;
+  int A, dh, Lmax;
+  const int32_t* row_seq;
+  const int32_t* row_node;
+  const int32_t* seq_slot;
+  const int32_t* seq_len;
+  void* kcache;
+  void* vcache;
+} propd_gemm_epi;
+int propd_gemm(int dtype, int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W,
+               int ldw, const propd_gemm_epi* epi, void* stream);
 /* acc[M, 3H] fp32 -> qkv bf16 [M, 3H] and K/V rows into the layer cache
  * (slot seq_len[seq_slot[row_seq[m]]] + row_node[m]); acc re-zeroed. */
 int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,

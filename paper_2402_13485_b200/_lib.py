@@ -44,6 +44,7 @@ SIGNATURES = {
     "propd_tree_attention": [I, I, I, I, I, I, I, I, I, I, P, I, P, P, P, P, P, P, P, I, I, P, I, P, L, P],
     "propd_gemm_ws": [I, P, I, I, P, I, P, I, P, I, I, I, P],
     "propd_gemm_ws_ph": [I, P, I, I, P, I, P, I, P, I, I, I, "phases", P],
+    "propd_gemm": [I, I, P, I, I, P, I, P, I, "epi", P],
     "propd_qkv_finish": [I, P, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
     "propd_gelu_finish": [I, P, I, P, I, P, I, P],
     "propd_early_member": [I, I, I, I, I, P, P, P, P, P, P],
@@ -74,6 +75,16 @@ class WsPhases(ctypes.Structure):
                 ("kcache", P), ("vcache", P), ("bar", P)]
 
 
+EPI_STORE, EPI_STORE_F32, EPI_ADD_F32, EPI_GELU, EPI_QKV = 0, 1, 2, 3, 4
+
+
+class GemmEpi(ctypes.Structure):
+    """propd_gemm_epi (include/propd.h): epilogue of a many-row projection."""
+
+    _fields_ = [("mode", c_int), ("Y", P), ("ldy", c_int), ("A", c_int), ("dh", c_int), ("Lmax", c_int),
+                ("row_seq", P), ("row_node", P), ("seq_slot", P), ("seq_len", P), ("kcache", P), ("vcache", P)]
+
+
 class Typical(ctypes.Structure):
     """propd_typical (include/propd.h): typical-acceptance inputs of propd_verify_commit_ex."""
 
@@ -101,7 +112,7 @@ def load():
     lib = ctypes.CDLL(LIB_PATH)
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
-        structs = {"phases": WsPhases, "typical": Typical}
+        structs = {"phases": WsPhases, "typical": Typical, "epi": GemmEpi}
         fn.argtypes = [ctypes.POINTER(structs[a]) if isinstance(a, str) else a for a in argtypes]
         fn.restype = _RESTYPES.get(name, c_int)
     if lib.propd_abi_version() != ABI_VERSION:

@@ -687,3 +687,89 @@ def test_typical_acceptance_matches_oracle(eps, alpha, temp):
             bonus]
         deep = max(deep, L)
     assert deep >= 2  # the cases exercise multi-node paths
+
+
+# --------------------------------------------------------------- many-row projections (propd_gemm)
+def _epi(mode, Y, ldy, **kw):
+    e = _lib.GemmEpi(mode=mode, Y=ptr(Y), ldy=ldy)
+    for k, v in kw.items():
+        setattr(e, k, v)
+    return e
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("M,N,K,mode", [(129, 4096, 4096, "store"), (300, 12288, 4096, "qkv"),
+                                         (1000, 16384, 4096, "gelu"), (4096, 4096, 16384, "add"),
+                                         (257, 32000, 4096, "f32"), (700, 4128, 1024, "add"), (1, 256, 64, "f32")])
+def test_gemm_matches_fp32_reference(dtype, M, N, K, mode):
+    """Y = epilogue(X . W): tcgen05 (bf16 operands, fp32 accumulation) and the fp32 CUDA-core path vs torch
+    fp32 on the same (bf16-rounded) operands.  bf16: |err| <= 1e-3 * max(1, |ref|) on fp32 outputs
+    (+ bf16 output rounding 8e-3 relative); fp32: 1e-5 relative."""
+    if dtype == "fp32" and M * N * K > 2e10:
+        pytest.skip("large shape: tensor-core path only")
+    torch.manual_seed(M + N + K)
+    T = torch.bfloat16 if dtype == "bf16" else torch.float32
+    code = _lib.BF16 if dtype == "bf16" else _lib.F32
+    X = torch.randn(M, K, device=DEV).to(T)
+    W = (torch.randn(K, N, device=DEV) / K ** 0.5).to(T)
+    ref = X.float() @ W.float()
+    tol = (1e-3 if dtype == "bf16" else 1e-5) * max(1.0, ref.abs().max().item())
+    otol = 8e-3 if dtype == "bf16" else 1e-5  # rounding of a dtype output
+    if mode in ("f32", "add"):
+        base = torch.randn(M, N, device=DEV) if mode == "add" else torch.full((M, N), float("nan"), device=DEV)
+        Y = base.clone()
+        epi = _epi(_lib.EPI_ADD_F32 if mode == "add" else _lib.EPI_STORE_F32, Y, N)
+        call("propd_gemm", code, M, None, N, K, ptr(X), K, ptr(W), N, epi, st())
+        torch.cuda.synchronize()
+        want = ref + (base if mode == "add" else 0)
+        assert (Y - want).abs().max().item() <= tol
+    elif mode in ("store", "gelu"):
+        Y = torch.full((M, N), float("nan"), device=DEV).to(T)
+        epi = _epi(_lib.EPI_GELU if mode == "gelu" else _lib.EPI_STORE, Y, N)
+        call("propd_gemm", code, M, None, N, K, ptr(X), K, ptr(W), N, epi, st())
+        torch.cuda.synchronize()
+        want = torch.nn.functional.gelu(ref, approximate="tanh") if mode == "gelu" else ref
+        assert (Y.float() - want).abs().max().item() <= tol + otol * want.abs().max().item()
+    else:  # QKV: Q -> Y, K/V -> cache slots seq_len[slot] + node
+        A, dh, Lmax = 32, 128, 400
+        H = A * dh
+        assert N == 3 * H
+        nseq = 3
+        per = [100, 120, 80]
+        row_seq = i32(np.repeat(np.arange(nseq), per))
+        row_node = i32(np.concatenate([np.arange(p) for p in per]))
+        seq_slot, seq_len = i32([2, 0, 1]), i32([7, 250, 31])
+        kc = torch.zeros(3, A, Lmax, dh, device=DEV, dtype=T)
+        vc = torch.zeros_like(kc)
+        Y = torch.zeros(M, 3 * H, device=DEV, dtype=T)
+        epi = _epi(_lib.EPI_QKV, Y, 3 * H, A=A, dh=dh, Lmax=Lmax, row_seq=ptr(row_seq), row_node=ptr(row_node),
+                   seq_slot=ptr(seq_slot), seq_len=ptr(seq_len), kcache=ptr(kc), vcache=ptr(vc))
+        call("propd_gemm", code, M, None, N, K, ptr(X), K, ptr(W), N, epi, st())
+        torch.cuda.synchronize()
+        lim = tol + otol * ref.abs().max().item()
+        assert (Y[:, :H].float() - ref[:, :H]).abs().max().item() <= lim
+        rs, rn = row_seq.cpu().numpy(), row_node.cpu().numpy()
+        slots, lens = seq_slot.cpu().numpy(), seq_len.cpu().numpy()
+        for m in range(M):
+            s = slots[rs[m]]
+            pos = lens[s] + rn[m]
+            assert (kc[s, :, pos].float().reshape(-1) - ref[m, H:2 * H]).abs().max().item() <= lim
+            assert (vc[s, :, pos].float().reshape(-1) - ref[m, 2 * H:]).abs().max().item() <= lim
+
+
+@pytest.mark.parametrize("live", [0, 129, 255, 1000])
+def test_gemm_device_row_count(live):
+    """rows_dev: rows < min(M, *rows_dev) are computed, the rest of Y is untouched (bit-exact)."""
+    M, N, K = 700, 4096, 1024
+    torch.manual_seed(live)
+    X = torch.randn(M, K, device=DEV).bfloat16()
+    W = (torch.randn(K, N, device=DEV) / K ** 0.5).bfloat16()
+    ref = X.float() @ W.float()
+    base = torch.randn(M, N, device=DEV)
+    Y = base.clone()
+    call("propd_gemm", _lib.BF16, M, ptr(i32([live])), N, K, ptr(X), K, ptr(W), N, _epi(_lib.EPI_ADD_F32, Y, N), st())
+    torch.cuda.synchronize()
+    r = min(M, live)
+    if r:
+        assert (Y[:r] - ref[:r] - base[:r]).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
+    assert torch.equal(Y[r:], base[r:])
