@@ -362,13 +362,13 @@ def timeline_step(be, eng, seqs, prime, dev, prune_layer):
     out = {"step_ms": t0.elapsed_time(t1), "records": n}
     kinds = rec[:, 7] & 0xFF
     hbm, _ = peaks()
-    for kind, name in ((1, "gemm"), (2, "attn")):
+    for kind, name in ((1, "gemm"), (2, "attn"), (5, "gemm_tc")):
         # kind 4 = the transposed attention kernel (same release / exit columns)
         r = rec[(kinds == kind) | ((kinds == 4) if kind == 2 else False)]
         if len(r) == 0:
             continue
         spans = []
-        nbytes = 0
+        nbytes = flops = 0
         for tag in np.unique(r[:, 0]):
             g = r[r[:, 0] == tag]
             spans.append((int(g[:, 4].min()), int(g[:, 6].max())))
@@ -380,6 +380,11 @@ def timeline_step(be, eng, seqs, prime, dev, prune_layer):
                 per = -(-(Kd // 64) // max(1, ctas // tiles))
                 pre = ctas * min(stages, per) * 128 * 64 * 2
                 nbytes += Kd * N * 2 + M * Kd * 2 + M * N * 4 * (2 if acc else 1) - pre
+            elif kind == 5:  # many-row tcgen05 GEMM: shape in the kind word (gemm_tc.cu)
+                w = int(g[0, 7])
+                N, Kd, M = ((w >> 8) & 0xFFFF) * 32, ((w >> 24) & 0xFFFF) * 64, (w >> 40) & 0xFFFF
+                flops += 2 * M * N * Kd
+                nbytes += Kd * N * 2 + M * Kd * 2 + M * N * 2
         spans.sort()
         busy, cur0, cur1 = 0, None, None
         for a, b in spans:
@@ -396,6 +401,10 @@ def timeline_step(be, eng, seqs, prime, dev, prune_layer):
         gbs = nbytes / (busy_ms * 1e-3) / 1e9 if busy_ms > 0 else 0.0
         out[name] = {"launches": len(spans), "busy_ms": busy_ms, "bytes": nbytes, "achieved": gbs, "frac": gbs / hbm,
                      "share_of_step": busy_ms / out["step_ms"]}
+        if kind == 5:  # tensor-bound at these row counts: TFLOP/s against the sustained bf16 peak
+            tpk = tensor_peak()[0]
+            tf = flops / (busy_ms * 1e-3) / 1e12 if busy_ms > 0 else 0.0
+            out[name].update({"flops": flops, "tflops": tf, "tensor_frac": tf / tpk})
     return out
 
 
@@ -501,7 +510,7 @@ def run_b200(args, rank: int, world: int, group):
     in_step = timeline_step(be, eng, seqs, prime, dev, prune_layer)
     hbm, peak_kind = peaks()
     kernels = {}
-    for kind in ("gemm", "attn", "cublas"):
+    for kind in ("gemm", "attn", "gemm_tc"):
         rs = [r for r in events if r.get("kind", "attn") == kind]
         k_ms, k_bytes = sum(r["ms"] for r in rs), sum(r["bytes"] for r in rs)
         k_flops = sum(r.get("flops", 0) for r in rs)
@@ -596,6 +605,7 @@ def run_sweep(args, dev):
                         "tree_size_mean": sum(x.tree_size for x in m) / K,
                         "k2_frac_in_step": ins.get("attn", {}).get("frac"),
                         "gemm_frac_in_step": ins.get("gemm", {}).get("frac"),
+                        "gemm_tc_tensor_frac_in_step": ins.get("gemm_tc", {}).get("tensor_frac"),
                         "k2_share_of_step": ins.get("attn", {}).get("share_of_step"),
                         "clocks": r["clock"], "captures_in_timed_region": r["captures"]})
             for st in states:
@@ -623,7 +633,15 @@ def roofline(res, args) -> dict:
     hbm, peak_kind = peaks()
     ev = res["kernels"].get(dom, {})
     names = {"gemm": "weight-streaming tcgen05 projections (propd_gemm_ws, <= 128 rows)",
-             "attn": "K2 tree-masked verification attention (tcgen05 tcT / tc2 kernels + streaming decode kernel)"}
+             "attn": "K2 tree-masked verification attention (tcgen05 tcT / tc2 kernels + streaming decode kernel)",
+             "gemm_tc": "many-row tcgen05 projections (propd_gemm, > 128 rows)"}
+    if dom == "gemm_tc":
+        tpk, tburst, tkind = tensor_peak()
+        return {"kernel": names[dom], "bound": "tensor", "achieved": d["tflops"], "peak": tpk, "unit": "TFLOP/s",
+                "frac": d["tflops"] / tpk, "burst_peak": tburst, "traffic": ncu_traffic(dom, args).get("bytes_per_launch"),
+                "peak_kind": tkind, "launches_per_step": d["launches"], "share_of_step": d["share_of_step"],
+                "algorithmic_flops_per_step": d["flops"],
+                "timer": "device globaltimer per CTA: union of [dependency release, last CTA exit] per launch, one step"}
     out = {"kernel": names[dom], "bound": "hbm", "achieved": d["achieved"], "peak": hbm, "unit": "GB/s",
            "frac": d["achieved"] / hbm, "traffic": ncu_traffic(dom, args).get("bytes_per_launch"),
            "traffic_note": ncu_traffic(dom, args).get("note"), "peak_kind": peak_kind,

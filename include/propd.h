@@ -194,6 +194,7 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
  * kernel (128 x 256 tiles, TMA, TMEM double-buffered accumulator; N % 32 == 0,
  * K % 64 == 0, 16-byte aligned rows); fp32 (parity mode): CUDA-core SGEMM.
  * rows_dev (nullable): live row count on the device (rows past it untouched).
+ * ADD_F32 at few 128 x 256 tiles: K split across CTAs, reduced into Y.
  * Epilogue modes:
  *   STORE_F32  Y fp32 [M, N] = acc          (logits)
  *   ADD_F32    Y fp32 += acc                 (residual stream: W_o, W_2)

@@ -299,28 +299,39 @@ class B200Backend:
         torch, T, H, st = self.torch, self.tdtype, self.H, self.stream()
         M = rt.M
         ws = self._workspace(M, rt.B)
+        live = ptr(rt.live)
         h = torch.empty(M, H, device=self.device, dtype=T)
         ctx = torch.empty(M, H, device=self.device, dtype=T)
+        q = torch.empty(M, H, device=self.device, dtype=T)  # Q operand (K/V go straight to the cache)
+        g = torch.empty(M, 4 * H, device=self.device, dtype=T)
         for l in range(l0, l1):
-            self._call("propd_add_ln", self.code, M, None, H, ptr(x), ptr(pending), ptr(h), None, None, st)
-            qkv = self._timed("cublas", lambda: torch.mm(h, self.w.wqkv[l]), M, H, 3 * H)
-            kc, vc = self.kcache[l], self.vcache[l]
-            self._call("propd_kv_append", self.code, M, self.A, self.dh, self.Lmax, ptr(qkv), 3 * H,
-                       ptr(rt.row_seq), ptr(rt.row_node), ptr(rt.seq_slot), ptr(self.seq_len), ptr(kc), ptr(vc), st)
-            self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
-            o = self._timed("cublas", lambda: torch.mm(ctx, self.w.wo[l]), M, H, H)
-            self._call("propd_add_ln", self.code, M, None, H, ptr(x), ptr(o), ptr(h), None, None, st)
-            g = self._timed("cublas", lambda: torch.mm(h, self.w.w1[l]), M, H, 4 * H)
-            self._call("propd_gelu", self.code, g.numel(), ptr(g), st)
-            pending = self._timed("cublas", lambda: torch.mm(g, self.w.w2[l]), M, 4 * H, H)
-        return pending
+            self._call("propd_add_ln", self.code, M, live, H, ptr(x), ptr(pending), ptr(h), None, None, st)
+            pending = None
+            qkv_epi = _lib.GemmEpi(mode=_lib.EPI_QKV, Y=ptr(q), ldy=H, A=self.A, dh=self.dh, Lmax=self.Lmax,
+                                   row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node), seq_slot=ptr(rt.seq_slot),
+                                   seq_len=ptr(self.seq_len), kcache=ptr(self.kcache[l]), vcache=ptr(self.vcache[l]))
+            self._gemm(M, live, 3 * H, H, h, self.w.wqkv[l], qkv_epi)
+            self._attention(rt, q, l, mask, n_tmpl, W, ctx, ws)
+            self._gemm(M, live, H, H, ctx, self.w.wo[l], _lib.GemmEpi(mode=_lib.EPI_ADD_F32, Y=ptr(x), ldy=H))
+            self._call("propd_add_ln", self.code, M, live, H, ptr(x), None, ptr(h), None, None, st)
+            self._gemm(M, live, 4 * H, H, h, self.w.w1[l], _lib.GemmEpi(mode=_lib.EPI_GELU, Y=ptr(g), ldy=4 * H))
+            self._gemm(M, live, H, 4 * H, g, self.w.w2[l], _lib.GemmEpi(mode=_lib.EPI_ADD_F32, Y=ptr(x), ldy=H))
+        return None
+
+    def _gemm(self, M, live, N, K, X, W, epi) -> None:
+        """Many-row projection epilogue(X[M,K] W[K,N]) (propd_gemm: tcgen05 in bf16,
+        the CUDA-core SGEMM in the fp32 parity mode)."""
+        st = self.stream()
+        self._keepalive.append(epi)
+        self._timed("gemm_tc", lambda: self._call("propd_gemm", self.code, M, live, N, K, ptr(X), K, ptr(W), N, epi,
+                                                  st), M, K, N, epi.mode == _lib.EPI_ADD_F32)
 
     # ------------------------------------------------- per-launch timing (bench)
     def _timed(self, kind: str, launch, M: int = 0, K: int = 0, N: int = 0, acc: bool = False, shapes=None):
         """Run `launch` bracketed by CUDA events when the bench's kernel timer
         is on (kind "attn": K2; "gemm": weight-streaming projections [M,K] x
         [K,N], one or a chain given as `shapes` = [(K, N, accumulate), ...];
-        "cublas": torch.mm above 128 rows)."""
+        "gemm_tc": the many-row tcgen05 / fp32 projections)."""
         if self.attn_timer is None or self.mark_only:
             return launch()
         ev0 = self._timing_event()
@@ -466,12 +477,12 @@ class B200Backend:
         (rows >= *live, when given, are left unwritten)."""
         torch = self.torch
         M = X.shape[0]
+        out = torch.empty(M, N, device=self.device, dtype=torch.float32)
         if self.use_gws and M <= 128 and N % 128 == 0 and X.dtype == torch.bfloat16:
-            out = torch.empty(M, N, device=self.device, dtype=torch.float32)
             self._gemm_ws(M, ptr(live), N, self.H, X, Wt, out, N, 0)
-            return out
-        out = self._timed("cublas", lambda: torch.mm(X, Wt), M, self.H, N)
-        return out if out.dtype == torch.float32 else out.float()
+        else:
+            self._gemm(M, ptr(live), N, self.H, X, Wt, _lib.GemmEpi(mode=_lib.EPI_STORE_F32, Y=ptr(out), ldy=N))
+        return out
 
     def _flush(self, x, pending):
         if pending is not None:
@@ -633,9 +644,7 @@ class B200Backend:
             pending = self._run_layers(x, rt, 0, prune_layer, bits, n, W)
             self._flush(x, pending)
             xe = x.to(self.tdtype)
-            early = torch.mm(xe, self.w.w_early)
-            if early.dtype != torch.float32:
-                early = early.float()
+            early = self._proj_f32(xe, self.w.w_early, self.V)
             kk = min(early_topk, cfg.vocab)
             if kk > 1024:
                 raise ValueError("early top-K above 1024 is not supported by the device top-k")
@@ -752,13 +761,7 @@ class B200Backend:
             torch = self.torch
             n0 = self.launches
             if self._cap_stream is None:
-                # cuBLAS handles/workspaces must exist for the capture stream
-                # before capture begins (they cannot be created while capturing)
                 self._cap_stream = torch.cuda.Stream(self.device)
-                with torch.cuda.stream(self._cap_stream):
-                    for dt in {self.tdtype, torch.float32}:
-                        z = torch.zeros(16, 16, device=self.device, dtype=dt)
-                        torch.mm(z, z)
             torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
             self._capturing, self._capture_events = True, []
@@ -976,12 +979,13 @@ class B200Backend:
             None, accept)
         self._role = "tree"
         a = self._run(("A", B, tmpl.paths, k, pkey), lambda: self._part_a(B, tmpl, k, prune, slot_buf, kb))
-        # Layers > p run on the survivors.  When every projection of that pass
-        # is a weight-streaming GEMM (<= 128 rows), part B is launched for the
-        # padded capacity and the GEMMs read the live row count on the device
-        # (rows past it are never written back), so there is no mid-step sync.
+        # Layers > p run on the survivors.  Part B is launched for the padded
+        # capacity and every kernel of it reads the live row count on the
+        # device (weight-streaming GEMMs up to 128 rows, the many-row GEMM
+        # above; rows past it are never written back), so a step has no
+        # mid-step sync; device_rows=False sizes it on the host instead.
         cap = self._s_bucket(B * n)
-        device_rows = prune is not None and self.use_gws and self.device_rows and cap <= 128
+        device_rows = prune is not None and self.device_rows
         if prune is None:
             S_pad = B * n
         elif device_rows:

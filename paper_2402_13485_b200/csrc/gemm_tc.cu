@@ -38,6 +38,7 @@ constexpr int TMEM_COLS = 2 * BN;            // two accumulators of 256 fp32 col
 
 struct Args {
   int M, N, K;
+  int split;  // K splits (ADD_F32 only: partial sums are reduced into Y by red.global.add)
   const int32_t* rows_dev;
   propd_gemm_epi epi;
   unsigned long long* trace;
@@ -73,21 +74,30 @@ __device__ __forceinline__ void store32<float>(float* dst, const float* v) {
 
 // 32 consecutive output features f0.. of token row `row` (f0 % 32 == 0, f0 + 32 <= N).
 template <typename T>
-__device__ __forceinline__ void epilogue32(const propd_gemm_epi& e, int row, int f0, float* v) {
+__device__ __forceinline__ void epilogue32(const propd_gemm_epi& e, int split, int row, int f0, float* v) {
   switch (e.mode) {
     case PROPD_EPI_STORE_F32:
       store32<float>(reinterpret_cast<float*>(e.Y) + (size_t)row * e.ldy + f0, v);
       break;
     case PROPD_EPI_ADD_F32: {
-      float4* y = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.Y) + (size_t)row * e.ldy + f0);
+      float* y = reinterpret_cast<float*>(e.Y) + (size_t)row * e.ldy + f0;
+      if (split > 1) {  // K splits add into the same rows: one reduction per 4 features
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 a = __ldcg(y + q);
-        a.x += v[4 * q];
-        a.y += v[4 * q + 1];
-        a.z += v[4 * q + 2];
-        a.w += v[4 * q + 3];
-        y[q] = a;
+        for (int q = 0; q < 8; ++q)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(y + 4 * q), "f"(v[4 * q]),
+                       "f"(v[4 * q + 1]), "f"(v[4 * q + 2]), "f"(v[4 * q + 3])
+                       : "memory");
+      } else {  // the only writer of these rows: plain read-modify-write (cheaper than reductions)
+        float4* y4 = reinterpret_cast<float4*>(y);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 a = __ldcg(y4 + q);
+          a.x += v[4 * q];
+          a.y += v[4 * q + 1];
+          a.z += v[4 * q + 2];
+          a.w += v[4 * q + 3];
+          y4[q] = a;
+        }
       }
       break;
     }
@@ -154,13 +164,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   const unsigned long long t_wait = p.trace ? gtimer() : 0ull;
   const int M = p.rows_dev ? min(p.M, *p.rows_dev) : p.M;
   const int Mb = (M + BM - 1) / BM, Nb = (p.N + BN - 1) / BN, Kb = p.K / BK;
-  const int tiles = Mb * Nb;
+  const int tiles = Mb * Nb, units = tiles * p.split;
+  const int kper = (Kb + p.split - 1) / p.split;  // k-blocks per split
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int t = u % tiles, s = u / tiles;
         const int mb = t % Mb, nb = t / Mb;
-        for (int kb = 0; kb < Kb; ++kb, ++it) {
+        const int kb1 = min(Kb, (s + 1) * kper);
+        for (int kb = s * kper; kb < kb1; ++kb, ++it) {
           const int st = it % STAGES;
           mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1, 81);
           mbar_expect_tx(&full[st], STAGE);
@@ -176,12 +189,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       // A = X K-major, B = W MN-major (features contiguous); M = 128, N = 256
       constexpr uint32_t idesc = idesc_bf16(true, BN, BM);
       int it = 0, i = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+        const int s = u / tiles;
+        const int kb0 = s * kper, kb1 = min(Kb, (s + 1) * kper);
         const int buf = i & 1;
         mbar_wait(&acc_empty[buf], ((i >> 1) & 1) ^ 1, 82);
         tc_after_sync();
         const uint32_t d = tmem + buf * BN;
-        for (int kb = 0; kb < Kb; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int st = it % STAGES;
           mbar_wait(&full[st], (it / STAGES) & 1, 83);
           tc_after_sync();
@@ -191,7 +206,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = sw128_desc(a + kk * 32, 16, 1024);
             const uint64_t bd = sw128_desc(b + kk * 2048, B_BLOCK, 1024);
-            mma_bf16(d, ad, bd, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16(d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
           }
           mma_commit(&empty[st]);
         }
@@ -200,9 +215,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else {
     // epilogue: TMEM lane quarter q4 = warp % 4 holds token rows q4*32 .. q4*32+31
-    const int q4 = warp & 3;
+    const int q4 = warp & 3, tid = threadIdx.x - 64;
     int i = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++i) {
+      const int t = u % tiles;
       const int mb = t % Mb, nb = t / Mb;
       const int buf = i & 1;
       mbar_wait(&acc_full[buf], (i >> 1) & 1, 84);
@@ -219,11 +235,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          epilogue32<__nv_bfloat16>(p.epi, row, f0, v);
+          epilogue32<__nv_bfloat16>(p.epi, p.split, row, f0, v);
         }
       }
       tc_before_sync();
-      mbar_arrive(&acc_empty[buf]);
+      mbar_arrive(&acc_empty[buf]);  // the accumulator is free for the unit after next
     }
   }
   tc_before_sync();
@@ -386,9 +402,31 @@ int propd_gemm(int dtype, int M, const int32_t* rows_dev, int N, int K, const vo
     if (e != cudaSuccess) return fail("gemm: %s", cudaGetErrorString(e));
     attr = true;
   }
-  gtc::Args p{M, N, K, rows_dev, *epi, g_dbg_trace, g_dbg_tag++};
   const int tiles = ((M + gtc::BM - 1) / gtc::BM) * ((N + gtc::BN - 1) / gtc::BN);
-  const int grid = tiles < propd_num_sms() ? tiles : propd_num_sms();
+  const int sms = propd_num_sms();
+  // Few tiles (a few hundred rows) leave SMs idle or a short last wave: for the
+  // residual-stream epilogue K is split so the work units fill the waves
+  // (partial sums reduced into Y).  split minimises waves / split + a small
+  // per-split cost for the reductions, >= 4 k-blocks per split.  (A split
+  // through an fp32 workspace for the other epilogues was measured slower:
+  // the reductions and the last-split finish cost more than the wave fill.)
+  int split = 1;
+  if (epi->mode == PROPD_EPI_ADD_F32) {
+    const int kb = K / gtc::BK;
+    double best = 1e30;
+    for (int s = 1; s <= 8 && kb / s >= 4; ++s) {
+      const double cost = (double)((tiles * s + sms - 1) / sms) / s + 0.04 * (s - 1);
+      if (cost < best - 1e-9) {
+        best = cost;
+        split = s;
+      }
+    }
+    const int kper = (kb + split - 1) / split;
+    split = (kb + kper - 1) / kper;  // no empty split (the kernel derives kper from split the same way)
+  }
+  gtc::Args p{M, N, K, split, rows_dev, *epi, g_dbg_trace, g_dbg_tag++};
+  const int units = tiles * split;
+  const int grid = units < sms ? units : sms;
   return launch_pdl("gemm(tcgen05)", gtc::gemm_tc_kernel, dim3(grid), dim3(gtc::THREADS), gtc::SMEM, st, xm, wm, p);
 }
 

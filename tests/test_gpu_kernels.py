@@ -700,7 +700,9 @@ def _epi(mode, Y, ldy, **kw):
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
 @pytest.mark.parametrize("M,N,K,mode", [(129, 4096, 4096, "store"), (300, 12288, 4096, "qkv"),
                                          (1000, 16384, 4096, "gelu"), (4096, 4096, 16384, "add"),
-                                         (257, 32000, 4096, "f32"), (700, 4128, 1024, "add"), (1, 256, 64, "f32")])
+                                         (257, 32000, 4096, "f32"), (700, 4128, 1024, "add"), (1, 256, 64, "f32"),
+                                         (160, 12288, 4096, "qkv"), (200, 16384, 4096, "gelu"),
+                                         (512, 12288, 4096, "qkv"), (130, 4096, 1024, "store")])
 def test_gemm_matches_fp32_reference(dtype, M, N, K, mode):
     """Y = epilogue(X . W): tcgen05 (bf16 operands, fp32 accumulation) and the fp32 CUDA-core path vs torch
     fp32 on the same (bf16-rounded) operands.  bf16: |err| <= 1e-3 * max(1, |ref|) on fp32 outputs
@@ -715,27 +717,29 @@ def test_gemm_matches_fp32_reference(dtype, M, N, K, mode):
     ref = X.float() @ W.float()
     tol = (1e-3 if dtype == "bf16" else 1e-5) * max(1.0, ref.abs().max().item())
     otol = 8e-3 if dtype == "bf16" else 1e-5  # rounding of a dtype output
+    wkw = {}
     if mode in ("f32", "add"):
         base = torch.randn(M, N, device=DEV) if mode == "add" else torch.full((M, N), float("nan"), device=DEV)
         Y = base.clone()
-        epi = _epi(_lib.EPI_ADD_F32 if mode == "add" else _lib.EPI_STORE_F32, Y, N)
+        epi = _epi(_lib.EPI_ADD_F32 if mode == "add" else _lib.EPI_STORE_F32, Y, N, **wkw)
         call("propd_gemm", code, M, None, N, K, ptr(X), K, ptr(W), N, epi, st())
         torch.cuda.synchronize()
         want = ref + (base if mode == "add" else 0)
         assert (Y - want).abs().max().item() <= tol
     elif mode in ("store", "gelu"):
         Y = torch.full((M, N), float("nan"), device=DEV).to(T)
-        epi = _epi(_lib.EPI_GELU if mode == "gelu" else _lib.EPI_STORE, Y, N)
+        epi = _epi(_lib.EPI_GELU if mode == "gelu" else _lib.EPI_STORE, Y, N, **wkw)
         call("propd_gemm", code, M, None, N, K, ptr(X), K, ptr(W), N, epi, st())
         torch.cuda.synchronize()
         want = torch.nn.functional.gelu(ref, approximate="tanh") if mode == "gelu" else ref
         assert (Y.float() - want).abs().max().item() <= tol + otol * want.abs().max().item()
     else:  # QKV: Q -> Y, K/V -> cache slots seq_len[slot] + node
-        A, dh, Lmax = 32, 128, 400
+        A, dh, Lmax = 32, 128, 480
         H = A * dh
         assert N == 3 * H
         nseq = 3
-        per = [100, 120, 80]
+        per = [M // 3, M // 3 + M % 3, M // 3]  # rows of three sequences
+        assert max(per) + 250 <= Lmax
         row_seq = i32(np.repeat(np.arange(nseq), per))
         row_node = i32(np.concatenate([np.arange(p) for p in per]))
         seq_slot, seq_len = i32([2, 0, 1]), i32([7, 250, 31])
@@ -743,7 +747,7 @@ def test_gemm_matches_fp32_reference(dtype, M, N, K, mode):
         vc = torch.zeros_like(kc)
         Y = torch.zeros(M, 3 * H, device=DEV, dtype=T)
         epi = _epi(_lib.EPI_QKV, Y, 3 * H, A=A, dh=dh, Lmax=Lmax, row_seq=ptr(row_seq), row_node=ptr(row_node),
-                   seq_slot=ptr(seq_slot), seq_len=ptr(seq_len), kcache=ptr(kc), vcache=ptr(vc))
+                   seq_slot=ptr(seq_slot), seq_len=ptr(seq_len), kcache=ptr(kc), vcache=ptr(vc), **wkw)
         call("propd_gemm", code, M, None, N, K, ptr(X), K, ptr(W), N, epi, st())
         torch.cuda.synchronize()
         lim = tol + otol * ref.abs().max().item()
