@@ -360,6 +360,8 @@ def timeline_step(be, eng, seqs, prime, dev, prune_layer):
     n = min(int(buf[0].item()), cap)
     rec = buf[8: 8 + 8 * n].view(n, 8).cpu().numpy()
     out = {"step_ms": t0.elapsed_time(t1), "records": n}
+    if os.environ.get("PROPD_BENCH_DUMP"):  # development aid: the raw per-CTA records of the traced step
+        np.save(os.environ["PROPD_BENCH_DUMP"], rec)
     kinds = rec[:, 7] & 0xFF
     hbm, _ = peaks()
     for kind, name in ((1, "gemm"), (2, "attn"), (5, "gemm_tc")):

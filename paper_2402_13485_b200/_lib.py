@@ -12,7 +12,7 @@ import os
 from ctypes import c_double, c_int, c_int64, c_void_p
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpropd.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 F32 = 0
 BF16 = 1
@@ -44,6 +44,8 @@ SIGNATURES = {
     "propd_tree_attention": [I, I, I, I, I, I, I, I, I, I, P, I, P, P, P, P, P, P, P, I, I, P, I, P, L, P],
     "propd_gemm_ws": [I, P, I, I, P, I, P, I, P, I, I, I, P],
     "propd_gemm_ws_ph": [I, P, I, I, P, I, P, I, P, I, I, I, "phases", P],
+    "propd_ws_split_count": [I, I],
+    "propd_ws_colsum": [I, I, P, I, P, P],
     "propd_gemm": [I, I, P, I, I, P, I, P, I, "epi", P],
     "propd_qkv_finish": [I, P, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
     "propd_gelu_finish": [I, P, I, P, I, P, I, P],
@@ -62,7 +64,7 @@ SIGNATURES = {
 _RESTYPES = {"propd_last_error": ctypes.c_char_p, "propd_attn_workspace_bytes": c_int64}
 
 
-PRO_NONE, PRO_LN, PRO_GELU = 0, 1, 2
+PRO_NONE, PRO_LN, PRO_GELU, PRO_XLN, PRO_XGELU = 0, 1, 2, 3, 4
 TAIL_NONE, TAIL_QKV = 0, 1
 
 
@@ -72,7 +74,8 @@ class WsPhases(ctypes.Structure):
     _fields_ = [("pro_mode", c_int), ("pro_src", P), ("pro_ld", c_int), ("pro_dst", P), ("pro_ldd", c_int),
                 ("pro_cols", c_int), ("tail_mode", c_int), ("tail_q", P), ("tail_ldq", c_int), ("A", c_int),
                 ("dh", c_int), ("Lmax", c_int), ("row_seq", P), ("row_node", P), ("seq_slot", P), ("seq_len", P),
-                ("kcache", P), ("vcache", P), ("bar", P)]
+                ("kcache", P), ("vcache", P), ("bar", P), ("colsum", P), ("stats_rec", P), ("stats_cnt", P),
+                ("stats_cnt_reset", P), ("zero_buf", P), ("zero_ld", c_int), ("zero_cols", c_int)]
 
 
 EPI_STORE, EPI_STORE_F32, EPI_ADD_F32, EPI_GELU, EPI_QKV = 0, 1, 2, 3, 4

@@ -379,6 +379,8 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   if (nsplit > cap) nsplit = cap;
   if (nsplit > dec::MAX_SPLIT) nsplit = dec::MAX_SPLIT;
   if (nsplit < 1) nsplit = 1;
+  static const int split_override = env_int("PROPD_DEC_SPLIT");
+  if (split_override > 0) nsplit = split_override < dec::MAX_SPLIT ? split_override : dec::MAX_SPLIT;
   // boundaries: any multiple of 16 keys from the device length (chunks start
   // at the split's first key and the last one loads only the keys left, so
   // splits stay balanced across SMs); no split empty at max_keys

@@ -632,6 +632,8 @@ int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq
   if (nsplit > nh) nsplit = nh;
   if (nsplit > tct::MAX_SPLIT) nsplit = tct::MAX_SPLIT;
   if (nsplit < 1) nsplit = 1;
+  static const int split_override = env_int("PROPD_TCT_SPLIT");
+  if (split_override > 0) nsplit = split_override < tct::MAX_SPLIT ? split_override : tct::MAX_SPLIT;
   const int per = (nh + nsplit - 1) / nsplit;  // 64-key units per split at max_keys
   nsplit = (nh + per - 1) / per;               // no split empty at max_keys
   tct::Args p{};

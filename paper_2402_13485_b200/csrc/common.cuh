@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdlib>
 #include <string>
 #include <utility>
 
@@ -82,7 +83,7 @@ __device__ __forceinline__ unsigned int smid() {
 // GEMM records carry their shape above it (gemm_ws.cu: N / 128, K / 64, live rows, accumulate)
 __device__ __forceinline__ void trace_record(unsigned long long* buf, unsigned int tag, unsigned long long t0,
                                              unsigned long long t1, unsigned long long t2,
-                                             unsigned long long kind = 0) {
+                                             unsigned long long kind = 0, unsigned long long slot2 = ~0ull) {
   if (buf == nullptr) return;
   const unsigned long long t3 = gtimer();
   const unsigned long long i = atomicAdd(buf, 1ull);
@@ -90,7 +91,7 @@ __device__ __forceinline__ void trace_record(unsigned long long* buf, unsigned i
   unsigned long long* r = buf + 8 + i * 8;
   r[0] = tag;
   r[1] = blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
-  r[2] = smid();
+  r[2] = slot2 != ~0ull ? slot2 : smid();  // (debug builds may put a timestamp here)
   r[3] = t0;
   r[4] = t1;
   r[5] = t2;
@@ -104,6 +105,12 @@ __device__ __forceinline__ void trace_record(unsigned long long* buf, unsigned i
 // one wave, take as many as fit (latency-bound small batches); otherwise the
 // split count in [1, max_split] whose grid fills its last wave best
 // (>= 95 %, else the best fill), so large batches do not lose a partial wave.
+// development override of a launch heuristic's split count (0 = unset)
+inline int env_int(const char* name) {
+  const char* e = getenv(name);
+  return e != nullptr ? atoi(e) : 0;
+}
+
 inline int wave_split(int units, int slots, int max_split) {
   if (max_split < 1) return 1;
   if (units * max_split <= slots) return max_split;

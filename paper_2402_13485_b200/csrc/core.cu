@@ -438,7 +438,7 @@ int propd_debug_timeline(void* buf) {  // development aid: per-CTA timeline reco
 }
 
 const char* propd_last_error(void) { return g_error.c_str(); }
-int propd_abi_version(void) { return 4; }
+int propd_abi_version(void) { return 5; }
 int propd_num_sms(void) {
   static int cached = 0;  // launch heuristics call this per launch
   if (cached > 0) return cached;

@@ -13,6 +13,7 @@
 // Finish kernels turn fp32 accumulators into the bf16 operands of the next
 // op: QKV (+ K/V scattered into the cache, replacing kv_append) and
 // W1 (+ tanh-GELU), re-zeroing the accumulator for the next use.
+#include <cstring>
 #include <unordered_map>
 
 #include "tc_common.cuh"
@@ -153,6 +154,116 @@ __device__ __forceinline__ void tail_phase(float* Y, int ldy, const propd_ws_pha
   }
 }
 
+// ---- barrier-free prologues (PROPD_PRO_XLN / PROPD_PRO_XGELU) ----
+// The four epilogue warps convert the fp32 source rows of each ring stage
+// into the stage's bf16 X tile themselves (the layout TMA SW128 would write:
+// 16-row boxes of 2 KB, 16-byte chunk c of row r at chunk c ^ (r & 7)), warp
+// w taking stages j = w, w + 4, ...: no grid barrier, no bf16 X buffer, and
+// the weight ring never waits for a cooperative prologue.
+__device__ __forceinline__ bool conv_mode(int m) { return m == PROPD_PRO_XLN || m == PROPD_PRO_XGELU; }
+
+__device__ __forceinline__ uint4 cvt8(float4 a, float4 b, bool gelu) {
+  if (gelu) {
+    a = make_float4(gelu_tanh(a.x), gelu_tanh(a.y), gelu_tanh(a.z), gelu_tanh(a.w));
+    b = make_float4(gelu_tanh(b.x), gelu_tanh(b.y), gelu_tanh(b.z), gelu_tanh(b.w));
+  }
+  const uint2 lo = pack_bf16x4(a.x, a.y, a.z, a.w), hi = pack_bf16x4(b.x, b.y, b.z, b.w);
+  return make_uint4(lo.x, lo.y, hi.x, hi.y);
+}
+
+// Stage X tile: rows [0, M) x 64 k columns starting at k0 of src, in
+// batches of 4 (row, chunk) tasks per lane.  The first batch is loaded ahead
+// (load_batch) into registers as soon as the warp's previous stage is done,
+// so its L2 latency (the N-tiles of a split all read the same lines) hides
+// behind the wait for the ring slot; further batches (M > 16) load in place.
+struct XBatch {
+  float4 v[4][2];
+};
+__device__ __forceinline__ void load_batch(XBatch& b, const float* __restrict__ src, int ld, int k0, int tasks,
+                                           int base, int lane) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int task = base + u * 32 + lane;
+    if (task < tasks) {
+      const float4* g = reinterpret_cast<const float4*>(src + (size_t)(task >> 3) * ld + k0 + (task & 7) * 8);
+      b.v[u][0] = __ldcg(g);
+      b.v[u][1] = __ldcg(g + 1);
+    }
+  }
+}
+__device__ __forceinline__ void store_batch(const XBatch& b, uint8_t* xs, int tasks, int base, int lane, bool gelu) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int task = base + u * 32 + lane;
+    if (task < tasks) {
+      const int t = task >> 3, c = task & 7;
+      *reinterpret_cast<uint4*>(xs + (t >> 4) * 2048 + (t & 15) * 128 + ((c ^ (t & 7)) << 4)) =
+          cvt8(b.v[u][0], b.v[u][1], gelu);
+    }
+  }
+}
+
+// LayerNorm statistics for PROPD_PRO_XLN, published while the weights stream:
+// warp `gw` of the launch takes 256-column sub-chunks (row t, part q) and
+// writes their two-pass (mean, M2) record; the arrival that completes row t
+// (stats_cnt[t] reaches K / 256) combines the records (Chan's parallel
+// combination of equal-size groups) and publishes (mu, rstd) as one 64-bit
+// word after the counters (rstd > 0 doubles as the ready flag).
+constexpr int SUB = 256, MAX_SUB = 32;
+__device__ __forceinline__ unsigned long long* stats_word(const propd_ws_phases& ph, int t) {
+  return reinterpret_cast<unsigned long long*>(ph.stats_cnt + 128) + t;
+}
+__device__ __forceinline__ void stats_chunks(const propd_ws_phases& ph, int M, int K, int gw, int nw, int lane) {
+  const int nsub = K / SUB;
+  for (int item = gw; item < M * nsub; item += nw) {
+    const int t = item / nsub, q = item - t * nsub;
+    const float4* g = reinterpret_cast<const float4*>(ph.pro_src + (size_t)t * ph.pro_ld + q * SUB + lane * 8);
+    const float4 a = __ldcg(g), b = __ldcg(g + 1);
+    const float mean = warp_sum(((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) * (1.f / SUB);
+    float d, m2 = 0.f;
+    d = a.x - mean; m2 += d * d; d = a.y - mean; m2 += d * d; d = a.z - mean; m2 += d * d; d = a.w - mean; m2 += d * d;
+    d = b.x - mean; m2 += d * d; d = b.y - mean; m2 += d * d; d = b.z - mean; m2 += d * d; d = b.w - mean; m2 += d * d;
+    m2 = warp_sum(m2);
+    if (lane == 0) {
+      float2* rec = reinterpret_cast<float2*>(ph.stats_rec) + (size_t)t * MAX_SUB;
+      __stcg(rec + q, make_float2(mean, m2));
+      unsigned old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ph.stats_cnt + t) : "memory");
+      if (old == (unsigned)nsub - 1) {  // last record of row t: combine and publish
+        float s = 0.f;
+        for (int i = 0; i < nsub; ++i) s += __ldcg(rec + i).x;
+        const float mu = s / (float)nsub;
+        float acc = 0.f;
+        for (int i = 0; i < nsub; ++i) {
+          const float2 r = __ldcg(rec + i);
+          const float dd = r.x - mu;
+          acc += r.y + (float)SUB * dd * dd;
+        }
+        const float rstd = 1.f / sqrtf(acc / (float)K + 1e-5f);
+        const unsigned long long word = (unsigned long long)__float_as_uint(mu) |
+                                        ((unsigned long long)__float_as_uint(rstd) << 32);
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(stats_word(ph, t)), "l"(word) : "memory");
+      }
+    }
+  }
+}
+
+// (mu, rstd) of rows [t0, t1): lane t0 + i polls its row's published word
+// (relaxed 64-bit loads, converged; the word is its own flag).
+__device__ __forceinline__ float2 row_stats(const propd_ws_phases& ph, int t0, int t1, int lane) {
+  const int t = t0 + lane;
+  unsigned long long w = 0ull;
+  bool ok = t >= t1;
+  while (!__all_sync(0xffffffffu, ok)) {
+    if (!ok) {
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(stats_word(ph, t)) : "memory");
+      ok = (w >> 32) != 0ull;
+    }
+  }
+  return t < t1 ? make_float2(__uint_as_float((unsigned)w), __uint_as_float((unsigned)(w >> 32)))
+                : make_float2(0.f, 0.f);
+}
+
 // Ring depth per X-tile size: as deep as two CTAs per SM allow (deeper rings
 // keep more weight bytes in flight and prefetch more of them while the
 // predecessor kernel drains).
@@ -173,16 +284,21 @@ __global__ void __launch_bounds__(THREADS, 2)
   uint64_t* acc_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const unsigned long long t_entry = p.trace ? gtimer() : 0ull;
-  __shared__ unsigned long long s_t[2];
+  __shared__ unsigned long long s_t[4];
   __shared__ int s_pro_done;
+  __shared__ float2 s_ms[128];  // PROPD_PRO_XLN: (mu, rstd) of the live rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BF;
   const int kb0 = blockIdx.y * p.kblk_per_split;
   const int nkb = min(p.kblk_per_split, p.K / BK - kb0);
   if (nkb <= 0) return;
+  // every N-tile walks its k-blocks in the same order: at any moment the CTAs
+  // stream the same W rows (DRAM page locality; measured: staggering the
+  // start block per N-tile slows the 7B projections by 1-2 us)
+  auto kblk = [&](int j) { return kb0 + j; };
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], conv_mode(p.ph.pro_mode) ? 2 : 1);  // + the converting warp's arrival
       mbar_init(&empty[i], 1);
     }
     mbar_init(acc_full, 1);
@@ -199,6 +315,9 @@ __global__ void __launch_bounds__(THREADS, 2)
   tc_after_sync();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();  // after the TMEM allocation (see common.cuh)
+  // every weight byte is read once per launch: evict it first, so the
+  // activations, accumulators and statistics of the layer stay in L2
+  const uint64_t wpol = l2_evict_first_policy();
   if (warp == 0 && lane == 0) {
     // The weights do not depend on the preceding kernels: fill the first
     // stages with W while the predecessor drains (tx bytes announced without
@@ -207,9 +326,9 @@ __global__ void __launch_bounds__(THREADS, 2)
     for (int j = 0; j < pre; ++j) {
       mbar_add_tx(&full[j], A_BYTES);
       uint8_t* a = smem + j * STAGE;
-      const int k = (kb0 + j) * BK;
-      tma_load_2d(a, &wmap, &full[j], n0, k);
-      tma_load_2d(a + A_BYTES / 2, &wmap, &full[j], n0 + 64, k);
+      const int k = kblk(j) * BK;
+      tma_load_2d_hint(a, &wmap, &full[j], n0, k, wpol);
+      tma_load_2d_hint(a + A_BYTES / 2, &wmap, &full[j], n0 + 64, k, wpol);
     }
   }
   pdl_wait();
@@ -219,8 +338,21 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
   const int nbox = max(1, (M + 15) >> 4);
   const int cta = blockIdx.y * gridDim.x + blockIdx.x, ncta = gridDim.x * gridDim.y;
+  const bool conv = conv_mode(p.ph.pro_mode);
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0 && conv) {  // W only: the epilogue warps write the X tiles
+      const int pre = min(nkb, STAGES);
+      for (int j = 0; j < pre; ++j) mbar_arrive(&full[j]);
+      for (int j = pre; j < nkb; ++j) {
+        const int st = j % STAGES;
+        mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 31);
+        mbar_expect_tx(&full[st], A_BYTES);
+        uint8_t* a = smem + st * STAGE;
+        const int k = kblk(j) * BK;
+        tma_load_2d_hint(a, &wmap, &full[st], n0, k, wpol);
+        tma_load_2d_hint(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k, wpol);
+      }
+    } else if (lane == 0) {
       if (p.ph.pro_mode != PROPD_PRO_NONE) {
         // X is produced in this launch's prologue by every CTA: wait for the
         // grid barrier (the weight stages above keep streaming meanwhile),
@@ -232,16 +364,16 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int j = 0; j < pre; ++j) {
         mbar_expect_tx(&full[j], nbox * 2048);
         for (int i = 0; i < nbox; ++i)
-          tma_load_2d(smem + j * STAGE + A_BYTES + i * 2048, &xmap, &full[j], (kb0 + j) * BK, i * 16);
+          tma_load_2d(smem + j * STAGE + A_BYTES + i * 2048, &xmap, &full[j], kblk(j) * BK, i * 16);
       }
       for (int j = pre; j < nkb; ++j) {
         const int st = j % STAGES;
         mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 31);
         mbar_expect_tx(&full[st], A_BYTES + nbox * 2048);
         uint8_t* a = smem + st * STAGE;
-        const int k = (kb0 + j) * BK;
-        tma_load_2d(a, &wmap, &full[st], n0, k);
-        tma_load_2d(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k);
+        const int k = kblk(j) * BK;
+        tma_load_2d_hint(a, &wmap, &full[st], n0, k, wpol);
+        tma_load_2d_hint(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k, wpol);
         for (int i = 0; i < nbox; ++i) tma_load_2d(a + A_BYTES + i * 2048, &xmap, &full[st], k, i * 16);
       }
     }
@@ -253,6 +385,10 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int j = 0; j < nkb; ++j) {
         const int st = j % STAGES;
         mbar_wait(&full[st], (j / STAGES) & 1, 32);
+#ifdef PROPD_DBG_TS
+        if (p.trace && j == 0) s_t[2] = gtimer();
+        if (p.trace && j == nkb - 1) s_t[3] = gtimer();
+#endif
         tc_after_sync();
         const uint32_t a = smem_u32(smem + st * STAGE);
         const uint32_t b = a + A_BYTES;
@@ -268,13 +404,67 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
   } else {
     const int tid = threadIdx.x - 64;
-    if (p.ph.pro_mode != PROPD_PRO_NONE) {
+    if (conv) {
+      const int w = warp - 2;
+      const bool gelu = p.ph.pro_mode == PROPD_PRO_XGELU;
+      // after this warp's first stage (or at once if it has none): statistics,
+      // then the launch's zeroing duties
+      auto duties = [&]() {
+        if (!gelu) stats_chunks(p.ph, M, p.K, cta * 4 + w, ncta * 4, lane);
+        if (p.ph.zero_buf) {
+          const int per_row = p.ph.zero_cols / 4;
+          for (int e = (cta * 4 + w) * 32 + lane; e < M * per_row; e += ncta * 128) {
+            const int t = e / per_row;
+            __stcg(reinterpret_cast<float4*>(p.ph.zero_buf + (size_t)t * p.ph.zero_ld) + (e - t * per_row),
+                   make_float4(0.f, 0.f, 0.f, 0.f));
+          }
+        }
+        if (p.ph.stats_cnt_reset && cta == 0)  // the other LN launch: 128 counters + 128 published words
+          for (int e = w * 32 + lane; e < 384; e += 128) p.ph.stats_cnt_reset[e] = 0u;
+      };
+      bool dut = false;
+      const int tasks = M * 8;  // (row, 16-byte chunk) per stage
+      XBatch nb;
+      if (w < nkb) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(w) * BK, tasks, 0, lane);
+      for (int j = w; j < nkb; j += 4) {
+        const int st = j % STAGES;
+        if (j >= STAGES) mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 34);
+        uint8_t* xs = smem + st * STAGE + A_BYTES;
+        store_batch(nb, xs, tasks, 0, lane, gelu);
+        for (int base = 128; base < tasks; base += 128) {
+          XBatch b;
+          load_batch(b, p.ph.pro_src, p.ph.pro_ld, kblk(j) * BK, tasks, base, lane);
+          store_batch(b, xs, tasks, base, lane, gelu);
+        }
+        if (j + 4 < nkb) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(j + 4) * BK, tasks, 0, lane);
+        fence_proxy_async();  // generic shared-memory writes -> tensor-core operand reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[st]);
+        if (!dut) {
+          duties();
+          dut = true;
+        }
+      }
+      if (!dut) duties();
+      // the row statistics this CTA's epilogue needs, fetched once per CTA
+      // (warp w: rows 32w..32w+31) after the last conversion, ahead of the
+      // accumulator: off the epilogue's critical path and 4x fewer readers
+      if (!gelu && w * 32 < M) s_ms[w * 32 + lane] = row_stats(p.ph, w * 32, min(M, w * 32 + 32), lane);
+    } else if (p.ph.pro_mode != PROPD_PRO_NONE) {
       prologue_phase(p.ph, M, tid, cta, ncta);
       __threadfence();  // every writer fences before the CTA's arrival
       epi_sync();
       if (tid == 0) {
         grid_barrier(p.ph.bar, (unsigned)ncta);
         *reinterpret_cast<volatile int*>(&s_pro_done) = 1;
+      }
+    }
+    if (!conv && p.ph.zero_buf) {  // zero-ahead duty of a barrier-prologue launch (after its dependency wait)
+      const int per_row = p.ph.zero_cols / 4;
+      for (int e = cta * 128 + tid; e < M * per_row; e += ncta * 128) {
+        const int t = e / per_row;
+        __stcg(reinterpret_cast<float4*>(p.ph.zero_buf + (size_t)t * p.ph.zero_ld) + (e - t * per_row),
+               make_float4(0.f, 0.f, 0.f, 0.f));
       }
     }
     // epilogue: lane = output feature, columns = tokens
@@ -297,6 +487,16 @@ __global__ void __launch_bounds__(THREADS, 2)
       uint32_t rr[32];
       TMEM_LD32(lane_addr + c * 32, rr);
       tmem_wait_ld();
+      if (p.ph.pro_mode == PROPD_PRO_XLN) {  // LN by linearity: rstd_t (acc - mu_t c_f)
+        if (c == 0) epi_sync();  // s_ms complete
+        const float2 ms = s_ms[c * 32 + lane];
+        const float cf = __ldg(p.ph.colsum + (size_t)blockIdx.y * p.N + n0 + q4 * 32 + lane);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float mu = __shfl_sync(0xffffffffu, ms.x, i), rs = __shfl_sync(0xffffffffu, ms.y, i);
+          rr[i] = __float_as_uint(rs * (__uint_as_float(rr[i]) - mu * cf));
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 32; ++i) tile[i * 36 + lane] = __uint_as_float(rr[i]);
       __syncwarp();
@@ -333,10 +533,18 @@ __global__ void __launch_bounds__(THREADS, 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
   }
   if (p.trace && threadIdx.x == 0)  // shape in the kind word: bench.py computes this launch's algorithmic bytes
+#ifdef PROPD_DBG_TS  // debug builds: slot 2 = first full stage, slot 3 = last full stage
+    trace_record(p.trace, p.tag, s_t[3], s_t[0], s_t[1],
+#else
     trace_record(p.trace, p.tag, t_entry, s_t[0], s_t[1],
+#endif
                  1ull | ((unsigned long long)(p.N / BF) << 8) | ((unsigned long long)(p.K / BK) << 24) |
                      ((unsigned long long)M << 40) | ((unsigned long long)(p.accumulate ? 1 : 0) << 56) |
-                     ((unsigned long long)STAGES << 57));  // W stages prefetched before the dependency release
+                     ((unsigned long long)STAGES << 57)
+#ifdef PROPD_DBG_TS
+                 , s_t[2]
+#endif
+    );  // W stages prefetched before the dependency release
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -497,8 +705,8 @@ static int run_probe() {
     const int o = occupancy(mp);
     if (o < 0) return 1;
     per_sm = min(per_sm, o);
-    // + 1 KB for the static shared memory of gemm_ws_kernel (timeline scratch, reductions)
-    max_smem = max(max_smem, stages_for(mp) * (A_BYTES + mp * 128) + 256 + 1024 + 1024);
+    // + 2 KB for the static shared memory of gemm_ws_kernel (timeline scratch, reductions, LN stats)
+    max_smem = max(max_smem, stages_for(mp) * (A_BYTES + mp * 128) + 256 + 1024 + 2048);
   }
   const int n = per_sm * propd_num_sms();
   cudaError_t e = cudaFuncSetAttribute(coresidency_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
@@ -545,6 +753,19 @@ static void split_k(int N, int K, int accumulate, int max_split, int* split_out,
   const int per = (kb + split - 1) / split;
   *split_out = (kb + per - 1) / per;
   *per_out = per;
+}
+
+// Per-split column sums of W (PROPD_PRO_XLN's LayerNorm correction): one
+// thread per column, rows of split blockIdx.y in order.
+__global__ void colsum_kernel(int N, int K, int rows_per_split, const __nv_bfloat16* __restrict__ W, int ldw,
+                              float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k0 = blockIdx.y * rows_per_split, k1 = min(K, k0 + rows_per_split);
+  float s = 0.f;
+  for (int k = k0; k < k1; ++k) s += __bfloat162float(W[(size_t)k * ldw + n]);
+  out[(size_t)blockIdx.y * N + n] = s;
 }
 
 // ------------------------------------------------------------------ finish
@@ -625,9 +846,11 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
                     (ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0),
                 "gemm_ws: Y must be 16-byte aligned with ldy %% 4 == 0 (vector stores / reductions)");
   const int mp = ((M + 15) / 16) * 16;
+  const bool conv = ph != nullptr && (ph->pro_mode == PROPD_PRO_XLN || ph->pro_mode == PROPD_PRO_XGELU);
   CUtensorMap wm, xm;
+  memset(&xm, 0, sizeof(xm));  // unused when the CTAs convert X themselves
   PROPD_REQUIRE(gws::map2d(&wm, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw, 64) &&
-                    gws::map2d(&xm, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, 16),
+                    (conv || gws::map2d(&xm, X, (uint64_t)M, (uint64_t)K, (uint64_t)ldx, 16)),
                 "gemm_ws: tensor map encode failed");
   const int tiles = N / gws::BF;
   int split, per;
@@ -648,9 +871,18 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
                   "gemm_ws: %d CTAs cannot all be co-resident for the grid barrier (%d per SM x %d SMs)",
                   tiles * split, occ, sms);
     PROPD_REQUIRE(ph->bar != nullptr, "gemm_ws: phases need the barrier counters");
-    PROPD_REQUIRE(ph->pro_mode == PROPD_PRO_NONE ||
+    PROPD_REQUIRE(ph->pro_mode == PROPD_PRO_NONE || conv ||
                       (ph->pro_src && ph->pro_dst == X && ph->pro_ldd == ldx && ph->pro_cols == K && K <= 4096 * 4),
                   "gemm_ws: the prologue must produce this launch's X operand");
+    PROPD_REQUIRE(!conv || (ph->pro_src && ph->pro_cols == K && ph->pro_ld % 4 == 0 &&
+                            (reinterpret_cast<uintptr_t>(ph->pro_src) & 15) == 0),
+                  "gemm_ws: converting prologues read 16-byte aligned fp32 rows of K columns");
+    PROPD_REQUIRE(ph->pro_mode != PROPD_PRO_XLN ||
+                      (ph->colsum && ph->stats_rec && ph->stats_cnt && K % gws::SUB == 0 && K / gws::SUB <= gws::MAX_SUB),
+                  "gemm_ws: PRO_XLN needs colsum, stats_rec, stats_cnt and K %% 256 == 0, K <= 8192");
+    PROPD_REQUIRE(ph->zero_buf == nullptr || (ph->zero_cols % 4 == 0 && ph->zero_ld % 4 == 0 &&
+                                              (reinterpret_cast<uintptr_t>(ph->zero_buf) & 15) == 0),
+                  "gemm_ws: zero_buf rows must be float4-aligned");
     PROPD_REQUIRE(ph->pro_mode != PROPD_PRO_LN || K <= 4096, "gemm_ws: LN prologue supports rows <= 4096");
     PROPD_REQUIRE(ph->tail_mode == PROPD_TAIL_NONE ||
                       (accumulate && N == 3 * ph->A * ph->dh && (ph->dh % 4) == 0 && ph->tail_q && ph->kcache &&
@@ -670,6 +902,21 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
     case 112: return gws::launch<112>(wm, xm, p, grid, st);
     default: return gws::launch<128>(wm, xm, p, grid, st);
   }
+}
+
+int propd_ws_split_count(int N, int K) {
+  if (N <= 0 || K <= 0 || N % gws::BF || K % gws::BK) return 0;
+  int split, per;
+  gws::split_k(N, K, 1, 0, &split, &per);
+  return split;
+}
+
+int propd_ws_colsum(int N, int K, const void* W, int ldw, float* out, void* stream) {
+  PROPD_REQUIRE(N % gws::BF == 0 && K % gws::BK == 0, "ws_colsum: N=%d must be a multiple of 128, K=%d of 64", N, K);
+  int split, per;
+  gws::split_k(N, K, 1, 0, &split, &per);
+  return launch_pdl("ws_colsum", gws::colsum_kernel, dim3(N / gws::BF, split), dim3(gws::BF), 0, as_stream(stream),
+                    N, K, per * gws::BK, reinterpret_cast<const __nv_bfloat16*>(W), ldw, out);
 }
 
 int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,

@@ -28,6 +28,7 @@ ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--show", type=int, default=2, help="layers to print")
 ap.add_argument("--unfused", action="store_true")
 ap.add_argument("--per-cta", action="store_true", help="attention: per-CTA phase percentiles")
+ap.add_argument("--dump", default=None, help="save the raw CTA records (.npy)")
 args = ap.parse_args()
 
 cfg = TinyTransformerConfig(layers=args.layers, hidden=4096, heads=32, vocab=32000, draft_heads=4,
@@ -57,6 +58,8 @@ lib.propd_debug_timeline(ctypes.c_void_p(0))
 cnt = int(buf[0].item())
 rec = buf[8: 8 + 8 * cnt].view(cnt, 8).cpu().numpy().astype(np.int64)
 t_ref = rec[:, 3].min()
+if args.dump:
+    np.save(args.dump, rec)
 print(f"rows {n}, kv {args.kv}, {'unfused' if args.unfused else 'fused'}: {cnt} CTA records")
 print(f"{'tag':>4} {'ctas':>5} {'entry0':>8} {'entry1':>8} {'wait_max':>8} {'main_max':>8} {'exit_min':>8} "
       f"{'exit_max':>8} {'gap':>6}  (us)")

@@ -518,12 +518,14 @@ def test_qkv_and_gelu_finish():
 
 
 # --------------------------------------------------------------- in-kernel GEMM phases
-@pytest.mark.parametrize("rows,live", [(1, None), (16, None), (40, 23), (128, None)])
-def test_phased_layers_match_separate_kernels(rows, live):
+@pytest.mark.parametrize("rows,live,offset", [(1, None, 0.0), (16, None, 0.0), (40, 23, 0.0), (128, None, 0.0),
+                                              (20, None, 2.0)])
+def test_phased_layers_match_separate_kernels(rows, live, offset):
     """Layer stack with the LN / GELU prologues and the QKV tail inside the weight-streaming GEMMs
-    (propd_gemm_ws_ph, grid barriers) == the same stack with separate add_ln / finish kernels: residual
+    (propd_gemm_ws_ph: grid-barrier prologues, and the barrier-free converting prologues with LayerNorm
+    applied by linearity in the epilogue) == the same stack with separate add_ln / finish kernels: residual
     stream and the K/V rows written to the cache within bf16 rounding (the paths differ only in where the
-    bf16 conversions happen)."""
+    bf16 conversions happen; `offset` shifts every row mean, the case LN-by-linearity must absorb)."""
     from paper_2402_13485_b200 import B200Backend, TinyTransformerConfig
     from paper_2402_13485_b200.backend import Rows
 
@@ -537,9 +539,11 @@ def test_phased_layers_match_separate_kernels(rows, live):
               i32(list(range(half)) + list(range(n - half))), i32([0, half, n]), max_keys=300 + n, max_rows=half,
               live=i32([live]) if live is not None else None)
     torch.manual_seed(rows)
-    x0 = torch.randn(n, 1024, device=DEV)
+    x0 = torch.randn(n, 1024, device=DEV) + offset
     outs = []
-    for phased in (False, True):
+    assert be.ws_conv, "the converting prologues should be on for H = 1024"
+    for phased, be.ws_conv, be.ws_conv_ln in ((False, False, False), (True, False, False), (True, True, False),
+                                              (True, True, True)):
         be.ws_phases = phased
         be.kcache.zero_()
         be.vcache.zero_()
@@ -555,7 +559,10 @@ def test_phased_layers_match_separate_kernels(rows, live):
         assert (xa[:r] - xb[:r]).abs().max().item() <= 3e-2 * scale
         assert (ka - kb).abs().max().item() <= 3e-2 * max(1.0, ka.abs().max().item())
         assert (va - vb).abs().max().item() <= 3e-2 * max(1.0, va.abs().max().item())
-    assert be._bar.abs().max().item() == 0 and be._acc.abs().max().item() == 0 and be._acc2.abs().max().item() == 0
+    # the barrier path leaves its scratch zeroed; the converting path zeroes the W_1 accumulator ahead (in
+    # the next QKV launch) and leaves the QKV launch's statistics counters reset by the last W_1 launch
+    assert be._bar.abs().max().item() == 0 and be._acc.abs().max().item() == 0
+    assert be._st_cnt[0].abs().max().item() == 0 and be._st_cnt[1, :r].min().item() == 1024 // 256
 
 
 # --------------------------------------------------------------- probability pruning / typical acceptance
