@@ -128,7 +128,12 @@ int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, 
  * (S^T = K Q^T, O^T += V^T P^T, keys on the MMA M dimension; <= 64 rows per
  * sequence; auto for 5..64 rows), 3 = streaming decode kernel (<= 4 rows per
  * sequence; auto for the bonus pass).  impls 3-5 need bf16 and dh = 128.  n_slots = number of [A, Lmax, dh] slot blocks in the
- * cache layer (bounds of the TMA tensor map). */
+ * cache layer (bounds of the TMA tensor map).
+ * impl | PROPD_ATTN_SCRATCH_LAST: the last batch entry holds only the pad rows
+ * of a pass captured at a padded row capacity (the scratch slot, a few keys):
+ * it is excluded from the launch-geometry heuristics (key splits per
+ * sequence), so a B-sequence step gets the splits of B, not B + 1. */
+#define PROPD_ATTN_SCRATCH_LAST 0x100
 int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits);
 int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int n_slots,
                          int max_rows_per_seq, int max_keys,

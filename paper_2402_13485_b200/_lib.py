@@ -65,6 +65,7 @@ _RESTYPES = {"propd_last_error": ctypes.c_char_p, "propd_attn_workspace_bytes": 
 
 
 PRO_NONE, PRO_LN, PRO_GELU, PRO_XLN, PRO_XGELU = 0, 1, 2, 3, 4
+ATTN_SCRATCH_LAST = 0x100  # propd_tree_attention impl flag (include/propd.h)
 TAIL_NONE, TAIL_QKV = 0, 1
 
 

@@ -104,6 +104,7 @@ class Rows:
     max_rows: int
     kv_keys: int = 0  # host count of K/V rows the pass streams (roofline accounting)
     live: object = None  # device int32 [1]: live row count when M is a padded capacity
+    scratch_last: bool = False  # entry B-1 is the scratch slot holding the pad rows
 
 
 @dataclass
@@ -426,7 +427,7 @@ class B200Backend:
         H, M = self.H, rt.M
         ws_bytes = 0 if ws is None else ws.numel()
         self._timed("attn", lambda: self._call(
-            "propd_tree_attention", self.code, self.attn_impl, rt.B, M, self.A, self.dh, self.Lmax, self.n_slots,
+            "propd_tree_attention", self.code, self.attn_impl | (_lib.ATTN_SCRATCH_LAST if rt.scratch_last else 0), rt.B, M, self.A, self.dh, self.Lmax, self.n_slots,
             rt.max_rows, rt.max_keys, ptr(qkv), qkv.shape[1], ptr(self.kcache[l]), ptr(self.vcache[l]),
             ptr(rt.seq_slot), ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx),
             H, ptr(ws), ws_bytes, self.stream()), M)
@@ -932,7 +933,7 @@ class B200Backend:
             x = torch.empty(S_pad, H, device=dev, dtype=torch.float32)
             self._call("propd_gather_rows", 0, S_pad, H, ptr(a["x"]), ptr(a["nsrc"]), ptr(x), st)
             rt = Rows(S_pad, B + 1, slot_buf, a["nrs"], a["nrn"], a["noff"], max_keys=kb, max_rows=n,
-                      live=a["total"] if device_rows else None)
+                      live=a["total"] if device_rows else None, scratch_last=True)
             pending = self._run_layers(x, rt, prune.layer, cfg.layers, td["mask"], n, tmpl.words)
             alive, node_row = a["alive"], a["node_row"]
         else:

@@ -220,17 +220,17 @@ static int choose_splits(int B, int A, int max_keys, int max_splits) {
   return want < 1 ? 1 : want;
 }
 
-int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys,
+int attention_tc2_bf16(int B, int Bg, int M, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys,
                        const void* qkv, int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot,
                        const int32_t* seq_len, const int32_t* row_off, const int32_t* row_node, const uint64_t* mask,
                        int n_tmpl, int W, void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st,
                        bool* handled);
-int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
+int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
                        int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                        const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                        void* out, int ldout, cudaStream_t st, bool force, bool* handled);
 
-int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
+int attention_decode_bf16(int B, int Bg, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
                           int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                           const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                           void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled);
@@ -267,13 +267,16 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
                          const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W, void* out, int ldout,
                          void* workspace, int64_t workspace_bytes, void* stream) {
   if (B == 0 || M == 0) return 0;
+  // launch geometry counts the sequences with a real KV cache (not the scratch entry)
+  const int Bg = (impl & PROPD_ATTN_SCRATCH_LAST) && B > 1 ? B - 1 : B;
+  impl &= 0xFF;
   PROPD_REQUIRE(mask == nullptr || (W <= ATT_MAXW && W * 64 >= n_tmpl),
                 "tree_attention: template of %d nodes needs W=%d <= %d", n_tmpl, W, ATT_MAXW);
   PROPD_REQUIRE(max_keys >= 1, "tree_attention: max_keys must be positive");
   cudaStream_t st = as_stream(stream);
   if (impl == 3 || (impl == 0 && dtype == PROPD_BF16 && dh == 128 && max_rows_per_seq <= 4)) {
     bool handled = false;
-    int e = attention_decode_bf16(B, M, A, Lmax, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
+    int e = attention_decode_bf16(B, Bg, M, A, Lmax, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
                                   seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, workspace,
                                   workspace_bytes, st, &handled);
     if (e || handled) return e;
@@ -281,14 +284,14 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
   }
   if (impl == 5 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {  // <= 64 rows: transposed kernel
     bool handled = false;
-    int e = attention_tct_bf16(B, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
+    int e = attention_tct_bf16(B, Bg, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache, seq_slot,
                                seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, st, impl == 5, &handled);
     if (e || handled) return e;
     PROPD_REQUIRE(impl != 5, "tree_attention: transposed tcgen05 kernel serves <= 64 rows per sequence");
   }
   if (impl == 4 || (impl == 0 && dtype == PROPD_BF16 && dh == 128)) {
     bool handled = false;
-    int e = attention_tc2_bf16(B, M, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache,
+    int e = attention_tc2_bf16(B, Bg, M, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache,
                                seq_slot, seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, workspace,
                                workspace_bytes, st, &handled);
     if (e || handled) return e;

@@ -315,6 +315,45 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
   if (p.tl && threadIdx.x == 0) trace_record(p.tl, p.tag, t_entry, t_wait, t_loop, 2);
 }
 
+// Clusters of `cs` decode CTAs resident at once (cudaOccupancyMaxActiveClusters,
+// cached per (rows variant, cluster size)); 0 on a query error.
+template <int ROWS>
+static int max_clusters_t(int cs) {
+  static int cache[MAX_SPLIT + 1] = {};
+  if (cs < 1 || cs > MAX_SPLIT) return 0;
+  if (cache[cs] == 0) {
+    constexpr int smem = (int)sizeof(Smem<ROWS>);
+    if (cudaFuncSetAttribute(decode_kernel<ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaFuncSetAttribute(decode_kernel<ROWS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs, 1, 1);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, decode_kernel<ROWS>, &cfg) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return 0;
+    }
+    cache[cs] = n > 0 ? n : -1;
+  }
+  return cache[cs] > 0 ? cache[cs] : 0;
+}
+static int max_clusters(int rows, int cs) {
+  if (cs <= 1) return 1 << 30;
+  return rows <= 1 ? max_clusters_t<1>(cs) : (rows <= 2 ? max_clusters_t<2>(cs) : max_clusters_t<4>(cs));
+}
+
 template <int ROWS>
 static int launch(const Args& p, dim3 grid, cudaStream_t st) {
   static bool attr = false;
@@ -359,7 +398,7 @@ static int launch(const Args& p, dim3 grid, cudaStream_t st) {
 }  // namespace dec
 
 // Called by propd_tree_attention for bf16 / dh = 128 with <= 4 rows per sequence.
-int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
+int attention_decode_bf16(int B, int Bg, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
                           int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                           const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                           void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled) {
@@ -371,7 +410,7 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   // splits per (sequence, head), one cluster each: enough CTAs for ~2 per SM
   // at small batch; at large batch (>= one wave of pairs) the split count
   // whose last wave is fullest (measured: 2 splits at B=32 x 32 heads)
-  const int pairs = B * A;
+  const int pairs = Bg * A;  // sequences with a KV cache (Bg <= B)
   const int slots = 2 * propd_num_sms();
   int nsplit = (slots + pairs - 1) / pairs;
   if (2 * pairs > slots) nsplit = wave_split(pairs, slots, 2);
@@ -379,6 +418,15 @@ int attention_decode_bf16(int B, int M, int A, int Lmax, int max_rows_per_seq, i
   if (nsplit > cap) nsplit = cap;
   if (nsplit > dec::MAX_SPLIT) nsplit = dec::MAX_SPLIT;
   if (nsplit < 1) nsplit = 1;
+  // all clusters of one wave must fit at once (clusters of s CTAs are placed
+  // within a GPC: at B = 1, 32 clusters of 8 do not, and the second wave
+  // costs ~5 us per launch): the largest split whose clusters are co-resident
+  if (Bg * A * nsplit <= slots)
+    while (nsplit > 1) {
+      const int mc = dec::max_clusters(max_rows_per_seq, nsplit);
+      if (mc == 0 || pairs <= mc) break;  // (0: query failed, keep the split)
+      --nsplit;
+    }
   static const int split_override = env_int("PROPD_DEC_SPLIT");
   if (split_override > 0) nsplit = split_override < dec::MAX_SPLIT ? split_override : dec::MAX_SPLIT;
   // boundaries: any multiple of 16 keys from the device length (chunks start

@@ -538,7 +538,7 @@ int attention_tc2_prepare() {
   return e == cudaSuccess ? 0 : fail("prepare(tc2): %s", cudaGetErrorString(e));
 }
 
-int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys,
+int attention_tc2_bf16(int B, int Bg, int M, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys,
                        const void* qkv, int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot,
                        const int32_t* seq_len, const int32_t* row_off, const int32_t* row_node, const uint64_t* mask,
                        int n_tmpl, int W, void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st,
@@ -549,7 +549,7 @@ int attention_tc2_bf16(int B, int M, int A, int Lmax, int n_slots, int max_rows_
   const uint64_t rows = (uint64_t)n_slots * A * Lmax;
   if (!tc2::kv_map64(&km, kc, rows) || !tc2::kv_map64(&vm, vc, rows)) return 0;
   const int mtiles = (max_rows_per_seq + tc2::BM - 1) / tc2::BM;
-  const int ctas = B * A * mtiles;
+  const int ctas = Bg * A * mtiles;  // sequences with a KV cache (Bg <= B)
   const int nblk_max = (max_keys + tc2::BN - 1) / tc2::BN;
   // key splits per row tile (one cluster each, <= 8): one wave of one CTA
   // per SM at small batch (more, shorter splits measured slower at B=8-16)

@@ -607,7 +607,7 @@ static int tct_launch(const CUtensorMap& km, const CUtensorMap& vm, const tct::A
   return check_launch("tree_attention(tcT)");
 }
 
-int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
+int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
                        int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                        const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
                        void* out, int ldout, cudaStream_t st, bool force, bool* handled) {
@@ -618,12 +618,12 @@ int attention_tct_bf16(int B, int A, int Lmax, int n_slots, int max_rows_per_seq
   // latency-bound, where the row-major tc2 kernel's shorter per-block chain
   // wins (measured: 11.2 vs 14.7 us at B=1/KV 512, 22.2 vs 25.0 at B=4/KV 1K)
   if (!force && tct_mode() != 2 && max_rows_per_seq > 32 &&
-      (long long)B * A * ((max_keys + 127) / 128) < 16LL * propd_num_sms())
+      (long long)Bg * A * ((max_keys + 127) / 128) < 16LL * propd_num_sms())
     return 0;
   CUtensorMap km, vm;
   const uint64_t rows = (uint64_t)n_slots * A * Lmax;
   if (!tct::kv_map128(&km, kc, rows) || !tct::kv_map128(&vm, vc, rows)) return 0;
-  const int ctas = B * A;
+  const int ctas = Bg * A;  // sequences with a KV cache (Bg <= B)
   // key splits per (sequence, head), one cluster each (<= 8): one wave of one
   // CTA per SM at small batch; split boundaries on 64-key multiples (a
   // split's last 128-key block may be partly masked)

@@ -37,6 +37,8 @@ for rel0, rel1, ex, name in rows:
     a[2] += ((rel1 - prev_exit) / 1e3) if prev_exit is not None else 0.0
     prev_exit = ex
 total = (rows[-1][2] - rows[0][0]) / 1e3
-print(f"{len(rows)} traced launches, span {total:.1f} us")
+win_all = sum(a[1] for a in agg.values())
+gap_all = sum(a[2] for a in agg.values())
+print(f"{len(rows)} traced launches, span {total:.1f} us: windows {win_all:.1f} us, gaps before releases {gap_all:.1f} us")
 for name, (n, win, gap) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     print(f"{name:34s} x{n:4d}  window {win / n:7.2f} us  gap {gap / n:6.2f} us  sum {win:8.1f} us")
