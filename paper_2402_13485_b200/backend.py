@@ -465,7 +465,9 @@ class B200Backend:
             xln = lambda i, cs: dict(pro_mode=_lib.PRO_XLN, pro_src=ptr(x), pro_ld=H, pro_cols=H, bar=bar,
                                      colsum=ptr(cs), stats_rec=ptr(rec[i]), stats_cnt=ptr(cnt[i]),
                                      stats_cnt_reset=ptr(cnt[1 - i]))
-            gelu = _lib.WsPhases(pro_mode=_lib.PRO_XGELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_cols=4 * H, bar=bar)
+            # converted per stage at <= 32 live rows, the barrier GELU phase into g above
+            gelu = _lib.WsPhases(pro_mode=_lib.PRO_XGELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g),
+                                 pro_ldd=4 * H, pro_cols=4 * H, bar=bar)
         zero_acc2 = dict(zero_buf=ptr(acc2), zero_ld=4 * H, zero_cols=4 * H) if self.ws_conv else {}
         for l in range(l0, l1):
             # with the converting GELU, QKV zeroes the W_1 accumulator rows ahead (W_2 read them last)

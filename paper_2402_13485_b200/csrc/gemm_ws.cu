@@ -68,11 +68,12 @@ __device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d)
 //         normalises rows c, c + nCTA, ... (backends.py:135-142)
 //   GELU: X = bf16(tanh-GELU(src)), src re-zeroed (the split-K accumulator of
 //         the previous launch)
-__device__ __forceinline__ void prologue_phase(const propd_ws_phases& ph, int M, int tid, int cta, int ncta) {
+__device__ __forceinline__ void prologue_phase(const propd_ws_phases& ph, int mode, int M, int tid, int cta,
+                                               int ncta) {
   __shared__ float red[2][4];
   __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ph.pro_dst);
   const int C = ph.pro_cols;
-  if (ph.pro_mode == PROPD_PRO_LN) {
+  if (mode == PROPD_PRO_LN) {
     const int w = tid >> 5, lane = tid & 31;
     for (int t = cta; t < M; t += ncta) {
       const float* xr = ph.pro_src + (size_t)t * ph.pro_ld;
@@ -114,7 +115,7 @@ __device__ __forceinline__ void prologue_phase(const propd_ws_phases& ph, int M,
       }
       epi_sync();  // red[] is reused by the next row
     }
-  } else if (ph.pro_mode == PROPD_PRO_GELU) {
+  } else if (mode == PROPD_PRO_GELU) {
     const int per_row = C / 4;
     for (int e = cta * 128 + tid; e < M * per_row; e += ncta * 128) {
       const int t = e / per_row, c = (e - t * per_row) * 4;
@@ -338,7 +339,13 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
   const int nbox = max(1, (M + 15) >> 4);
   const int cta = blockIdx.y * gridDim.x + blockIdx.x, ncta = gridDim.x * gridDim.y;
-  const bool conv = conv_mode(p.ph.pro_mode);
+  // PROPD_PRO_XGELU converts in-CTA at <= 32 live rows; above that (and when
+  // a bf16 X buffer is given) it runs the grid-barrier GELU phase instead:
+  // the per-stage conversion would read 4 x the weight bytes from L2
+  const bool conv = p.ph.pro_mode == PROPD_PRO_XLN ||
+                    (p.ph.pro_mode == PROPD_PRO_XGELU && (M <= 32 || p.ph.pro_dst == nullptr));
+  const int pro_mode = (p.ph.pro_mode == PROPD_PRO_XGELU && !conv) ? PROPD_PRO_GELU : p.ph.pro_mode;
+  const bool two_arrivals = conv_mode(p.ph.pro_mode);  // full[] was initialised for 2 arrivals
   if (warp == 0) {
     if (lane == 0 && conv) {  // W only: the epilogue warps write the X tiles
       const int pre = min(nkb, STAGES);
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         tma_load_2d_hint(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k, wpol);
       }
     } else if (lane == 0) {
-      if (p.ph.pro_mode != PROPD_PRO_NONE) {
+      if (pro_mode != PROPD_PRO_NONE) {
         // X is produced in this launch's prologue by every CTA: wait for the
         // grid barrier (the weight stages above keep streaming meanwhile),
         // then order those generic writes before the TMA reads of X
@@ -363,6 +370,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       const int pre = min(nkb, STAGES);
       for (int j = 0; j < pre; ++j) {
         mbar_expect_tx(&full[j], nbox * 2048);
+        if (two_arrivals) mbar_arrive(&full[j]);
         for (int i = 0; i < nbox; ++i)
           tma_load_2d(smem + j * STAGE + A_BYTES + i * 2048, &xmap, &full[j], kblk(j) * BK, i * 16);
       }
@@ -370,6 +378,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         const int st = j % STAGES;
         mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 31);
         mbar_expect_tx(&full[st], A_BYTES + nbox * 2048);
+        if (two_arrivals) mbar_arrive(&full[st]);
         uint8_t* a = smem + st * STAGE;
         const int k = kblk(j) * BK;
         tma_load_2d_hint(a, &wmap, &full[st], n0, k, wpol);
@@ -450,8 +459,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       // (warp w: rows 32w..32w+31) after the last conversion, ahead of the
       // accumulator: off the epilogue's critical path and 4x fewer readers
       if (!gelu && w * 32 < M) s_ms[w * 32 + lane] = row_stats(p.ph, w * 32, min(M, w * 32 + 32), lane);
-    } else if (p.ph.pro_mode != PROPD_PRO_NONE) {
-      prologue_phase(p.ph, M, tid, cta, ncta);
+    } else if (pro_mode != PROPD_PRO_NONE) {
+      prologue_phase(p.ph, pro_mode, M, tid, cta, ncta);
       __threadfence();  // every writer fences before the CTA's arrival
       epi_sync();
       if (tid == 0) {
@@ -846,7 +855,8 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
                     (ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0),
                 "gemm_ws: Y must be 16-byte aligned with ldy %% 4 == 0 (vector stores / reductions)");
   const int mp = ((M + 15) / 16) * 16;
-  const bool conv = ph != nullptr && (ph->pro_mode == PROPD_PRO_XLN || ph->pro_mode == PROPD_PRO_XGELU);
+  const bool conv = ph != nullptr && (ph->pro_mode == PROPD_PRO_XLN ||
+                                     (ph->pro_mode == PROPD_PRO_XGELU && ph->pro_dst == nullptr));
   CUtensorMap wm, xm;
   memset(&xm, 0, sizeof(xm));  // unused when the CTAs convert X themselves
   PROPD_REQUIRE(gws::map2d(&wm, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw, 64) &&
@@ -874,7 +884,8 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
     PROPD_REQUIRE(ph->pro_mode == PROPD_PRO_NONE || conv ||
                       (ph->pro_src && ph->pro_dst == X && ph->pro_ldd == ldx && ph->pro_cols == K && K <= 4096 * 4),
                   "gemm_ws: the prologue must produce this launch's X operand");
-    PROPD_REQUIRE(!conv || (ph->pro_src && ph->pro_cols == K && ph->pro_ld % 4 == 0 &&
+    PROPD_REQUIRE(!(conv || ph->pro_mode == PROPD_PRO_XGELU) ||
+                      (ph->pro_src && ph->pro_cols == K && ph->pro_ld % 4 == 0 &&
                             (reinterpret_cast<uintptr_t>(ph->pro_src) & 15) == 0),
                   "gemm_ws: converting prologues read 16-byte aligned fp32 rows of K columns");
     PROPD_REQUIRE(ph->pro_mode != PROPD_PRO_XLN ||
