@@ -463,6 +463,7 @@ class B200Backend:
         if self.ws_conv:
             rec, cnt = self._st_rec, self._st_cnt
             xln = lambda i, cs: dict(pro_mode=_lib.PRO_XLN, pro_src=ptr(x), pro_ld=H, pro_cols=H, bar=bar,
+                                     pro_dst=ptr(h), pro_ldd=H,  # hybrid: later stages load bf16(x) by TMA
                                      colsum=ptr(cs), stats_rec=ptr(rec[i]), stats_cnt=ptr(cnt[i]),
                                      stats_cnt_reset=ptr(cnt[1 - i]))
             # converted per stage at <= 32 live rows, the barrier GELU phase into g above

@@ -116,41 +116,75 @@ __device__ __forceinline__ void prologue_phase(const propd_ws_phases& ph, int mo
       epi_sync();  // red[] is reused by the next row
     }
   } else if (mode == PROPD_PRO_GELU) {
-    const int per_row = C / 4;
-    for (int e = cta * 128 + tid; e < M * per_row; e += ncta * 128) {
-      const int t = e / per_row, c = (e - t * per_row) * 4;
-      float4* a = reinterpret_cast<float4*>(ph.pro_src + (size_t)t * ph.pro_ld + c);
-      const float4 f = __ldcg(a);
-      *a = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<uint2*>(dst + (size_t)t * ph.pro_ldd + c) =
-          pack_bf16x4(gelu_tanh(f.x), gelu_tanh(f.y), gelu_tanh(f.z), gelu_tanh(f.w));
+    // loads of a batch first (the re-zeroing stores alias them, so the
+    // compiler would otherwise serialise one L2 round trip per element)
+    const int per_row = C / 4, total = M * per_row, stride = ncta * 128;
+    for (int e0 = cta * 128 + tid; e0 < total; e0 += 4 * stride) {
+      float4 f[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * stride;
+        if (e < total) {
+          const int t = e / per_row;
+          f[u] = __ldcg(reinterpret_cast<const float4*>(ph.pro_src + (size_t)t * ph.pro_ld) + (e - t * per_row));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * stride;
+        if (e < total) {
+          const int t = e / per_row, c = (e - t * per_row) * 4;
+          *reinterpret_cast<float4*>(ph.pro_src + (size_t)t * ph.pro_ld + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<uint2*>(dst + (size_t)t * ph.pro_ldd + c) =
+              pack_bf16x4(gelu_tanh(f[u].x), gelu_tanh(f[u].y), gelu_tanh(f[u].z), gelu_tanh(f[u].w));
+        }
+      }
     }
   }
 }
 
 // Tail (QKV): after every CTA's split-K reduction into Y, the fp32 Q/K/V rows
 // become bf16 Q rows (tail_q) and K/V rows of the layer cache, Y re-zeroed
-// (same contract as propd_qkv_finish), spread over all CTAs.
+// (same contract as propd_qkv_finish), spread over all CTAs.  rowdst[t] =
+// (cache slot, position) of row t, filled by the CTA before its main loop
+// ends (tail_rows); loads of a batch are issued before its stores.
+__device__ __forceinline__ void tail_rows(const propd_ws_phases& ph, int M, int tid, int2* rowdst) {
+  for (int t = tid; t < M; t += 128) {
+    const int slot = ph.seq_slot[ph.row_seq[t]];
+    rowdst[t] = make_int2(slot, ph.seq_len[slot] + ph.row_node[t]);
+  }
+}
 __device__ __forceinline__ void tail_phase(float* Y, int ldy, const propd_ws_phases& ph, int M, int tid, int cta,
-                                           int ncta) {
-  const int H = ph.A * ph.dh, per_row = 3 * H / 4;
+                                           int ncta, const int2* rowdst) {
+  const int H = ph.A * ph.dh, per_row = 3 * H / 4, total = M * per_row, stride = ncta * 128;
   __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(ph.tail_q);
-  for (int e = cta * 128 + tid; e < M * per_row; e += ncta * 128) {
-    const int t = e / per_row, c = (e - t * per_row) * 4;
-    float4* a = reinterpret_cast<float4*>(Y + (size_t)t * ldy + c);
-    const float4 f = __ldcg(a);
-    *a = make_float4(0.f, 0.f, 0.f, 0.f);
-    const uint2 pk = pack_bf16x4(f.x, f.y, f.z, f.w);
-    if (c < H) {
-      *reinterpret_cast<uint2*>(q + (size_t)t * ph.tail_ldq + c) = pk;
-    } else {
-      const int kv = c >= 2 * H;
-      const int ee = c - (kv ? 2 * H : H);
-      const int ah = ee / ph.dh, d = ee - ah * ph.dh;
-      const int slot = ph.seq_slot[ph.row_seq[t]];
-      const int pos = ph.seq_len[slot] + ph.row_node[t];
-      __nv_bfloat16* cache = reinterpret_cast<__nv_bfloat16*>(kv ? ph.vcache : ph.kcache);
-      *reinterpret_cast<uint2*>(cache + (((size_t)slot * ph.A + ah) * ph.Lmax + pos) * ph.dh + d) = pk;
+  for (int e0 = cta * 128 + tid; e0 < total; e0 += 4 * stride) {
+    float4 f[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * stride;
+      if (e < total) {
+        const int t = e / per_row;
+        f[u] = __ldcg(reinterpret_cast<const float4*>(Y + (size_t)t * ldy) + (e - t * per_row));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * stride;
+      if (e >= total) continue;
+      const int t = e / per_row, c = (e - t * per_row) * 4;
+      *reinterpret_cast<float4*>(Y + (size_t)t * ldy + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint2 pk = pack_bf16x4(f[u].x, f[u].y, f[u].z, f[u].w);
+      if (c < H) {
+        *reinterpret_cast<uint2*>(q + (size_t)t * ph.tail_ldq + c) = pk;
+      } else {
+        const int kv = c >= 2 * H;
+        const int ee = c - (kv ? 2 * H : H);
+        const int ah = ee / ph.dh, d = ee - ah * ph.dh;
+        const int2 sp = rowdst[t];
+        __nv_bfloat16* cache = reinterpret_cast<__nv_bfloat16*>(kv ? ph.vcache : ph.kcache);
+        *reinterpret_cast<uint2*>(cache + (((size_t)sp.x * ph.A + ah) * ph.Lmax + sp.y) * ph.dh + d) = pk;
+      }
     }
   }
 }
@@ -287,7 +321,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   const unsigned long long t_entry = p.trace ? gtimer() : 0ull;
   __shared__ unsigned long long s_t[4];
   __shared__ int s_pro_done;
-  __shared__ float2 s_ms[128];  // PROPD_PRO_XLN: (mu, rstd) of the live rows
+  __shared__ float2 s_ms[128];    // PROPD_PRO_XLN: (mu, rstd) of the live rows
+  __shared__ int2 s_rowdst[128];  // PROPD_TAIL_QKV: (cache slot, position) of the live rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BF;
   const int kb0 = blockIdx.y * p.kblk_per_split;
@@ -344,20 +379,33 @@ __global__ void __launch_bounds__(THREADS, 2)
   // the per-stage conversion would read 4 x the weight bytes from L2
   const bool conv = p.ph.pro_mode == PROPD_PRO_XLN ||
                     (p.ph.pro_mode == PROPD_PRO_XGELU && (M <= 32 || p.ph.pro_dst == nullptr));
+  // PROPD_PRO_XLN with a bf16 X buffer (pro_dst): only the first ring stages
+  // are converted in-CTA; meanwhile the CTAs write bf16(pro_src) into X
+  // together and the later stages load X by TMA after a producer-only barrier
+  const bool hybrid = p.ph.pro_mode == PROPD_PRO_XLN && p.ph.pro_dst != nullptr;
+  const int nconv = hybrid ? min(nkb, STAGES) : nkb;  // stages converted by the epilogue warps
   const int pro_mode = (p.ph.pro_mode == PROPD_PRO_XGELU && !conv) ? PROPD_PRO_GELU : p.ph.pro_mode;
   const bool two_arrivals = conv_mode(p.ph.pro_mode);  // full[] was initialised for 2 arrivals
   if (warp == 0) {
-    if (lane == 0 && conv) {  // W only: the epilogue warps write the X tiles
+    if (lane == 0 && conv) {  // W (+ X by TMA past the converted stages in the hybrid mode)
       const int pre = min(nkb, STAGES);
       for (int j = 0; j < pre; ++j) mbar_arrive(&full[j]);
       for (int j = pre; j < nkb; ++j) {
         const int st = j % STAGES;
         mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 31);
-        mbar_expect_tx(&full[st], A_BYTES);
+        const bool xt = j >= nconv;
+        if (xt && j == nconv) {  // the bf16 X buffer is complete (producer-only barrier)
+          while (*reinterpret_cast<volatile int*>(&s_pro_done) == 0) __nanosleep(32);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        mbar_expect_tx(&full[st], A_BYTES + (xt ? nbox * 2048 : 0));
+        if (xt) mbar_arrive(&full[st]);  // (the converting warp's arrival)
         uint8_t* a = smem + st * STAGE;
         const int k = kblk(j) * BK;
         tma_load_2d_hint(a, &wmap, &full[st], n0, k, wpol);
         tma_load_2d_hint(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k, wpol);
+        if (xt)
+          for (int i = 0; i < nbox; ++i) tma_load_2d(a + A_BYTES + i * 2048, &xmap, &full[st], k, i * 16);
       }
     } else if (lane == 0) {
       if (pro_mode != PROPD_PRO_NONE) {
@@ -434,8 +482,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       bool dut = false;
       const int tasks = M * 8;  // (row, 16-byte chunk) per stage
       XBatch nb;
-      if (w < nkb) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(w) * BK, tasks, 0, lane);
-      for (int j = w; j < nkb; j += 4) {
+      if (w < nconv) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(w) * BK, tasks, 0, lane);
+      for (int j = w; j < nconv; j += 4) {
         const int st = j % STAGES;
         if (j >= STAGES) mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 34);
         uint8_t* xs = smem + st * STAGE + A_BYTES;
@@ -445,13 +493,36 @@ __global__ void __launch_bounds__(THREADS, 2)
           load_batch(b, p.ph.pro_src, p.ph.pro_ld, kblk(j) * BK, tasks, base, lane);
           store_batch(b, xs, tasks, base, lane, gelu);
         }
-        if (j + 4 < nkb) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(j + 4) * BK, tasks, 0, lane);
+        if (j + 4 < nconv) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(j + 4) * BK, tasks, 0, lane);
         fence_proxy_async();  // generic shared-memory writes -> tensor-core operand reads
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[st]);
         if (!dut) {
           duties();
           dut = true;
+        }
+      }
+      if (hybrid) {  // X = bf16(pro_src) by every CTA, then the producer-only barrier
+        const int total = M * (p.K / 4);
+        const int nprod = min(ncta, (total + 127) / 128);
+        __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(p.ph.pro_dst);
+        for (int e = cta * 128 + tid; e < total; e += ncta * 128) {
+          const int t = e / (p.K / 4), c = (e - t * (p.K / 4)) * 4;
+          const float4 f = __ldcg(reinterpret_cast<const float4*>(p.ph.pro_src + (size_t)t * p.ph.pro_ld + c));
+          *reinterpret_cast<uint2*>(xb + (size_t)t * p.ph.pro_ldd + c) = pack_bf16x4(f.x, f.y, f.z, f.w);
+        }
+        const bool producer = cta < nprod;
+        if (producer) __threadfence();
+        epi_sync();
+        if (tid == 0) {
+          unsigned* ctr = p.ph.bar;
+          if (producer) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+          while (ld_acquire(ctr) < (unsigned)nprod) __nanosleep(32);
+          *reinterpret_cast<volatile int*>(&s_pro_done) = 1;
+          if (atomicAdd(ctr + 1, 1u) == (unsigned)ncta - 1) {
+            ctr[0] = 0u;
+            ctr[1] = 0u;
+          }
         }
       }
       if (!dut) duties();
@@ -461,13 +532,25 @@ __global__ void __launch_bounds__(THREADS, 2)
       if (!gelu && w * 32 < M) s_ms[w * 32 + lane] = row_stats(p.ph, w * 32, min(M, w * 32 + 32), lane);
     } else if (pro_mode != PROPD_PRO_NONE) {
       prologue_phase(p.ph, pro_mode, M, tid, cta, ncta);
-      __threadfence();  // every writer fences before the CTA's arrival
+      // only the CTAs that wrote X arrive (LN: one per row; GELU: one per 128
+      // elements); every CTA waits for them, then counts its departure (off
+      // the critical path) so the last one re-arms the counters
+      const int nprod = pro_mode == PROPD_PRO_LN ? min(M, ncta) : min(ncta, (M * (p.ph.pro_cols / 4) + 127) / 128);
+      const bool producer = cta < nprod;
+      if (producer) __threadfence();  // every writer fences before the CTA's arrival
       epi_sync();
       if (tid == 0) {
-        grid_barrier(p.ph.bar, (unsigned)ncta);
+        unsigned* ctr = p.ph.bar;
+        if (producer) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        while (ld_acquire(ctr) < (unsigned)nprod) __nanosleep(32);
         *reinterpret_cast<volatile int*>(&s_pro_done) = 1;
+        if (atomicAdd(ctr + 1, 1u) == (unsigned)ncta - 1) {
+          ctr[0] = 0u;
+          ctr[1] = 0u;
+        }
       }
     }
+    if (p.ph.tail_mode != PROPD_TAIL_NONE) tail_rows(p.ph, M, tid, s_rowdst);  // read by this CTA's tail
     if (!conv && p.ph.zero_buf) {  // zero-ahead duty of a barrier-prologue launch (after its dependency wait)
       const int per_row = p.ph.zero_cols / 4;
       for (int e = cta * 128 + tid; e < M * per_row; e += ncta * 128) {
@@ -531,7 +614,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       epi_sync();
       if (tid == 0) grid_barrier(p.ph.bar + 2, (unsigned)ncta);
       epi_sync();
-      tail_phase(p.Y, p.ldy, p.ph, M, tid, cta, ncta);
+      tail_phase(p.Y, p.ldy, p.ph, M, tid, cta, ncta, s_rowdst);
     }
   }
   tc_before_sync();
@@ -710,12 +793,18 @@ static int g_probe_per_sm = 0;
 static int run_probe() {
   if (g_probe_per_sm > 0) return 0;
   int max_smem = 0, per_sm = 1 << 30;
+  // the probe's shared-memory footprint (dynamic + static) matches the
+  // largest gemm_ws variant's: dynamic + the kernel's static - the probe's static
+  cudaFuncAttributes fk{}, fp{};
+  if (cudaFuncGetAttributes(&fk, gemm_ws_kernel<16>) != cudaSuccess ||
+      cudaFuncGetAttributes(&fp, coresidency_probe_kernel) != cudaSuccess)
+    return fail("gemm_ws co-residency probe: attribute query failed");
   for (int mp = 16; mp <= 128; mp += 16) {
     const int o = occupancy(mp);
     if (o < 0) return 1;
     per_sm = min(per_sm, o);
-    // + 2 KB for the static shared memory of gemm_ws_kernel (timeline scratch, reductions, LN stats)
-    max_smem = max(max_smem, stages_for(mp) * (A_BYTES + mp * 128) + 256 + 1024 + 2048);
+    max_smem = max(max_smem, stages_for(mp) * (A_BYTES + mp * 128) + 256 + 1024 + (int)fk.sharedSizeBytes -
+                                 (int)fp.sharedSizeBytes);
   }
   const int n = per_sm * propd_num_sms();
   cudaError_t e = cudaFuncSetAttribute(coresidency_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
@@ -855,8 +944,8 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
                     (ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0),
                 "gemm_ws: Y must be 16-byte aligned with ldy %% 4 == 0 (vector stores / reductions)");
   const int mp = ((M + 15) / 16) * 16;
-  const bool conv = ph != nullptr && (ph->pro_mode == PROPD_PRO_XLN ||
-                                     (ph->pro_mode == PROPD_PRO_XGELU && ph->pro_dst == nullptr));
+  const bool conv = ph != nullptr && (ph->pro_mode == PROPD_PRO_XLN || ph->pro_mode == PROPD_PRO_XGELU) &&
+                   ph->pro_dst == nullptr;  // (with pro_dst, X is also loaded by TMA)
   CUtensorMap wm, xm;
   memset(&xm, 0, sizeof(xm));  // unused when the CTAs convert X themselves
   PROPD_REQUIRE(gws::map2d(&wm, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw, 64) &&
@@ -884,7 +973,7 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
     PROPD_REQUIRE(ph->pro_mode == PROPD_PRO_NONE || conv ||
                       (ph->pro_src && ph->pro_dst == X && ph->pro_ldd == ldx && ph->pro_cols == K && K <= 4096 * 4),
                   "gemm_ws: the prologue must produce this launch's X operand");
-    PROPD_REQUIRE(!(conv || ph->pro_mode == PROPD_PRO_XGELU) ||
+    PROPD_REQUIRE(!(conv || ph->pro_mode == PROPD_PRO_XGELU || ph->pro_mode == PROPD_PRO_XLN) ||
                       (ph->pro_src && ph->pro_cols == K && ph->pro_ld % 4 == 0 &&
                             (reinterpret_cast<uintptr_t>(ph->pro_src) & 15) == 0),
                   "gemm_ws: converting prologues read 16-byte aligned fp32 rows of K columns");
