@@ -320,11 +320,24 @@ def attn_step_bytes(be, m, prune_layer) -> float:
     L0 = m.mean_seqlen * B
     f = lambda keys, rows: (2 * keys + 2 * rows) * H * elt
     if n == 0:  # autoregressive
-        return Ly * f(L0 + B, B)
+        return 0.0 if bonus_fused(be, B) else Ly * f(L0 + B, B)
     p = prune_layer if prune_layer is not None else Ly
     S = m.mean_survivors * B
     tree = p * f(L0 + B * n, B * n) + (Ly - p) * f(L0 + B * n, S)
-    return tree + Ly * f(L0 + m.mean_accepted * B + B, B)
+    return tree + (0 if bonus_fused(be, B) else bonus_attn_bytes(be, m))
+
+
+def bonus_fused(be, B) -> bool:
+    """The bonus pass's attention runs inside its QKV launches (one-row fusion)."""
+    return bool(getattr(be, "ws_fuse_attn", False)) and be.fused_one_row_splits(B) > 0
+
+
+def bonus_attn_bytes(be, m) -> float:
+    """Algorithmic K/V + q/o bytes of the bonus pass's attention (all layers)."""
+    elt = 2 if be.tdtype != be.torch.float32 else 4
+    B = m.batch
+    keys = m.mean_seqlen * B + m.mean_accepted * B + B
+    return be.num_layers * (2 * keys + 2 * B) * be.H * elt
 
 
 def timeline_step(be, eng, seqs, prime, dev, prune_layer):
@@ -399,6 +412,8 @@ def timeline_step(be, eng, seqs, prime, dev, prune_layer):
         busy += cur1 - cur0
         if kind == 2:
             nbytes = attn_step_bytes(be, m, prune_layer)
+        elif kind == 1 and bonus_fused(be, m.batch):  # the bonus pass's attention runs in its QKV launches
+            nbytes += bonus_attn_bytes(be, m)
         busy_ms = busy / 1e6
         gbs = nbytes / (busy_ms * 1e-3) / 1e9 if busy_ms > 0 else 0.0
         out[name] = {"launches": len(spans), "busy_ms": busy_ms, "bytes": nbytes, "achieved": gbs, "frac": gbs / hbm,

@@ -196,6 +196,19 @@ int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, i
 #define PROPD_PRO_GELU 2
 #define PROPD_PRO_XLN 3
 #define PROPD_PRO_XGELU 4
+/* Fused one-row attention (bonus / autoregressive passes at small batch):
+ *   QKV launch, attn_splits = S > 0 (with PROPD_TAIL_QKV, one row per
+ *            sequence): after the tail, the CTAs also compute the attention
+ *            of every (row t, head a) over its sequence's keys 0..seq_len
+ *            (the committed cache rows, streamed by bulk copies issued before
+ *            the tail barrier, and the row's own K/V from Y) in S key splits,
+ *            writing (m, l, -, -, o[dh]) partials (log2 domain, o unnormalised)
+ *            to attn_part[t][a][S][4 + dh]; Y is not re-zeroed (the W_o launch's
+ *            zero_buf duty does it).  M * A * S <= the launch's CTAs.
+ *   PROPD_PRO_XATTN (W_o launch): X = bf16(combine of the S partials), built
+ *            per ring stage inside every CTA (pro_src = attn_part,
+ *            attn_splits = S, A, dh). */
+#define PROPD_PRO_XATTN 5
 #define PROPD_TAIL_NONE 0
 #define PROPD_TAIL_QKV 1
 typedef struct propd_ws_phases {
@@ -221,6 +234,8 @@ typedef struct propd_ws_phases {
   uint32_t* stats_cnt_reset;
   float* zero_buf;
   int zero_ld, zero_cols;
+  int attn_splits;
+  float* attn_part;
 } propd_ws_phases;
 /* Per-split column sums of a weight-streaming projection's W [K, N] (bf16,
  * row stride ldw) for PROPD_PRO_XLN: out[s][n] = sum over the k rows of

@@ -64,7 +64,7 @@ SIGNATURES = {
 _RESTYPES = {"propd_last_error": ctypes.c_char_p, "propd_attn_workspace_bytes": c_int64}
 
 
-PRO_NONE, PRO_LN, PRO_GELU, PRO_XLN, PRO_XGELU = 0, 1, 2, 3, 4
+PRO_NONE, PRO_LN, PRO_GELU, PRO_XLN, PRO_XGELU, PRO_XATTN = 0, 1, 2, 3, 4, 5
 ATTN_SCRATCH_LAST = 0x100  # propd_tree_attention impl flag (include/propd.h)
 TAIL_NONE, TAIL_QKV = 0, 1
 
@@ -76,7 +76,8 @@ class WsPhases(ctypes.Structure):
                 ("pro_cols", c_int), ("tail_mode", c_int), ("tail_q", P), ("tail_ldq", c_int), ("A", c_int),
                 ("dh", c_int), ("Lmax", c_int), ("row_seq", P), ("row_node", P), ("seq_slot", P), ("seq_len", P),
                 ("kcache", P), ("vcache", P), ("bar", P), ("colsum", P), ("stats_rec", P), ("stats_cnt", P),
-                ("stats_cnt_reset", P), ("zero_buf", P), ("zero_ld", c_int), ("zero_cols", c_int)]
+                ("stats_cnt_reset", P), ("zero_buf", P), ("zero_ld", c_int), ("zero_cols", c_int),
+                ("attn_splits", c_int), ("attn_part", P)]
 
 
 EPI_STORE, EPI_STORE_F32, EPI_ADD_F32, EPI_GELU, EPI_QKV = 0, 1, 2, 3, 4

@@ -201,6 +201,14 @@ class B200Backend:
                         os.environ.get("PROPD_WS_CONV", "1") != "0")  # "0": the grid-barrier prologues (A/B runs)
         self.ws_conv_ln = self.ws_conv and os.environ.get("PROPD_WS_CONV_LN", "0") == "1"
         self._colsum = None  # per-split column sums of W_qkv / W_1 (converting LN, built on first use)
+        # one-row passes (bonus / AR) at small batch: the attention runs inside
+        # the QKV launch (one (row, head, key split) per CTA) and W_o combines
+        # the partials (propd_ws_phases.attn_splits, PRO_XATTN)
+        self.ws_fuse_attn = (self.ws_phases and self.dh == 128 and os.environ.get("PROPD_FUSE_ATTN", "1") != "0")
+        if self.ws_fuse_attn:
+            H = cfg.hidden
+            self._qkv_ctas = (3 * H // 128) * self.lib.propd_ws_split_count(3 * H, H)
+            self._attn_part = torch.empty(self._qkv_ctas * (4 + self.dh), device=dev, dtype=torch.float32)
         if self.ws_conv:
             # per-row LN statistics records of the QKV / W_1 launches and their counters
             self._st_rec = torch.zeros(2, 128, 32, 2, device=dev, dtype=torch.float32)
@@ -470,6 +478,14 @@ class B200Backend:
             gelu = _lib.WsPhases(pro_mode=_lib.PRO_XGELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g),
                                  pro_ldd=4 * H, pro_cols=4 * H, bar=bar)
         zero_acc2 = dict(zero_buf=ptr(acc2), zero_ld=4 * H, zero_cols=4 * H) if self.ws_conv else {}
+        splits = 0  # fused one-row attention: key splits per (row, head)
+        if rt.max_rows == 1 and mask is self._one_mask and rt.live is None:
+            splits = self.fused_one_row_splits(M)
+        fused = dict(attn_splits=splits, attn_part=ptr(self._attn_part)) if splits else {}
+        if splits:
+            wo_phases = _lib.WsPhases(pro_mode=_lib.PRO_XATTN, pro_src=ptr(self._attn_part), pro_cols=H, A=self.A,
+                                      dh=self.dh, bar=bar, zero_buf=ptr(acc1), zero_ld=3 * H, zero_cols=3 * H,
+                                      **fused)
         for l in range(l0, l1):
             # with the converting GELU, QKV zeroes the W_1 accumulator rows ahead (W_2 read them last)
             if self.ws_conv_ln:
@@ -480,13 +496,25 @@ class B200Backend:
             qkv_phases = _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A, dh=self.dh,
                                        Lmax=self.Lmax, row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node),
                                        seq_slot=ptr(rt.seq_slot), seq_len=ptr(self.seq_len),
-                                       kcache=ptr(self.kcache[l]), vcache=ptr(self.vcache[l]), **pro_qkv)
+                                       kcache=ptr(self.kcache[l]), vcache=ptr(self.vcache[l]), **pro_qkv,
+                                       **fused)
             self._gemm_ws(M, live, 3 * H, H, h, self.w.wqkv[l], acc1, 3 * H, 1, qkv_phases)
-            self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
-            self._gemm_ws(M, live, H, H, ctx, self.w.wo[l], x, H, 1)
+            if splits:  # attention inside the QKV launch, partials combined by W_o (which re-zeroes acc1)
+                self._gemm_ws(M, live, H, H, ctx, self.w.wo[l], x, H, 1, wo_phases)
+            else:
+                self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
+                self._gemm_ws(M, live, H, H, ctx, self.w.wo[l], x, H, 1)
             self._gemm_ws(M, live, 4 * H, H, h, self.w.w1[l], acc2, 4 * H, 1, pro_w1)
             self._gemm_ws(M, live, H, 4 * H, g, self.w.w2[l], x, H, 1, gelu)
         return None
+
+    def fused_one_row_splits(self, M: int) -> int:
+        """Key splits of the attention fused into the QKV launch for a one-row
+        pass (bonus / AR) over M sequences (0: the separate attention kernel)."""
+        if not (self.ws_fuse_attn and 1 <= M <= 128):
+            return 0
+        splits = min(16, self._qkv_ctas // (M * self.A))
+        return splits if splits >= 2 else 0
 
     def _run_layers_ws(self, x, rt: Rows, l0: int, l1: int, mask, n_tmpl: int, W: int, pending=None):
         """Same blocks with separate LN / finish kernels between the

@@ -173,7 +173,8 @@ __device__ __forceinline__ void tail_phase(float* Y, int ldy, const propd_ws_pha
       const int e = e0 + u * stride;
       if (e >= total) continue;
       const int t = e / per_row, c = (e - t * per_row) * 4;
-      *reinterpret_cast<float4*>(Y + (size_t)t * ldy + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ph.attn_splits == 0)  // (with the fused attention, Y is read after the tail and zeroed by W_o)
+        *reinterpret_cast<float4*>(Y + (size_t)t * ldy + c) = make_float4(0.f, 0.f, 0.f, 0.f);
       const uint2 pk = pack_bf16x4(f[u].x, f[u].y, f[u].z, f[u].w);
       if (c < H) {
         *reinterpret_cast<uint2*>(q + (size_t)t * ph.tail_ldq + c) = pk;
@@ -189,13 +190,191 @@ __device__ __forceinline__ void tail_phase(float* Y, int ldy, const propd_ws_pha
   }
 }
 
+// ---- fused one-row attention (propd_ws_phases.attn_splits, include/propd.h) ----
+// Bonus / autoregressive passes (one row per sequence) at small batch: the
+// QKV launch's CTAs also run the attention, one (row, head, key split) item
+// per CTA, so the pass has no attention launch and no wave of 8-CTA clusters
+// to place.  The committed K/V rows of the item stream through the idle
+// weight ring in 64-key chunks (two buffers; the first two chunks are issued
+// before the tail barrier, so they land while the tail runs); the row's own
+// K/V and q come from the fp32 accumulator Y (bf16-rounded, as the cache and
+// the Q operand hold them).  Partials (m, l in the log2 domain, o
+// unnormalised) go to attn_part; the W_o launch combines them (PRO_XATTN).
+constexpr int ACH = 64, ADH = 128, ACH_BYTES = ACH * ADH * 2;  // 16 KB of K (or V) per chunk
+constexpr int ATT_OFF = 20 * 1024;                             // past the epilogue transpose tiles
+constexpr int PSTRIDE = 4 + ADH;  // partial record: m, l, 2 pad, o[dh] (16-byte aligned o)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+struct AttnItem {
+  int t, a, slot, pos, k0, k1;  // keys [k0, k1) of row t's sequence (key `pos` = the row itself)
+};
+__device__ __forceinline__ AttnItem attn_item(const propd_ws_phases& ph, int item, const int2* rowdst) {
+  const int S = ph.attn_splits;
+  AttnItem it;
+  const int ta = item / S, s = item - ta * S;
+  it.a = ta % ph.A;
+  it.t = ta / ph.A;
+  it.slot = rowdst[it.t].x;
+  it.pos = rowdst[it.t].y;
+  const int nkeys = it.pos + 1, len = (((nkeys + S - 1) / S) + 15) / 16 * 16;
+  it.k0 = min(nkeys, s * len);
+  it.k1 = min(nkeys, it.k0 + len);
+  return it;
+}
+// one thread: chunk c of the item into buffer c & 1 (committed rows only)
+__device__ __forceinline__ void attn_issue(const propd_ws_phases& ph, const AttnItem& it, int c, uint8_t* buf,
+                                           uint64_t* bar) {
+  const int kc = it.k0 + c * ACH;
+  const int n = min(ACH, min(it.k1, it.pos) - kc);
+  if (n > 0) {
+    const size_t row0 = (((size_t)it.slot * ph.A + it.a) * ph.Lmax + kc) * ADH;
+    mbar_expect_tx(bar, 2u * n * ADH * 2);
+    bulk_g2s(buf, reinterpret_cast<const __nv_bfloat16*>(ph.kcache) + row0, n * ADH * 2, bar);
+    bulk_g2s(buf + ACH_BYTES, reinterpret_cast<const __nv_bfloat16*>(ph.vcache) + row0, n * ADH * 2, bar);
+  } else {
+    mbar_arrive(bar);
+  }
+}
+__device__ __forceinline__ float bf16r(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+// 128 threads; scratch (shared, 1 KB): q[128] fp32, p[64], 4 per-warp maxima.
+// Scores: two threads per key (64 dims each, 16-byte column chunks staggered
+// by key against bank conflicts, q broadcast from shared memory); P.V: thread
+// = output dim.
+__device__ __forceinline__ void attn_run(const propd_ws_phases& ph, const AttnItem& it, int item, const float* Y,
+                                         int ldy, uint8_t* ring, uint64_t* abar, float* scratch, int tid) {
+  const int lane = tid & 31, w = tid >> 5, H = ph.A * ADH;
+  float* q_s = scratch;         // [128]
+  float* p_s = scratch + 128;   // [64]
+  float* wm_s = scratch + 192;  // [4]
+  const float* yrow = Y + (size_t)it.t * ldy + it.a * ADH;
+  const float scale = 1.4426950408889634f / sqrtf((float)ADH);
+  q_s[tid] = bf16r(__ldcg(yrow + tid)) * scale;  // (scores in the log2 domain)
+  const bool own = it.pos >= it.k0 && it.pos < it.k1;
+  const float vn = own ? bf16r(__ldcg(yrow + 2 * H + tid)) : 0.f;
+  const int cend = min(it.k1, it.pos);  // committed keys end
+  const int nch = (it.k1 - it.k0 + ACH - 1) / ACH;
+  const int kj = tid >> 1, half = tid & 1;  // score side: key kj of the chunk, dims half*64 .. +64
+  float m = -INFINITY, l = 0.f, o = 0.f;
+  epi_sync();  // q_s
+  for (int c = 0; c < nch; ++c) {
+    const int b = c & 1;
+    mbar_wait(&abar[b], (c >> 1) & 1, 35);
+    const uint8_t* kb = ring + b * 2 * ACH_BYTES;
+    const __nv_bfloat16* vbuf = reinterpret_cast<const __nv_bfloat16*>(kb + ACH_BYTES);
+    const int kc = it.k0 + c * ACH, key = kc + kj;
+    float d = 0.f;
+    if (key < cend) {
+      const uint8_t* krow = kb + kj * (ADH * 2) + half * 128;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int ci = (i + kj) & 7;
+        const uint4 kv = *reinterpret_cast<const uint4*>(krow + ci * 16);
+        const float4 qa = *reinterpret_cast<const float4*>(q_s + half * 64 + ci * 8);
+        const float4 qb = *reinterpret_cast<const float4*>(q_s + half * 64 + ci * 8 + 4);
+        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kv);
+        d += qa.x * __low2float(k2[0]) + qa.y * __high2float(k2[0]) + qa.z * __low2float(k2[1]) +
+             qa.w * __high2float(k2[1]) + qb.x * __low2float(k2[2]) + qb.y * __high2float(k2[2]) +
+             qb.z * __low2float(k2[3]) + qb.w * __high2float(k2[3]);
+      }
+    } else if (key == it.pos && own) {  // the row's own key, from Y
+      const float* kn = yrow + H + half * 64;
+      for (int i = 0; i < 64; ++i) d += q_s[half * 64 + i] * bf16r(__ldcg(kn + i));
+    }
+    d += __shfl_xor_sync(0xffffffffu, d, 1);
+    const float sj = key < it.k1 ? d : -INFINITY;
+    float cm = sj;  // chunk max: warp, then the 4 warps
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, off));
+    if (lane == 0) wm_s[w] = cm;
+    epi_sync();
+    const float mn = fmaxf(m, fmaxf(fmaxf(wm_s[0], wm_s[1]), fmaxf(wm_s[2], wm_s[3])));
+    if (half == 0) p_s[kj] = (mn == -INFINITY) ? 0.f : exp2f(sj - mn);
+    epi_sync();
+    if (mn != -INFINITY) {
+      const float alpha = exp2f(m - mn);  // (m = -inf: 0)
+      l *= alpha;
+      o *= alpha;
+      const int nc = min(ACH, cend - kc);  // committed keys of this chunk
+#pragma unroll 8
+      for (int j2 = 0; j2 < ACH; ++j2) {
+        const float pj = p_s[j2];
+        l += pj;
+        if (j2 < nc) o += pj * __bfloat162float(vbuf[j2 * ADH + tid]);
+      }
+      if (own && it.pos >= kc && it.pos < kc + ACH) o += p_s[it.pos - kc] * vn;
+      m = mn;
+    }
+    epi_sync();  // buffer b, p_s and wm_s are free
+    if (tid == 0 && c + 2 < nch) attn_issue(ph, it, c + 2, ring + b * 2 * ACH_BYTES, &abar[b]);
+  }
+  float* part = ph.attn_part + (size_t)item * PSTRIDE;
+  if (tid == 0) {
+    part[0] = m;
+    part[1] = l;
+  }
+  part[4 + tid] = o;
+}
+
+// PRO_XATTN stage builder (W_o): X[t, k0 .. k0+64) = combine of the S <= 16
+// partials of (row t, head k0 / 128), dims (k0 % 128) .. +64, per warp (lane
+// = (row, 8-dim chunk)); every load of a batch is issued before its use.
+constexpr int MAX_ASPLIT = 16;
+__device__ __forceinline__ void xattn_stage(const propd_ws_phases& ph, int k0, int M, uint8_t* xs, int lane) {
+  const int S = ph.attn_splits, h = k0 / ADH, d0 = k0 - h * ADH;
+  for (int task = lane; task < M * 8; task += 32) {
+    const int t = task >> 3, c = task & 7;
+    const float* base = ph.attn_part + (size_t)(t * ph.A + h) * S * PSTRIDE;
+    float2 ml[MAX_ASPLIT];
+#pragma unroll
+    for (int s = 0; s < MAX_ASPLIT; ++s)
+      ml[s] = s < S ? __ldcg(reinterpret_cast<const float2*>(base + s * PSTRIDE)) : make_float2(-INFINITY, 0.f);
+    float mx = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < MAX_ASPLIT; ++s) mx = fmaxf(mx, ml[s].x);
+    float l = 0.f, acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int s0 = 0; s0 < MAX_ASPLIT; s0 += 4) {
+      float4 a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float* ps = base + (s0 + u) * PSTRIDE + 4 + d0 + c * 8;
+        if (s0 + u < S) {
+          a[u] = __ldcg(reinterpret_cast<const float4*>(ps));
+          b[u] = __ldcg(reinterpret_cast<const float4*>(ps + 4));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = s0 + u;
+        if (s < S && ml[s].x != -INFINITY) {
+          const float f = exp2f(ml[s].x - mx);
+          l += ml[s].y * f;
+          acc[0] += a[u].x * f; acc[1] += a[u].y * f; acc[2] += a[u].z * f; acc[3] += a[u].w * f;
+          acc[4] += b[u].x * f; acc[5] += b[u].y * f; acc[6] += b[u].z * f; acc[7] += b[u].w * f;
+        }
+      }
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const uint2 lo = pack_bf16x4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    const uint2 hi = pack_bf16x4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+    *reinterpret_cast<uint4*>(xs + (t >> 4) * 2048 + (t & 15) * 128 + ((c ^ (t & 7)) << 4)) =
+        make_uint4(lo.x, lo.y, hi.x, hi.y);
+  }
+}
+
 // ---- barrier-free prologues (PROPD_PRO_XLN / PROPD_PRO_XGELU) ----
 // The four epilogue warps convert the fp32 source rows of each ring stage
 // into the stage's bf16 X tile themselves (the layout TMA SW128 would write:
 // 16-row boxes of 2 KB, 16-byte chunk c of row r at chunk c ^ (r & 7)), warp
 // w taking stages j = w, w + 4, ...: no grid barrier, no bf16 X buffer, and
 // the weight ring never waits for a cooperative prologue.
-__device__ __forceinline__ bool conv_mode(int m) { return m == PROPD_PRO_XLN || m == PROPD_PRO_XGELU; }
+__device__ __forceinline__ bool conv_mode(int m) {
+  return m == PROPD_PRO_XLN || m == PROPD_PRO_XGELU || m == PROPD_PRO_XATTN;
+}
 
 __device__ __forceinline__ uint4 cvt8(float4 a, float4 b, bool gelu) {
   if (gelu) {
@@ -318,10 +497,11 @@ __global__ void __launch_bounds__(THREADS, 2)
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  uint64_t* abar = full + 16;  // fused attention: the two K/V chunk buffers (128 B into the barrier area)
   const unsigned long long t_entry = p.trace ? gtimer() : 0ull;
   __shared__ unsigned long long s_t[4];
   __shared__ int s_pro_done;
-  __shared__ float2 s_ms[128];    // PROPD_PRO_XLN: (mu, rstd) of the live rows
+  __shared__ __align__(16) float2 s_ms[128];  // PROPD_PRO_XLN: (mu, rstd) of the live rows
   __shared__ int2 s_rowdst[128];  // PROPD_TAIL_QKV: (cache slot, position) of the live rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BF;
@@ -338,6 +518,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       mbar_init(&empty[i], 1);
     }
     mbar_init(acc_full, 1);
+    mbar_init(&abar[0], 1);
+    mbar_init(&abar[1], 1);
     fence_barrier_init();
     s_pro_done = 0;
   }
@@ -377,8 +559,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   // PROPD_PRO_XGELU converts in-CTA at <= 32 live rows; above that (and when
   // a bf16 X buffer is given) it runs the grid-barrier GELU phase instead:
   // the per-stage conversion would read 4 x the weight bytes from L2
-  const bool conv = p.ph.pro_mode == PROPD_PRO_XLN ||
-                    (p.ph.pro_mode == PROPD_PRO_XGELU && (M <= 32 || p.ph.pro_dst == nullptr));
+  const bool conv = p.ph.pro_mode == PROPD_PRO_XLN || p.ph.pro_mode == PROPD_PRO_XATTN ||
+                    (p.ph.pro_mode == PROPD_PRO_XGELU && ((M <= 32 && STAGES >= 4) || p.ph.pro_dst == nullptr));
   // PROPD_PRO_XLN with a bf16 X buffer (pro_dst): only the first ring stages
   // are converted in-CTA; meanwhile the CTAs write bf16(pro_src) into X
   // together and the later stages load X by TMA after a producer-only barrier
@@ -466,8 +648,9 @@ __global__ void __launch_bounds__(THREADS, 2)
       const bool gelu = p.ph.pro_mode == PROPD_PRO_XGELU;
       // after this warp's first stage (or at once if it has none): statistics,
       // then the launch's zeroing duties
+      const bool xattn = p.ph.pro_mode == PROPD_PRO_XATTN, xln = p.ph.pro_mode == PROPD_PRO_XLN;
       auto duties = [&]() {
-        if (!gelu) stats_chunks(p.ph, M, p.K, cta * 4 + w, ncta * 4, lane);
+        if (xln) stats_chunks(p.ph, M, p.K, cta * 4 + w, ncta * 4, lane);
         if (p.ph.zero_buf) {
           const int per_row = p.ph.zero_cols / 4;
           for (int e = (cta * 4 + w) * 32 + lane; e < M * per_row; e += ncta * 128) {
@@ -482,18 +665,32 @@ __global__ void __launch_bounds__(THREADS, 2)
       bool dut = false;
       const int tasks = M * 8;  // (row, 16-byte chunk) per stage
       XBatch nb;
-      if (w < nconv) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(w) * BK, tasks, 0, lane);
-      for (int j = w; j < nconv; j += 4) {
+      // warp w owns the ring slots st with st % 4 == w and fills every use of
+      // them in order, so it never waits more than one phase ahead on a slot's
+      // barrier (with 3 slots and 4 warps, round-robin stages would alias the
+      // mbarrier parity and overwrite a slot still being read)
+      auto next_own = [&](int j) {
+        while (j < nconv && ((j % STAGES) & 3) != w) ++j;
+        return j;
+      };
+      const int j_first = next_own(0);
+      if (j_first < nconv && !xattn) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(j_first) * BK, tasks, 0, lane);
+      for (int j = j_first; j < nconv;) {
+        const int jn = next_own(j + 1);
         const int st = j % STAGES;
         if (j >= STAGES) mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 34);
         uint8_t* xs = smem + st * STAGE + A_BYTES;
-        store_batch(nb, xs, tasks, 0, lane, gelu);
-        for (int base = 128; base < tasks; base += 128) {
-          XBatch b;
-          load_batch(b, p.ph.pro_src, p.ph.pro_ld, kblk(j) * BK, tasks, base, lane);
-          store_batch(b, xs, tasks, base, lane, gelu);
+        if (xattn) {
+          xattn_stage(p.ph, kblk(j) * BK, M, xs, lane);
+        } else {
+          store_batch(nb, xs, tasks, 0, lane, gelu);
+          for (int base = 128; base < tasks; base += 128) {
+            XBatch b;
+            load_batch(b, p.ph.pro_src, p.ph.pro_ld, kblk(j) * BK, tasks, base, lane);
+            store_batch(b, xs, tasks, base, lane, gelu);
+          }
+          if (jn < nconv) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(jn) * BK, tasks, 0, lane);
         }
-        if (j + 4 < nconv) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(j + 4) * BK, tasks, 0, lane);
         fence_proxy_async();  // generic shared-memory writes -> tensor-core operand reads
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[st]);
@@ -501,6 +698,7 @@ __global__ void __launch_bounds__(THREADS, 2)
           duties();
           dut = true;
         }
+        j = jn;
       }
       if (hybrid) {  // X = bf16(pro_src) by every CTA, then the producer-only barrier
         const int total = M * (p.K / 4);
@@ -529,7 +727,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       // the row statistics this CTA's epilogue needs, fetched once per CTA
       // (warp w: rows 32w..32w+31) after the last conversion, ahead of the
       // accumulator: off the epilogue's critical path and 4x fewer readers
-      if (!gelu && w * 32 < M) s_ms[w * 32 + lane] = row_stats(p.ph, w * 32, min(M, w * 32 + 32), lane);
+      if (xln && w * 32 < M) s_ms[w * 32 + lane] = row_stats(p.ph, w * 32, min(M, w * 32 + 32), lane);
     } else if (pro_mode != PROPD_PRO_NONE) {
       prologue_phase(p.ph, pro_mode, M, tid, cta, ncta);
       // only the CTAs that wrote X arrive (LN: one per row; GELU: one per 128
@@ -610,11 +808,23 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
     (void)f;
     if (p.ph.tail_mode != PROPD_TAIL_NONE) {  // every CTA's reduction lands, then the tile rows are finished
+      const int items = p.ph.attn_splits > 0 ? M * p.ph.A * p.ph.attn_splits : 0;
+      uint8_t* ring = smem + ATT_OFF;
+      AttnItem it{};
+      epi_sync();  // (the transpose tiles and s_rowdst are complete; the ring is idle since acc_full)
+      if (cta < items) {  // the item's first two K/V chunks stream in while the tail runs
+        it = attn_item(p.ph, cta, s_rowdst);
+        if (tid == 0) {
+          const int nch = (it.k1 - it.k0 + ACH - 1) / ACH;
+          for (int c = 0; c < 2 && c < nch; ++c) attn_issue(p.ph, it, c, ring + c * 2 * ACH_BYTES, &abar[c]);
+        }
+      }
       __threadfence();
       epi_sync();
       if (tid == 0) grid_barrier(p.ph.bar + 2, (unsigned)ncta);
       epi_sync();
       tail_phase(p.Y, p.ldy, p.ph, M, tid, cta, ncta, s_rowdst);
+      if (cta < items) attn_run(p.ph, it, cta, p.Y, p.ldy, ring, abar, reinterpret_cast<float*>(s_ms), tid);
     }
   }
   tc_before_sync();
@@ -944,8 +1154,9 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
                     (ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0),
                 "gemm_ws: Y must be 16-byte aligned with ldy %% 4 == 0 (vector stores / reductions)");
   const int mp = ((M + 15) / 16) * 16;
-  const bool conv = ph != nullptr && (ph->pro_mode == PROPD_PRO_XLN || ph->pro_mode == PROPD_PRO_XGELU) &&
-                   ph->pro_dst == nullptr;  // (with pro_dst, X is also loaded by TMA)
+  const bool conv = ph != nullptr && (((ph->pro_mode == PROPD_PRO_XLN || ph->pro_mode == PROPD_PRO_XGELU) &&
+                                      ph->pro_dst == nullptr) ||  // (with pro_dst, X is also loaded by TMA)
+                                     ph->pro_mode == PROPD_PRO_XATTN);
   CUtensorMap wm, xm;
   memset(&xm, 0, sizeof(xm));  // unused when the CTAs convert X themselves
   PROPD_REQUIRE(gws::map2d(&wm, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw, 64) &&
@@ -973,7 +1184,20 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
     PROPD_REQUIRE(ph->pro_mode == PROPD_PRO_NONE || conv ||
                       (ph->pro_src && ph->pro_dst == X && ph->pro_ldd == ldx && ph->pro_cols == K && K <= 4096 * 4),
                   "gemm_ws: the prologue must produce this launch's X operand");
+    PROPD_REQUIRE(ph->pro_mode != PROPD_PRO_XATTN ||
+                      (ph->attn_part && ph->attn_splits >= 1 && ph->attn_splits <= gws::MAX_ASPLIT &&
+                       ph->dh == gws::ADH && K == ph->A * ph->dh &&
+                       (reinterpret_cast<uintptr_t>(ph->attn_part) & 15) == 0),
+                  "gemm_ws: PRO_XATTN combines attn_part partials (dh = 128, K = A * dh)");
+    PROPD_REQUIRE(ph->attn_splits == 0 || ph->tail_mode == PROPD_TAIL_NONE ||
+                      (ph->tail_mode == PROPD_TAIL_QKV && ph->dh == gws::ADH && ph->attn_part &&
+                       ph->attn_splits <= gws::MAX_ASPLIT &&
+                       (long long)M * ph->A * ph->attn_splits <= (long long)tiles * split &&
+                       (reinterpret_cast<uintptr_t>(ph->attn_part) & 15) == 0 &&
+                       gws::stages_for(mp) * (gws::A_BYTES + mp * 128) >= gws::ATT_OFF + 4 * gws::ACH_BYTES),
+                  "gemm_ws: the fused attention needs the QKV tail, dh = 128, M * A * splits <= CTAs");
     PROPD_REQUIRE(!(conv || ph->pro_mode == PROPD_PRO_XGELU || ph->pro_mode == PROPD_PRO_XLN) ||
+                      ph->pro_mode == PROPD_PRO_XATTN ||
                       (ph->pro_src && ph->pro_cols == K && ph->pro_ld % 4 == 0 &&
                             (reinterpret_cast<uintptr_t>(ph->pro_src) & 15) == 0),
                   "gemm_ws: converting prologues read 16-byte aligned fp32 rows of K columns");

@@ -519,7 +519,7 @@ def test_qkv_and_gelu_finish():
 
 # --------------------------------------------------------------- in-kernel GEMM phases
 @pytest.mark.parametrize("rows,live,offset", [(1, None, 0.0), (16, None, 0.0), (40, 23, 0.0), (128, None, 0.0),
-                                              (20, None, 2.0)])
+                                              (20, None, 2.0), (128, 32, 0.0), (128, 17, 0.0), (96, 30, 0.0)])
 def test_phased_layers_match_separate_kernels(rows, live, offset):
     """Layer stack with the LN / GELU prologues and the QKV tail inside the weight-streaming GEMMs
     (propd_gemm_ws_ph: grid-barrier prologues, and the barrier-free converting prologues with LayerNorm
@@ -784,3 +784,57 @@ def test_gemm_device_row_count(live):
     if r:
         assert (Y[:r] - ref[:r] - base[:r]).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
     assert torch.equal(Y[r:], base[r:])
+
+
+# --------------------------------------------------------------- fused one-row attention
+@pytest.mark.parametrize("B,L", [(1, 300), (3, 517), (4, 70), (2, 1024), (1, 1030)])
+def test_fused_bonus_attention_matches_decode_kernel(B, L):
+    """Bonus pass with the attention inside the QKV launch (key-split partials, combined in W_o's
+    converting prologue) == the same pass with the decode attention kernel: final hidden rows, the
+    root argmax and the appended K/V rows within bf16 rounding (backends.py:239-259)."""
+    from paper_2402_13485_b200 import B200Backend, TinyTransformerConfig
+
+    cfg = TinyTransformerConfig(layers=3, hidden=1024, heads=8, vocab=1024, draft_heads=2, max_positions=1100, seed=2)
+    be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=4, max_tree=16)
+    assert be.ws_fuse_attn
+    states = be.synthetic_states(B, L, seed=B)
+    slots = i32([s.slot for s in states])
+    lens0 = be.seq_len.clone()
+    bonus = i32([(7 * b + 3) % 1024 for b in range(B)])
+    outs = []
+    for fuse in (False, True):
+        be.ws_fuse_attn = fuse
+        be.seq_len.copy_(lens0)
+        be._bonus_program(slots, bonus, B, L + 2)
+        torch.cuda.synchronize()
+        hid = be.hidden[slots.long()].float().clone()
+        kv = torch.stack([be.kcache[:, s.slot, :, L].float() for s in states]).clone()
+        vv = torch.stack([be.vcache[:, s.slot, :, L].float() for s in states]).clone()
+        outs.append((hid, kv, vv, be.seq_len.clone()))
+    (h0, k0, v0, n0), (h1, k1, v1, n1) = outs
+    assert torch.equal(n0, n1)
+    for a, b in ((h0, h1), (k0, k1), (v0, v1)):
+        assert (a - b).abs().max().item() <= 3e-2 * max(1.0, a.abs().max().item()), (a - b).abs().max().item()
+    assert be._acc.abs().max().item() == 0  # the W_o launches re-zeroed the QKV accumulator
+
+
+@pytest.mark.parametrize("cap,live", [(16, 1), (32, 20), (64, 32), (96, 32), (128, 30), (128, 1)])
+def test_gemm_ws_gelu_prologue_7b_shape(cap, live):
+    """W_2-shaped weight-streaming launch (K = 16384: ~29 k-blocks per CTA, so the converting warps cycle
+    the ring many times) with the GELU prologue at every row capacity: equals GELU(src) @ W in fp32 on the
+    live rows (regression: with 3 ring slots and 4 converting warps the slot barriers' parity aliased)."""
+    N, K = 4096, 16384
+    torch.manual_seed(cap + live)
+    W = (torch.randn(K, N, device=DEV) / K ** 0.5).bfloat16()
+    src = torch.randn(cap, K, device=DEV)
+    ref = torch.nn.functional.gelu(src[:live], approximate="tanh").bfloat16().float() @ W.float()
+    g = torch.empty(cap, K, device=DEV, dtype=torch.bfloat16)
+    Y = torch.zeros(cap, N, device=DEV)
+    bar = torch.zeros(32, device=DEV, dtype=torch.int32)
+    ph = _lib.WsPhases(pro_mode=_lib.PRO_XGELU, pro_src=ptr(src), pro_ld=K, pro_dst=ptr(g), pro_ldd=K, pro_cols=K,
+                       bar=ptr(bar))
+    call("propd_gemm_ws_ph", cap, ptr(i32([live])), N, K, ptr(g), K, ptr(W), N, ptr(Y), N, 1, 0, ph, st())
+    torch.cuda.synchronize()
+    assert (Y[:live] - ref).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
+    assert Y[live:].abs().max().item() == 0.0
+    assert bar.abs().max().item() == 0
