@@ -187,10 +187,9 @@ int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, i
  *            after its dependency wait.
  *   PROPD_PRO_XGELU: X = bf16(tanh-GELU(pro_src)) (pro_src is not re-zeroed:
  *            a later launch zeroes it through zero_buf).  With pro_dst = X
- *            (bf16, stride pro_ldd = ldx) given, launches with more than 32
- *            live rows run the PROPD_PRO_GELU grid-barrier phase instead (and
- *            re-zero pro_src): the per-stage conversion would read 4x the
- *            weight bytes from L2 there. */
+ *            (bf16, stride pro_ldd = ldx) given, launches with more than 16
+ *            live rows (or fewer than 4 ring slots) run the PROPD_PRO_GELU
+ *            grid-barrier phase instead (and re-zero pro_src). */
 #define PROPD_PRO_NONE 0
 #define PROPD_PRO_LN 1
 #define PROPD_PRO_GELU 2

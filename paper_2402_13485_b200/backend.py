@@ -474,7 +474,7 @@ class B200Backend:
                                      pro_dst=ptr(h), pro_ldd=H,  # hybrid: later stages load bf16(x) by TMA
                                      colsum=ptr(cs), stats_rec=ptr(rec[i]), stats_cnt=ptr(cnt[i]),
                                      stats_cnt_reset=ptr(cnt[1 - i]))
-            # converted per stage at <= 32 live rows, the barrier GELU phase into g above
+            # converted per stage at <= 16 live rows, the barrier GELU phase into g above
             gelu = _lib.WsPhases(pro_mode=_lib.PRO_XGELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g),
                                  pro_ldd=4 * H, pro_cols=4 * H, bar=bar)
         zero_acc2 = dict(zero_buf=ptr(acc2), zero_ld=4 * H, zero_cols=4 * H) if self.ws_conv else {}
