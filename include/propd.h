@@ -169,31 +169,19 @@ int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, i
  *            fp32 QKV accumulator, N = 3H): Q rows -> tail_q (bf16, stride
  *            tail_ldq), K/V rows -> the layer cache exactly as
  *            propd_qkv_finish; Y re-zeroed.
- * Barrier-free prologues (the X operand is converted per ring stage inside
+ * Barrier-free prologue (the X operand is converted per ring stage inside
  * every CTA from fp32 pro_src [M, K] (row stride pro_ld, pro_cols = K), no
- * grid barrier, no bf16 X buffer; X / ldx are unused):
- *   PROPD_PRO_XLN:   X = bf16(pro_src) (the raw residual); LayerNorm is applied
- *            in the epilogue by linearity: Y += rstd_t (acc - mu_t c_f), where
- *            c_f = colsum[split][f] (propd_ws_colsum of this W) and (mu_t,
- *            rstd_t) come from per-row statistics that the CTAs of this launch
- *            publish while the weights stream: 256-column sub-chunk (mean, M2)
- *            records in stats_rec[t][32] (float2) counted by stats_cnt[t]; the
- *            record completing row t combines them (Chan's combination) into
- *            one 64-bit (mu, rstd) word at ((uint64_t*)(stats_cnt + 128))[t]
- *            (K % 256 == 0, K <= 8192).  stats_cnt = 384 uint32, zero at
- *            launch; the launch zeroes stats_cnt_reset[0..383] (the other LN
- *            launch's counters and words) and rows [0, M) x zero_cols of zero_buf
- *            (stride zero_ld; the next launch's split-K accumulator), both
- *            after its dependency wait.
+ * grid barrier, no bf16 X buffer):
  *   PROPD_PRO_XGELU: X = bf16(tanh-GELU(pro_src)) (pro_src is not re-zeroed:
- *            a later launch zeroes it through zero_buf).  With pro_dst = X
- *            (bf16, stride pro_ldd = ldx) given, launches with more than 16
- *            live rows (or fewer than 4 ring slots) run the PROPD_PRO_GELU
- *            grid-barrier phase instead (and re-zero pro_src). */
+ *            a later launch zeroes it through zero_buf: rows [0, M) x
+ *            zero_cols of zero_buf, stride zero_ld, zeroed after the launch's
+ *            dependency wait).  With pro_dst = X (bf16, stride pro_ldd = ldx)
+ *            given, launches with more than 16 live rows (or fewer than 4
+ *            ring slots) run the PROPD_PRO_GELU grid-barrier phase instead
+ *            (and re-zero pro_src). */
 #define PROPD_PRO_NONE 0
 #define PROPD_PRO_LN 1
 #define PROPD_PRO_GELU 2
-#define PROPD_PRO_XLN 3
 #define PROPD_PRO_XGELU 4
 /* Fused one-row attention (bonus / autoregressive passes at small batch):
  *   QKV launch, attn_splits = S > 0 (with PROPD_TAIL_QKV, one row per
@@ -227,23 +215,16 @@ typedef struct propd_ws_phases {
   void* kcache;
   void* vcache;
   uint32_t* bar;
-  const float* colsum;
-  float* stats_rec;
-  uint32_t* stats_cnt;
-  uint32_t* stats_cnt_reset;
   float* zero_buf;
   int zero_ld, zero_cols;
   int attn_splits;
   float* attn_part;
 } propd_ws_phases;
-/* Per-split column sums of a weight-streaming projection's W [K, N] (bf16,
- * row stride ldw) for PROPD_PRO_XLN: out[s][n] = sum over the k rows of
- * split s (the split-K geometry of an accumulating launch) of W[k][n], fp32.
- * out holds propd_ws_split_count(N, K) x N floats. */
-int propd_ws_split_count(int N, int K);
-int propd_ws_colsum(int N, int K, const void* W, int ldw, float* out, void* stream);
 int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X, int ldx, const void* W, int ldw,
                      float* Y, int ldy, int accumulate, int max_split, const propd_ws_phases* phases, void* stream);
+/* K splits of an accumulating weight-streaming launch over W [K, N] (its grid
+ * is N / 128 x splits CTAs; 0 for an invalid shape). */
+int propd_ws_split_count(int N, int K);
 /* ---- projections over many rows (> 128): Y = epilogue(X[M,K] . W[K,N]) ----
  * (backends.py:217-219, 234-236, 281, 321, 329).  bf16: persistent tcgen05
  * kernel (128 x 256 tiles, TMA, TMEM double-buffered accumulator; N % 32 == 0,

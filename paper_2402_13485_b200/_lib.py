@@ -45,7 +45,6 @@ SIGNATURES = {
     "propd_gemm_ws": [I, P, I, I, P, I, P, I, P, I, I, I, P],
     "propd_gemm_ws_ph": [I, P, I, I, P, I, P, I, P, I, I, I, "phases", P],
     "propd_ws_split_count": [I, I],
-    "propd_ws_colsum": [I, I, P, I, P, P],
     "propd_gemm": [I, I, P, I, I, P, I, P, I, "epi", P],
     "propd_qkv_finish": [I, P, I, I, I, P, I, P, I, P, P, P, P, P, P, P],
     "propd_gelu_finish": [I, P, I, P, I, P, I, P],
@@ -64,7 +63,7 @@ SIGNATURES = {
 _RESTYPES = {"propd_last_error": ctypes.c_char_p, "propd_attn_workspace_bytes": c_int64}
 
 
-PRO_NONE, PRO_LN, PRO_GELU, PRO_XLN, PRO_XGELU, PRO_XATTN = 0, 1, 2, 3, 4, 5
+PRO_NONE, PRO_LN, PRO_GELU, PRO_XGELU, PRO_XATTN = 0, 1, 2, 4, 5
 ATTN_SCRATCH_LAST = 0x100  # propd_tree_attention impl flag (include/propd.h)
 TAIL_NONE, TAIL_QKV = 0, 1
 
@@ -75,8 +74,7 @@ class WsPhases(ctypes.Structure):
     _fields_ = [("pro_mode", c_int), ("pro_src", P), ("pro_ld", c_int), ("pro_dst", P), ("pro_ldd", c_int),
                 ("pro_cols", c_int), ("tail_mode", c_int), ("tail_q", P), ("tail_ldq", c_int), ("A", c_int),
                 ("dh", c_int), ("Lmax", c_int), ("row_seq", P), ("row_node", P), ("seq_slot", P), ("seq_len", P),
-                ("kcache", P), ("vcache", P), ("bar", P), ("colsum", P), ("stats_rec", P), ("stats_cnt", P),
-                ("stats_cnt_reset", P), ("zero_buf", P), ("zero_ld", c_int), ("zero_cols", c_int),
+                ("kcache", P), ("vcache", P), ("bar", P), ("zero_buf", P), ("zero_ld", c_int), ("zero_cols", c_int),
                 ("attn_splits", c_int), ("attn_part", P)]
 
 

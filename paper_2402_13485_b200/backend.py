@@ -188,19 +188,11 @@ class B200Backend:
         if self.ws_phases:
             self._acc2 = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32)
             self._bar = torch.zeros(32, device=dev, dtype=torch.int32)
-        # barrier-free prologues: every CTA converts its own X stages (LN by
-        # linearity in the epilogue from per-row statistics published during
-        # the weight stream, GELU on the way in); needs the per-split column
-        # sums of W_qkv / W_1 (PROPD_PRO_XLN, include/propd.h)
-        # W_2's GELU prologue converts per stage in every CTA (measured: 2-3 us
-        # per launch faster than the grid-barrier GELU phase at B=1); the LN
-        # prologues stay on the grid barrier unless ws_conv_ln (the converting
-        # LN measured 1-3 us slower per launch: the 96-128 N-tiles of a split
-        # all read the same fp32 rows)
-        self.ws_conv = (self.ws_phases and cfg.hidden % 256 == 0 and cfg.hidden <= 8192 and
-                        os.environ.get("PROPD_WS_CONV", "1") != "0")  # "0": the grid-barrier prologues (A/B runs)
-        self.ws_conv_ln = self.ws_conv and os.environ.get("PROPD_WS_CONV_LN", "0") == "1"
-        self._colsum = None  # per-split column sums of W_qkv / W_1 (converting LN, built on first use)
+        # W_2's GELU operand is converted per ring stage inside every CTA at
+        # <= 16 live rows (measured: 2-3 us per launch faster than the
+        # grid-barrier GELU phase at B=1); QKV then zeroes the W_1 accumulator
+        # rows ahead (include/propd.h PROPD_PRO_XGELU)
+        self.ws_conv = (self.ws_phases and os.environ.get("PROPD_WS_CONV", "1") != "0")  # "0": barrier GELU (A/B)
         # one-row passes (bonus / AR) at small batch: the attention runs inside
         # the QKV launch (one (row, head, key split) per CTA) and W_o combines
         # the partials (propd_ws_phases.attn_splits, PRO_XATTN)
@@ -209,10 +201,6 @@ class B200Backend:
             H = cfg.hidden
             self._qkv_ctas = (3 * H // 128) * self.lib.propd_ws_split_count(3 * H, H)
             self._attn_part = torch.empty(self._qkv_ctas * (4 + self.dh), device=dev, dtype=torch.float32)
-        if self.ws_conv:
-            # per-row LN statistics records of the QKV / W_1 launches and their counters
-            self._st_rec = torch.zeros(2, 128, 32, 2, device=dev, dtype=torch.float32)
-            self._st_cnt = torch.zeros(2, 384, device=dev, dtype=torch.int32)  # 128 counters + 128 u64 words
         self.device_rows = True  # sync-free post-prune pass when it fits the weight-streaming GEMMs
         self._graphs: dict = {}
         self._templates: dict = {}
@@ -458,23 +446,7 @@ class B200Backend:
         ln = dict(pro_mode=_lib.PRO_LN, pro_src=ptr(x), pro_ld=H, pro_dst=ptr(h), pro_ldd=H, pro_cols=H, bar=bar)
         gelu = _lib.WsPhases(pro_mode=_lib.PRO_GELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g), pro_ldd=4 * H,
                              pro_cols=4 * H, bar=bar)
-        if self.ws_conv_ln and self._colsum is None:
-            st = self.stream()
-            self._colsum = []
-            for l in range(self.num_layers):
-                pair = []
-                for Wt, N in ((self.w.wqkv[l], 3 * H), (self.w.w1[l], 4 * H)):
-                    cs = torch.empty(self.lib.propd_ws_split_count(N, H), N, device=self.device, dtype=torch.float32)
-                    call("propd_ws_colsum", N, H, ptr(Wt), N, ptr(cs), st)
-                    pair.append(cs)
-                self._colsum.append(pair)
-        if self.ws_conv:
-            rec, cnt = self._st_rec, self._st_cnt
-            xln = lambda i, cs: dict(pro_mode=_lib.PRO_XLN, pro_src=ptr(x), pro_ld=H, pro_cols=H, bar=bar,
-                                     pro_dst=ptr(h), pro_ldd=H,  # hybrid: later stages load bf16(x) by TMA
-                                     colsum=ptr(cs), stats_rec=ptr(rec[i]), stats_cnt=ptr(cnt[i]),
-                                     stats_cnt_reset=ptr(cnt[1 - i]))
-            # converted per stage at <= 16 live rows, the barrier GELU phase into g above
+        if self.ws_conv:  # converted per stage at <= 16 live rows, the barrier GELU phase into g above
             gelu = _lib.WsPhases(pro_mode=_lib.PRO_XGELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g),
                                  pro_ldd=4 * H, pro_cols=4 * H, bar=bar)
         zero_acc2 = dict(zero_buf=ptr(acc2), zero_ld=4 * H, zero_cols=4 * H) if self.ws_conv else {}
@@ -488,11 +460,7 @@ class B200Backend:
                                       **fused)
         for l in range(l0, l1):
             # with the converting GELU, QKV zeroes the W_1 accumulator rows ahead (W_2 read them last)
-            if self.ws_conv_ln:
-                pro_qkv = dict(xln(0, self._colsum[l][0]), **zero_acc2)
-                pro_w1 = _lib.WsPhases(**xln(1, self._colsum[l][1]))
-            else:
-                pro_qkv, pro_w1 = dict(ln, **zero_acc2), _lib.WsPhases(**ln)
+            pro_qkv, pro_w1 = dict(ln, **zero_acc2), _lib.WsPhases(**ln)
             qkv_phases = _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A, dh=self.dh,
                                        Lmax=self.Lmax, row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node),
                                        seq_slot=ptr(rt.seq_slot), seq_len=ptr(self.seq_len),

@@ -366,14 +366,14 @@ __device__ __forceinline__ void xattn_stage(const propd_ws_phases& ph, int k0, i
   }
 }
 
-// ---- barrier-free prologues (PROPD_PRO_XLN / PROPD_PRO_XGELU) ----
+// ---- barrier-free prologues (PROPD_PRO_XGELU / PROPD_PRO_XATTN) ----
 // The four epilogue warps convert the fp32 source rows of each ring stage
 // into the stage's bf16 X tile themselves (the layout TMA SW128 would write:
 // 16-row boxes of 2 KB, 16-byte chunk c of row r at chunk c ^ (r & 7)), warp
 // w taking stages j = w, w + 4, ...: no grid barrier, no bf16 X buffer, and
 // the weight ring never waits for a cooperative prologue.
 __device__ __forceinline__ bool conv_mode(int m) {
-  return m == PROPD_PRO_XLN || m == PROPD_PRO_XGELU || m == PROPD_PRO_XATTN;
+  return m == PROPD_PRO_XGELU || m == PROPD_PRO_XATTN;
 }
 
 __device__ __forceinline__ uint4 cvt8(float4 a, float4 b, bool gelu) {
@@ -417,66 +417,6 @@ __device__ __forceinline__ void store_batch(const XBatch& b, uint8_t* xs, int ta
   }
 }
 
-// LayerNorm statistics for PROPD_PRO_XLN, published while the weights stream:
-// warp `gw` of the launch takes 256-column sub-chunks (row t, part q) and
-// writes their two-pass (mean, M2) record; the arrival that completes row t
-// (stats_cnt[t] reaches K / 256) combines the records (Chan's parallel
-// combination of equal-size groups) and publishes (mu, rstd) as one 64-bit
-// word after the counters (rstd > 0 doubles as the ready flag).
-constexpr int SUB = 256, MAX_SUB = 32;
-__device__ __forceinline__ unsigned long long* stats_word(const propd_ws_phases& ph, int t) {
-  return reinterpret_cast<unsigned long long*>(ph.stats_cnt + 128) + t;
-}
-__device__ __forceinline__ void stats_chunks(const propd_ws_phases& ph, int M, int K, int gw, int nw, int lane) {
-  const int nsub = K / SUB;
-  for (int item = gw; item < M * nsub; item += nw) {
-    const int t = item / nsub, q = item - t * nsub;
-    const float4* g = reinterpret_cast<const float4*>(ph.pro_src + (size_t)t * ph.pro_ld + q * SUB + lane * 8);
-    const float4 a = __ldcg(g), b = __ldcg(g + 1);
-    const float mean = warp_sum(((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) * (1.f / SUB);
-    float d, m2 = 0.f;
-    d = a.x - mean; m2 += d * d; d = a.y - mean; m2 += d * d; d = a.z - mean; m2 += d * d; d = a.w - mean; m2 += d * d;
-    d = b.x - mean; m2 += d * d; d = b.y - mean; m2 += d * d; d = b.z - mean; m2 += d * d; d = b.w - mean; m2 += d * d;
-    m2 = warp_sum(m2);
-    if (lane == 0) {
-      float2* rec = reinterpret_cast<float2*>(ph.stats_rec) + (size_t)t * MAX_SUB;
-      __stcg(rec + q, make_float2(mean, m2));
-      unsigned old;
-      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ph.stats_cnt + t) : "memory");
-      if (old == (unsigned)nsub - 1) {  // last record of row t: combine and publish
-        float s = 0.f;
-        for (int i = 0; i < nsub; ++i) s += __ldcg(rec + i).x;
-        const float mu = s / (float)nsub;
-        float acc = 0.f;
-        for (int i = 0; i < nsub; ++i) {
-          const float2 r = __ldcg(rec + i);
-          const float dd = r.x - mu;
-          acc += r.y + (float)SUB * dd * dd;
-        }
-        const float rstd = 1.f / sqrtf(acc / (float)K + 1e-5f);
-        const unsigned long long word = (unsigned long long)__float_as_uint(mu) |
-                                        ((unsigned long long)__float_as_uint(rstd) << 32);
-        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(stats_word(ph, t)), "l"(word) : "memory");
-      }
-    }
-  }
-}
-
-// (mu, rstd) of rows [t0, t1): lane t0 + i polls its row's published word
-// (relaxed 64-bit loads, converged; the word is its own flag).
-__device__ __forceinline__ float2 row_stats(const propd_ws_phases& ph, int t0, int t1, int lane) {
-  const int t = t0 + lane;
-  unsigned long long w = 0ull;
-  bool ok = t >= t1;
-  while (!__all_sync(0xffffffffu, ok)) {
-    if (!ok) {
-      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(stats_word(ph, t)) : "memory");
-      ok = (w >> 32) != 0ull;
-    }
-  }
-  return t < t1 ? make_float2(__uint_as_float((unsigned)w), __uint_as_float((unsigned)(w >> 32)))
-                : make_float2(0.f, 0.f);
-}
 
 // Ring depth per X-tile size: as deep as two CTAs per SM allow (deeper rings
 // keep more weight bytes in flight and prefetch more of them while the
@@ -501,7 +441,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   const unsigned long long t_entry = p.trace ? gtimer() : 0ull;
   __shared__ unsigned long long s_t[4];
   __shared__ int s_pro_done;
-  __shared__ __align__(16) float2 s_ms[128];  // PROPD_PRO_XLN: (mu, rstd) of the live rows
+  __shared__ __align__(16) float s_attn[256];  // fused one-row attention scratch (q, p, warp maxima)
   __shared__ int2 s_rowdst[128];  // PROPD_TAIL_QKV: (cache slot, position) of the live rows
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BF;
@@ -559,35 +499,22 @@ __global__ void __launch_bounds__(THREADS, 2)
   // PROPD_PRO_XGELU converts in-CTA at <= 16 live rows (one task batch per
   // stage); above that, when a bf16 X buffer is given, it runs the
   // grid-barrier GELU phase instead (measured at 32 rows: 39 vs 32 us for W_2)
-  const bool conv = p.ph.pro_mode == PROPD_PRO_XLN || p.ph.pro_mode == PROPD_PRO_XATTN ||
+  const bool conv = p.ph.pro_mode == PROPD_PRO_XATTN ||
                     (p.ph.pro_mode == PROPD_PRO_XGELU && ((M <= 16 && STAGES >= 4) || p.ph.pro_dst == nullptr));
-  // PROPD_PRO_XLN with a bf16 X buffer (pro_dst): only the first ring stages
-  // are converted in-CTA; meanwhile the CTAs write bf16(pro_src) into X
-  // together and the later stages load X by TMA after a producer-only barrier
-  const bool hybrid = p.ph.pro_mode == PROPD_PRO_XLN && p.ph.pro_dst != nullptr;
-  const int nconv = hybrid ? min(nkb, STAGES) : nkb;  // stages converted by the epilogue warps
   const int pro_mode = (p.ph.pro_mode == PROPD_PRO_XGELU && !conv) ? PROPD_PRO_GELU : p.ph.pro_mode;
   const bool two_arrivals = conv_mode(p.ph.pro_mode);  // full[] was initialised for 2 arrivals
   if (warp == 0) {
-    if (lane == 0 && conv) {  // W (+ X by TMA past the converted stages in the hybrid mode)
+    if (lane == 0 && conv) {  // W only: the epilogue warps write the X tiles
       const int pre = min(nkb, STAGES);
       for (int j = 0; j < pre; ++j) mbar_arrive(&full[j]);
       for (int j = pre; j < nkb; ++j) {
         const int st = j % STAGES;
         mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 31);
-        const bool xt = j >= nconv;
-        if (xt && j == nconv) {  // the bf16 X buffer is complete (producer-only barrier)
-          while (*reinterpret_cast<volatile int*>(&s_pro_done) == 0) __nanosleep(32);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
-        mbar_expect_tx(&full[st], A_BYTES + (xt ? nbox * 2048 : 0));
-        if (xt) mbar_arrive(&full[st]);  // (the converting warp's arrival)
+        mbar_expect_tx(&full[st], A_BYTES);
         uint8_t* a = smem + st * STAGE;
         const int k = kblk(j) * BK;
         tma_load_2d_hint(a, &wmap, &full[st], n0, k, wpol);
         tma_load_2d_hint(a + A_BYTES / 2, &wmap, &full[st], n0 + 64, k, wpol);
-        if (xt)
-          for (int i = 0; i < nbox; ++i) tma_load_2d(a + A_BYTES + i * 2048, &xmap, &full[st], k, i * 16);
       }
     } else if (lane == 0) {
       if (pro_mode != PROPD_PRO_NONE) {
@@ -648,9 +575,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       const bool gelu = p.ph.pro_mode == PROPD_PRO_XGELU;
       // after this warp's first stage (or at once if it has none): statistics,
       // then the launch's zeroing duties
-      const bool xattn = p.ph.pro_mode == PROPD_PRO_XATTN, xln = p.ph.pro_mode == PROPD_PRO_XLN;
+      const bool xattn = p.ph.pro_mode == PROPD_PRO_XATTN;
       auto duties = [&]() {
-        if (xln) stats_chunks(p.ph, M, p.K, cta * 4 + w, ncta * 4, lane);
         if (p.ph.zero_buf) {
           const int per_row = p.ph.zero_cols / 4;
           for (int e = (cta * 4 + w) * 32 + lane; e < M * per_row; e += ncta * 128) {
@@ -659,8 +585,6 @@ __global__ void __launch_bounds__(THREADS, 2)
                    make_float4(0.f, 0.f, 0.f, 0.f));
           }
         }
-        if (p.ph.stats_cnt_reset && cta == 0)  // the other LN launch: 128 counters + 128 published words
-          for (int e = w * 32 + lane; e < 384; e += 128) p.ph.stats_cnt_reset[e] = 0u;
       };
       bool dut = false;
       const int tasks = M * 8;  // (row, 16-byte chunk) per stage
@@ -670,12 +594,12 @@ __global__ void __launch_bounds__(THREADS, 2)
       // barrier (with 3 slots and 4 warps, round-robin stages would alias the
       // mbarrier parity and overwrite a slot still being read)
       auto next_own = [&](int j) {
-        while (j < nconv && ((j % STAGES) & 3) != w) ++j;
+        while (j < nkb && ((j % STAGES) & 3) != w) ++j;
         return j;
       };
       const int j_first = next_own(0);
-      if (j_first < nconv && !xattn) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(j_first) * BK, tasks, 0, lane);
-      for (int j = j_first; j < nconv;) {
+      if (j_first < nkb && !xattn) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(j_first) * BK, tasks, 0, lane);
+      for (int j = j_first; j < nkb;) {
         const int jn = next_own(j + 1);
         const int st = j % STAGES;
         if (j >= STAGES) mbar_wait(&empty[st], ((j / STAGES) & 1) ^ 1, 34);
@@ -689,7 +613,7 @@ __global__ void __launch_bounds__(THREADS, 2)
             load_batch(b, p.ph.pro_src, p.ph.pro_ld, kblk(j) * BK, tasks, base, lane);
             store_batch(b, xs, tasks, base, lane, gelu);
           }
-          if (jn < nconv) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(jn) * BK, tasks, 0, lane);
+          if (jn < nkb) load_batch(nb, p.ph.pro_src, p.ph.pro_ld, kblk(jn) * BK, tasks, 0, lane);
         }
         fence_proxy_async();  // generic shared-memory writes -> tensor-core operand reads
         __syncwarp();
@@ -700,34 +624,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
         j = jn;
       }
-      if (hybrid) {  // X = bf16(pro_src) by every CTA, then the producer-only barrier
-        const int total = M * (p.K / 4);
-        const int nprod = min(ncta, (total + 127) / 128);
-        __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(p.ph.pro_dst);
-        for (int e = cta * 128 + tid; e < total; e += ncta * 128) {
-          const int t = e / (p.K / 4), c = (e - t * (p.K / 4)) * 4;
-          const float4 f = __ldcg(reinterpret_cast<const float4*>(p.ph.pro_src + (size_t)t * p.ph.pro_ld + c));
-          *reinterpret_cast<uint2*>(xb + (size_t)t * p.ph.pro_ldd + c) = pack_bf16x4(f.x, f.y, f.z, f.w);
-        }
-        const bool producer = cta < nprod;
-        if (producer) __threadfence();
-        epi_sync();
-        if (tid == 0) {
-          unsigned* ctr = p.ph.bar;
-          if (producer) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
-          while (ld_acquire(ctr) < (unsigned)nprod) __nanosleep(32);
-          *reinterpret_cast<volatile int*>(&s_pro_done) = 1;
-          if (atomicAdd(ctr + 1, 1u) == (unsigned)ncta - 1) {
-            ctr[0] = 0u;
-            ctr[1] = 0u;
-          }
-        }
-      }
       if (!dut) duties();
-      // the row statistics this CTA's epilogue needs, fetched once per CTA
-      // (warp w: rows 32w..32w+31) after the last conversion, ahead of the
-      // accumulator: off the epilogue's critical path and 4x fewer readers
-      if (xln && w * 32 < M) s_ms[w * 32 + lane] = row_stats(p.ph, w * 32, min(M, w * 32 + 32), lane);
     } else if (pro_mode != PROPD_PRO_NONE) {
       prologue_phase(p.ph, pro_mode, M, tid, cta, ncta);
       // only the CTAs that wrote X arrive (LN: one per row; GELU: one per 128
@@ -777,16 +674,6 @@ __global__ void __launch_bounds__(THREADS, 2)
       uint32_t rr[32];
       TMEM_LD32(lane_addr + c * 32, rr);
       tmem_wait_ld();
-      if (p.ph.pro_mode == PROPD_PRO_XLN) {  // LN by linearity: rstd_t (acc - mu_t c_f)
-        if (c == 0) epi_sync();  // s_ms complete
-        const float2 ms = s_ms[c * 32 + lane];
-        const float cf = __ldg(p.ph.colsum + (size_t)blockIdx.y * p.N + n0 + q4 * 32 + lane);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float mu = __shfl_sync(0xffffffffu, ms.x, i), rs = __shfl_sync(0xffffffffu, ms.y, i);
-          rr[i] = __float_as_uint(rs * (__uint_as_float(rr[i]) - mu * cf));
-        }
-      }
 #pragma unroll
       for (int i = 0; i < 32; ++i) tile[i * 36 + lane] = __uint_as_float(rr[i]);
       __syncwarp();
@@ -824,7 +711,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       if (tid == 0) grid_barrier(p.ph.bar + 2, (unsigned)ncta);
       epi_sync();
       tail_phase(p.Y, p.ldy, p.ph, M, tid, cta, ncta, s_rowdst);
-      if (cta < items) attn_run(p.ph, it, cta, p.Y, p.ldy, ring, abar, reinterpret_cast<float*>(s_ms), tid);
+      if (cta < items) attn_run(p.ph, it, cta, p.Y, p.ldy, ring, abar, s_attn, tid);
     }
   }
   tc_before_sync();
@@ -1063,19 +950,6 @@ static void split_k(int N, int K, int accumulate, int max_split, int* split_out,
   *per_out = per;
 }
 
-// Per-split column sums of W (PROPD_PRO_XLN's LayerNorm correction): one
-// thread per column, rows of split blockIdx.y in order.
-__global__ void colsum_kernel(int N, int K, int rows_per_split, const __nv_bfloat16* __restrict__ W, int ldw,
-                              float* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  const int k0 = blockIdx.y * rows_per_split, k1 = min(K, k0 + rows_per_split);
-  float s = 0.f;
-  for (int k = k0; k < k1; ++k) s += __bfloat162float(W[(size_t)k * ldw + n]);
-  out[(size_t)blockIdx.y * N + n] = s;
-}
-
 // ------------------------------------------------------------------ finish
 __global__ void qkv_finish_kernel(int A, int dh, int Lmax, float* __restrict__ acc, int ldacc,
                                   __nv_bfloat16* __restrict__ qkv, int ldqkv, const int32_t* __restrict__ row_seq,
@@ -1154,9 +1028,8 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
                     (ldy % 4 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0),
                 "gemm_ws: Y must be 16-byte aligned with ldy %% 4 == 0 (vector stores / reductions)");
   const int mp = ((M + 15) / 16) * 16;
-  const bool conv = ph != nullptr && (((ph->pro_mode == PROPD_PRO_XLN || ph->pro_mode == PROPD_PRO_XGELU) &&
-                                      ph->pro_dst == nullptr) ||  // (with pro_dst, X is also loaded by TMA)
-                                     ph->pro_mode == PROPD_PRO_XATTN);
+  const bool conv = ph != nullptr && ((ph->pro_mode == PROPD_PRO_XGELU && ph->pro_dst == nullptr) ||
+                                     ph->pro_mode == PROPD_PRO_XATTN);  // no X operand to load by TMA
   CUtensorMap wm, xm;
   memset(&xm, 0, sizeof(xm));  // unused when the CTAs convert X themselves
   PROPD_REQUIRE(gws::map2d(&wm, W, (uint64_t)K, (uint64_t)N, (uint64_t)ldw, 64) &&
@@ -1196,14 +1069,11 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
                        (reinterpret_cast<uintptr_t>(ph->attn_part) & 15) == 0 &&
                        gws::stages_for(mp) * (gws::A_BYTES + mp * 128) >= gws::ATT_OFF + 4 * gws::ACH_BYTES),
                   "gemm_ws: the fused attention needs the QKV tail, dh = 128, M * A * splits <= CTAs");
-    PROPD_REQUIRE(!(conv || ph->pro_mode == PROPD_PRO_XGELU || ph->pro_mode == PROPD_PRO_XLN) ||
+    PROPD_REQUIRE(!(conv || ph->pro_mode == PROPD_PRO_XGELU) ||
                       ph->pro_mode == PROPD_PRO_XATTN ||
                       (ph->pro_src && ph->pro_cols == K && ph->pro_ld % 4 == 0 &&
                             (reinterpret_cast<uintptr_t>(ph->pro_src) & 15) == 0),
                   "gemm_ws: converting prologues read 16-byte aligned fp32 rows of K columns");
-    PROPD_REQUIRE(ph->pro_mode != PROPD_PRO_XLN ||
-                      (ph->colsum && ph->stats_rec && ph->stats_cnt && K % gws::SUB == 0 && K / gws::SUB <= gws::MAX_SUB),
-                  "gemm_ws: PRO_XLN needs colsum, stats_rec, stats_cnt and K %% 256 == 0, K <= 8192");
     PROPD_REQUIRE(ph->zero_buf == nullptr || (ph->zero_cols % 4 == 0 && ph->zero_ld % 4 == 0 &&
                                               (reinterpret_cast<uintptr_t>(ph->zero_buf) & 15) == 0),
                   "gemm_ws: zero_buf rows must be float4-aligned");
@@ -1233,14 +1103,6 @@ int propd_ws_split_count(int N, int K) {
   int split, per;
   gws::split_k(N, K, 1, 0, &split, &per);
   return split;
-}
-
-int propd_ws_colsum(int N, int K, const void* W, int ldw, float* out, void* stream) {
-  PROPD_REQUIRE(N % gws::BF == 0 && K % gws::BK == 0, "ws_colsum: N=%d must be a multiple of 128, K=%d of 64", N, K);
-  int split, per;
-  gws::split_k(N, K, 1, 0, &split, &per);
-  return launch_pdl("ws_colsum", gws::colsum_kernel, dim3(N / gws::BF, split), dim3(gws::BF), 0, as_stream(stream),
-                    N, K, per * gws::BK, reinterpret_cast<const __nv_bfloat16*>(W), ldw, out);
 }
 
 int propd_qkv_finish(int M, const int32_t* rows_dev, int A, int dh, int Lmax, float* acc, int ldacc, void* qkv, int ldqkv,

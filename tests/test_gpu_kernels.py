@@ -522,10 +522,10 @@ def test_qkv_and_gelu_finish():
                                               (20, None, 2.0), (128, 32, 0.0), (128, 17, 0.0), (96, 30, 0.0)])
 def test_phased_layers_match_separate_kernels(rows, live, offset):
     """Layer stack with the LN / GELU prologues and the QKV tail inside the weight-streaming GEMMs
-    (propd_gemm_ws_ph: grid-barrier prologues, and the barrier-free converting prologues with LayerNorm
-    applied by linearity in the epilogue) == the same stack with separate add_ln / finish kernels: residual
+    (propd_gemm_ws_ph: grid-barrier prologues, and the GELU operand converted per ring stage inside every
+    CTA) == the same stack with separate add_ln / finish kernels: residual
     stream and the K/V rows written to the cache within bf16 rounding (the paths differ only in where the
-    bf16 conversions happen; `offset` shifts every row mean, the case LN-by-linearity must absorb)."""
+    bf16 conversions happen; `offset` shifts every row mean)."""
     from paper_2402_13485_b200 import B200Backend, TinyTransformerConfig
     from paper_2402_13485_b200.backend import Rows
 
@@ -542,8 +542,7 @@ def test_phased_layers_match_separate_kernels(rows, live, offset):
     x0 = torch.randn(n, 1024, device=DEV) + offset
     outs = []
     assert be.ws_conv, "the converting prologues should be on for H = 1024"
-    for phased, be.ws_conv, be.ws_conv_ln in ((False, False, False), (True, False, False), (True, True, False),
-                                              (True, True, True)):
+    for phased, be.ws_conv in ((False, False), (True, False), (True, True)):
         be.ws_phases = phased
         be.kcache.zero_()
         be.vcache.zero_()
@@ -559,10 +558,9 @@ def test_phased_layers_match_separate_kernels(rows, live, offset):
         assert (xa[:r] - xb[:r]).abs().max().item() <= 3e-2 * scale
         assert (ka - kb).abs().max().item() <= 3e-2 * max(1.0, ka.abs().max().item())
         assert (va - vb).abs().max().item() <= 3e-2 * max(1.0, va.abs().max().item())
-    # the barrier path leaves its scratch zeroed; the converting path zeroes the W_1 accumulator ahead (in
-    # the next QKV launch) and leaves the QKV launch's statistics counters reset by the last W_1 launch
+    # the barrier path leaves its scratch zeroed; the converting GELU path zeroes the W_1 accumulator
+    # ahead (in the next QKV launch), so only the barrier counters and the QKV accumulator are checked
     assert be._bar.abs().max().item() == 0 and be._acc.abs().max().item() == 0
-    assert be._st_cnt[0].abs().max().item() == 0 and be._st_cnt[1, :r].min().item() == 1024 // 256
 
 
 # --------------------------------------------------------------- probability pruning / typical acceptance
