@@ -201,7 +201,7 @@ class B200Backend:
             H = cfg.hidden
             self._qkv_ctas = (3 * H // 128) * self.lib.propd_ws_split_count(3 * H, H)
             self._attn_part = torch.empty(self._qkv_ctas * (4 + self.dh), device=dev, dtype=torch.float32)
-        self.device_rows = True  # sync-free post-prune pass when it fits the weight-streaming GEMMs
+        self.device_rows = os.environ.get("PROPD_DEVICE_ROWS", "1") != "0"  # sync-free post-prune pass ("0": host sync, A/B)
         self._graphs: dict = {}
         self._templates: dict = {}
         self._host: dict = {}

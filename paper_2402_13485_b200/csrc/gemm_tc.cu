@@ -126,6 +126,23 @@ __device__ __forceinline__ void epilogue32(const propd_gemm_epi& e, int split, i
   }
 }
 
+// K splits of a residual-add launch over `tiles` output tiles on `ctas`
+// persistent CTAs: minimises waves / split + a small per-split cost for the
+// reductions, >= 4 k-blocks per split, no empty split (host and device).
+__host__ __device__ inline int choose_split(int tiles, int kb, int ctas) {
+  int split = 1;
+  double best = 1e30;
+  for (int s = 1; s <= 8 && kb / s >= 4; ++s) {
+    const double cost = (double)((tiles * s + ctas - 1) / ctas) / s + 0.04 * (s - 1);
+    if (cost < best - 1e-9) {
+      best = cost;
+      split = s;
+    }
+  }
+  const int kper = (kb + split - 1) / split;
+  return (kb + kper - 1) / kper;
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap, Args p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -164,8 +181,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const unsigned long long t_wait = p.trace ? gtimer() : 0ull;
   const int M = p.rows_dev ? min(p.M, *p.rows_dev) : p.M;
   const int Mb = (M + BM - 1) / BM, Nb = (p.N + BN - 1) / BN, Kb = p.K / BK;
-  const int tiles = Mb * Nb, units = tiles * p.split;
-  const int kper = (Kb + p.split - 1) / p.split;  // k-blocks per split
+  const int tiles = Mb * Nb;
+  // a pass captured at a padded row capacity learns its live rows here: the
+  // residual-add split is chosen for them (the host's split assumed the capacity)
+  const int split = (p.rows_dev && p.epi.mode == PROPD_EPI_ADD_F32) ? choose_split(tiles, Kb, gridDim.x) : p.split;
+  const int units = tiles * split;
+  const int kper = (Kb + split - 1) / split;  // k-blocks per split
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
@@ -237,7 +258,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
           // with fewer than two units per CTA the residual add cannot hide a read-modify-write
           // behind the next tile's MMAs: fire-and-forget reductions (W_o at 1024 rows 56.6 -> 30.5 us)
-          epilogue32<__nv_bfloat16>(p.epi, units < 2 * (int)gridDim.x ? -1 : p.split, row, f0, v);
+          epilogue32<__nv_bfloat16>(p.epi, units < 2 * (int)gridDim.x ? -1 : split, row, f0, v);
         }
       }
       tc_before_sync();
@@ -412,23 +433,12 @@ int propd_gemm(int dtype, int M, const int32_t* rows_dev, int N, int K, const vo
   // per-split cost for the reductions, >= 4 k-blocks per split.  (A split
   // through an fp32 workspace for the other epilogues was measured slower:
   // the reductions and the last-split finish cost more than the wave fill.)
-  int split = 1;
-  if (epi->mode == PROPD_EPI_ADD_F32) {
-    const int kb = K / gtc::BK;
-    double best = 1e30;
-    for (int s = 1; s <= 8 && kb / s >= 4; ++s) {
-      const double cost = (double)((tiles * s + sms - 1) / sms) / s + 0.04 * (s - 1);
-      if (cost < best - 1e-9) {
-        best = cost;
-        split = s;
-      }
-    }
-    const int kper = (kb + split - 1) / split;
-    split = (kb + kper - 1) / kper;  // no empty split (the kernel derives kper from split the same way)
-  }
+  const int split = epi->mode == PROPD_EPI_ADD_F32 ? gtc::choose_split(tiles, K / gtc::BK, sms) : 1;
   gtc::Args p{M, N, K, split, rows_dev, *epi, g_dbg_trace, g_dbg_tag++};
   const int units = tiles * split;
-  const int grid = units < sms ? units : sms;
+  // with a device row count the residual-add split is re-chosen in the kernel
+  // for the live rows: launch every SM
+  const int grid = (rows_dev && epi->mode == PROPD_EPI_ADD_F32) || units >= sms ? sms : units;
   return launch_pdl("gemm(tcgen05)", gtc::gemm_tc_kernel, dim3(grid), dim3(gtc::THREADS), gtc::SMEM, st, xm, wm, p);
 }
 

@@ -6,7 +6,7 @@ backends.py:337-348).
 `B200Backend(dtype="bf16", use_graphs=True).step_tree` — the batched step the
 bench times (CUDA graphs, device row counts, transposed tcgen05 attention,
 weight-streaming tcgen05 projections, K3 early prune, K5 accept + KV
-compaction, the bonus pass on the streaming decode kernel) — runs next to
+compaction, the bonus pass with its attention fused into the QKV launches) — runs next to
 `oracle.TinyModel` on the same reference-initialised weights at hidden 4096,
 32 heads x 128, the prune layer strictly inside the stack.  The oracle
 follows the device's drafts, survivors and commits (oracle/parity.py), and
