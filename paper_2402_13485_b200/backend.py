@@ -202,6 +202,8 @@ class B200Backend:
             self._qkv_ctas = (3 * H // 128) * self.lib.propd_ws_split_count(3 * H, H)
             self._attn_part = torch.empty(self._qkv_ctas * (4 + self.dh), device=dev, dtype=torch.float32)
         self.device_rows = os.environ.get("PROPD_DEVICE_ROWS", "1") != "0"  # sync-free post-prune pass ("0": host sync, A/B)
+        # trees of > 128 rows: one survivor-count read per step selects the <= 128-row part B
+        self.ws_split_sync = os.environ.get("PROPD_SPLIT_SYNC", "1") != "0"
         self._graphs: dict = {}
         self._templates: dict = {}
         self._host: dict = {}
@@ -818,6 +820,31 @@ class B200Backend:
         self._pending_events.extend(ent[3])
         return ent[1]
 
+    def _precapture(self, key, fn) -> None:
+        """Graph mode: capture fn for key now (not replayed), so a variant the
+        step may switch to later is not captured inside a timed region."""
+        if not self.use_graphs:
+            return
+        full = key + (self.attn_timer is not None, self.mark_only, self.timeline is not None)
+        if full in self._graphs:
+            return
+        n0 = self.launches
+        try:
+            torch = self.torch
+            if self._cap_stream is None:
+                self._cap_stream = torch.cuda.Stream(self.device)
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            self._capturing, self._capture_events = True, []
+            try:
+                with torch.cuda.graph(g, pool=self._pool, stream=self._cap_stream):
+                    outs = fn()
+            finally:
+                self._capturing = False
+            self._graphs[full] = (g, outs, self.launches - n0, self._capture_events)
+        finally:
+            self.launches = n0  # nothing was launched
+
     def _bonus_program(self, seq_slot, bonus, B: int, max_keys: int, keep_logits: bool = False):
         """One committed row per sequence at position seq_len (backends.py:239-259
         for the bonus token): K/V append, hidden/root update, seq_len += 1."""
@@ -1031,6 +1058,15 @@ class B200Backend:
             S_pad = B * n
         elif device_rows:
             S_pad = cap
+            if cap > 128 and self.use_gws and self.ws_split_sync:
+                # survivors that fit the weight-streaming GEMMs (<= 128 rows: HBM-bound, ~1.5x the
+                # many-row GEMM there) get the 128-row variant of part B; one host read of the
+                # survivor count picks between the two captured variants (both captured up front)
+                fits = int(a["total"].item()) <= 128
+                S_pad = 128 if fits else cap
+                other = cap if fits else 128
+                self._precapture(("B", B, tmpl.paths, k, pkey, other, device_rows),
+                                 lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, other, device_rows, accept))
         else:
             S = int(a["total"].item())  # mid-step sync: row count of layers > p
             S_pad = self._s_bucket(S) if self.use_graphs else S
