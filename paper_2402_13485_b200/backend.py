@@ -1058,15 +1058,19 @@ class B200Backend:
             S_pad = B * n
         elif device_rows:
             S_pad = cap
-            if cap > 128 and self.use_gws and self.ws_split_sync:
+            if cap > 128 and self.use_gws and self.ws_split_sync:  # (at cap <= 128 the read costs what a tier gains)
                 # survivors that fit the weight-streaming GEMMs (<= 128 rows: HBM-bound, ~1.5x the
-                # many-row GEMM there) get the 128-row variant of part B; one host read of the
-                # survivor count picks between the two captured variants (both captured up front)
-                fits = int(a["total"].item()) <= 128
-                S_pad = 128 if fits else cap
-                other = cap if fits else 128
-                self._precapture(("B", B, tmpl.paths, k, pkey, other, device_rows),
-                                 lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, other, device_rows, accept))
+                # many-row GEMM there; <= 64 rows: a deeper weight ring) get a smaller part-B
+                # variant; one host read of the survivor count picks among the variants, all
+                # captured up front
+                tiers = [t for t in (64, 128) if t < cap] + [cap]
+                live = int(a["total"].item())
+                S_pad = next(t for t in tiers if live <= t)
+                for other in tiers:
+                    if other != S_pad:
+                        self._precapture(("B", B, tmpl.paths, k, pkey, other, device_rows),
+                                         lambda o=other: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, o,
+                                                                      device_rows, accept))
         else:
             S = int(a["total"].item())  # mid-step sync: row count of layers > p
             S_pad = self._s_bucket(S) if self.use_graphs else S
