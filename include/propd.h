@@ -176,7 +176,7 @@ int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, i
  *            a later launch zeroes it through zero_buf: rows [0, M) x
  *            zero_cols of zero_buf, stride zero_ld, zeroed after the launch's
  *            dependency wait).  With pro_dst = X (bf16, stride pro_ldd = ldx)
- *            given, launches with more than 16 live rows (or fewer than 4
+ *            given, launches with more than 20 live rows (or fewer than 4
  *            ring slots) run the PROPD_PRO_GELU grid-barrier phase instead
  *            (and re-zero pro_src). */
 #define PROPD_PRO_NONE 0

@@ -189,7 +189,7 @@ class B200Backend:
             self._acc2 = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32)
             self._bar = torch.zeros(32, device=dev, dtype=torch.int32)
         # W_2's GELU operand is converted per ring stage inside every CTA at
-        # <= 16 live rows (measured: 2-3 us per launch faster than the
+        # <= 20 live rows (measured: 2-3 us per launch faster than the
         # grid-barrier GELU phase at B=1); QKV then zeroes the W_1 accumulator
         # rows ahead (include/propd.h PROPD_PRO_XGELU)
         self.ws_conv = (self.ws_phases and os.environ.get("PROPD_WS_CONV", "1") != "0")  # "0": barrier GELU (A/B)
@@ -448,7 +448,7 @@ class B200Backend:
         ln = dict(pro_mode=_lib.PRO_LN, pro_src=ptr(x), pro_ld=H, pro_dst=ptr(h), pro_ldd=H, pro_cols=H, bar=bar)
         gelu = _lib.WsPhases(pro_mode=_lib.PRO_GELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g), pro_ldd=4 * H,
                              pro_cols=4 * H, bar=bar)
-        if self.ws_conv:  # converted per stage at <= 16 live rows, the barrier GELU phase into g above
+        if self.ws_conv:  # converted per stage at <= 20 live rows, the barrier GELU phase into g above
             gelu = _lib.WsPhases(pro_mode=_lib.PRO_XGELU, pro_src=ptr(acc2), pro_ld=4 * H, pro_dst=ptr(g),
                                  pro_ldd=4 * H, pro_cols=4 * H, bar=bar)
         zero_acc2 = dict(zero_buf=ptr(acc2), zero_ld=4 * H, zero_cols=4 * H) if self.ws_conv else {}

@@ -390,13 +390,14 @@ __device__ __forceinline__ uint4 cvt8(float4 a, float4 b, bool gelu) {
 // (load_batch) into registers as soon as the warp's previous stage is done,
 // so its L2 latency (the N-tiles of a split all read the same lines) hides
 // behind the wait for the ring slot; further batches (M > 16) load in place.
+constexpr int XB = 5;  // tasks per lane per batch: one batch covers <= 20 rows
 struct XBatch {
-  float4 v[4][2];
+  float4 v[XB][2];
 };
 __device__ __forceinline__ void load_batch(XBatch& b, const float* __restrict__ src, int ld, int k0, int tasks,
                                            int base, int lane) {
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < XB; ++u) {
     const int task = base + u * 32 + lane;
     if (task < tasks) {
       const float4* g = reinterpret_cast<const float4*>(src + (size_t)(task >> 3) * ld + k0 + (task & 7) * 8);
@@ -407,7 +408,7 @@ __device__ __forceinline__ void load_batch(XBatch& b, const float* __restrict__ 
 }
 __device__ __forceinline__ void store_batch(const XBatch& b, uint8_t* xs, int tasks, int base, int lane, bool gelu) {
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < XB; ++u) {
     const int task = base + u * 32 + lane;
     if (task < tasks) {
       const int t = task >> 3, c = task & 7;
@@ -496,11 +497,11 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int M = p.m_dev ? min(p.M, *p.m_dev) : p.M;
   const int nbox = max(1, (M + 15) >> 4);
   const int cta = blockIdx.y * gridDim.x + blockIdx.x, ncta = gridDim.x * gridDim.y;
-  // PROPD_PRO_XGELU converts in-CTA at <= 16 live rows (one task batch per
+  // PROPD_PRO_XGELU converts in-CTA at <= 20 live rows (one task batch per
   // stage); above that, when a bf16 X buffer is given, it runs the
   // grid-barrier GELU phase instead (measured at 32 rows: 39 vs 32 us for W_2)
   const bool conv = p.ph.pro_mode == PROPD_PRO_XATTN ||
-                    (p.ph.pro_mode == PROPD_PRO_XGELU && ((M <= 16 && STAGES >= 4) || p.ph.pro_dst == nullptr));
+                    (p.ph.pro_mode == PROPD_PRO_XGELU && ((M <= 20 && STAGES >= 4) || p.ph.pro_dst == nullptr));
   const int pro_mode = (p.ph.pro_mode == PROPD_PRO_XGELU && !conv) ? PROPD_PRO_GELU : p.ph.pro_mode;
   const bool two_arrivals = conv_mode(p.ph.pro_mode);  // full[] was initialised for 2 arrivals
   if (warp == 0) {
@@ -608,7 +609,7 @@ __global__ void __launch_bounds__(THREADS, 2)
           xattn_stage(p.ph, kblk(j) * BK, M, xs, lane);
         } else {
           store_batch(nb, xs, tasks, 0, lane, gelu);
-          for (int base = 128; base < tasks; base += 128) {
+          for (int base = 32 * XB; base < tasks; base += 32 * XB) {
             XBatch b;
             load_batch(b, p.ph.pro_src, p.ph.pro_ld, kblk(j) * BK, tasks, base, lane);
             store_batch(b, xs, tasks, base, lane, gelu);
