@@ -183,7 +183,7 @@ class B200Backend:
         call("propd_prepare")
         # the phases meet at grid barriers: only when the split-K grids (<= 2
         # CTAs per SM) are confirmed co-resident on this device
-        self.ws_phases = (self.use_gws and cfg.hidden <= 4096 and
+        self.ws_phases = (self.use_gws and cfg.hidden <= 4096 and os.environ.get("PROPD_WS_PHASES", "1") != "0" and
                           self.lib.propd_gemm_ws_barrier_ctas() >= 2 * self.lib.propd_num_sms())
         if self.ws_phases:
             self._acc2 = torch.zeros(128, 4 * cfg.hidden, device=dev, dtype=torch.float32)
