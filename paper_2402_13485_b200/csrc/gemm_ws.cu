@@ -10,9 +10,17 @@
 // ~2 CTAs per SM stream weights; partial sums are reduced with fp32
 // red.global.add into Y (for W_o / W_2 that is the fp32 residual stream
 // itself, which fuses the residual add).  With one split the tile is stored.
-// Finish kernels turn fp32 accumulators into the bf16 operands of the next
-// op: QKV (+ K/V scattered into the cache, replacing kv_append) and
-// W1 (+ tanh-GELU), re-zeroing the accumulator for the next use.
+// Every weight load carries an L2 evict-first policy (each weight byte is
+// read once per pass; activations, accumulators and K/V stay in L2).
+//
+// In-kernel phases (propd_ws_phases, include/propd.h) replace the small
+// kernels between the projections of a layer: LN / GELU prologues behind a
+// producer-only grid barrier while the weight ring fills, the QKV tail (fp32
+// accumulator -> bf16 Q and K/V cache rows) behind a grid barrier, W_2's GELU
+// operand converted per ring stage inside every CTA at <= 20 rows, and for
+// one-row passes the attention itself (QKV tail) with its key-split combine in
+// W_o's prologue.  Finish kernels (qkv_finish, gelu_finish) serve the
+// unphased layer path (H > 4096).
 #include <cstring>
 #include <unordered_map>
 
