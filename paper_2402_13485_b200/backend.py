@@ -946,7 +946,10 @@ class B200Backend:
                    ptr(o["total"]), st)
         return o
 
-    def _part_b(self, B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows=False, accept=None):
+    def _part_b(self, B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows=False, accept=None, row_cap=None):
+        """Layers p+1..Ly over the survivors (row capacity S_pad; at most
+        row_cap survivors per sequence, default the tree size), LM argmax, K5
+        accept + KV compaction, bonus pass."""
         torch, st, cfg = self.torch, self.stream(), self.config
         n, D, H = len(tmpl), cfg.draft_heads, self.H
         dev = self.device
@@ -958,8 +961,9 @@ class B200Backend:
                        ptr(a["noff"]), st)
             x = torch.empty(S_pad, H, device=dev, dtype=torch.float32)
             self._call("propd_gather_rows", 0, S_pad, H, ptr(a["x"]), ptr(a["nsrc"]), ptr(x), st)
-            rt = Rows(S_pad, B + 1, slot_buf, a["nrs"], a["nrn"], a["noff"], max_keys=kb, max_rows=n,
-                      live=a["total"] if device_rows else None, scratch_last=True)
+            rt = Rows(S_pad, B + 1, slot_buf, a["nrs"], a["nrn"], a["noff"], max_keys=kb,
+                      max_rows=min(n, row_cap) if row_cap else n, live=a["total"] if device_rows else None,
+                      scratch_last=True)
             pending = self._run_layers(x, rt, prune.layer, cfg.layers, td["mask"], n, tmpl.words)
             alive, node_row = a["alive"], a["node_row"]
         else:
@@ -1054,6 +1058,7 @@ class B200Backend:
         # mid-step sync; device_rows=False sizes it on the host instead.
         cap = self._s_bucket(B * n)
         device_rows = prune is not None and self.device_rows
+        row_cap = None  # survivors per sequence bound of part B (None: the tree size)
         if prune is None:
             S_pad = B * n
         elif device_rows:
@@ -1063,20 +1068,25 @@ class B200Backend:
                 # many-row GEMM there; <= 64 rows: a deeper weight ring) get a smaller part-B
                 # variant; one host read of the survivor count picks among the variants, all
                 # captured up front
+                # the same read gives the largest survivor count of a sequence: <= 32 lets the
+                # tree attention run 32-row tiles (two CTAs per SM where one would need two waves)
                 tiers = [t for t in (64, 128) if t < cap] + [cap]
-                live = int(a["total"].item())
+                caps = [32, n] if n > 32 else [n]
+                live, most = (int(v) for v in self.torch.stack([a["total"][0], a["surv_cnt"].max()]).cpu())
                 S_pad = next(t for t in tiers if live <= t)
+                row_cap = next(c for c in caps if most <= c)
                 for other in tiers:
-                    if other != S_pad:
-                        self._precapture(("B", B, tmpl.paths, k, pkey, other, device_rows),
-                                         lambda o=other: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, o,
-                                                                      device_rows, accept))
+                    for oc in caps:
+                        if (other, oc) != (S_pad, row_cap):
+                            self._precapture(("B", B, tmpl.paths, k, pkey, other, device_rows, oc),
+                                             lambda o=other, c=oc: self._part_b(B, tmpl, k, prune, slot_buf, kb, a,
+                                                                                o, device_rows, accept, c))
         else:
             S = int(a["total"].item())  # mid-step sync: row count of layers > p
             S_pad = self._s_bucket(S) if self.use_graphs else S
         self._role = "tree_pruned"
-        b = self._run(("B", B, tmpl.paths, k, pkey, S_pad, device_rows),
-                      lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows, accept))
+        b = self._run(("B", B, tmpl.paths, k, pkey, S_pad, device_rows, row_cap),
+                      lambda: self._part_b(B, tmpl, k, prune, slot_buf, kb, a, S_pad, device_rows, accept, row_cap))
         if stats is not None:  # single process: replay this batch's records right away (K4)
             P, counts, alpha, order_dev, lcurve_dev = stats
             self.stats_replay_select(b["ranks"], B, P, counts, alpha, order_dev, lcurve_dev)

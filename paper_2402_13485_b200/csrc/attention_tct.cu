@@ -34,17 +34,21 @@ using namespace propd::tc;
 
 constexpr int BK = 128;   // keys per block (M of S^T)
 constexpr int DH = 128;
-constexpr int KS = 3, VS = 3;  // K / V ring stages (32 KB each)
-static_assert(KS == VS, "the first ring fill assumes equal K and V rings");
 constexpr int NSB = 4;         // S^T buffers in TMEM (S runs up to NSB blocks ahead of PV)
 constexpr int MAX_SPLIT = 8;
 constexpr int KV_HALF = BK * 128;     // [128 keys x 64 dims] SW128 = 16 KB
 constexpr int KV_TILE = 2 * KV_HALF;  // 32 KB
 
-// Shared-memory / TMEM plan for NR query rows per tile (32 or 64).
-template <int NR_>
+// Shared-memory / TMEM plan for NR query rows per tile (32 or 64) and RING
+// K / V ring stages (32 KB each): 3 with one CTA per SM; 1 with two CTAs per
+// SM (32 rows: 90 KB, 256 TMEM columns, <= 146 registers), which runs the
+// 149-296-tile launches in one wave instead of two (B = 5-9 at 32 heads).
+template <int NR_, int RING = 3>
 struct Cfg {
   static constexpr int NR = NR_;
+  static constexpr int KS = RING, VS = RING;
+  static constexpr int MINB = RING == 1 ? 2 : 1;  // CTAs per SM (launch bounds)
+  static_assert(RING >= 3 || NR == 32, "two CTAs per SM: 32-row tiles only");
   static constexpr int NH = NR / 32;             // softmax warpgroups, one per 32-row half
   static constexpr int NPB = NR == 32 ? 2 : 1;   // P^T buffers (one at 64 rows: shared memory)
   static constexpr int VWARP = 2 + 4 * NH;       // V producer warp (after the softmax warps)
@@ -184,16 +188,16 @@ __device__ __forceinline__ void lane_transpose_reduce(float (&t)[32], int lane) 
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, 1)
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
     attn_tct_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, Args p) {
   constexpr int NR = C::NR, NH = C::NH, NPB = C::NPB;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::SMEM_BAR);
   uint64_t* k_full = bars;
-  uint64_t* k_empty = k_full + KS;
-  uint64_t* v_full = k_empty + KS;
-  uint64_t* v_empty = v_full + VS;
-  uint64_t* s_full = v_empty + VS;   // [NSB]
+  uint64_t* k_empty = k_full + C::KS;
+  uint64_t* v_full = k_empty + C::KS;
+  uint64_t* v_empty = v_full + C::VS;
+  uint64_t* s_full = v_empty + C::VS;   // [NSB]
   uint64_t* p_full = s_full + NSB;   // [NPB]
   uint64_t* pv_done = p_full + NPB;  // [NPB]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + NPB);
@@ -202,16 +206,16 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   // development timeline (first S seen, softmax loop end): the tail of the
   // barrier block (static shared memory would push the 64-row plan past 227 KB)
   unsigned long long* s_t = reinterpret_cast<unsigned long long*>(smem + C::SMEM_BAR + 176);
-  static_assert(8 * (2 * KS + 2 * VS + NSB + 2 * C::NPB) + 4 <= 176, "barrier block");
+  static_assert(8 * (2 * C::KS + 2 * C::VS + NSB + 2 * C::NPB) + 4 <= 176, "barrier block");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // independent of the predecessor: barriers, tensor-map prefetch
   if (threadIdx.x == 0) {
-    for (int i = 0; i < KS; ++i) {
+    for (int i = 0; i < C::KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
     }
-    for (int i = 0; i < VS; ++i) {
+    for (int i = 0; i < C::VS; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   // the first ring fill goes out before anything else (its latency overlaps
   // the Q load, the TMEM allocation and the block-wide sync)
   const bool producer = (warp == 0 || warp == C::VWARP) && lane == 0;
-  const int npre = min(KS, nblk);  // KS == VS
+  const int npre = min(C::KS, nblk);  // C::KS == C::VS
   if (producer) {
     const bool isk = warp == 0;
     uint64_t* full = isk ? k_full : v_full;
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     // ================= TMA producers: warp 0 streams K, warp VWARP streams V =================
     if (lane == 0) {
       const bool isk = warp == 0;
-      const int NS = isk ? KS : VS;
+      const int NS = isk ? C::KS : C::VS;
       uint64_t* full = isk ? k_full : v_full;
       uint64_t* empty = isk ? k_empty : v_empty;
       const CUtensorMap* map = isk ? &kmap : &vmap;
@@ -333,8 +337,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       uint32_t idle = 0;
       while (np < nblk) {
         bool prog = false;
-        if (ns < nblk && ns < np + NSB && mbar_try(&k_full[ns % KS], (ns / KS) & 1)) {
-          const int st = ns % KS;
+        if (ns < nblk && ns < np + NSB && mbar_try(&k_full[ns % C::KS], (ns / C::KS) & 1)) {
+          const int st = ns % C::KS;
           tc_after_sync();
           const uint32_t k_addr = smem_u32(smem + C::SMEM_K + st * KV_TILE);
 #pragma unroll
@@ -349,8 +353,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           prog = true;
         }
         if (np < ns) {
-          const int st = np % VS, pb = np % NPB;
-          if (mbar_try(&p_full[pb], (np / NPB) & 1) && mbar_try(&v_full[st], (np / VS) & 1)) {
+          const int st = np % C::VS, pb = np % NPB;
+          if (mbar_try(&p_full[pb], (np / NPB) & 1) && mbar_try(&v_full[st], (np / C::VS) & 1)) {
             tc_after_sync();
             const uint32_t v_addr = smem_u32(smem + C::SMEM_V + st * KV_TILE);
             const uint32_t p_addr = smem_u32(smem + C::SMEM_P + pb * C::P_TILE);
@@ -575,6 +579,9 @@ static int tct_launch(const CUtensorMap& km, const CUtensorMap& vm, const tct::A
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tct::attn_tct_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::SMEM_TOTAL);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(tct::attn_tct_kernel<C>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return fail("prepare(tcT): %s", cudaGetErrorString(e));
     attr = true;
   }
@@ -624,6 +631,11 @@ int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows
   const uint64_t rows = (uint64_t)n_slots * A * Lmax;
   if (!tct::kv_map128(&km, kc, rows) || !tct::kv_map128(&vm, vc, rows)) return 0;
   const int ctas = Bg * A;  // sequences with a KV cache (Bg <= B)
+  // <= 32-row tiles whose one-CTA-per-SM launch would need two waves: the
+  // 1-stage shape at two CTAs per SM
+  static const int two_override = env_int("PROPD_TCT_TWO");  // -1: never (A/B)
+  const bool two = two_override != -1 && max_rows_per_seq <= 32 && ctas > propd_num_sms() &&
+                   ctas <= 2 * propd_num_sms();
   // key splits per (sequence, head), one cluster each (<= 8): one wave of one
   // CTA per SM at small batch; split boundaries on 64-key multiples (a
   // split's last 128-key block may be partly masked)
@@ -655,6 +667,7 @@ int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows
   p.tl = g_dbg_trace;
   p.tag = g_dbg_tag++;
   *handled = true;
+  if (two) return tct_launch<tct::Cfg<32, 1>>(km, vm, p, nsplit, A, B, st);
   return max_rows_per_seq <= 32 ? tct_launch<tct::Cfg<32>>(km, vm, p, nsplit, A, B, st)
                                 : tct_launch<tct::Cfg<64>>(km, vm, p, nsplit, A, B, st);
 }
