@@ -41,8 +41,9 @@ constexpr int KV_TILE = 2 * KV_HALF;  // 32 KB
 
 // Shared-memory / TMEM plan for NR query rows per tile (32 or 64) and RING
 // K / V ring stages (32 KB each): 3 with one CTA per SM; 1 with two CTAs per
-// SM (32 rows: 90 KB, 256 TMEM columns, <= 146 registers), which runs the
-// 149-296-tile launches in one wave instead of two (B = 5-9 at 32 heads).
+// SM (32 rows: 90 KB, 256 TMEM columns, <= 146 registers) for launches of
+// more tiles than SMs (one wave instead of two at B = 5-9, and the other CTA of
+// an SM hides each CTA's exposed K/V latency at larger batch).
 template <int NR_, int RING = 3>
 struct Cfg {
   static constexpr int NR = NR_;
@@ -631,11 +632,11 @@ int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows
   const uint64_t rows = (uint64_t)n_slots * A * Lmax;
   if (!tct::kv_map128(&km, kc, rows) || !tct::kv_map128(&vm, vc, rows)) return 0;
   const int ctas = Bg * A;  // sequences with a KV cache (Bg <= B)
-  // <= 32-row tiles whose one-CTA-per-SM launch would need two waves: the
-  // 1-stage shape at two CTAs per SM
-  static const int two_override = env_int("PROPD_TCT_TWO");  // -1: never (A/B)
-  const bool two = two_override != -1 && max_rows_per_seq <= 32 && ctas > propd_num_sms() &&
-                   ctas <= 2 * propd_num_sms();
+  // <= 32-row tiles over more tiles than SMs: the 1-stage shape at two CTAs per SM
+  static const int two_override = env_int("PROPD_TCT_TWO");  // -1: never, 1: whenever the tiles fit (A/B)
+  // (measured, scripts/attn_probe.py at 16 rows: 0.58 -> 0.75 of the copy peak at B=8 / KV 1024, 0.74 -> 0.91
+  // at B=64 / KV 1024, 1.04 -> 1.08 at B=64 / KV 4096; equal at B=1)
+  const bool two = two_override != -1 && max_rows_per_seq <= 32 && (two_override == 1 || ctas > propd_num_sms());
   // key splits per (sequence, head), one cluster each (<= 8): one wave of one
   // CTA per SM at small batch; split boundaries on 64-key multiples (a
   // split's last 128-key block may be partly masked)
