@@ -792,30 +792,38 @@ class B200Backend:
             ent[2] = key
         return buf
 
+    def _graph_key(self, key) -> tuple:
+        # graphs with K2 timing event nodes are kept apart from clean ones
+        # (an event node between two kernels also breaks their PDL overlap)
+        return key + (self.attn_timer is not None, self.mark_only, self.timeline is not None)
+
+    def _capture(self, full_key, fn):
+        """Capture fn into a CUDA graph under full_key (nothing is launched)."""
+        torch = self.torch
+        n0 = self.launches
+        if self._cap_stream is None:
+            self._cap_stream = torch.cuda.Stream(self.device)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        self._capturing, self._capture_events = True, []
+        try:
+            with torch.cuda.graph(g, pool=self._pool, stream=self._cap_stream):
+                outs = fn()
+        finally:
+            self._capturing = False
+        ent = self._graphs[full_key] = (g, outs, self.launches - n0, self._capture_events)
+        self.launches = n0  # counted when replayed
+        return ent
+
     def _run(self, key, fn):
         """Eager: run fn.  Graph mode: capture fn once per key, then replay."""
         if not self.use_graphs:
             return fn()
-        # graphs with K2 timing event nodes are kept apart from clean ones
-        # (an event node between two kernels also breaks their PDL overlap)
-        key = key + (self.attn_timer is not None, self.mark_only, self.timeline is not None)
-        ent = self._graphs.get(key)
+        full = self._graph_key(key)
+        ent = self._graphs.get(full)
         if ent is None:
-            torch = self.torch
-            n0 = self.launches
-            if self._cap_stream is None:
-                self._cap_stream = torch.cuda.Stream(self.device)
-            torch.cuda.synchronize(self.device)
-            g = torch.cuda.CUDAGraph()
-            self._capturing, self._capture_events = True, []
-            try:
-                with torch.cuda.graph(g, pool=self._pool, stream=self._cap_stream):
-                    outs = fn()
-            finally:
-                self._capturing = False
-            ent = self._graphs[key] = (g, outs, self.launches - n0, self._capture_events)
-        else:
-            self.launches += ent[2]
+            ent = self._capture(full, fn)
+        self.launches += ent[2]
         ent[0].replay()
         self._pending_events.extend(ent[3])
         return ent[1]
@@ -823,27 +831,8 @@ class B200Backend:
     def _precapture(self, key, fn) -> None:
         """Graph mode: capture fn for key now (not replayed), so a variant the
         step may switch to later is not captured inside a timed region."""
-        if not self.use_graphs:
-            return
-        full = key + (self.attn_timer is not None, self.mark_only, self.timeline is not None)
-        if full in self._graphs:
-            return
-        n0 = self.launches
-        try:
-            torch = self.torch
-            if self._cap_stream is None:
-                self._cap_stream = torch.cuda.Stream(self.device)
-            torch.cuda.synchronize(self.device)
-            g = torch.cuda.CUDAGraph()
-            self._capturing, self._capture_events = True, []
-            try:
-                with torch.cuda.graph(g, pool=self._pool, stream=self._cap_stream):
-                    outs = fn()
-            finally:
-                self._capturing = False
-            self._graphs[full] = (g, outs, self.launches - n0, self._capture_events)
-        finally:
-            self.launches = n0  # nothing was launched
+        if self.use_graphs and self._graph_key(key) not in self._graphs:
+            self._capture(self._graph_key(key), fn)
 
     def _bonus_program(self, seq_slot, bonus, B: int, max_keys: int, keep_logits: bool = False):
         """One committed row per sequence at position seq_len (backends.py:239-259
