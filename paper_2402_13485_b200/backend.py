@@ -1064,6 +1064,7 @@ class B200Backend:
                 live, most = (int(v) for v in self.torch.stack([a["total"][0], a["surv_cnt"].max()]).cpu())
                 S_pad = next(t for t in tiers if live <= t)
                 row_cap = next(c for c in caps if most <= c)
+                self._role = "tree_pruned"  # (role of the timing events the variants record)
                 for other in tiers:
                     for oc in caps:
                         if (other, oc) != (S_pad, row_cap):
