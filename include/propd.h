@@ -161,7 +161,9 @@ int propd_gemm_ws(int M, const int32_t* rows_dev, int N, int K, const void* X, i
  * between projections, so a layer is five launches and the weight stream of
  * a launch keeps flowing while its prologue runs:
  *   prologue PROPD_PRO_LN:   X[t] = bf16(LN(pro_src[t])) (no affine, eps 1e-5,
- *            population variance; backends.py:135-142), pro_cols = K <= 4096
+ *            population variance; backends.py:135-142), pro_cols = K <= 4096;
+ *            at <= 2 live rows every CTA normalises them itself and writes its
+ *            own k-range of X (no grid barrier)
  *   prologue PROPD_PRO_GELU: X = bf16(tanh-GELU(pro_src)), pro_src re-zeroed
  *            (the previous launch's split-K accumulator)
  *   (X = pro_dst must be this launch's X operand, row stride pro_ldd = ldx)

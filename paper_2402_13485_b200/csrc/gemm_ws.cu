@@ -77,7 +77,7 @@ __device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d)
 //   GELU: X = bf16(tanh-GELU(src)), src re-zeroed (the split-K accumulator of
 //         the previous launch)
 __device__ __forceinline__ void prologue_phase(const propd_ws_phases& ph, int mode, int M, int tid, int cta,
-                                               int ncta) {
+                                               int ncta, int k_lo = 0, int k_hi = 1 << 30) {
   __shared__ float red[2][4];
   __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ph.pro_dst);
   const int C = ph.pro_cols;
@@ -117,7 +117,7 @@ __device__ __forceinline__ void prologue_phase(const propd_ws_phases& ph, int mo
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int c = (i * 128 + tid) * 4;
-        if (c < C)
+        if (c < C && c >= k_lo && c < k_hi)
           *reinterpret_cast<uint2*>(o + c) = pack_bf16x4((v[4 * i] - mu) * inv, (v[4 * i + 1] - mu) * inv,
                                                          (v[4 * i + 2] - mu) * inv, (v[4 * i + 3] - mu) * inv);
       }
@@ -634,6 +634,15 @@ __global__ void __launch_bounds__(THREADS, 2)
         j = jn;
       }
       if (!dut) duties();
+    } else if (pro_mode == PROPD_PRO_LN && M <= 2) {
+      // one or two rows: every CTA normalises them itself (full-row
+      // statistics from L2) and writes only its own k-range of X, which its
+      // own TMA loads read next: no grid barrier (the CTAs of a split write
+      // identical values to the same addresses)
+      prologue_phase(p.ph, pro_mode, M, tid, 0, 1, kb0 * BK, (kb0 + nkb) * BK);
+      __threadfence();
+      epi_sync();
+      if (tid == 0) *reinterpret_cast<volatile int*>(&s_pro_done) = 1;
     } else if (pro_mode != PROPD_PRO_NONE) {
       prologue_phase(p.ph, pro_mode, M, tid, cta, ncta);
       // only the CTAs that wrote X arrive (LN: one per row; GELU: one per 128
