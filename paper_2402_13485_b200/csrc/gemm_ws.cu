@@ -164,7 +164,10 @@ __device__ __forceinline__ void tail_rows(const propd_ws_phases& ph, int M, int 
 }
 __device__ __forceinline__ void tail_phase(float* Y, int ldy, const propd_ws_phases& ph, int M, int tid, int cta,
                                            int ncta, const int2* rowdst) {
-  const int H = ph.A * ph.dh, per_row = 3 * H / 4, total = M * per_row, stride = ncta * 128;
+  // with the fused one-row attention the Q columns stay in Y (the attention
+  // reads them there): only the K / V columns are converted
+  const int H = ph.A * ph.dh, c0 = ph.attn_splits ? H : 0;
+  const int per_row = (3 * H - c0) / 4, total = M * per_row, stride = ncta * 128;
   __nv_bfloat16* q = reinterpret_cast<__nv_bfloat16*>(ph.tail_q);
   for (int e0 = cta * 128 + tid; e0 < total; e0 += 4 * stride) {
     float4 f[4];
@@ -173,14 +176,14 @@ __device__ __forceinline__ void tail_phase(float* Y, int ldy, const propd_ws_pha
       const int e = e0 + u * stride;
       if (e < total) {
         const int t = e / per_row;
-        f[u] = __ldcg(reinterpret_cast<const float4*>(Y + (size_t)t * ldy) + (e - t * per_row));
+        f[u] = __ldcg(reinterpret_cast<const float4*>(Y + (size_t)t * ldy + c0) + (e - t * per_row));
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = e0 + u * stride;
       if (e >= total) continue;
-      const int t = e / per_row, c = (e - t * per_row) * 4;
+      const int t = e / per_row, c = c0 + (e - t * per_row) * 4;
       if (ph.attn_splits == 0)  // (with the fused attention, Y is read after the tail and zeroed by W_o)
         *reinterpret_cast<float4*>(Y + (size_t)t * ldy + c) = make_float4(0.f, 0.f, 0.f, 0.f);
       const uint2 pk = pack_bf16x4(f[u].x, f[u].y, f[u].z, f[u].w);
