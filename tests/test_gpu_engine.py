@@ -263,6 +263,34 @@ def test_sync_free_post_prune_pass_matches_synced_pass():
         assert np.array_equal(a.committed, b.committed) and np.array_equal(a.acc_len, b.acc_len)
 
 
+def test_survivor_tier_variants_match_full_capacity_pass():
+    """bf16 at 7B width, B=4 with a 64-node tree (256 pre-prune rows): the part-B variant chosen from the
+    step's survivor-count read (<= 64 / 128 rows on the weight-streaming GEMMs, 32-row attention tiles
+    when no sequence has more than 32 survivors) against the full-capacity variant (many-row GEMM, 64-row
+    tiles).  Structural outputs bit-exact; argmax of the surviving rows >= 95% equal (fp32 reduction order
+    differs between the two GEMM paths)."""
+    cfg = TinyTransformerConfig(layers=3, hidden=4096, heads=32, vocab=32000, draft_heads=4, max_positions=512, seed=3)
+    tmpl = TreeTemplate.from_paths(op.grid_candidates(4, 16))
+    outs = []
+    for split_sync in (True, False):
+        be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=4, max_tree=64, use_graphs=True)
+        be.ws_split_sync = split_sync
+        states = be.synthetic_states(4, 300, seed=6)
+        outs.append(be.step_tree(states, tmpl, 16, prune=PruneConfig(1, 50), trace=True))
+        if split_sync:  # the tiered variants were captured up front
+            assert sum(1 for key in be._graphs if key[0] == "B") >= 2
+        del be
+    a, b = outs
+    assert np.array_equal(a.trace["alive"], b.trace["alive"])
+    assert np.array_equal(a.surv_cnt, b.surv_cnt)
+    alive = a.trace["alive"].astype(bool)
+    ra = a.trace["row_argmax"][a.trace["node_row"][alive]]
+    rb = b.trace["row_argmax"][b.trace["node_row"][alive]]
+    assert (ra == rb).mean() >= 0.95
+    if np.array_equal(ra, rb):
+        assert np.array_equal(a.committed, b.committed) and np.array_equal(a.acc_len, b.acc_len)
+
+
 @pytest.mark.parametrize("mode", ["static_tree", "propd_full"])
 def test_planted_acceptance_matches_oracle(mode):
     """Planted-acceptance harness: draft head 0 := the LM head on the same seeded weights for

@@ -785,14 +785,16 @@ def test_gemm_device_row_count(live):
 
 
 # --------------------------------------------------------------- fused one-row attention
-@pytest.mark.parametrize("B,L", [(1, 300), (3, 517), (4, 70), (2, 1024), (1, 1030)])
-def test_fused_bonus_attention_matches_decode_kernel(B, L):
+@pytest.mark.parametrize("B,L,hidden,heads", [(1, 300, 1024, 8), (3, 517, 1024, 8), (4, 70, 1024, 8),
+                                              (2, 1024, 1024, 8), (1, 1030, 1024, 8), (1, 1024, 4096, 32)])
+def test_fused_bonus_attention_matches_decode_kernel(B, L, hidden, heads):
     """Bonus pass with the attention inside the QKV launch (key-split partials, combined in W_o's
     converting prologue) == the same pass with the decode attention kernel: final hidden rows, the
     root argmax and the appended K/V rows within bf16 rounding (backends.py:239-259)."""
     from paper_2402_13485_b200 import B200Backend, TinyTransformerConfig
 
-    cfg = TinyTransformerConfig(layers=3, hidden=1024, heads=8, vocab=1024, draft_heads=2, max_positions=1100, seed=2)
+    cfg = TinyTransformerConfig(layers=3 if hidden <= 1024 else 2, hidden=hidden, heads=heads, vocab=1024,
+                                draft_heads=2, max_positions=1100, seed=2)
     be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=4, max_tree=16)
     assert be.ws_fuse_attn
     states = be.synthetic_states(B, L, seed=B)
