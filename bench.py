@@ -340,13 +340,22 @@ def bonus_attn_bytes(be, m) -> float:
     return be.num_layers * (2 * keys + 2 * B) * be.H * elt
 
 
-def timeline_step(be, eng, seqs, prime, dev, prune_layer):
+def modal_size(metrics):
+    """Most frequent tree size of the timed steps (None without steps)."""
+    sizes = [x.tree_size for x in metrics]
+    return max(set(sizes), key=sizes.count) if sizes else None
+
+
+def timeline_step(be, eng, seqs, prime, dev, prune_layer, tree_size=None):
     """One step with per-CTA globaltimer records (graphs captured with the
     trace on): busy time of each kernel family inside the PDL-chained step =
     union over its launches of [dependency release, last CTA exit]; GEMM bytes
     from the shapes in the trace records (weight stages streamed before a
     launch's release are left out of its window's bytes: conservative),
-    attention bytes from the step's metrics."""
+    attention bytes from the step's metrics.  tree_size: the timed steps'
+    (modal) tree size — the dynamic plan may have moved since, so up to 12
+    steps are traced until one has that size (`traced_tree_size` reports the
+    size of the step actually traced)."""
     import ctypes
 
     import numpy as np
@@ -360,19 +369,22 @@ def timeline_step(be, eng, seqs, prime, dev, prune_layer):
     be.timeline = buf
     try:
         prime()
-        torch.cuda.synchronize()
-        buf[0] = 0
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record()
-        m = eng._step(seqs, 10 ** 9)
-        t1.record()
-        torch.cuda.synchronize()
+        for _ in range(12):
+            torch.cuda.synchronize()
+            buf[0] = 0
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            m = eng._step(seqs, 10 ** 9)
+            t1.record()
+            torch.cuda.synchronize()
+            if tree_size is None or m.tree_size == tree_size:
+                break
     finally:
         lib.propd_debug_timeline(ctypes.c_void_p(0))
         be.timeline = None
     n = min(int(buf[0].item()), cap)
     rec = buf[8: 8 + 8 * n].view(n, 8).cpu().numpy()
-    out = {"step_ms": t0.elapsed_time(t1), "records": n}
+    out = {"step_ms": t0.elapsed_time(t1), "records": n, "traced_tree_size": m.tree_size}
     if os.environ.get("PROPD_BENCH_DUMP"):  # development aid: the raw per-CTA records of the traced step
         np.save(os.environ["PROPD_BENCH_DUMP"], rec)
     kinds = rec[:, 7] & 0xFF
@@ -524,7 +536,7 @@ def run_b200(args, rank: int, world: int, group):
     be.attn_timer = None
     vms = verify_ms(be, eng, seqs, prime, args.steps)
     prune_layer = ecfg.prune.layer if ecfg.uses_prune else None
-    in_step = timeline_step(be, eng, seqs, prime, dev, prune_layer)
+    in_step = timeline_step(be, eng, seqs, prime, dev, prune_layer, modal_size(main["metrics"]))
     hbm, peak_kind = peaks()
     kernels = {}
     for kind in ("gemm", "attn", "gemm_tc"):
@@ -616,10 +628,12 @@ def run_sweep(args, dev):
             r = timed_steps(be, eng, seqs, K, None, dev)
             m = r["metrics"]
             vms = verify_ms(be, eng, seqs, prime, 3)
-            ins = timeline_step(be, eng, seqs, prime, dev, ecfg.prune.layer if ecfg.uses_prune else None)
+            ins = timeline_step(be, eng, seqs, prime, dev, ecfg.prune.layer if ecfg.uses_prune else None,
+                                modal_size(m))
             row.update({"tok_s": sum(x.tokens_committed for x in m) / (r["ms"] * 1e-3), "ms_per_step": r["ms"] / K,
                         "verify_ms_per_step": vms, "accepted_len_per_step": sum(x.mean_accepted for x in m) / K,
                         "tree_size_mean": sum(x.tree_size for x in m) / K,
+                        "traced_tree_size": ins.get("traced_tree_size"),
                         "k2_frac_in_step": ins.get("attn", {}).get("frac"),
                         "gemm_frac_in_step": ins.get("gemm", {}).get("frac"),
                         "gemm_tc_tensor_frac_in_step": ins.get("gemm_tc", {}).get("tensor_frac"),

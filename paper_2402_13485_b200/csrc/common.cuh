@@ -39,6 +39,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();
+bool pdl_skip(const char* what);  // PROPD_PDL_SKIP="name,..." (dev A/B): launches of these names without PDL
 
 template <typename... Exp, typename... Act>
 inline int launch_pdl(const char* what, void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -52,7 +53,7 @@ inline int launch_pdl(const char* what, void (*kern)(Exp...), dim3 grid, dim3 bl
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = (pdl_enabled() && !pdl_skip(what)) ? 1 : 0;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...);
   if (e != cudaSuccess) {
     (void)cudaGetLastError();

@@ -44,7 +44,7 @@ def _vocab() -> int:
         return 8192
 
 
-@pytest.mark.parametrize("B,kv,k,layers,p", [(4, 1024, 16, 5, 3)])
+@pytest.mark.parametrize("B,kv,k,layers,p", [(4, 1024, 16, 5, 3), (1, 1024, 16, 5, 3)])
 def test_bf16_batched_step_teacher_forced_at_7b_width(B, kv, k, layers, p):
     V = _vocab()
     mc = op.TinyCfg(layers=layers, hidden=4096, heads=32, vocab=V, draft_heads=4, max_positions=kv + 64, seed=11)
