@@ -476,6 +476,24 @@ def timed_steps(be, eng, seqs, K, group, dev):
             "launches": be.launches - launches0, "captures": len(be._graphs) - graphs0}
 
 
+class pinned_plan:
+    """Within the block the engine keeps the tree plan `paths` (the plan of
+    the timed steps: the dynamic plan may move afterwards, and the verify-ms,
+    per-launch and traced-step measurements must see the same trees)."""
+
+    def __init__(self, eng, paths):
+        self.eng, self.paths = eng, paths
+
+    def __enter__(self):
+        if self.paths is not None:
+            self.eng._plan = lambda batch, mean_seqlen: (self.paths, False)
+        return self
+
+    def __exit__(self, *exc):
+        self.eng.__dict__.pop("_plan", None)
+        return False
+
+
 def verify_ms(be, eng, seqs, prime, K):
     """BASELINE's verify ms/step: two event nodes per step bracketing the tree
     pass (K1 -> layers -> K3 -> LM argmax -> K5) in otherwise unmodified graphs."""
@@ -524,19 +542,20 @@ def run_b200(args, rank: int, world: int, group):
         eng._step(seqs, 10 ** 9)
     be.attn_timer = None  # clean timed region: no per-launch event harvesting on the host
     main = timed_steps(be, eng, seqs, args.steps, group, dev)
-    # second region of K steps: CUDA events around every K2 / GEMM launch
-    # (event nodes inside separately captured graphs, each launch serialised)
-    be.attn_timer = []
-    prime()
-    be.attn_timer = []
-    for _ in range(args.steps):
-        eng._step(seqs, 10 ** 9)
-    torch.cuda.synchronize()
-    events = be.attn_timer
-    be.attn_timer = None
-    vms = verify_ms(be, eng, seqs, prime, args.steps)
-    prune_layer = ecfg.prune.layer if ecfg.uses_prune else None
-    in_step = timeline_step(be, eng, seqs, prime, dev, prune_layer, modal_size(main["metrics"]))
+    with pinned_plan(eng, eng._selection if ecfg.uses_dynamic else None):
+        # second region of K steps: CUDA events around every K2 / GEMM launch
+        # (event nodes inside separately captured graphs, each launch serialised)
+        be.attn_timer = []
+        prime()
+        be.attn_timer = []
+        for _ in range(args.steps):
+            eng._step(seqs, 10 ** 9)
+        torch.cuda.synchronize()
+        events = be.attn_timer
+        be.attn_timer = None
+        vms = verify_ms(be, eng, seqs, prime, args.steps)
+        prune_layer = ecfg.prune.layer if ecfg.uses_prune else None
+        in_step = timeline_step(be, eng, seqs, prime, dev, prune_layer, modal_size(main["metrics"]))
     hbm, peak_kind = peaks()
     kernels = {}
     for kind in ("gemm", "attn", "gemm_tc"):
@@ -627,9 +646,10 @@ def run_sweep(args, dev):
             prime()
             r = timed_steps(be, eng, seqs, K, None, dev)
             m = r["metrics"]
-            vms = verify_ms(be, eng, seqs, prime, 3)
-            ins = timeline_step(be, eng, seqs, prime, dev, ecfg.prune.layer if ecfg.uses_prune else None,
-                                modal_size(m))
+            with pinned_plan(eng, eng._selection if ecfg.uses_dynamic else None):
+                vms = verify_ms(be, eng, seqs, prime, 3)
+                ins = timeline_step(be, eng, seqs, prime, dev, ecfg.prune.layer if ecfg.uses_prune else None,
+                                    modal_size(m))
             row.update({"tok_s": sum(x.tokens_committed for x in m) / (r["ms"] * 1e-3), "ms_per_step": r["ms"] / K,
                         "verify_ms_per_step": vms, "accepted_len_per_step": sum(x.mean_accepted for x in m) / K,
                         "tree_size_mean": sum(x.tree_size for x in m) / K,
