@@ -408,12 +408,17 @@ int attention_decode_bf16(int B, int Bg, int M, int A, int Lmax, int max_rows_pe
   (void)ws_bytes;
   if (max_rows_per_seq > 4 || W > 4 || (ldqkv % 8) != 0) return 0;
   // splits per (sequence, head), one cluster each: enough CTAs for ~2 per SM
-  // at small batch; at large batch (>= one wave of pairs) the split count
-  // whose last wave is fullest (measured: 2 splits at B=32 x 32 heads)
+  // at small batch; at large batch (>= one wave of pairs) one split unless
+  // its last wave leaves over 20 % of the CTA slots idle, then the split
+  // count whose last wave is fullest (measured at B=32 x 32 heads, KV 1024:
+  // 1 split 110 us per launch vs 127 us for the 2 splits wave filling picks)
   const int pairs = Bg * A;  // sequences with a KV cache (Bg <= B)
   const int slots = 2 * propd_num_sms();
   int nsplit = (slots + pairs - 1) / pairs;
-  if (2 * pairs > slots) nsplit = wave_split(pairs, slots, 2);
+  if (2 * pairs > slots) {
+    const int waves = (pairs + slots - 1) / slots;
+    nsplit = (double)pairs / ((double)waves * slots) >= 0.8 ? 1 : wave_split(pairs, slots, 2);
+  }
   const int cap = (max_keys + dec::CHUNK - 1) / dec::CHUNK;
   if (nsplit > cap) nsplit = cap;
   if (nsplit > dec::MAX_SPLIT) nsplit = dec::MAX_SPLIT;
