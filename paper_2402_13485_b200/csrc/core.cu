@@ -50,6 +50,31 @@ int check_launch(const char* what) {
   return 0;
 }
 
+// x row = emb row + pos row (fp32 out): 16-byte loads of 8 bf16 (or 4 fp32)
+// elements per thread when the width allows it (the K1 / bonus / prefill
+// embeds: one dependent gather per row, latency-bound at small batch)
+template <typename T>
+__device__ __forceinline__ void embed_add_row(const T* __restrict__ e, const T* __restrict__ q, float* __restrict__ o,
+                                              int H) {
+  constexpr int VW = 16 / sizeof(T);  // elements per 16-byte load
+  if (H % VW == 0 && (reinterpret_cast<uintptr_t>(e) & 15) == 0 && (reinterpret_cast<uintptr_t>(q) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+    for (int h = threadIdx.x * VW; h < H; h += blockDim.x * VW) {
+      const uint4 ev = __ldg(reinterpret_cast<const uint4*>(e + h));
+      const uint4 qv = __ldg(reinterpret_cast<const uint4*>(q + h));
+      const T* ea = reinterpret_cast<const T*>(&ev);
+      const T* qa = reinterpret_cast<const T*>(&qv);
+#pragma unroll
+      for (int k = 0; k < VW; k += 4)
+        *reinterpret_cast<float4*>(o + h + k) = make_float4(to_f(ea[k]) + to_f(qa[k]), to_f(ea[k + 1]) + to_f(qa[k + 1]),
+                                                            to_f(ea[k + 2]) + to_f(qa[k + 2]),
+                                                            to_f(ea[k + 3]) + to_f(qa[k + 3]));
+    }
+  } else {
+    for (int h = threadIdx.x; h < H; h += blockDim.x) o[h] = to_f(e[h]) + to_f(q[h]);
+  }
+}
+
 // ---------------------------------------------------------------- K1 ------
 template <typename T>
 __global__ void tree_embed_kernel(int n, int D, int kmax, int H, const int32_t* __restrict__ depth,
@@ -74,7 +99,7 @@ __global__ void tree_embed_kernel(int n, int D, int kmax, int H, const int32_t* 
   const T* e = emb + (size_t)tok * H;
   const T* q = pos + (size_t)p * H;
   float* o = x + (size_t)m * H;
-  for (int h = threadIdx.x; h < H; h += blockDim.x) o[h] = to_f(e[h]) + to_f(q[h]);
+  embed_add_row(e, q, o, H);
 }
 
 template <typename T>
@@ -84,7 +109,7 @@ __global__ void embed_rows_kernel(int H, const int32_t* __restrict__ tokens, con
   const T* e = emb + (size_t)tokens[m] * H;
   const T* q = pos + (size_t)positions[m] * H;
   float* o = x + (size_t)m * H;
-  for (int h = threadIdx.x; h < H; h += blockDim.x) o[h] = to_f(e[h]) + to_f(q[h]);
+  embed_add_row(e, q, o, H);
 }
 
 template <typename T>
@@ -105,7 +130,7 @@ __global__ void bonus_embed_kernel(int B, int H, const int32_t* __restrict__ bon
   const T* e = emb + (size_t)tok * H;
   const T* q = pos + (size_t)p * H;
   float* o = x + (size_t)b * H;
-  for (int h = threadIdx.x; h < H; h += blockDim.x) o[h] = to_f(e[h]) + to_f(q[h]);
+  embed_add_row(e, q, o, H);
 }
 
 // ------------------------------------------------------------- dense ------
@@ -432,19 +457,43 @@ __global__ void __launch_bounds__(512) topk_rows_kernel(int V, int ld, int k, co
       if (pass == 0 || (kk >> (shift + 8)) == (pre >> (shift + 8))) atomicAdd(&hist[(kk >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int need = s_need;
-      unsigned cum = 0;
-      int bsel = 0;
-      for (int bkt = 255; bkt >= 0; --bkt) {
-        if (cum + hist[bkt] >= (unsigned)need) { bsel = bkt; break; }
-        cum += hist[bkt];
+    if (threadIdx.x < 32) {
+      // the bin holding the need-th largest key: lane l owns bins 255-8l .. 248-8l
+      // (descending), a warp scan of the lane totals finds the lane, the lane
+      // walks its 8 bins (a serial scan of 256 bins cost ~1-2 us per pass)
+      const int lane = threadIdx.x, need = s_need;
+      unsigned c[8], tot = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        c[i] = hist[255 - 8 * lane - i];
+        tot += c[i];
       }
-      need -= (int)cum;  // still needed from bucket bsel
-      s_prefix = pre | ((unsigned long long)bsel << shift);
-      s_shift = shift;
-      s_need = need;
-      if (hist[bsel] == (unsigned)need) s_done = 1;
+      unsigned incl = tot;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
+      }
+      const unsigned excl = incl - tot;
+      if (excl < (unsigned)need && (unsigned)need <= incl) {
+        unsigned cum = excl;
+        int bsel = 255 - 8 * lane - 7;
+        unsigned cnt = c[7];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (cum + c[i] >= (unsigned)need) {
+            bsel = 255 - 8 * lane - i;
+            cnt = c[i];
+            break;
+          }
+          cum += c[i];
+        }
+        const int left = need - (int)cum;  // still needed from bucket bsel
+        s_prefix = pre | ((unsigned long long)bsel << shift);
+        s_shift = shift;
+        s_need = left;
+        if (cnt == (unsigned)left) s_done = 1;
+      }
     }
     __syncthreads();
     if (s_done) break;

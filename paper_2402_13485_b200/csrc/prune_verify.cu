@@ -15,14 +15,37 @@
 namespace propd {
 
 // ---------------------------------------------------------------- K3 ------
-// One CTA per (sequence, parent row): the parent's early-logit row is read
-// once and every child of that parent is ranked against it in the same pass.
-// Counting rank of child token t: the number of vocabulary entries a stable
-// descending argsort places before t, #{v: l[v] > l[t]} + #{v < t: l[v] == l[t]};
-// the child is a member iff that rank is < K (the parent's K-th order
-// statistic under the (value desc, index asc) order).  Depth-1 nodes are
-// exempt (pruning.py:60-61) and written by the CTAs of parent row 0.
-constexpr int K3_THREADS = 512, K3_CH = 16, K3_MAXN = 1024;
+// One thread-block cluster per (sequence, parent row): the parent's
+// early-logit row is split across the cluster's CTAs (a row of 32000 logits
+// scanned by one CTA took ~50 us at batch 1, three parent rows on three SMs),
+// every child of that parent is ranked against each slice in the same pass,
+// and the per-CTA partial ranks are summed through distributed shared memory
+// by CTA rank 0.  Counting rank of child token t: the number of vocabulary
+// entries a stable descending argsort places before t,
+// #{v: l[v] > l[t]} + #{v < t: l[v] == l[t]}; the child is a member iff that
+// rank is < K (the parent's K-th order statistic under the (value desc,
+// index asc) order).  Depth-1 nodes are exempt (pruning.py:60-61) and
+// written by the clusters of parent row 0.
+constexpr int K3_THREADS = 512, K3_CH = 16, K3_MAXN = 1024, K3_MAXCL = 8;
+__device__ __forceinline__ uint32_t k3_cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t k3_cl_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void k3_cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ int k3_cl_ld(const int* p, uint32_t rank) {
+  uint32_t a, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return (int)v;
+}
 __global__ void __launch_bounds__(K3_THREADS) early_member_kernel(int n, int P, int V, int topk,
                                                                   const float* __restrict__ early,
                                                                   const int32_t* __restrict__ parent,
@@ -32,25 +55,31 @@ __global__ void __launch_bounds__(K3_THREADS) early_member_kernel(int n, int P, 
   __shared__ int s_idx[K3_MAXN];
   __shared__ int s_cnt;
   __shared__ int red[K3_THREADS / 32][K3_CH];
+  __shared__ int s_part[K3_CH];
   const int Pe = P > 0 ? P : 1;
-  const int b = blockIdx.x / Pe, j = blockIdx.x - b * Pe;
+  const int cs = (int)k3_cl_size(), cr = (int)k3_cl_rank();
+  const int pr = blockIdx.x / cs;  // (sequence, parent row) of this cluster
+  const int b = pr / Pe, j = pr - b * Pe;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int par = parent[i];
     if (par < 0) {
-      if (j == 0) member[b * n + i] = 1;
+      if (j == 0 && cr == 0) member[b * n + i] = 1;
     } else if (parent_slot[par] == j) {
       s_idx[atomicAdd(&s_cnt, 1)] = i;
     }
   }
   __syncthreads();
-  const int nc = s_cnt;
+  const int nc = s_cnt;  // (the same on every CTA of the cluster)
   if (nc == 0) return;
   const float* row = early + ((size_t)b * P + j) * V;
   const bool vec = (V & 3) == 0 && (reinterpret_cast<uintptr_t>(early) & 15) == 0;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int c0 = 0; c0 < nc; c0 += K3_CH) {  // children in chunks held in registers (one row pass each)
+  // this CTA's slice of the row (float4 units when vectorised)
+  const int units = vec ? (V >> 2) : V, per = (units + cs - 1) / cs;
+  const int u0 = min(units, cr * per), u1 = min(units, u0 + per);
+  for (int c0 = 0; c0 < nc; c0 += K3_CH) {  // children in chunks held in registers (one slice pass each)
     float tv[K3_CH];
     int tk[K3_CH], cnt[K3_CH];
 #pragma unroll
@@ -62,29 +91,19 @@ __global__ void __launch_bounds__(K3_THREADS) early_member_kernel(int n, int P, 
     }
     if (vec) {
       const float4* r4 = reinterpret_cast<const float4*>(row);
-      const int V4 = V >> 2;
-      constexpr int U = 2;
-      for (int base = threadIdx.x; base < V4; base += U * blockDim.x) {
-        float4 f[U];
+      for (int i = u0 + threadIdx.x; i < u1; i += blockDim.x) {
+        const float4 f = __ldg(r4 + i);
+        const int v = 4 * i;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = base + u * blockDim.x;
-          f[u] = i < V4 ? __ldg(r4 + i) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int v = 4 * (base + u * blockDim.x);
-#pragma unroll
-          for (int c = 0; c < K3_CH; ++c) {
-            cnt[c] += (f[u].x > tv[c]) || (f[u].x == tv[c] && v < tk[c]);
-            cnt[c] += (f[u].y > tv[c]) || (f[u].y == tv[c] && v + 1 < tk[c]);
-            cnt[c] += (f[u].z > tv[c]) || (f[u].z == tv[c] && v + 2 < tk[c]);
-            cnt[c] += (f[u].w > tv[c]) || (f[u].w == tv[c] && v + 3 < tk[c]);
-          }
+        for (int c = 0; c < K3_CH; ++c) {
+          cnt[c] += (f.x > tv[c]) || (f.x == tv[c] && v < tk[c]);
+          cnt[c] += (f.y > tv[c]) || (f.y == tv[c] && v + 1 < tk[c]);
+          cnt[c] += (f.z > tv[c]) || (f.z == tv[c] && v + 2 < tk[c]);
+          cnt[c] += (f.w > tv[c]) || (f.w == tv[c] && v + 3 < tk[c]);
         }
       }
     } else {
-      for (int v = threadIdx.x; v < V; v += blockDim.x) {
+      for (int v = u0 + threadIdx.x; v < u1; v += blockDim.x) {
         const float x = row[v];
 #pragma unroll
         for (int c = 0; c < K3_CH; ++c) cnt[c] += (x > tv[c]) || (x == tv[c] && v < tk[c]);
@@ -96,12 +115,20 @@ __global__ void __launch_bounds__(K3_THREADS) early_member_kernel(int n, int P, 
       if (lane == 0) red[wid][c] = s;
     }
     __syncthreads();
-    if (threadIdx.x < K3_CH && c0 + (int)threadIdx.x < nc) {
+    if (threadIdx.x < K3_CH) {
       int s = 0;
       for (int w = 0; w < K3_THREADS / 32; ++w) s += red[w][threadIdx.x];
+      s_part[threadIdx.x] = s;
+    }
+    if (cs > 1) k3_cl_sync();  // every slice's partial ranks are visible cluster-wide
+    else __syncthreads();
+    if (cr == 0 && threadIdx.x < K3_CH && c0 + (int)threadIdx.x < nc) {
+      int s = 0;
+      for (int r = 0; r < cs; ++r) s += r == 0 ? s_part[threadIdx.x] : k3_cl_ld(&s_part[threadIdx.x], r);
       member[b * n + s_idx[c0 + threadIdx.x]] = s < topk ? 1 : 0;
     }
-    __syncthreads();
+    if (cs > 1) k3_cl_sync();  // s_part / red reused by the next chunk (and read remotely until here)
+    else __syncthreads();
   }
 }
 
@@ -434,8 +461,27 @@ int propd_early_member(int B, int n, int P, int V, int topk, const float* early_
   if (B == 0 || n == 0) return 0;
   PROPD_REQUIRE(topk >= 1, "early_member: topk must be positive");
   PROPD_REQUIRE(n <= K3_MAXN, "early_member: tree of %d nodes > %d", n, K3_MAXN);
-  early_member_kernel<<<B * (P > 0 ? P : 1), K3_THREADS, 0, as_stream(stream)>>>(n, P, V, topk, early_logits, parent,
-                                                                                parent_slot, tokens, member);
+  // cluster size: up to 8 slices per parent row while the clusters fit in about two waves of CTAs
+  const int rows = B * (P > 0 ? P : 1);
+  int cs = 1;
+  while (cs < K3_MAXCL && rows * cs * 2 <= 2 * propd_num_sms() && V / (cs * 2) >= 4 * K3_THREADS) cs *= 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(rows * cs);
+  cfg.blockDim = dim3(K3_THREADS);
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, early_member_kernel, n, P, V, topk, early_logits, parent,
+                                           parent_slot, tokens, member);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    return fail("early_member: %s", cudaGetErrorString(e));
+  }
   return check_launch("early_member");
 }
 
