@@ -134,6 +134,13 @@ int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, 
  * it is excluded from the launch-geometry heuristics (key splits per
  * sequence), so a B-sequence step gets the splits of B, not B + 1. */
 #define PROPD_ATTN_SCRATCH_LAST 0x100
+/* impl | PROPD_ATTN_QKV_F32: qkv is the fp32 QKV accumulator [M, 3H] of a QKV
+ * launch without a tail (row stride ldqkv floats): Q and the tree rows' K/V
+ * are read from it (bf16-rounded as propd_qkv_finish would store them), and
+ * the kernel itself writes the tree rows' K/V into the layer cache (slot
+ * seq_len + row_node); the accumulator is left as it is.  Transposed kernel
+ * only (bf16, dh = 128, <= 64 rows per sequence, a tree mask). */
+#define PROPD_ATTN_QKV_F32 0x200
 int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits);
 int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int n_slots,
                          int max_rows_per_seq, int max_keys,

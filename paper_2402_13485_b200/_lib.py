@@ -65,6 +65,7 @@ _RESTYPES = {"propd_last_error": ctypes.c_char_p, "propd_attn_workspace_bytes": 
 
 PRO_NONE, PRO_LN, PRO_GELU, PRO_XGELU, PRO_XATTN = 0, 1, 2, 4, 5
 ATTN_SCRATCH_LAST = 0x100  # propd_tree_attention impl flag (include/propd.h)
+ATTN_QKV_F32 = 0x200  # propd_tree_attention: Q / tree K/V from the fp32 QKV accumulator
 TAIL_NONE, TAIL_QKV = 0, 1
 
 

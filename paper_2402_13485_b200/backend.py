@@ -197,6 +197,8 @@ class B200Backend:
         # the QKV launch (one (row, head, key split) per CTA) and W_o combines
         # the partials (propd_ws_phases.attn_splits, PRO_XATTN)
         self.ws_fuse_attn = (self.ws_phases and self.dh == 128 and os.environ.get("PROPD_FUSE_ATTN", "1") != "0")
+        # tree passes: the QKV tail folded into the transposed attention kernel (PROPD_ATTN_QKV_F32)
+        self.ws_qkv_fold = (self.ws_phases and self.dh == 128 and os.environ.get("PROPD_QKV_FOLD", "1") != "0")
         if self.ws_fuse_attn:
             H = cfg.hidden
             self._qkv_ctas = (3 * H // 128) * self.lib.propd_ws_split_count(3 * H, H)
@@ -420,13 +422,19 @@ class B200Backend:
                                         phases, st)
         self._timed("gemm", launch, M, K, N, bool(acc))
 
-    def _attention(self, rt: Rows, qkv, l: int, mask, n_tmpl: int, W: int, ctx, ws) -> None:
-        """K2 over the rows of `rt` for layer l (Q = columns [0, H) of qkv)."""
+    def _attention(self, rt: Rows, qkv, l: int, mask, n_tmpl: int, W: int, ctx, ws, acc=None) -> None:
+        """K2 over the rows of `rt` for layer l (Q = columns [0, H) of qkv; with
+        `acc`, Q and the tree rows' K/V come from the fp32 QKV accumulator and
+        the kernel writes the tree rows into the cache: PROPD_ATTN_QKV_F32)."""
         H, M = self.H, rt.M
         ws_bytes = 0 if ws is None else ws.numel()
+        impl = self.attn_impl | (_lib.ATTN_SCRATCH_LAST if rt.scratch_last else 0)
+        if acc is not None:
+            impl |= _lib.ATTN_QKV_F32
+            qkv = acc
         self._timed("attn", lambda: self._call(
-            "propd_tree_attention", self.code, self.attn_impl | (_lib.ATTN_SCRATCH_LAST if rt.scratch_last else 0), rt.B, M, self.A, self.dh, self.Lmax, self.n_slots,
-            rt.max_rows, rt.max_keys, ptr(qkv), qkv.shape[1], ptr(self.kcache[l]), ptr(self.vcache[l]),
+            "propd_tree_attention", self.code, impl, rt.B, M, self.A, self.dh, self.Lmax, self.n_slots,
+            rt.max_rows, rt.max_keys, ptr(qkv), 3 * H if acc is not None else qkv.shape[1], ptr(self.kcache[l]), ptr(self.vcache[l]),
             ptr(rt.seq_slot), ptr(self.seq_len), ptr(rt.row_off), ptr(rt.row_node), ptr(mask), n_tmpl, W, ptr(ctx),
             H, ptr(ws), ws_bytes, self.stream()), M)
 
@@ -460,17 +468,30 @@ class B200Backend:
             wo_phases = _lib.WsPhases(pro_mode=_lib.PRO_XATTN, pro_src=ptr(self._attn_part), pro_cols=H, A=self.A,
                                       dh=self.dh, bar=bar, zero_buf=ptr(acc1), zero_ld=3 * H, zero_cols=3 * H,
                                       **fused)
+        # tree passes on the transposed attention kernel: QKV has no tail (no
+        # grid barrier, no bf16 Q / K/V pass); the attention reads Q and the tree
+        # rows' K/V from the fp32 accumulator and writes those K/V rows into the
+        # cache itself; W_o re-zeroes the accumulator (PROPD_ATTN_QKV_F32)
+        fold = (not splits and self.ws_qkv_fold and mask is not None and mask is not self._one_mask
+                and self.dh == 128 and rt.max_rows <= 64 and W <= 4)
+        wo_zero = _lib.WsPhases(bar=bar, zero_buf=ptr(acc1), zero_ld=3 * H, zero_cols=3 * H) if fold else None
         for l in range(l0, l1):
             # with the converting GELU, QKV zeroes the W_1 accumulator rows ahead (W_2 read them last)
             pro_qkv, pro_w1 = dict(ln, **zero_acc2), _lib.WsPhases(**ln)
-            qkv_phases = _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A, dh=self.dh,
-                                       Lmax=self.Lmax, row_seq=ptr(rt.row_seq), row_node=ptr(rt.row_node),
-                                       seq_slot=ptr(rt.seq_slot), seq_len=ptr(self.seq_len),
-                                       kcache=ptr(self.kcache[l]), vcache=ptr(self.vcache[l]), **pro_qkv,
-                                       **fused)
+            if fold:
+                qkv_phases = _lib.WsPhases(**pro_qkv)
+            else:
+                qkv_phases = _lib.WsPhases(tail_mode=_lib.TAIL_QKV, tail_q=ptr(qkv), tail_ldq=3 * H, A=self.A,
+                                           dh=self.dh, Lmax=self.Lmax, row_seq=ptr(rt.row_seq),
+                                           row_node=ptr(rt.row_node), seq_slot=ptr(rt.seq_slot),
+                                           seq_len=ptr(self.seq_len), kcache=ptr(self.kcache[l]),
+                                           vcache=ptr(self.vcache[l]), **pro_qkv, **fused)
             self._gemm_ws(M, live, 3 * H, H, h, self.w.wqkv[l], acc1, 3 * H, 1, qkv_phases)
             if splits:  # attention inside the QKV launch, partials combined by W_o (which re-zeroes acc1)
                 self._gemm_ws(M, live, H, H, ctx, self.w.wo[l], x, H, 1, wo_phases)
+            elif fold:
+                self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws, acc=acc1)
+                self._gemm_ws(M, live, H, H, ctx, self.w.wo[l], x, H, 1, wo_zero)
             else:
                 self._attention(rt, qkv, l, mask, n_tmpl, W, ctx, ws)
                 self._gemm_ws(M, live, H, H, ctx, self.w.wo[l], x, H, 1)

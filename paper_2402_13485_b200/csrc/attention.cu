@@ -228,7 +228,7 @@ int attention_tc2_bf16(int B, int Bg, int M, int A, int Lmax, int n_slots, int m
 int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
                        int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                        const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
-                       void* out, int ldout, cudaStream_t st, bool force, bool* handled);
+                       void* out, int ldout, cudaStream_t st, bool force, bool* handled, bool qy = false);
 
 int attention_decode_bf16(int B, int Bg, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
                           int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
@@ -269,7 +269,19 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
   if (B == 0 || M == 0) return 0;
   // launch geometry counts the sequences with a real KV cache (not the scratch entry)
   const int Bg = (impl & PROPD_ATTN_SCRATCH_LAST) && B > 1 ? B - 1 : B;
+  const bool qy = (impl & PROPD_ATTN_QKV_F32) != 0;
   impl &= 0xFF;
+  if (qy) {  // fp32 QKV accumulator input: the transposed kernel only
+    PROPD_REQUIRE(dtype == PROPD_BF16 && dh == 128 && mask != nullptr && (impl == 0 || impl == 5),
+                  "tree_attention: QKV_F32 input needs bf16, dh = 128, a tree mask and the transposed kernel");
+    bool handled = false;
+    int e = attention_tct_bf16(B, Bg, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache,
+                               seq_slot, seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, as_stream(stream),
+                               true, &handled, true);
+    if (e) return e;
+    PROPD_REQUIRE(handled, "tree_attention: QKV_F32 input: the transposed kernel serves <= 64 rows per sequence");
+    return 0;
+  }
   PROPD_REQUIRE(mask == nullptr || (W <= ATT_MAXW && W * 64 >= n_tmpl),
                 "tree_attention: template of %d nodes needs W=%d <= %d", n_tmpl, W, ATT_MAXW);
   PROPD_REQUIRE(max_keys >= 1, "tree_attention: max_keys must be positive");

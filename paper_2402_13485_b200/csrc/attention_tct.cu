@@ -80,6 +80,13 @@ struct Cfg {
 struct Args {
   const __nv_bfloat16* qkv;
   int ldq;
+  // PROPD_ATTN_QKV_F32: Q and the tree rows' K/V from the fp32 QKV accumulator
+  // (row stride ldy floats; bf16-rounded as the QKV tail would store them); the
+  // CTA writes the tree rows of its key range into the cache itself
+  const float* y;
+  int ldy;
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
   const int32_t* seq_slot;
   const int32_t* seq_len;
   const int32_t* row_off;
@@ -258,7 +265,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   // the first ring fill goes out before anything else (its latency overlaps
   // the Q load, the TMEM allocation and the block-wide sync)
   const bool producer = (warp == 0 || warp == C::VWARP) && lane == 0;
-  const int npre = min(C::KS, nblk);  // C::KS == C::VS
+  // (with the tree rows written by this CTA below, only blocks wholly below L go out early)
+  const int npre = p.y ? max(0, min(min(C::KS, nblk), (L - k_begin) / BK)) : min(C::KS, nblk);  // C::KS == C::VS
   if (producer) {
     const bool isk = warp == 0;
     uint64_t* full = isk ? k_full : v_full;
@@ -285,7 +293,34 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
                  "r"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  {  // Q rows -> SW128 K-major [NR rows x 128 dims] (rows past nrows zero)
+  if (p.y) {  // Q rows from the fp32 accumulator; this split's tree rows -> the cache
+    const int H = p.A * DH;
+    for (int i = threadIdx.x; i < NR * 16; i += C::THREADS) {
+      const int r = i >> 4, c = i & 15;
+      uint8_t* dst =
+          smem + C::SMEM_Q + (c >> 3) * C::Q_HALF + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4);
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < nrows) {
+        const float4* src = reinterpret_cast<const float4*>(p.y + (size_t)(r0 + r) * p.ldy + a * DH + c * 8);
+        const float4 f0 = __ldcg(src), f1 = __ldcg(src + 1);
+        v = make_uint4(pack_bf16(f0.x, f0.y), pack_bf16(f0.z, f0.w), pack_bf16(f1.x, f1.y), pack_bf16(f1.z, f1.w));
+      }
+      *reinterpret_cast<uint4*>(dst) = v;
+    }
+    for (int i = threadIdx.x; i < nrows * 32; i += C::THREADS) {
+      const int r = i >> 5, kv = (i >> 4) & 1, c = i & 15;
+      const int pos = L + p.row_node[r0 + r];
+      if (pos < k_begin || pos >= k_end) continue;
+      const float4* src =
+          reinterpret_cast<const float4*>(p.y + (size_t)(r0 + r) * p.ldy + (1 + kv) * H + a * DH + c * 8);
+      const float4 f0 = __ldcg(src), f1 = __ldcg(src + 1);
+      __nv_bfloat16* dst = (kv ? p.vc : p.kc) + (row_base + pos) * DH + c * 8;
+      *reinterpret_cast<uint4*>(dst) =
+          make_uint4(pack_bf16(f0.x, f0.y), pack_bf16(f0.z, f0.w), pack_bf16(f1.x, f1.y), pack_bf16(f1.z, f1.w));
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic cache writes -> the TMA reads below
+    for (int r = threadIdx.x; r < NR; r += C::THREADS) rnode[r] = r < nrows ? p.row_node[r0 + r] : 0;
+  } else {  // Q rows -> SW128 K-major [NR rows x 128 dims] (rows past nrows zero)
     const __nv_bfloat16* qbase = p.qkv + a * DH;
     for (int i = threadIdx.x; i < NR * 16; i += C::THREADS) {
       const int r = i >> 4, c = i & 15;
@@ -618,10 +653,10 @@ static int tct_launch(const CUtensorMap& km, const CUtensorMap& vm, const tct::A
 int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
                        int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                        const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
-                       void* out, int ldout, cudaStream_t st, bool force, bool* handled) {
+                       void* out, int ldout, cudaStream_t st, bool force, bool* handled, bool qy) {
   *handled = false;
   if (!force && tct_mode() == 0) return 0;
-  if (n_slots <= 0 || max_rows_per_seq > 64 || W > 4 || (ldqkv % 8) != 0) return 0;
+  if (n_slots <= 0 || max_rows_per_seq > 64 || W > 4 || (ldqkv % (qy ? 4 : 8)) != 0) return 0;
   // > 32-row capacity with few 128-key blocks per SM (B=1-4 at KV <= 2K) is
   // latency-bound, where the row-major tc2 kernel's shorter per-block chain
   // wins (measured: 11.2 vs 14.7 us at B=1/KV 512, 22.2 vs 25.0 at B=4/KV 1K)
@@ -650,8 +685,12 @@ int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows
   const int per = (nh + nsplit - 1) / nsplit;  // 64-key units per split at max_keys
   nsplit = (nh + per - 1) / per;               // no split empty at max_keys
   tct::Args p{};
-  p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  p.qkv = qy ? nullptr : reinterpret_cast<const __nv_bfloat16*>(qkv);
   p.ldq = ldqkv;
+  p.y = qy ? reinterpret_cast<const float*>(qkv) : nullptr;
+  p.ldy = ldqkv;
+  p.kc = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(kc));
+  p.vc = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(vc));
   p.seq_slot = seq_slot;
   p.seq_len = seq_len;
   p.row_off = row_off;

@@ -1060,7 +1060,7 @@ int propd_gemm_ws_ph(int M, const int32_t* rows_dev, int N, int K, const void* X
   int split, per;
   gws::split_k(N, K, accumulate, max_split, &split, &per);
   gws::Args p{M, N, K, per, ldy, mp, rows_dev, Y, accumulate, g_dbg_trace, g_dbg_tag++, {}};
-  if (ph != nullptr && (ph->pro_mode != PROPD_PRO_NONE || ph->tail_mode != PROPD_TAIL_NONE)) {
+  if (ph != nullptr && (ph->pro_mode != PROPD_PRO_NONE || ph->tail_mode != PROPD_TAIL_NONE || ph->zero_buf)) {
     // the grid barriers need every CTA resident at once: checked against the
     // occupancy the runtime reports for this kernel variant (a launch that
     // could not be co-resident fails here instead of hanging the device)

@@ -291,6 +291,49 @@ def test_survivor_tier_variants_match_full_capacity_pass():
         assert np.array_equal(a.committed, b.committed) and np.array_equal(a.acc_len, b.acc_len)
 
 
+@pytest.mark.parametrize("B,L,k", [(1, 1000, 16), (2, 37, 16), (4, 300, 16), (8, 200, 8)])
+def test_qkv_tail_folded_into_attention_matches_tail_path(B, L, k):
+    """bf16 at 7B width: tree passes whose QKV launch has no tail — the transposed attention reads Q and the
+    tree rows' K/V from the fp32 accumulator and writes those K/V rows into the cache itself
+    (PROPD_ATTN_QKV_F32) — against the QKV-tail path, pre-prune (64-node tree) and post-prune, ragged committed
+    lengths (L - 13 b, one shorter than a key block).  Structural outputs bit-exact; the surviving tree rows'
+    cache K/V within 2e-2 * max(1, |ref|_inf) (two runs: the split-K fp32 accumulation order differs, so bf16
+    roundings may differ by an ulp); surviving rows' logits within 3e-2 * max(1, |ref|_inf) (the tail path may
+    route latency-bound launches to the row-major kernel); argmax >= 95% equal."""
+    cfg = TinyTransformerConfig(layers=3, hidden=4096, heads=32, vocab=32000, draft_heads=4, max_positions=1100,
+                                seed=5)
+    tmpl = TreeTemplate.from_paths(op.grid_candidates(4, k))
+    outs, caches = [], []
+    for fold in (True, False):
+        be = B200Backend(cfg, dtype="bf16", random_device_init=True, max_slots=B, max_tree=64, use_graphs=True)
+        be.ws_qkv_fold = fold
+        states = be.synthetic_states(B, L, seed=9)
+        for b, st in enumerate(states):  # ragged lengths
+            Lb = max(1, L - 13 * b)
+            be._len[st.slot] = Lb
+            be.seq_len[st.slot] = Lb
+            st.committed = st.committed[:Lb]
+        lens = [be._len[st.slot] for st in states]
+        outs.append(be.step_tree(states, tmpl, k, prune=PruneConfig(1, 50), trace=True))
+        # tree rows of the last layer: cache slots L_b + node (before K5 compaction moved the accepted ones)
+        caches.append([be.kcache[-1, st.slot, :, Lb + 1: Lb + len(tmpl)].float().cpu().numpy()
+                       for st, Lb in zip(states, lens)])
+        del be
+    a, b = outs
+    assert np.array_equal(a.trace["alive"], b.trace["alive"])
+    assert np.array_equal(a.surv_cnt, b.surv_cnt)
+    la, lb = a.trace["row_logits"], b.trace["row_logits"]
+    assert np.abs(la - lb).max() <= 3e-2 * max(1.0, np.abs(lb).max())
+    alive = a.trace["alive"].astype(bool)
+    ra = a.trace["row_argmax"][a.trace["node_row"][alive]]
+    rb = b.trace["row_argmax"][b.trace["node_row"][alive]]
+    assert (ra == rb).mean() >= 0.95
+    if np.array_equal(a.acc_len, b.acc_len) and not a.acc_len.any():  # nothing committed: rows stayed in place
+        for ca, cb, al in zip(caches[0], caches[1], alive):
+            keep = al[1:]  # surviving tree rows (node 0 is overwritten by the bonus row)
+            assert keep.any() and np.abs(ca[:, keep] - cb[:, keep]).max() <= 2e-2 * max(1.0, np.abs(cb).max())
+
+
 @pytest.mark.parametrize("mode", ["static_tree", "propd_full"])
 def test_planted_acceptance_matches_oracle(mode):
     """Planted-acceptance harness: draft head 0 := the LM head on the same seeded weights for
