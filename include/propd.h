@@ -138,8 +138,9 @@ int propd_kv_append(int dtype, int M, int A, int dh, int Lmax, const void* qkv, 
  * launch without a tail (row stride ldqkv floats): Q and the tree rows' K/V
  * are read from it (bf16-rounded as propd_qkv_finish would store them), and
  * the kernel itself writes the tree rows' K/V into the layer cache (slot
- * seq_len + row_node); the accumulator is left as it is.  Transposed kernel
- * only (bf16, dh = 128, <= 64 rows per sequence, a tree mask). */
+ * seq_len + row_node); the accumulator is left as it is.  Decode kernel
+ * (<= 4 rows per sequence) or transposed kernel (<= 64); bf16, dh = 128, a
+ * mask (the single-node mask for one-row passes). */
 #define PROPD_ATTN_QKV_F32 0x200
 int64_t propd_attn_workspace_bytes(int M, int A, int dh, int max_splits);
 int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int Lmax, int n_slots,

@@ -472,8 +472,8 @@ class B200Backend:
         # grid barrier, no bf16 Q / K/V pass); the attention reads Q and the tree
         # rows' K/V from the fp32 accumulator and writes those K/V rows into the
         # cache itself; W_o re-zeroes the accumulator (PROPD_ATTN_QKV_F32)
-        fold = (not splits and self.ws_qkv_fold and mask is not None and mask is not self._one_mask
-                and self.dh == 128 and rt.max_rows <= 64 and W <= 4)
+        fold = (not splits and self.ws_qkv_fold and mask is not None and self.dh == 128 and rt.max_rows <= 64
+                and W <= 4 and (mask is not self._one_mask or rt.max_rows <= 4))
         wo_zero = _lib.WsPhases(bar=bar, zero_buf=ptr(acc1), zero_ld=3 * H, zero_cols=3 * H) if fold else None
         for l in range(l0, l1):
             # with the converting GELU, QKV zeroes the W_1 accumulator rows ahead (W_2 read them last)

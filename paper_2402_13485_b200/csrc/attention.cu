@@ -233,7 +233,7 @@ int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows
 int attention_decode_bf16(int B, int Bg, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
                           int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                           const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
-                          void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled);
+                          void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled, bool qy = false);
 
 }  // namespace propd
 
@@ -271,10 +271,16 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
   const int Bg = (impl & PROPD_ATTN_SCRATCH_LAST) && B > 1 ? B - 1 : B;
   const bool qy = (impl & PROPD_ATTN_QKV_F32) != 0;
   impl &= 0xFF;
-  if (qy) {  // fp32 QKV accumulator input: the transposed kernel only
-    PROPD_REQUIRE(dtype == PROPD_BF16 && dh == 128 && mask != nullptr && (impl == 0 || impl == 5),
-                  "tree_attention: QKV_F32 input needs bf16, dh = 128, a tree mask and the transposed kernel");
+  if (qy) {  // fp32 QKV accumulator input: the decode (<= 4 rows) or the transposed kernel
+    PROPD_REQUIRE(dtype == PROPD_BF16 && dh == 128 && mask != nullptr && (impl == 0 || impl == 3 || impl == 5),
+                  "tree_attention: QKV_F32 input needs bf16, dh = 128, a mask and the decode / transposed kernel");
     bool handled = false;
+    if (impl != 5 && max_rows_per_seq <= 4) {
+      int e = attention_decode_bf16(B, Bg, M, A, Lmax, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache,
+                                    seq_slot, seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, workspace,
+                                    workspace_bytes, as_stream(stream), &handled, true);
+      if (e || handled) return e;
+    }
     int e = attention_tct_bf16(B, Bg, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache,
                                seq_slot, seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, as_stream(stream),
                                true, &handled, true);

@@ -42,6 +42,11 @@ struct Args {
   int ldout;
   unsigned long long* tl;  // development timeline (common.cuh)
   unsigned int tag;
+  // PROPD_ATTN_QKV_F32: Q and the rows' own K/V from the fp32 QKV accumulator
+  // (row stride ldy floats, bf16-rounded); the CTA whose key range holds a
+  // row's cache slot writes its K/V there before the bulk copies read it
+  const float* y;
+  int ldy;
 };
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
@@ -124,6 +129,24 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
   const int k_end = nrows > 0 ? min(nkeys, k_begin + split_len) : k_begin;
   const int nchunk = k_end > k_begin ? (k_end - k_begin + CHUNK - 1) / CHUNK : 0;
   const size_t tile = ((size_t)slot * p.A + a) * p.Lmax;  // first cache row of this (sequence, head)
+  if (p.y) {  // this split's rows -> the cache (their K/V exist only in the accumulator)
+    const int H = p.A * DH;
+    for (int i = threadIdx.x; i < nrows * 32; i += THREADS) {
+      const int r = i >> 5, kv = (i >> 4) & 1, c = i & 15;
+      const int pos = L + p.row_node[r0 + r];
+      if (pos < k_begin || pos >= k_end) continue;
+      const float4* src =
+          reinterpret_cast<const float4*>(p.y + (size_t)(r0 + r) * p.ldy + (1 + kv) * H + a * DH + c * 8);
+      const float4 f0 = __ldcg(src), f1 = __ldcg(src + 1);
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(f0.x, f0.y), h1 = __floats2bfloat162_rn(f0.z, f0.w);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(f1.x, f1.y), h3 = __floats2bfloat162_rn(f1.z, f1.w);
+      *reinterpret_cast<uint4*>(const_cast<__nv_bfloat16*>(kv ? p.vc : p.kc) + (tile + pos) * DH + c * 8) =
+          make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                     *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic cache writes -> the bulk copies below
+    __syncthreads();
+  }
   auto issue = [&](int c) {
     const int st = c % RING;
     const int key0 = k_begin + c * CHUNK;
@@ -146,8 +169,16 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
 #pragma unroll
     for (int w = 0; w < 4; ++w) bits[r][w] = 0ull;
     if (r < nrows) {
-      const uint4 u = *reinterpret_cast<const uint4*>(p.qkv + (size_t)(r0 + r) * p.ldq + a * DH + hl * 8);
-      bf16x8_to_f32(u, q[r]);
+      if (p.y) {  // bf16-rounded as the Q operand would hold it
+        const float4* src = reinterpret_cast<const float4*>(p.y + (size_t)(r0 + r) * p.ldy + a * DH + hl * 8);
+        const float4 f0 = __ldcg(src), f1 = __ldcg(src + 1);
+        const float fv[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[r][i] = __bfloat162float(__float2bfloat16_rn(fv[i]));
+      } else {
+        const uint4 u = *reinterpret_cast<const uint4*>(p.qkv + (size_t)(r0 + r) * p.ldq + a * DH + hl * 8);
+        bf16x8_to_f32(u, q[r]);
+      }
       node[r] = p.row_node[r0 + r];
       if (p.mask != nullptr)
 #pragma unroll
@@ -401,12 +432,13 @@ static int launch(const Args& p, dim3 grid, cudaStream_t st) {
 int attention_decode_bf16(int B, int Bg, int M, int A, int Lmax, int max_rows_per_seq, int max_keys, const void* qkv,
                           int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                           const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
-                          void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled) {
+                          void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st, bool* handled,
+                          bool qy) {
   *handled = false;
   (void)M;
   (void)ws;
   (void)ws_bytes;
-  if (max_rows_per_seq > 4 || W > 4 || (ldqkv % 8) != 0) return 0;
+  if (max_rows_per_seq > 4 || W > 4 || (ldqkv % (qy ? 4 : 8)) != 0) return 0;
   // splits per (sequence, head), one cluster each: enough CTAs for ~2 per SM
   // at small batch; at large batch (>= one wave of pairs) one split unless
   // its last wave leaves over 20 % of the CTA slots idle, then the split
@@ -440,8 +472,10 @@ int attention_decode_bf16(int B, int Bg, int M, int A, int Lmax, int max_rows_pe
   const int split_len = (((max_keys + nsplit - 1) / nsplit + 15) / 16) * 16;
   nsplit = (max_keys + split_len - 1) / split_len;
   dec::Args p{};
-  p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  p.qkv = qy ? nullptr : reinterpret_cast<const __nv_bfloat16*>(qkv);
   p.ldq = ldqkv;
+  p.y = qy ? reinterpret_cast<const float*>(qkv) : nullptr;
+  p.ldy = ldqkv;
   p.kc = reinterpret_cast<const __nv_bfloat16*>(kc);
   p.vc = reinterpret_cast<const __nv_bfloat16*>(vc);
   p.seq_slot = seq_slot;
