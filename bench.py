@@ -318,13 +318,28 @@ def attn_step_bytes(be, m, prune_layer) -> float:
     elt = 2 if be.tdtype != be.torch.float32 else 4
     B, n = m.batch, m.tree_size
     L0 = m.mean_seqlen * B
-    f = lambda keys, rows: (2 * keys + 2 * rows) * H * elt
+    f = lambda keys, rows, cap: ((2 * keys + 2 * rows) * H * elt +
+                                 fold_bytes(be, rows, cap, B, keys / max(1, B)))
     if n == 0:  # autoregressive
-        return 0.0 if bonus_fused(be, B) else Ly * f(L0 + B, B)
+        return 0.0 if bonus_fused(be, B) else Ly * f(L0 + B, B, 1)
     p = prune_layer if prune_layer is not None else Ly
     S = m.mean_survivors * B
-    tree = p * f(L0 + B * n, B * n) + (Ly - p) * f(L0 + B * n, S)
+    tree = p * f(L0 + B * n, B * n, n) + (Ly - p) * f(L0 + B * n, S, n)
     return tree + (0 if bonus_fused(be, B) else bonus_attn_bytes(be, m))
+
+
+def fold_bytes(be, rows, cap=1, nseq=1, keys=0) -> float:
+    """Extra algorithmic bytes of a pass whose QKV tail is folded into the
+    attention (B200Backend.ws_qkv_fold: weight-streaming passes of <= 128
+    rows not routed to the row-major tc2 kernel; cap = row capacity per
+    sequence, keys = keys per sequence): the kernel reads its rows' fp32
+    Q / K / V (3 H x 4 B) and writes their bf16 K/V (2 H x 2 B) instead of
+    reading a bf16 Q (H x 2 B)."""
+    if not (getattr(be, "ws_qkv_fold", False) and be.tdtype != be.torch.float32 and nseq * cap <= 128):
+        return 0.0
+    if cap > 32 and nseq * be.A * -(-int(keys) // 128) < 16 * be.lib.propd_num_sms():
+        return 0.0  # (tc2-routed: the QKV tail stays)
+    return rows * be.H * (12 + 4 - 2)
 
 
 def bonus_fused(be, B) -> bool:
@@ -337,7 +352,7 @@ def bonus_attn_bytes(be, m) -> float:
     elt = 2 if be.tdtype != be.torch.float32 else 4
     B = m.batch
     keys = m.mean_seqlen * B + m.mean_accepted * B + B
-    return be.num_layers * (2 * keys + 2 * B) * be.H * elt
+    return be.num_layers * ((2 * keys + 2 * B) * be.H * elt + fold_bytes(be, B, 1, B, keys / max(1, B)))
 
 
 def modal_size(metrics):

@@ -131,10 +131,12 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
   const size_t tile = ((size_t)slot * p.A + a) * p.Lmax;  // first cache row of this (sequence, head)
   if (p.y) {  // this split's rows -> the cache (their K/V exist only in the accumulator)
     const int H = p.A * DH;
+    bool wrote = false;
     for (int i = threadIdx.x; i < nrows * 32; i += THREADS) {
       const int r = i >> 5, kv = (i >> 4) & 1, c = i & 15;
       const int pos = L + p.row_node[r0 + r];
       if (pos < k_begin || pos >= k_end) continue;
+      wrote = true;
       const float4* src =
           reinterpret_cast<const float4*>(p.y + (size_t)(r0 + r) * p.ldy + (1 + kv) * H + a * DH + c * 8);
       const float4 f0 = __ldcg(src), f1 = __ldcg(src + 1);
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(THREADS) decode_kernel(Args p) {
           make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
                      *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic cache writes -> the bulk copies below
+    if (wrote) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic cache writes -> the bulk copies below
     __syncthreads();
   }
   auto issue = [&](int c) {

@@ -307,10 +307,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       }
       *reinterpret_cast<uint4*>(dst) = v;
     }
+    bool wrote = false;
     for (int i = threadIdx.x; i < nrows * 32; i += C::THREADS) {
       const int r = i >> 5, kv = (i >> 4) & 1, c = i & 15;
       const int pos = L + p.row_node[r0 + r];
       if (pos < k_begin || pos >= k_end) continue;
+      wrote = true;
       const float4* src =
           reinterpret_cast<const float4*>(p.y + (size_t)(r0 + r) * p.ldy + (1 + kv) * H + a * DH + c * 8);
       const float4 f0 = __ldcg(src), f1 = __ldcg(src + 1);
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       *reinterpret_cast<uint4*>(dst) =
           make_uint4(pack_bf16(f0.x, f0.y), pack_bf16(f0.z, f0.w), pack_bf16(f1.x, f1.y), pack_bf16(f1.z, f1.w));
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic cache writes -> the TMA reads below
+    if (wrote) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic cache writes -> the TMA reads below
     for (int r = threadIdx.x; r < NR; r += C::THREADS) rnode[r] = r < nrows ? p.row_node[r0 + r] : 0;
   } else {  // Q rows -> SW128 K-major [NR rows x 128 dims] (rows past nrows zero)
     const __nv_bfloat16* qbase = p.qkv + a * DH;
