@@ -331,14 +331,11 @@ def attn_step_bytes(be, m, prune_layer) -> float:
 def fold_bytes(be, rows, cap=1, nseq=1, keys=0) -> float:
     """Extra algorithmic bytes of a pass whose QKV tail is folded into the
     attention (B200Backend.ws_qkv_fold: weight-streaming passes of <= 128
-    rows not routed to the row-major tc2 kernel; cap = row capacity per
-    sequence, keys = keys per sequence): the kernel reads its rows' fp32
+    rows; cap = row capacity per sequence): the kernel reads its rows' fp32
     Q / K / V (3 H x 4 B) and writes their bf16 K/V (2 H x 2 B) instead of
     reading a bf16 Q (H x 2 B)."""
     if not (getattr(be, "ws_qkv_fold", False) and be.tdtype != be.torch.float32 and nseq * cap <= 128):
         return 0.0
-    if cap > 32 and nseq * be.A * -(-int(keys) // 128) < 16 * be.lib.propd_num_sms():
-        return 0.0  # (tc2-routed: the QKV tail stays)
     return rows * be.H * (12 + 4 - 2)
 
 

@@ -473,7 +473,7 @@ class B200Backend:
         # rows' K/V from the fp32 accumulator and writes those K/V rows into the
         # cache itself; W_o re-zeroes the accumulator (PROPD_ATTN_QKV_F32)
         fold = (not splits and self.ws_qkv_fold and mask is not None and self.dh == 128 and rt.max_rows <= 64
-                and W <= 4 and (mask is not self._one_mask or rt.max_rows <= 4) and not self._tc2_routed(rt))
+                and W <= 4 and (mask is not self._one_mask or rt.max_rows <= 4))
         wo_zero = _lib.WsPhases(bar=bar, zero_buf=ptr(acc1), zero_ld=3 * H, zero_cols=3 * H) if fold else None
         for l in range(l0, l1):
             # with the converting GELU, QKV zeroes the W_1 accumulator rows ahead (W_2 read them last)
@@ -498,17 +498,6 @@ class B200Backend:
             self._gemm_ws(M, live, 4 * H, H, h, self.w.w1[l], acc2, 4 * H, 1, pro_w1)
             self._gemm_ws(M, live, H, 4 * H, g, self.w.w2[l], x, H, 1, gelu)
         return None
-
-    def _tc2_routed(self, rt: Rows) -> bool:
-        """Whether the attention dispatch sends this pass to the row-major tc2
-        kernel (> 32-row capacity, latency-bound: attention_tct.cu), which
-        keeps the QKV tail (the folded input needs the transposed kernel;
-        measured at B=1 with 64-row capacity: forcing it costs the attention
-        more than the tail saves)."""
-        if rt.max_rows <= 32 or self.attn_impl not in (0, 4) or os.environ.get("PROPD_TCT") == "2":
-            return False
-        nseq = rt.B - (1 if rt.scratch_last else 0)
-        return nseq * self.A * (-(-rt.max_keys // 128)) < 16 * self.lib.propd_num_sms()
 
     def fused_one_row_splits(self, M: int) -> int:
         """Key splits of the attention fused into the QKV launch for a one-row

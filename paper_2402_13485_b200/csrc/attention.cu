@@ -224,7 +224,7 @@ int attention_tc2_bf16(int B, int Bg, int M, int A, int Lmax, int n_slots, int m
                        const void* qkv, int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot,
                        const int32_t* seq_len, const int32_t* row_off, const int32_t* row_node, const uint64_t* mask,
                        int n_tmpl, int W, void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st,
-                       bool* handled);
+                       bool* handled, bool qy = false);
 int attention_tct_bf16(int B, int Bg, int A, int Lmax, int n_slots, int max_rows_per_seq, int max_keys, const void* qkv,
                        int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot, const int32_t* seq_len,
                        const int32_t* row_off, const int32_t* row_node, const uint64_t* mask, int n_tmpl, int W,
@@ -281,11 +281,16 @@ int propd_tree_attention(int dtype, int impl, int B, int M, int A, int dh, int L
                                     workspace_bytes, as_stream(stream), &handled, true);
       if (e || handled) return e;
     }
+    // the transposed kernel, or the row-major one where its latency heuristic routes the shape (impl 0)
     int e = attention_tct_bf16(B, Bg, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache,
                                seq_slot, seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, as_stream(stream),
-                               true, &handled, true);
+                               impl == 5, &handled, true);
+    if (e || handled) return e;
+    e = attention_tc2_bf16(B, Bg, M, A, Lmax, n_slots, max_rows_per_seq, max_keys, qkv, ldqkv, kcache, vcache,
+                           seq_slot, seq_len, row_off, row_node, mask, n_tmpl, W, out, ldout, workspace,
+                           workspace_bytes, as_stream(stream), &handled, true);
     if (e) return e;
-    PROPD_REQUIRE(handled, "tree_attention: QKV_F32 input: the transposed kernel serves <= 64 rows per sequence");
+    PROPD_REQUIRE(handled, "tree_attention: QKV_F32 input serves <= 64 rows per sequence (one row tile)");
     return 0;
   }
   PROPD_REQUIRE(mask == nullptr || (W <= ATT_MAXW && W * 64 >= n_tmpl),

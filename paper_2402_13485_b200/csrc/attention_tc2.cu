@@ -60,7 +60,20 @@ struct Args {
   int ldout;
   unsigned long long* tl;     // development timeline (common.cuh)
   unsigned int tag;
+  // PROPD_ATTN_QKV_F32 (one row tile per sequence): Q and the tree rows' K/V
+  // from the fp32 QKV accumulator (row stride ldy floats, bf16-rounded); the
+  // CTA writes the tree rows of its key range into the cache before its TMA
+  // stream reads them
+  const float* y;
+  int ldy;
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
 };
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
 
 // Bits [t0, t0+32) of a row's visibility over tree nodes (0 outside [0, 64W)).
 __device__ __forceinline__ uint32_t tree_bits32(const uint64_t* mrow, int W, int node, int t0) {
@@ -224,7 +237,33 @@ __global__ void __launch_bounds__(THREADS, 1)
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  {  // Q rows -> SW128 K-major smem (cp.async; rows past nrows zero)
+  if (p.y) {  // Q rows from the fp32 accumulator; this split's tree rows -> the cache
+    const int H = p.A * DH;
+    const size_t rb = ((size_t)slot * p.A + a) * p.Lmax;
+    for (int i = threadIdx.x; i < BM * 16; i += THREADS) {
+      const int r = i >> 4, c = i & 15;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < nrows) {
+        const float4* src = reinterpret_cast<const float4*>(p.y + (size_t)(r0 + r) * p.ldy + a * DH + c * 8);
+        const float4 f0 = __ldcg(src), f1 = __ldcg(src + 1);
+        v = make_uint4(pack_bf16(f0.x, f0.y), pack_bf16(f0.z, f0.w), pack_bf16(f1.x, f1.y), pack_bf16(f1.z, f1.w));
+      }
+      *reinterpret_cast<uint4*>(smem + SMEM_Q + sw128_chunk(r, c)) = v;
+    }
+    bool wrote = false;
+    for (int i = threadIdx.x; i < nrows * 32; i += THREADS) {
+      const int r = i >> 5, kv = (i >> 4) & 1, c = i & 15;
+      const int pos = L + p.row_node[r0 + r];
+      if (pos < k_begin || pos >= k_end) continue;
+      wrote = true;
+      const float4* src =
+          reinterpret_cast<const float4*>(p.y + (size_t)(r0 + r) * p.ldy + (1 + kv) * H + a * DH + c * 8);
+      const float4 f0 = __ldcg(src), f1 = __ldcg(src + 1);
+      *reinterpret_cast<uint4*>((kv ? p.vc : p.kc) + (rb + pos) * DH + c * 8) =
+          make_uint4(pack_bf16(f0.x, f0.y), pack_bf16(f0.z, f0.w), pack_bf16(f1.x, f1.y), pack_bf16(f1.z, f1.w));
+    }
+    if (wrote) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic cache writes -> the TMA reads
+  } else {  // Q rows -> SW128 K-major smem (cp.async; rows past nrows zero)
     const __nv_bfloat16* qbase = p.qkv + a * DH;
     for (int i = threadIdx.x; i < BM * 16; i += THREADS) {
       const int r = i >> 4, c = i & 15;
@@ -542,9 +581,10 @@ int attention_tc2_bf16(int B, int Bg, int M, int A, int Lmax, int n_slots, int m
                        const void* qkv, int ldqkv, const void* kc, const void* vc, const int32_t* seq_slot,
                        const int32_t* seq_len, const int32_t* row_off, const int32_t* row_node, const uint64_t* mask,
                        int n_tmpl, int W, void* out, int ldout, void* ws, int64_t ws_bytes, cudaStream_t st,
-                       bool* handled) {
+                       bool* handled, bool qy) {
   *handled = false;
-  if (n_slots <= 0 || W > 4 || (ldqkv % 8) != 0 || (ldout % 8) != 0) return 0;
+  if (n_slots <= 0 || W > 4 || (ldqkv % (qy ? 4 : 8)) != 0 || (ldout % 8) != 0) return 0;
+  if (qy && max_rows_per_seq > tc2::BM) return 0;  // (a second row tile would need the first tile's tree rows)
   CUtensorMap km, vm;
   const uint64_t rows = (uint64_t)n_slots * A * Lmax;
   if (!tc2::kv_map64(&km, kc, rows) || !tc2::kv_map64(&vm, vc, rows)) return 0;
@@ -562,8 +602,12 @@ int attention_tc2_bf16(int B, int Bg, int M, int A, int Lmax, int n_slots, int m
   const int blocks_per_split = (nblk_max + nsplit - 1) / nsplit;
   nsplit = (nblk_max + blocks_per_split - 1) / blocks_per_split;
   tc2::Args p{};
-  p.qkv = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  p.qkv = qy ? nullptr : reinterpret_cast<const __nv_bfloat16*>(qkv);
   p.ldq = ldqkv;
+  p.y = qy ? reinterpret_cast<const float*>(qkv) : nullptr;
+  p.ldy = ldqkv;
+  p.kc = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(kc));
+  p.vc = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(vc));
   p.seq_slot = seq_slot;
   p.seq_len = seq_len;
   p.row_off = row_off;
