@@ -349,7 +349,17 @@ __global__ void gather_rows_kernel(int H, const float* __restrict__ src, const i
   const int m = blockIdx.x;
   const float* s = src + (size_t)(idx ? idx[m] : m) * H;
   T* d = dst + (size_t)m * H;
-  for (int h = threadIdx.x; h < H; h += blockDim.x) d[h] = from_f<T>(s[h]);
+  if (H % 4 == 0 && (reinterpret_cast<uintptr_t>(s) & 15) == 0 && (reinterpret_cast<uintptr_t>(d) & 7) == 0) {
+    for (int h = threadIdx.x * 4; h < H; h += blockDim.x * 4) {  // 16-byte loads, 4 elements per thread
+      const float4 v = __ldg(reinterpret_cast<const float4*>(s + h));
+      d[h] = from_f<T>(v.x);
+      d[h + 1] = from_f<T>(v.y);
+      d[h + 2] = from_f<T>(v.z);
+      d[h + 3] = from_f<T>(v.w);
+    }
+  } else {
+    for (int h = threadIdx.x; h < H; h += blockDim.x) d[h] = from_f<T>(s[h]);
+  }
 }
 
 // First maximum of each row (numpy argmax semantics).  The scan is latency-bound (one row per CTA,
