@@ -372,13 +372,16 @@ __device__ __forceinline__ void argmax_take(float t, int v, float& best, int& bi
     bi = v;
   }
 }
-__global__ void __launch_bounds__(512) argmax_rows_kernel(int V, int ld, const float* __restrict__ logits,
+__global__ void __launch_bounds__(512) argmax_rows_kernel(int M, int V, int ld, const float* __restrict__ logits,
                                                             int32_t* __restrict__ out,
                                                             const int32_t* __restrict__ rows_dev) {
   __shared__ float sv[32];
   __shared__ int si[32];
-  if (rows_dev && (int)blockIdx.x >= *rows_dev) return;
-  const float* x = logits + (size_t)blockIdx.x * ld;
+  // rows strided over a grid of <= 2 CTAs per SM (a capacity-sized grid of
+  // mostly dead rows is CTA-launch-rate bound at large batch)
+  const int rows = rows_dev ? min((int)M, *rows_dev) : (int)M;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+  const float* x = logits + (size_t)row * ld;
   float best = -INFINITY;
   int bi = 0x7fffffff;
   const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(logits) & 15) == 0);
@@ -421,7 +424,9 @@ __global__ void __launch_bounds__(512) argmax_rows_kernel(int V, int ld, const f
       int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
     }
-    if (lane == 0) out[blockIdx.x] = bi;
+    if (lane == 0) out[row] = bi;
+  }
+  __syncthreads();  // sv / si reused by the next row
   }
 }
 
@@ -710,7 +715,8 @@ int propd_gather_rows(int dtype, int M, int H, const float* src, const int32_t* 
 int propd_argmax_rows(int M, const int32_t* rows_dev, int V, int ld, const float* logits, int32_t* out, void* stream) {
   if (M == 0) return 0;
   PROPD_REQUIRE(V > 0 && ld >= V, "argmax_rows: bad V=%d ld=%d", V, ld);
-  argmax_rows_kernel<<<M, 512, 0, as_stream(stream)>>>(V, ld, logits, out, rows_dev);
+  const int grid = M < 2 * propd_num_sms() ? M : 2 * propd_num_sms();
+  argmax_rows_kernel<<<grid, 512, 0, as_stream(stream)>>>(M, V, ld, logits, out, rows_dev);
   return check_launch("argmax_rows");
 }
 
