@@ -178,6 +178,64 @@ __global__ void prune_compact_kernel(int B, int n, const int32_t* __restrict__ p
   }
 }
 
+// Same outputs with the tree staged in shared memory (B * n <= K5S_MAX): the
+// closure of every (sequence, node) is an independent walk up its ancestor
+// chain (a node is alive iff it and all its ancestors are members), so it
+// runs on all threads at once instead of one dependent global-memory chain
+// per sequence; counts, scan and the row scatter then read shared memory.
+constexpr int K5S_MAX = 16384;
+__global__ void __launch_bounds__(1024) prune_compact_smem_kernel(
+    int B, int n, const int32_t* __restrict__ parent, const uint8_t* __restrict__ member, uint8_t* __restrict__ alive,
+    int32_t* new_row_seq, int32_t* new_row_node, int32_t* new_row_src, int32_t* new_row_off, int32_t* node_row,
+    int32_t* surv_cnt, int32_t* total) {
+  __shared__ int scan[1024];
+  __shared__ int s_par[1024];
+  __shared__ uint8_t s_mem[K5S_MAX], s_alive[K5S_MAX];
+  const int BN = B * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_par[i] = parent[i];
+  for (int e = threadIdx.x; e < BN; e += blockDim.x) s_mem[e] = member[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < BN; e += blockDim.x) {
+    const int b = e / n, i = e - b * n;
+    bool ok = s_mem[e] != 0;
+    for (int a = s_par[i]; ok && a >= 0; a = s_par[a]) ok = s_mem[b * n + a] != 0;
+    s_alive[e] = ok;
+    alive[e] = ok;
+  }
+  __syncthreads();
+  const int b = threadIdx.x;
+  int cnt = 0;
+  if (b < B)
+    for (int i = 0; i < n; ++i) cnt += s_alive[b * n + i];
+  scan[threadIdx.x] = cnt;
+  __syncthreads();
+  for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // Hillis-Steele inclusive scan
+    int v = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
+    __syncthreads();
+    scan[threadIdx.x] += v;
+    __syncthreads();
+  }
+  if (b < B) {
+    int o = scan[b] - cnt;
+    new_row_off[b] = o;
+    surv_cnt[b] = cnt;
+    for (int i = 0; i < n; ++i) {
+      if (s_alive[b * n + i]) {
+        new_row_seq[o] = b;
+        new_row_node[o] = i;
+        new_row_src[o] = b * n + i;
+        node_row[b * n + i] = o++;
+      } else {
+        node_row[b * n + i] = -1;
+      }
+    }
+    if (b == B - 1) {
+      new_row_off[B] = o;
+      *total = o;
+    }
+  }
+}
+
 // Graph-captured passes run layers > p on a padded row count: rows
 // [total, S_pad) become batch entry B (the scratch slot, node 0).
 __global__ void pad_rows_kernel(int B, int S_pad, int pad_seq, const int32_t* __restrict__ total, int32_t* row_seq,
@@ -490,6 +548,12 @@ int propd_prune_compact(int B, int n, const int32_t* parent, const uint8_t* memb
                         int32_t* node_row, int32_t* surv_cnt, int32_t* total, void* stream) {
   if (B == 0) return 0;
   PROPD_REQUIRE(B <= 1024, "prune_compact: batch %d > 1024", B);
+  if ((long long)B * n <= K5S_MAX && n <= 1024) {
+    prune_compact_smem_kernel<<<1, 1024, 0, as_stream(stream)>>>(B, n, parent, member, alive, new_row_seq,
+                                                                  new_row_node, new_row_src, new_row_off, node_row,
+                                                                  surv_cnt, total);
+    return check_launch("prune_compact");
+  }
   int threads = ((B + 31) / 32) * 32;
   prune_compact_kernel<<<1, threads, 0, as_stream(stream)>>>(B, n, parent, member, alive, new_row_seq, new_row_node,
                                                              new_row_src, new_row_off, node_row, surv_cnt, total);
